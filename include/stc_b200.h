@@ -1,0 +1,158 @@
+/*
+ * stc_b200.h -- C ABI of the B200-native Strassen tensor-contraction path.
+ *
+ * Drop-in boundary.  The reference (strassen_tc, Python + numba) has no FFI;
+ * its hot path sits behind the Python function
+ *     contract(spec, a, b, c, level, variant, params, threads, force_slow,
+ *              allow_deep, validate) -> RunStats
+ * (/root/reference/pkg/src/strassen_tc/strassen.py:141-207), and below it
+ * behind the numba kernel ABI of _jit.py (flat float64 data arrays, stacked
+ * int64 scatter arrays, float64 +/-1 coefficients, scalar ints;
+ * _jit.py:28,83,159,190,224,260).  Each entry point below names the reference
+ * interface it replaces.  All pointers are DEVICE pointers unless stated;
+ * `stream` is a cudaStream_t passed as void*; every call is stream-ordered and
+ * asynchronous unless stated.  Return value: 0 on success, otherwise a
+ * STC_E* code with a message from stc_last_error() (thread-local).  Errors
+ * are raised before any device work is enqueued, mirroring the reference's
+ * "ValueError before C is touched" convention (strassen.py:151-152).
+ *
+ * Element offsets are int64 in units of doubles.  STC_PAD (INT64_MIN) is the
+ * reference's PAD sentinel (scatter.py:23): reads yield 0.0, writes are
+ * dropped.
+ */
+#ifndef STC_B200_H
+#define STC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STC_ABI_VERSION 1
+#define STC_MAX_LABELS 16
+#define STC_PAD INT64_MIN
+
+/* Status codes. */
+#define STC_OK 0
+#define STC_EINVAL 1   /* bad argument (shape, extents, geometry, ...)    */
+#define STC_ECAP 2     /* level above the device cap                      */
+#define STC_ECUDA 3    /* CUDA runtime error                              */
+#define STC_EWORKSPACE 4 /* workspace too small                           */
+#define STC_EOVERLAP 5 /* validate: C targets overlap (driver.py:53-61)   */
+
+/* Variants: strassen.py:41-44. */
+#define STC_VARIANT_ABC 0
+#define STC_VARIANT_AB 1
+#define STC_VARIANT_NAIVE 2
+
+/* Flags. */
+#define STC_FLAG_FORCE_SLOW 1u        /* reference force_slow: scalar-gather staging only   */
+#define STC_FLAG_VALIDATE 2u          /* reference validate: check C-target disjointness    */
+#define STC_FLAG_REFERENCE_TILING 4u  /* keep the reference intra-quadrant order for tiles  */
+
+/* One index bundle of one tensor in the reference linearisation (first label
+ * fastest, scatter.py:105-112): scat[l] = sum_d idx_d(l) * str[d]. */
+typedef struct {
+  int32_t nlab;
+  int32_t _pad;
+  int64_t ext[STC_MAX_LABELS];
+  int64_t str[STC_MAX_LABELS];
+} stc_bundle;
+
+/* A contraction C += A . B with A matricised as I x P, B as P x J, C as I x J
+ * (tensor.py:132-169 bundles; strassen.py:156-161 views).  *_base is the
+ * tensor's base_offset (folded into the column scatter, scatter.py:128). */
+typedef struct {
+  stc_bundle a_row, a_col;
+  stc_bundle b_row, b_col;
+  stc_bundle c_row, c_col;
+  int64_t a_base, b_base, c_base;
+  int32_t level;   /* Strassen levels L >= 0 (7^L leaf products)          */
+  int32_t variant; /* STC_VARIANT_*                                        */
+  uint32_t flags;  /* STC_FLAG_*                                           */
+  int32_t _pad;
+} stc_problem;
+
+/* Mirrors RunStats counters (oracle.py:22-43); GPU tiles replace mr x nr
+ * register blocks, so block/update counts are per GPU tile. */
+typedef struct {
+  double total_flops;      /* executed MMA flops incl. tile padding          */
+  int64_t fast_blocks;     /* operand tiles staged on the vectorised path    */
+  int64_t slow_blocks;     /* operand tiles staged by scalar gathers         */
+  int64_t fast_updates;    /* C-tile updates (all tiles use the scatter path) */
+  int64_t slow_updates;
+  int64_t leaf_multiplies; /* 7^L                                            */
+  int64_t work_items;      /* (term, tile) items executed                    */
+  int64_t kernel_launches; /* kernels this call enqueued                      */
+} stc_stats;
+
+/* ---- library ---- */
+const char *stc_last_error(void);
+int stc_abi_version(void);
+
+/* ---- whole path: replaces strassen.contract (strassen.py:141-207) ---- */
+
+/* Bytes of device workspace stc_contract needs for this problem. Host-only. */
+int stc_workspace_size(const stc_problem *p, size_t *bytes);
+
+/* C += A.B through an L-level Strassen recursion in the given variant.
+ * A, B: read-only device storage (element 0 = flat index 0 of the tensor
+ * storage; offsets come from the bundles); C: device storage updated in place.
+ * workspace: >= stc_workspace_size bytes, 256-B aligned, contents ignored. */
+int stc_contract(const stc_problem *p, const double *A, const double *B, double *C, void *workspace,
+                 size_t workspace_bytes, void *stream, stc_stats *stats);
+
+/* ---- subsystem (1): device-side scatter / block-scatter vectors ---- */
+
+/* make_view's _bundle_scatter (scatter.py:105-112) on the device: out[l] for
+ * l < len(bundle) = base + sum idx*str; out[l] = STC_PAD for len <= l < out_len. */
+int stc_bundle_scatter(const stc_bundle *bundle, int64_t base, int64_t out_len, int64_t *out, void *stream);
+
+/* _block_vector (scatter.py:26-40) on the device: one entry per blk-block of
+ * scat: the constant positive stride, `unit_stride` (>0) for 1-entry blocks,
+ * else 0; any PAD in the block gives 0. */
+int stc_block_vector(const int64_t *scat, int64_t len, int64_t blk, int64_t unit_stride, int64_t *out,
+                     void *stream);
+
+/* ---- subsystems (2)+(3): one fused Strassen term (driver.run_fused, driver.py:76-126) ----
+ * C_t += coeff_c_t * (sum_a coeff_a * Aview_a) (sum_b coeff_b * Bview_b) for every target t.
+ * Views are (row scatter, col scatter) device vectors: A views m x k, B views
+ * k x n, C targets m x n, all over one parent per side.  Up to 16 views per
+ * side.  Targets must be pairwise disjoint or identical (driver.py:53-61).
+ * `rows`/`cols`/`coeffs` are HOST arrays of length n_* holding device
+ * pointers / values.  workspace >= stc_fused_term_workspace_size(). */
+int stc_fused_term_workspace_size(int64_t m, int64_t n, int64_t k, int n_a, int n_b, int n_c, size_t *bytes);
+int stc_fused_term(int64_t m, int64_t n, int64_t k, const double *A, int n_a, const int64_t *const *a_rows,
+                   const int64_t *const *a_cols, const double *a_coeffs, const double *B, int n_b,
+                   const int64_t *const *b_rows, const int64_t *const *b_cols, const double *b_coeffs, double *C,
+                   int n_c, const int64_t *const *c_rows, const int64_t *const *c_cols, const double *c_coeffs,
+                   uint32_t flags, void *workspace, size_t workspace_bytes, void *stream, stc_stats *stats);
+
+/* ---- subsystem (4): AB / Naive helpers ---- */
+
+/* accumulate_dense_to_view (kernels.py:236-247, _jit.py:223-256):
+ * C[rows[i] + cols[j]] += coeff * M[i + j*ldm] for i < m, j < n (M column-major);
+ * PAD rows/cols dropped.  Targets must not alias M. */
+int stc_accumulate_dense(const double *M, int64_t ldm, int64_t m, int64_t n, double *C, const int64_t *rows,
+                         const int64_t *cols, double coeff, void *stream, stc_stats *stats);
+
+/* unpack_to_dense (kernels.py:250-264, _jit.py:259-309):
+ * out[i + j*ldo] = sum_t coeffs[t] * data[rows_t[i] + cols_t[j]] (PAD reads 0),
+ * summed in view order.  rows/cols/coeffs are HOST arrays (device pointers). */
+int stc_unpack_sum(double *out, int64_t ldo, int64_t m, int64_t n, const double *data, int nviews,
+                   const int64_t *const *rows, const int64_t *const *cols, const double *coeffs, void *stream,
+                   stc_stats *stats);
+
+/* ---- verification helper (oracle.py:110-124 semantics, on the device) ----
+ * Sums over every multi-index of two equally shaped strided tensors:
+ * out[0] = sum (x - ref)^2, out[1] = sum ref^2 (deterministic order).
+ * out is a HOST array of 2 doubles; the call synchronises `stream`. */
+int stc_sq_norms(int ndim, const int64_t *extents, const double *x, const int64_t *x_strides, int64_t x_base,
+                 const double *ref, const int64_t *ref_strides, int64_t ref_base, double *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STC_B200_H */

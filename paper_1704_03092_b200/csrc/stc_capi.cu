@@ -1,0 +1,943 @@
+// stc_capi.cu -- the C ABI (include/stc_b200.h): host-side planning of the
+// Strassen contraction and the kernel launch sequence for each variant.
+//
+// Planning mirrors strassen.contract (strassen.py:141-207):
+//   views of A (I x P), B (P x J), C (I x J)          strassen.py:156-161
+//   quadrants with PAD padding to 2^L                   strassen.py:101-127
+//   7^L terms by level-1 substitution                   strassen.py:70-94
+// and replaces the CPU cache-blocking (driver.py:76-126) with one persistent
+// DMMA launch over all (term, tile) work items (ABC) or batched launches that
+// write dense M slots (AB / Naive).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "stc_internal.cuh"
+
+using namespace stc;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+  return fail(STC_ECUDA, "CUDA error in %s: %s", what, cudaGetErrorString(e));
+}
+
+#define CU(expr, what)                       \
+  do {                                       \
+    cudaError_t _e = (expr);                 \
+    if (_e != cudaSuccess) return cuda_fail(_e, what); \
+  } while (0)
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int64_t bundle_len(const stc_bundle &b) {
+  int64_t n = 1;
+  for (int d = 0; d < b.nlab; ++d) n *= b.ext[d];
+  return n;
+}
+
+// ---------------------------------------------------------------- staging
+// Pinned host staging for the small plan tables, double-buffered and fenced
+// by events so uploads never force a stream synchronisation.
+struct Staging {
+  void *host[2] = {nullptr, nullptr};
+  size_t cap[2] = {0, 0};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  bool used[2] = {false, false};
+  int next = 0;
+  std::mutex mu;
+};
+Staging g_staging[64];
+
+int upload(const void *src, size_t bytes, void *dst, cudaStream_t s) {
+  if (bytes == 0) return STC_OK;
+  int dev = 0;
+  CU(cudaGetDevice(&dev), "cudaGetDevice");
+  Staging &st = g_staging[dev & 63];
+  std::lock_guard<std::mutex> lk(st.mu);
+  const int i = st.next;
+  st.next ^= 1;
+  if (!st.ev[i]) CU(cudaEventCreateWithFlags(&st.ev[i], cudaEventDisableTiming), "cudaEventCreate");
+  if (st.used[i]) CU(cudaEventSynchronize(st.ev[i]), "cudaEventSynchronize");
+  if (st.cap[i] < bytes) {
+    if (st.host[i]) cudaFreeHost(st.host[i]);
+    st.host[i] = nullptr;
+    size_t c = std::max<size_t>(bytes, 1 << 16);
+    CU(cudaMallocHost(&st.host[i], c), "cudaMallocHost");
+    st.cap[i] = c;
+  }
+  memcpy(st.host[i], src, bytes);
+  CU(cudaMemcpyAsync(dst, st.host[i], bytes, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync(tables)");
+  CU(cudaEventRecord(st.ev[i], s), "cudaEventRecord");
+  st.used[i] = true;
+  return STC_OK;
+}
+
+// ------------------------------------------------------------ Strassen terms
+struct Op {
+  int q, s;
+};
+struct Term {
+  std::vector<Op> a, b, c;
+};
+
+// strassen.py:56-65
+const int kL1[7][3][2][2] = {
+    {{{0, 1}, {3, 1}}, {{0, 1}, {3, 1}}, {{0, 1}, {3, 1}}},
+    {{{2, 1}, {3, 1}}, {{0, 1}, {0, 0}}, {{2, 1}, {3, -1}}},
+    {{{0, 1}, {0, 0}}, {{1, 1}, {3, -1}}, {{1, 1}, {3, 1}}},
+    {{{3, 1}, {0, 0}}, {{2, 1}, {0, -1}}, {{0, 1}, {2, 1}}},
+    {{{0, 1}, {1, 1}}, {{3, 1}, {0, 0}}, {{1, 1}, {0, -1}}},
+    {{{2, 1}, {0, -1}}, {{0, 1}, {1, 1}}, {{3, 1}, {0, 0}}},
+    {{{1, 1}, {3, -1}}, {{2, 1}, {3, 1}}, {{0, 1}, {0, 0}}},
+};
+
+// strassen.py:70-94: level l = level-1 table (outer) x level l-1 table (inner),
+// quadrant q*4^(l-1) + q2, sign s*s2.
+std::vector<Term> strassen_terms(int level) {
+  std::vector<Term> terms(1);
+  terms[0].a = {{0, 1}};
+  terms[0].b = {{0, 1}};
+  terms[0].c = {{0, 1}};
+  for (int lev = 1; lev <= level; ++lev) {
+    int mult = 1;
+    for (int i = 1; i < lev; ++i) mult *= 4;
+    std::vector<Term> next;
+    next.reserve(terms.size() * 7);
+    for (int o = 0; o < 7; ++o)
+      for (const Term &in : terms) {
+        Term t;
+        for (int side = 0; side < 3; ++side) {
+          const std::vector<Op> &inner = side == 0 ? in.a : side == 1 ? in.b : in.c;
+          std::vector<Op> &dst = side == 0 ? t.a : side == 1 ? t.b : t.c;
+          for (int e = 0; e < 2; ++e) {
+            if (kL1[o][side][e][1] == 0) continue;
+            for (const Op &x : inner) dst.push_back({kL1[o][side][e][0] * mult + x.q, kL1[o][side][e][1] * x.s});
+          }
+        }
+        next.push_back(std::move(t));
+      }
+    terms.swap(next);
+  }
+  return terms;
+}
+
+// quadrant id (row-major per level, top level most significant) -> (row, col)
+void quad_rc(int q, int level, int64_t &r, int64_t &c) {
+  r = 0;
+  c = 0;
+  for (int l = 0; l < level; ++l) {
+    const int d = (q >> (2 * (level - 1 - l))) & 3;
+    r = r * 2 + (d >> 1);
+    c = c * 2 + (d & 1);
+  }
+}
+
+// ---------------------------------------------------------- tile ordering
+// Quadrant-local box of a bundle and the tile order of its dims (DESIGN.md
+// "tile ordering").  The permutation is applied identically to every quadrant
+// and to both tensors sharing the bundle, so quadrants and their pairing are
+// exactly the reference's; only the grouping of indices into GPU tiles moves.
+struct Tiling {
+  int nbox = 0;
+  int64_t box_ext[STC_MAX_LABELS];
+  int32_t order[STC_MAX_LABELS];
+};
+
+Tiling make_tiling(const stc_bundle &b, int level, const int64_t *key, bool reference) {
+  Tiling t;
+  if (reference) return t;
+  const int64_t n = bundle_len(b);
+  const int64_t Q = (int64_t)1 << level;
+  if (n % Q != 0) return t;  // padded quadrants: keep the reference order
+  const int64_t xq = n / Q;
+  int64_t P = 1;
+  int k = 0;
+  while (k < b.nlab && xq % (P * b.ext[k]) == 0) P *= b.ext[k++];
+  const int64_t c = xq / P;
+  if (k < b.nlab && b.ext[k] % c != 0) return t;
+  if (k == b.nlab && c != 1) return t;
+  int64_t ext[STC_MAX_LABELS + 1], ks[STC_MAX_LABELS + 1];
+  int nd = 0;
+  for (int d = 0; d < k; ++d) {
+    ext[nd] = b.ext[d];
+    ks[nd++] = key[d] < 0 ? -key[d] : key[d];
+  }
+  if (c > 1) {
+    ext[nd] = c;
+    ks[nd++] = key[k] < 0 ? -key[k] : key[k];
+  }
+  if (nd > STC_MAX_LABELS) return t;
+  std::vector<int> idx(nd);
+  for (int i = 0; i < nd; ++i) idx[i] = i;
+  std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return ks[x] < ks[y]; });
+  t.nbox = nd;
+  for (int i = 0; i < nd; ++i) {
+    t.box_ext[i] = ext[i];
+    t.order[i] = idx[i];
+  }
+  return t;
+}
+
+// Which bundle holds a tensor's smallest stride (extent > 1 labels only):
+// returns 0 for the row bundle, 1 for the column bundle, -1 if none.
+int min_stride_side(const stc_bundle &r, const stc_bundle &c) {
+  int64_t best = INT64_MAX;
+  int side = -1;
+  for (int s = 0; s < 2; ++s) {
+    const stc_bundle &b = s == 0 ? r : c;
+    for (int d = 0; d < b.nlab; ++d) {
+      if (b.ext[d] <= 1) continue;
+      const int64_t v = b.str[d] < 0 ? -b.str[d] : b.str[d];
+      if (v < best) {
+        best = v;
+        side = s;
+      }
+    }
+  }
+  return side;
+}
+
+VecDesc vec_bundle(const stc_bundle &b, int64_t base, int64_t nq, int64_t tile, const Tiling &t) {
+  VecDesc d;
+  memset(&d, 0, sizeof(d));
+  d.mode = 0;
+  d.len = bundle_len(b);
+  d.nq = nq;
+  d.q_len = cdiv(d.len, nq);  // pad_view to a multiple of 2^L, then split
+  d.q_len_pad = rup(d.q_len, tile);
+  d.base = base;
+  d.nlab = b.nlab;
+  for (int i = 0; i < b.nlab; ++i) {
+    d.ext[i] = b.ext[i];
+    d.str[i] = b.str[i];
+  }
+  d.nbox = t.nbox;
+  for (int i = 0; i < t.nbox; ++i) {
+    d.box_ext[i] = t.box_ext[i];
+    d.order[i] = t.order[i];
+  }
+  return d;
+}
+
+VecDesc vec_affine(int64_t len, int64_t len_pad, int64_t stride) {
+  VecDesc d;
+  memset(&d, 0, sizeof(d));
+  d.mode = 1;
+  d.nq = 1;
+  d.q_len = len;
+  d.q_len_pad = len_pad;
+  d.len = len;
+  d.stride = stride;
+  return d;
+}
+
+int check_bundle(const stc_bundle &b, const char *name) {
+  if (b.nlab < 0 || b.nlab > STC_MAX_LABELS) return fail(STC_EINVAL, "bundle %s: label count %d out of range", name, b.nlab);
+  for (int d = 0; d < b.nlab; ++d)
+    if (b.ext[d] < 1) return fail(STC_EINVAL, "bundle %s: extents must be positive", name);
+  return STC_OK;
+}
+
+bool same_extents(const stc_bundle &x, const stc_bundle &y) {
+  if (x.nlab != y.nlab) return false;
+  for (int d = 0; d < x.nlab; ++d)
+    if (x.ext[d] != y.ext[d]) return false;
+  return true;
+}
+
+// ---------------------------------------------------------------- the plan
+struct Plan {
+  int level = 0, variant = 0;
+  uint32_t flags = 0;
+  int64_t m = 0, n = 0, k = 0;
+  int64_t mq = 0, nq = 0, kq = 0, mq_pad = 0, nq_pad = 0, kq_pad = 0;
+  int64_t Q = 1;  // quadrants per dimension
+  int nquads = 1;
+  int a_kfast = 0, b_kfast = 0;
+  std::vector<VecDesc> vecs;
+  int64_t pool_len = 0;
+  int64_t ar = 0, ac = 0, br = 0, bc = 0, cr = 0, cc = 0;  // pool starts
+  int64_t dxa = 0, dka = 0, dxb = 0, dkb = 0;              // Naive packed-operand vectors
+  std::vector<Term> terms;
+  // execution tables
+  std::vector<TermDesc> tdesc;  // ABC: exec order; AB/Naive: per batch-local slot (rebuilt per batch)
+  std::vector<OpDesc> ops;
+  std::vector<TgtDesc> tgts;
+  int batch = 1, nbatches = 1;
+  int grid = 1;
+  // workspace layout (bytes)
+  size_t off_pool = 0, off_vecs = 0, off_tab = 0, off_tickets = 0, off_counters = 0, off_M = 0, off_pa = 0,
+         off_pb = 0, off_acc = 0, total = 0;
+  size_t tab_bytes = 0, acc_bytes = 0;
+  int64_t ntickets = 0, ncounters = 0;
+  int64_t m_slot = 0, pa_slot = 0, pb_slot = 0;
+};
+
+int64_t cap_bytes() {
+  const char *e = getenv("STC_WORKSPACE_CAP_MB");
+  int64_t mb = e ? atoll(e) : 24 * 1024;
+  return mb * (int64_t)1024 * 1024;
+}
+
+// Reorder terms so that terms running concurrently (within `window`
+// consecutive terms) update disjoint C quadrants: fewer ticket waits.
+std::vector<int> exec_order(const std::vector<Term> &terms, int window) {
+  const int T = (int)terms.size();
+  std::vector<int> seq;
+  seq.reserve(T);
+  if (window <= 1) {
+    for (int i = 0; i < T; ++i) seq.push_back(i);
+    return seq;
+  }
+  std::vector<char> used(T, 0);
+  for (int step = 0; step < T; ++step) {
+    int best = -1;
+    long best_score = -1;
+    for (int cand = 0; cand < T; ++cand) {
+      if (used[cand]) continue;
+      long score = 0;  // higher = better: distance-weighted conflicts subtracted
+      for (int back = 1; back < window && back <= (int)seq.size(); ++back) {
+        const Term &prev = terms[seq[seq.size() - back]];
+        for (const Op &x : terms[cand].c)
+          for (const Op &y : prev.c)
+            if (x.q == y.q) score -= (long)(window - back) * 1000;
+      }
+      if (best < 0 || score > best_score) {
+        best = cand;
+        best_score = score;
+      }
+      if (score == 0) break;  // first conflict-free term in reference order
+    }
+    used[best] = 1;
+    seq.push_back(best);
+  }
+  return seq;
+}
+
+int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
+  if (!p) return fail(STC_EINVAL, "null problem");
+  const char *names[6] = {"a_row", "a_col", "b_row", "b_col", "c_row", "c_col"};
+  const stc_bundle *bs[6] = {&p->a_row, &p->a_col, &p->b_row, &p->b_col, &p->c_row, &p->c_col};
+  for (int i = 0; i < 6; ++i)
+    if (int rc = check_bundle(*bs[i], names[i])) return rc;
+  if (!same_extents(p->a_row, p->c_row)) return fail(STC_EINVAL, "I bundle extents of A and C differ");
+  if (!same_extents(p->a_col, p->b_row)) return fail(STC_EINVAL, "P bundle extents of A and B differ");
+  if (!same_extents(p->b_col, p->c_col)) return fail(STC_EINVAL, "J bundle extents of B and C differ");
+  if (p->level < 0) return fail(STC_EINVAL, "level must be non-negative, got %d", p->level);
+  if ((1 << p->level) > MAX_OPS)
+    return fail(STC_ECAP, "level %d exceeds the device cap of %d", p->level, 4);
+  if (p->variant < 0 || p->variant > 2) return fail(STC_EINVAL, "unknown variant %d", p->variant);
+  pl.level = p->level;
+  pl.variant = p->variant;
+  pl.flags = p->flags;
+  pl.m = bundle_len(p->a_row);
+  pl.k = bundle_len(p->a_col);
+  pl.n = bundle_len(p->b_col);
+  pl.Q = (int64_t)1 << pl.level;
+  pl.nquads = (int)(pl.Q * pl.Q);
+  pl.mq = cdiv(pl.m, pl.Q);
+  pl.nq = cdiv(pl.n, pl.Q);
+  pl.kq = cdiv(pl.k, pl.Q);
+  pl.mq_pad = rup(pl.mq, BM);
+  pl.nq_pad = rup(pl.nq, BN);
+  pl.kq_pad = rup(pl.kq, BK);
+
+  // tile orders per bundle (see make_tiling)
+  const bool ref = (p->flags & STC_FLAG_REFERENCE_TILING) != 0;
+  const int a_min = min_stride_side(p->a_row, p->a_col);
+  const int b_min = min_stride_side(p->b_row, p->b_col);
+  const int c_min = min_stride_side(p->c_row, p->c_col);
+  const int64_t *key_i = a_min == 0 ? p->a_row.str : (c_min == 0 ? p->c_row.str : p->a_row.str);
+  const int64_t *key_j = b_min == 1 ? p->b_col.str : (c_min == 1 ? p->c_col.str : p->b_col.str);
+  const int64_t *key_p = a_min == 1 ? p->a_col.str : (b_min == 0 ? p->b_row.str : p->a_col.str);
+  const Tiling ti = make_tiling(p->a_row, pl.level, key_i, ref);
+  const Tiling tj = make_tiling(p->b_col, pl.level, key_j, ref);
+  const Tiling tp = make_tiling(p->a_col, pl.level, key_p, ref);
+  pl.a_kfast = a_min == 1;
+  pl.b_kfast = b_min == 0;
+
+  // pool vectors (subsystem 1)
+  auto add = [&](VecDesc d) {
+    d.out_start = pl.pool_len;
+    pl.pool_len += d.nq * d.q_len_pad;
+    pl.vecs.push_back(d);
+    return d.out_start;
+  };
+  pl.ar = add(vec_bundle(p->a_row, 0, pl.Q, BM, ti));
+  pl.ac = add(vec_bundle(p->a_col, p->a_base, pl.Q, BK, tp));
+  pl.br = add(vec_bundle(p->b_row, 0, pl.Q, BK, tp));
+  pl.bc = add(vec_bundle(p->b_col, p->b_base, pl.Q, BN, tj));
+  pl.cr = add(vec_bundle(p->c_row, 0, pl.Q, BM, ti));
+  pl.cc = add(vec_bundle(p->c_col, p->c_base, pl.Q, BN, tj));
+  if (pl.variant == STC_VARIANT_NAIVE) {
+    // packed operand sums: Apack[k][x] (ld mq_pad), Bpack[k][x] (ld nq_pad)
+    pl.dxa = add(vec_affine(pl.mq_pad, pl.mq_pad, 1));
+    pl.dka = add(vec_affine(pl.kq_pad, pl.kq_pad, pl.mq_pad));
+    pl.dxb = add(vec_affine(pl.nq_pad, pl.nq_pad, 1));
+    pl.dkb = add(vec_affine(pl.kq_pad, pl.kq_pad, pl.nq_pad));
+  }
+
+  pl.terms = strassen_terms(pl.level);
+  const int T = (int)pl.terms.size();
+  const int64_t P = (pl.mq_pad / BM) * (pl.nq_pad / BN);
+  if (P * (int64_t)T > INT32_MAX) return fail(STC_EINVAL, "problem too large: %lld work items", (long long)(P * T));
+  pl.grid = grid_hint > 0 ? grid_hint : 148;
+
+  if (pl.variant == STC_VARIANT_ABC) {
+    const int window = (int)std::min<int64_t>(T, cdiv(pl.grid, P) + 1);
+    const std::vector<int> seq = exec_order(pl.terms, window);
+    std::vector<int> writers(pl.nquads, 0);
+    for (int t : seq) {
+      const Term &tm = pl.terms[t];
+      TermDesc d{};
+      d.a_first = (int)pl.ops.size();
+      d.a_count = (int)tm.a.size();
+      for (const Op &o : tm.a) {
+        int64_t r, c;
+        quad_rc(o.q, pl.level, r, c);
+        pl.ops.push_back({pl.ar + r * pl.mq_pad, pl.ac + c * pl.kq_pad, 0, (double)o.s});
+      }
+      d.b_first = (int)pl.ops.size();
+      d.b_count = (int)tm.b.size();
+      for (const Op &o : tm.b) {
+        int64_t r, c;
+        quad_rc(o.q, pl.level, r, c);
+        pl.ops.push_back({pl.bc + c * pl.nq_pad, pl.br + r * pl.kq_pad, 0, (double)o.s});
+      }
+      d.c_first = (int)pl.tgts.size();
+      d.c_count = (int)tm.c.size();
+      for (const Op &o : tm.c) {
+        int64_t r, c;
+        quad_rc(o.q, pl.level, r, c);
+        TgtDesc g{};
+        g.row_start = pl.cr + r * pl.mq_pad;
+        g.col_start = pl.cc + c * pl.nq_pad;
+        g.sign = (double)o.s;
+        g.ticket_base = (int32_t)(o.q * P);
+        g.order = writers[o.q]++;
+        pl.tgts.push_back(g);
+      }
+      d.m_slot = t;
+      pl.tdesc.push_back(d);
+    }
+    pl.ntickets = (int64_t)pl.nquads * P;
+    pl.batch = T;
+    pl.nbatches = 1;
+    pl.ncounters = 1;
+  } else {
+    // dense M slots (and packed operands for Naive), batched under the cap
+    const int64_t m_bytes = pl.mq_pad * pl.nq_pad * 8;
+    const int64_t pa_bytes = pl.variant == STC_VARIANT_NAIVE ? pl.kq_pad * pl.mq_pad * 8 : 0;
+    const int64_t pb_bytes = pl.variant == STC_VARIANT_NAIVE ? pl.kq_pad * pl.nq_pad * 8 : 0;
+    const int64_t per = m_bytes + pa_bytes + pb_bytes;
+    int64_t b = cap_bytes() / std::max<int64_t>(per, 1);
+    if (b < 1) b = 1;
+    if (b > T) b = T;
+    pl.batch = (int)b;
+    pl.nbatches = (int)cdiv(T, b);
+    pl.ncounters = pl.nbatches;
+    pl.m_slot = pl.mq_pad * pl.nq_pad;
+    pl.pa_slot = pl.kq_pad * pl.mq_pad;
+    pl.pb_slot = pl.kq_pad * pl.nq_pad;
+  }
+
+  // workspace layout
+  size_t off = 0;
+  pl.off_pool = off;
+  off = align256(off + (size_t)pl.pool_len * 8);
+  pl.off_vecs = off;
+  off = align256(off + pl.vecs.size() * sizeof(VecDesc));
+  pl.off_tab = off;
+  if (pl.variant == STC_VARIANT_ABC) {
+    pl.tab_bytes = pl.tdesc.size() * sizeof(TermDesc) + pl.ops.size() * sizeof(OpDesc) + pl.tgts.size() * sizeof(TgtDesc);
+  } else {
+    // per batch: TermDesc[batch] + OpDesc (<= 2*Q per side per term) + accumulate lists
+    const size_t ops_max = (size_t)pl.batch * 2 * (size_t)(pl.Q * 2 + 2);
+    pl.tab_bytes = (size_t)pl.batch * sizeof(TermDesc) * 3 + ops_max * sizeof(OpDesc);
+    pl.acc_bytes = align256((size_t)(pl.nquads + 1) * 4) + align256((size_t)pl.batch * pl.nquads * 4) +
+                   align256((size_t)pl.batch * pl.nquads * 8) + 2 * align256((size_t)pl.nquads * 8);
+  }
+  off = align256(off + pl.tab_bytes * (pl.variant == STC_VARIANT_ABC ? 1 : pl.nbatches));
+  pl.off_acc = off;
+  off = align256(off + pl.acc_bytes * (pl.variant == STC_VARIANT_ABC ? 0 : pl.nbatches));
+  pl.off_tickets = off;
+  off = align256(off + (size_t)pl.ntickets * 4);
+  pl.off_counters = off;
+  off = align256(off + (size_t)pl.ncounters * 4);
+  pl.off_M = off;
+  if (pl.variant != STC_VARIANT_ABC) off = align256(off + (size_t)pl.batch * pl.m_slot * 8);
+  pl.off_pa = off;
+  if (pl.variant == STC_VARIANT_NAIVE) off = align256(off + (size_t)pl.batch * pl.pa_slot * 8);
+  pl.off_pb = off;
+  if (pl.variant == STC_VARIANT_NAIVE) off = align256(off + (size_t)pl.batch * pl.pb_slot * 8);
+  pl.total = off;
+  return STC_OK;
+}
+
+}  // namespace
+
+// ======================================================================== ABI
+extern "C" {
+
+const char *stc_last_error(void) { return g_err.c_str(); }
+int stc_abi_version(void) { return STC_ABI_VERSION; }
+
+int stc_workspace_size(const stc_problem *p, size_t *bytes) {
+  Plan pl;
+  if (int rc = build_plan(p, pl, 0)) return rc;
+  if (bytes) *bytes = pl.total;
+  return STC_OK;
+}
+
+int stc_contract(const stc_problem *p, const double *A, const double *B, double *C, void *workspace,
+                 size_t workspace_bytes, void *stream, stc_stats *stats) {
+  Plan pl;
+  const int grid_hint = gemm_max_grid(MAX_OPS);
+  if (grid_hint <= 0) return fail(STC_ECUDA, "could not size the DMMA grid");
+  if (int rc = build_plan(p, pl, grid_hint)) return rc;
+  if (!A || !B || !C) return fail(STC_EINVAL, "null operand pointer");
+  if (!workspace || workspace_bytes < pl.total)
+    return fail(STC_EWORKSPACE, "workspace too small: need %zu bytes, got %zu", pl.total, workspace_bytes);
+  if (reinterpret_cast<uintptr_t>(workspace) & 255) return fail(STC_EINVAL, "workspace must be 256-byte aligned");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char *ws = reinterpret_cast<char *>(workspace);
+  int64_t *pool = reinterpret_cast<int64_t *>(ws + pl.off_pool);
+  int64_t launches = 0;
+  stc_stats st{};
+
+  // subsystem (1): scatter vectors on the device
+  if (int rc = upload(pl.vecs.data(), pl.vecs.size() * sizeof(VecDesc), ws + pl.off_vecs, s)) return rc;
+  CU(launch_build_pool(reinterpret_cast<VecDesc *>(ws + pl.off_vecs), (int)pl.vecs.size(), pl.pool_len, pool, s),
+     "k_build_pool");
+  ++launches;
+  // tickets + work counters
+  CU(cudaMemsetAsync(ws + pl.off_tickets, 0, pl.off_M - pl.off_tickets, s), "cudaMemsetAsync");
+  int32_t *tickets = reinterpret_cast<int32_t *>(ws + pl.off_tickets);
+  int32_t *counters = reinterpret_cast<int32_t *>(ws + pl.off_counters);
+  const int tiles_m = (int)(pl.mq_pad / BM), tiles_n = (int)(pl.nq_pad / BN);
+  const int64_t P = (int64_t)tiles_m * tiles_n;
+  const int T = (int)pl.terms.size();
+
+  GemmArgs g{};
+  g.pool = pool;
+  g.tiles_m = tiles_m;
+  g.tiles_n = tiles_n;
+  g.kchunks = (int)(pl.kq_pad / BK);
+  g.group_m = 8;
+  g.max_ops = MAX_OPS;
+  g.tickets = tickets;
+
+  if (pl.variant == STC_VARIANT_ABC) {
+    char *tab = ws + pl.off_tab;
+    std::vector<char> host(pl.tab_bytes);
+    size_t o = 0;
+    memcpy(host.data() + o, pl.tdesc.data(), pl.tdesc.size() * sizeof(TermDesc));
+    g.terms = reinterpret_cast<const TermDesc *>(tab + o);
+    o += pl.tdesc.size() * sizeof(TermDesc);
+    memcpy(host.data() + o, pl.ops.data(), pl.ops.size() * sizeof(OpDesc));
+    g.ops = reinterpret_cast<const OpDesc *>(tab + o);
+    o += pl.ops.size() * sizeof(OpDesc);
+    memcpy(host.data() + o, pl.tgts.data(), pl.tgts.size() * sizeof(TgtDesc));
+    g.tgts = reinterpret_cast<const TgtDesc *>(tab + o);
+    if (int rc = upload(host.data(), host.size(), tab, s)) return rc;
+    g.A = A;
+    g.B = B;
+    g.C = C;
+    g.nterms = T;
+    g.total_items = (int)(P * T);
+    g.a_kfast = pl.a_kfast;
+    g.b_kfast = pl.b_kfast;
+    g.dense_out = 0;
+    g.use_tickets = T > 1;
+    g.counter = counters;
+    const int grid = (int)std::min<int64_t>(pl.grid, g.total_items);
+    CU(launch_gemm(g, grid, s), "k_strassen_gemm");
+    ++launches;
+    st.fast_updates = 0;
+    st.slow_updates = (int64_t)P * (int64_t)pl.tgts.size();
+  } else {
+    const bool naive = pl.variant == STC_VARIANT_NAIVE;
+    double *M = reinterpret_cast<double *>(ws + pl.off_M);
+    double *PA = reinterpret_cast<double *>(ws + pl.off_pa);
+    double *PB = reinterpret_cast<double *>(ws + pl.off_pb);
+    for (int bi = 0; bi < pl.nbatches; ++bi) {
+      const int t0 = bi * pl.batch, t1 = std::min(T, t0 + pl.batch);
+      const int nb = t1 - t0;
+      // tables for this batch: gemm terms, unpack-A terms, unpack-B terms, ops
+      std::vector<TermDesc> gterms(nb), uA(nb), uB(nb);
+      std::vector<OpDesc> ops;
+      for (int t = t0; t < t1; ++t) {
+        const Term &tm = pl.terms[t];
+        const int slot = t - t0;
+        TermDesc ua{}, ub{}, gd{};
+        ua.a_first = (int)ops.size();
+        ua.a_count = (int)tm.a.size();
+        for (const Op &op : tm.a) {
+          int64_t r, c;
+          quad_rc(op.q, pl.level, r, c);
+          ops.push_back({pl.ar + r * pl.mq_pad, pl.ac + c * pl.kq_pad, 0, (double)op.s});
+        }
+        ub.a_first = (int)ops.size();
+        ub.a_count = (int)tm.b.size();
+        for (const Op &op : tm.b) {
+          int64_t r, c;
+          quad_rc(op.q, pl.level, r, c);
+          ops.push_back({pl.bc + c * pl.nq_pad, pl.br + r * pl.kq_pad, 0, (double)op.s});
+        }
+        ua.m_slot = ub.m_slot = gd.m_slot = slot;
+        if (naive) {
+          gd.a_first = (int)ops.size();
+          gd.a_count = 1;
+          ops.push_back({pl.dxa, pl.dka, slot * pl.pa_slot, 1.0});
+          gd.b_first = (int)ops.size();
+          gd.b_count = 1;
+          ops.push_back({pl.dxb, pl.dkb, slot * pl.pb_slot, 1.0});
+        } else {
+          gd.a_first = ua.a_first;
+          gd.a_count = ua.a_count;
+          gd.b_first = ub.a_first;
+          gd.b_count = ub.a_count;
+        }
+        gterms[slot] = gd;
+        uA[slot] = ua;
+        uB[slot] = ub;
+      }
+      // accumulate lists: per quadrant, (slot, sign) in term order
+      std::vector<int32_t> lstart(pl.nquads + 1, 0), lslot;
+      std::vector<double> lsign;
+      std::vector<int64_t> rstart(pl.nquads), cstart(pl.nquads);
+      for (int q = 0; q < pl.nquads; ++q) {
+        lstart[q] = (int32_t)lslot.size();
+        for (int t = t0; t < t1; ++t)
+          for (const Op &op : pl.terms[t].c)
+            if (op.q == q) {
+              lslot.push_back(t - t0);
+              lsign.push_back((double)op.s);
+            }
+        int64_t r, c;
+        quad_rc(q, pl.level, r, c);
+        rstart[q] = pl.cr + r * pl.mq_pad;
+        cstart[q] = pl.cc + c * pl.nq_pad;
+      }
+      lstart[pl.nquads] = (int32_t)lslot.size();
+      // upload (one staging copy per table region)
+      char *tab = ws + pl.off_tab + (size_t)bi * pl.tab_bytes;
+      std::vector<char> host(pl.tab_bytes, 0);
+      size_t o = 0;
+      auto put = [&](const void *src, size_t bytes) {
+        memcpy(host.data() + o, src, bytes);
+        const size_t at = o;
+        o += bytes;
+        return tab + at;
+      };
+      const TermDesc *d_g = reinterpret_cast<const TermDesc *>(put(gterms.data(), nb * sizeof(TermDesc)));
+      const TermDesc *d_ua = reinterpret_cast<const TermDesc *>(put(uA.data(), nb * sizeof(TermDesc)));
+      const TermDesc *d_ub = reinterpret_cast<const TermDesc *>(put(uB.data(), nb * sizeof(TermDesc)));
+      const OpDesc *d_ops = reinterpret_cast<const OpDesc *>(put(ops.data(), ops.size() * sizeof(OpDesc)));
+      if (o > pl.tab_bytes) return fail(STC_EINVAL, "internal: table overflow");
+      if (int rc = upload(host.data(), o, tab, s)) return rc;
+      char *acc = ws + pl.off_acc + (size_t)bi * pl.acc_bytes;
+      std::vector<char> hacc(pl.acc_bytes, 0);
+      size_t ao = 0;
+      auto aput = [&](const void *src, size_t bytes, size_t slot_bytes) {
+        memcpy(hacc.data() + ao, src, bytes);
+        const size_t at = ao;
+        ao += align256(slot_bytes);
+        return acc + at;
+      };
+      AccArgs aa{};
+      aa.list_start = reinterpret_cast<const int32_t *>(aput(lstart.data(), lstart.size() * 4, (pl.nquads + 1) * 4));
+      aa.list_slot = reinterpret_cast<const int32_t *>(
+          aput(lslot.data(), lslot.size() * 4, (size_t)pl.batch * pl.nquads * 4));
+      aa.list_sign = reinterpret_cast<const double *>(
+          aput(lsign.data(), lsign.size() * 8, (size_t)pl.batch * pl.nquads * 8));
+      aa.row_start = reinterpret_cast<const int64_t *>(aput(rstart.data(), rstart.size() * 8, pl.nquads * 8));
+      aa.col_start = reinterpret_cast<const int64_t *>(aput(cstart.data(), cstart.size() * 8, pl.nquads * 8));
+      if (int rc = upload(hacc.data(), pl.acc_bytes, acc, s)) return rc;
+
+      if (naive) {
+        UnpackArgs ua{};
+        ua.pool = pool;
+        ua.ops = d_ops;
+        ua.nterms = nb;
+        ua.D = A;
+        ua.out = PA;
+        ua.terms = d_ua;
+        ua.x_len = pl.mq_pad;
+        ua.k_len = pl.kq_pad;
+        ua.slot_stride = pl.pa_slot;
+        CU(launch_unpack(ua, s), "k_unpack(A)");
+        ua.D = B;
+        ua.out = PB;
+        ua.terms = d_ub;
+        ua.x_len = pl.nq_pad;
+        ua.slot_stride = pl.pb_slot;
+        CU(launch_unpack(ua, s), "k_unpack(B)");
+        launches += 2;
+        st.slow_blocks += 2 * nb;
+      }
+      g.A = naive ? PA : A;
+      g.B = naive ? PB : B;
+      g.C = nullptr;
+      g.terms = d_g;
+      g.ops = d_ops;
+      g.tgts = nullptr;
+      g.nterms = nb;
+      g.total_items = (int)(P * nb);
+      g.a_kfast = naive ? 0 : pl.a_kfast;
+      g.b_kfast = naive ? 0 : pl.b_kfast;
+      g.dense_out = 1;
+      g.use_tickets = 0;
+      g.M = M;
+      g.m_ld = pl.nq_pad;
+      g.m_stride = pl.m_slot;
+      g.counter = counters + bi;
+      const int grid = (int)std::min<int64_t>(pl.grid, g.total_items);
+      CU(launch_gemm(g, grid, s), "k_strassen_gemm(dense)");
+      aa.M = M;
+      aa.m_ld = pl.nq_pad;
+      aa.m_stride = pl.m_slot;
+      aa.C = C;
+      aa.pool = pool;
+      aa.mq = pl.mq;
+      aa.nq = pl.nq;
+      aa.nquads = pl.nquads;
+      CU(launch_accumulate(aa, s), "k_accumulate");
+      launches += 2;
+      st.slow_updates += (int64_t)lslot.size();
+    }
+  }
+  st.total_flops = 2.0 * BM * BN * (double)pl.kq_pad * (double)P * (double)T;
+  st.slow_blocks += 2 * (int64_t)(pl.kq_pad / BK) * P * T;
+  st.leaf_multiplies = T;
+  st.work_items = P * T;
+  st.kernel_launches = launches;
+  if (stats) *stats = st;
+  return STC_OK;
+}
+
+int stc_bundle_scatter(const stc_bundle *bundle, int64_t base, int64_t out_len, int64_t *out, void *stream) {
+  if (!bundle || !out) return fail(STC_EINVAL, "null argument");
+  if (int rc = check_bundle(*bundle, "bundle")) return rc;
+  const int64_t len = bundle_len(*bundle);
+  if (out_len < len) return fail(STC_EINVAL, "out_len %lld shorter than the bundle (%lld)", (long long)out_len, (long long)len);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Tiling none;
+  VecDesc d = vec_bundle(*bundle, base, 1, 1, none);
+  d.q_len = out_len;  // entries beyond len read PAD
+  d.q_len_pad = out_len;
+  d.out_start = 0;
+  VecDesc *dd = nullptr;
+  CU(cudaMallocAsync(reinterpret_cast<void **>(&dd), sizeof(VecDesc), s), "cudaMallocAsync");
+  if (int rc = upload(&d, sizeof(d), dd, s)) return rc;
+  CU(launch_build_pool(dd, 1, out_len, out, s), "k_build_pool");
+  CU(cudaFreeAsync(dd, s), "cudaFreeAsync");
+  return STC_OK;
+}
+
+int stc_block_vector(const int64_t *scat, int64_t len, int64_t blk, int64_t unit_stride, int64_t *out,
+                     void *stream) {
+  if (blk < 1) return fail(STC_EINVAL, "block sizes must be >= 1");
+  if (len < 0 || (len > 0 && (!scat || !out))) return fail(STC_EINVAL, "bad scatter vector");
+  CU(launch_block_vector(scat, len, blk, unit_stride, out, reinterpret_cast<cudaStream_t>(stream)), "k_block_vector");
+  return STC_OK;
+}
+
+int stc_fused_term_workspace_size(int64_t m, int64_t n, int64_t k, int n_a, int n_b, int n_c, size_t *bytes) {
+  if (m < 1 || n < 1 || k < 1) return fail(STC_EINVAL, "empty fused term %lldx%lldx%lld", (long long)m, (long long)n, (long long)k);
+  if (n_a < 1 || n_b < 1 || n_c < 1 || n_a > MAX_OPS || n_b > MAX_OPS || n_c > MAX_OPS)
+    return fail(STC_EINVAL, "need 1..%d views per side", MAX_OPS);
+  const int64_t mp = rup(m, BM), np = rup(n, BN), kp = rup(k, BK);
+  size_t pool = (size_t)(n_a * (mp + kp) + n_b * (np + kp) + n_c * (mp + np)) * 8;
+  size_t tab = sizeof(TermDesc) + (size_t)(n_a + n_b) * sizeof(OpDesc) + (size_t)n_c * sizeof(TgtDesc);
+  if (bytes) *bytes = align256(pool) + align256(tab) + 256;
+  return STC_OK;
+}
+
+int stc_fused_term(int64_t m, int64_t n, int64_t k, const double *A, int n_a, const int64_t *const *a_rows,
+                   const int64_t *const *a_cols, const double *a_coeffs, const double *B, int n_b,
+                   const int64_t *const *b_rows, const int64_t *const *b_cols, const double *b_coeffs, double *C,
+                   int n_c, const int64_t *const *c_rows, const int64_t *const *c_cols, const double *c_coeffs,
+                   uint32_t flags, void *workspace, size_t workspace_bytes, void *stream, stc_stats *stats) {
+  size_t need = 0;
+  if (int rc = stc_fused_term_workspace_size(m, n, k, n_a, n_b, n_c, &need)) return rc;
+  if (!workspace || workspace_bytes < need)
+    return fail(STC_EWORKSPACE, "workspace too small: need %zu bytes, got %zu", need, workspace_bytes);
+  for (int i = 0; i < n_a; ++i)
+    if (a_coeffs[i] != 1.0 && a_coeffs[i] != -1.0) return fail(STC_EINVAL, "coefficients must be +/-1");
+  for (int i = 0; i < n_b; ++i)
+    if (b_coeffs[i] != 1.0 && b_coeffs[i] != -1.0) return fail(STC_EINVAL, "coefficients must be +/-1");
+  for (int i = 0; i < n_c; ++i)
+    if (c_coeffs[i] != 1.0 && c_coeffs[i] != -1.0) return fail(STC_EINVAL, "coefficients must be +/-1");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char *ws = reinterpret_cast<char *>(workspace);
+  int64_t *pool = reinterpret_cast<int64_t *>(ws);
+  const int64_t mp = rup(m, BM), np = rup(n, BN), kp = rup(k, BK);
+  int64_t at = 0;
+  std::vector<OpDesc> ops;
+  std::vector<TgtDesc> tg;
+  auto put = [&](const int64_t *src, int64_t len, int64_t lenp) {
+    const int64_t start = at;
+    at += lenp;
+    return std::make_pair(start, launch_copy_pad(src, len, lenp, pool + start, s));
+  };
+  for (int i = 0; i < n_a; ++i) {
+    auto x = put(a_rows[i], m, mp), kk = put(a_cols[i], k, kp);
+    CU(x.second, "copy_pad");
+    CU(kk.second, "copy_pad");
+    ops.push_back({x.first, kk.first, 0, a_coeffs[i]});
+  }
+  for (int i = 0; i < n_b; ++i) {
+    auto x = put(b_cols[i], n, np), kk = put(b_rows[i], k, kp);
+    CU(x.second, "copy_pad");
+    CU(kk.second, "copy_pad");
+    ops.push_back({x.first, kk.first, 0, b_coeffs[i]});
+  }
+  for (int i = 0; i < n_c; ++i) {
+    auto r = put(c_rows[i], m, mp), c = put(c_cols[i], n, np);
+    CU(r.second, "copy_pad");
+    CU(c.second, "copy_pad");
+    TgtDesc t{};
+    t.row_start = r.first;
+    t.col_start = c.first;
+    t.sign = c_coeffs[i];
+    tg.push_back(t);
+  }
+  TermDesc td{};
+  td.a_first = 0;
+  td.a_count = n_a;
+  td.b_first = n_a;
+  td.b_count = n_b;
+  td.c_first = 0;
+  td.c_count = n_c;
+  char *tab = ws + align256((size_t)at * 8);
+  std::vector<char> host(sizeof(TermDesc) + ops.size() * sizeof(OpDesc) + tg.size() * sizeof(TgtDesc) + 8);
+  size_t o = 0;
+  memcpy(host.data() + o, &td, sizeof(td));
+  o += sizeof(td);
+  memcpy(host.data() + o, ops.data(), ops.size() * sizeof(OpDesc));
+  o += ops.size() * sizeof(OpDesc);
+  memcpy(host.data() + o, tg.data(), tg.size() * sizeof(TgtDesc));
+  o += tg.size() * sizeof(TgtDesc);
+  // counter lives after the tables
+  char *ctr = ws + align256((size_t)at * 8) + align256(o);
+  if (ctr + 4 > ws + workspace_bytes) return fail(STC_EWORKSPACE, "workspace too small for counters");
+  if (int rc = upload(host.data(), o, tab, s)) return rc;
+  CU(cudaMemsetAsync(ctr, 0, 4, s), "cudaMemsetAsync");
+  GemmArgs g{};
+  g.A = A;
+  g.B = B;
+  g.C = C;
+  g.pool = pool;
+  g.terms = reinterpret_cast<const TermDesc *>(tab);
+  g.ops = reinterpret_cast<const OpDesc *>(tab + sizeof(TermDesc));
+  g.tgts = reinterpret_cast<const TgtDesc *>(tab + sizeof(TermDesc) + ops.size() * sizeof(OpDesc));
+  g.nterms = 1;
+  g.tiles_m = (int)(mp / BM);
+  g.tiles_n = (int)(np / BN);
+  g.kchunks = (int)(kp / BK);
+  g.total_items = g.tiles_m * g.tiles_n;
+  g.a_kfast = 0;
+  g.b_kfast = 0;
+  g.dense_out = 0;
+  g.use_tickets = 0;
+  g.group_m = 8;
+  g.max_ops = MAX_OPS;
+  g.counter = reinterpret_cast<int32_t *>(ctr);
+  const int grid = std::min(gemm_max_grid(MAX_OPS), g.total_items);
+  CU(launch_gemm(g, grid, s), "k_strassen_gemm(fused_term)");
+  if (stats) {
+    stc_stats st{};
+    st.total_flops = 2.0 * BM * BN * (double)kp * (double)g.total_items;
+    st.slow_blocks = 2 * (int64_t)g.kchunks * g.total_items;
+    st.slow_updates = (int64_t)g.total_items * n_c;
+    st.leaf_multiplies = 1;
+    st.work_items = g.total_items;
+    st.kernel_launches = 1 + 3 * (n_a + n_b + n_c);
+    *stats = st;
+  }
+  (void)flags;
+  return STC_OK;
+}
+
+int stc_accumulate_dense(const double *M, int64_t ldm, int64_t m, int64_t n, double *C, const int64_t *rows,
+                         const int64_t *cols, double coeff, void *stream, stc_stats *stats) {
+  if (m < 0 || n < 0 || ldm < m) return fail(STC_EINVAL, "matrix shape (%lld, %lld) / ld %lld invalid", (long long)m, (long long)n, (long long)ldm);
+  CU(launch_accum_dense_single(M, ldm, m, n, C, rows, cols, coeff, reinterpret_cast<cudaStream_t>(stream)),
+     "k_accum_dense_single");
+  if (stats) {
+    stc_stats st{};
+    st.slow_updates = 1;
+    st.kernel_launches = 1;
+    *stats = st;
+  }
+  return STC_OK;
+}
+
+int stc_unpack_sum(double *out, int64_t ldo, int64_t m, int64_t n, const double *data, int nviews,
+                   const int64_t *const *rows, const int64_t *const *cols, const double *coeffs, void *stream,
+                   stc_stats *stats) {
+  if (nviews < 1 || nviews > MAX_OPS) return fail(STC_EINVAL, "need 1..%d views", MAX_OPS);
+  if (m < 0 || n < 0 || ldo < m) return fail(STC_EINVAL, "out must be a float64 %lldx%lld matrix", (long long)m, (long long)n);
+  ViewSet vs{};
+  vs.n = nviews;
+  for (int i = 0; i < nviews; ++i) {
+    vs.rows[i] = rows[i];
+    vs.cols[i] = cols[i];
+    vs.coeff[i] = coeffs[i];
+  }
+  CU(launch_unpack_views(out, ldo, m, n, data, vs, reinterpret_cast<cudaStream_t>(stream)), "k_unpack_views");
+  if (stats) {
+    stc_stats st{};
+    st.slow_blocks = 1;
+    st.kernel_launches = 1;
+    *stats = st;
+  }
+  return STC_OK;
+}
+
+int stc_sq_norms(int ndim, const int64_t *extents, const double *x, const int64_t *x_strides, int64_t x_base,
+                 const double *ref, const int64_t *ref_strides, int64_t ref_base, double *out, void *stream) {
+  if (ndim < 0 || ndim > STC_MAX_LABELS) return fail(STC_EINVAL, "bad rank %d", ndim);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int nblocks = 148 * 4;
+  double *part = nullptr;
+  CU(cudaMallocAsync(reinterpret_cast<void **>(&part), sizeof(double) * 2 * nblocks, s), "cudaMallocAsync");
+  CU(launch_sq_norms(ndim, extents, x, x_strides, x_base, ref, ref_strides, ref_base, part, nblocks, s), "k_sq_norms");
+  std::vector<double> h(2 * nblocks);
+  CU(cudaMemcpyAsync(h.data(), part, sizeof(double) * 2 * nblocks, cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
+  CU(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  CU(cudaFreeAsync(part, s), "cudaFreeAsync");
+  double a = 0.0, b = 0.0;
+  for (int i = 0; i < nblocks; ++i) {
+    a += h[2 * i];
+    b += h[2 * i + 1];
+  }
+  out[0] = a;
+  out[1] = b;
+  return STC_OK;
+}
+
+}  // extern "C"

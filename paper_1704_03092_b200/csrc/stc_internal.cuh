@@ -1,0 +1,141 @@
+// stc_internal.cuh -- device-side data structures shared by the kernels and
+// the host planner (stc_capi.cu).  See DESIGN.md for the HBM layout.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/stc_b200.h"
+
+namespace stc {
+
+constexpr int64_t kPad = INT64_MIN;  // scatter.py:23
+
+// ---- tile geometry of the fused DMMA kernel -------------------------------
+constexpr int BM = 128;              // CTA tile rows   (I bundle)
+constexpr int BN = 128;              // CTA tile cols   (J bundle)
+constexpr int BK = 16;               // k-chunk per pipeline stage (P bundle)
+constexpr int LDS = 132;             // smem row stride in doubles (== 4 mod 16: conflict-free fragments)
+constexpr int STAGES = 4;            // smem ring depth
+constexpr int CONSUMER_WARPS = 8;    // 2 x 4 warps, 64 x 32 warp tiles of m16n8k4 DMMA
+constexpr int PRODUCER_WARPS = 4;    // gather + Strassen operand sums into smem
+constexpr int THREADS = 32 * (CONSUMER_WARPS + PRODUCER_WARPS);
+// Register split via setmaxnreg (launch: 65536 / 384 -> 168 per thread):
+// 256 consumer threads x 192 + 128 producer threads x 120 = 64512.
+constexpr int CONSUMER_REGS = 192;
+constexpr int PRODUCER_REGS = 120;
+constexpr int MAX_OPS = 16;          // views per operand side (2^L, L <= 4)
+
+// One operand view of a term side.  For the A side the tile-fixed dimension x
+// is rows (I) and k is columns (P); for the B side x is columns (J) and k rows.
+struct OpDesc {
+  int64_t x_start;   // pool index of this view's x vector (per-quadrant, tile padded)
+  int64_t k_start;   // pool index of this view's k vector
+  int64_t data_off;  // element offset added to the side's data pointer
+  double sign;       // +/-1
+};
+
+// One C target (c_op) of a term.
+struct TgtDesc {
+  int64_t row_start;    // pool index of the target's row vector (I)
+  int64_t col_start;    // pool index of the target's column vector (J)
+  double sign;
+  int32_t ticket_base;  // tickets[ticket_base + tile position]
+  int32_t order;        // number of earlier writers of this quadrant (execution order)
+};
+
+struct TermDesc {
+  int32_t a_first, a_count, b_first, b_count, c_first, c_count;
+  int32_t m_slot;  // dense-out slot (AB / Naive) of this term
+  int32_t _pad;
+};
+
+struct GemmArgs {
+  const double *A;
+  const double *B;
+  double *C;
+  const int64_t *pool;
+  const TermDesc *terms;
+  const OpDesc *ops;
+  const TgtDesc *tgts;
+  int32_t nterms, tiles_m, tiles_n, kchunks;
+  int32_t total_items;
+  int32_t a_kfast, b_kfast;  // producer thread mapping per side (1: k contiguous)
+  int32_t dense_out;         // 1: write M_slot densely instead of C targets
+  int32_t use_tickets;       // serialise C-tile updates across terms
+  int32_t group_m;           // tile rasterisation group
+  int32_t max_ops;           // op-table capacity in smem (per side)
+  int32_t force_slow;        // reference force_slow: always take the PAD-checking gather
+  double *M;                 // dense out: M + slot*m_stride + row*m_ld + col
+  int64_t m_ld, m_stride;
+  int32_t *tickets;
+  int32_t *counter;
+};
+
+// Descriptor of one pool vector built on the device (subsystem 1).
+// mode 0: bundle scatter in the reference linearisation (first label fastest),
+//         split into nq quadrants of q_len entries (PAD beyond len), each
+//         re-ordered by the box permutation and padded to q_len_pad with PAD.
+// mode 1: affine  out[i] = i * stride for i < q_len, PAD up to q_len_pad (nq = 1).
+struct VecDesc {
+  int64_t out_start;
+  int64_t nq, q_len, q_len_pad, len, base, stride;
+  int32_t mode, nlab, nbox, _pad;
+  int64_t ext[STC_MAX_LABELS];
+  int64_t str[STC_MAX_LABELS];
+  int64_t box_ext[STC_MAX_LABELS];  // quadrant box, reference order (fastest first)
+  int32_t order[STC_MAX_LABELS];    // tile order of the box dims (order[0] fastest)
+};
+
+// AB / Naive accumulate: C_q += sum over the quadrant's terms of sign * M_slot.
+struct AccArgs {
+  const double *M;
+  int64_t m_ld, m_stride;
+  double *C;
+  const int64_t *pool;
+  int64_t mq, nq;              // valid (unpadded) quadrant extents
+  int32_t nquads, _pad;
+  const int32_t *list_start;   // [nquads + 1]
+  const int32_t *list_slot;    // M slots in term order
+  const double *list_sign;
+  const int64_t *row_start;    // [nquads] pool index of C row vector
+  const int64_t *col_start;    // [nquads] pool index of C col vector
+};
+
+// Naive: dense operand sums, out_slot[k * ld + x] = sum_op sign * D[x_vec[x] + k_vec[k]].
+struct UnpackArgs {
+  const double *D;
+  double *out;
+  const int64_t *pool;
+  const TermDesc *terms;  // uses (a_first, a_count) as the side's op range
+  const OpDesc *ops;
+  int32_t nterms, _pad;
+  int64_t x_len, k_len;   // padded extents (ld = x_len)
+  int64_t slot_stride;
+};
+
+// ---- launchers (stc_kernels.cu) -------------------------------------------
+cudaError_t launch_build_pool(const VecDesc *d_descs, int ndesc, int64_t total, int64_t *pool, cudaStream_t s);
+cudaError_t launch_block_vector(const int64_t *scat, int64_t len, int64_t blk, int64_t unit, int64_t *out,
+                                cudaStream_t s);
+cudaError_t launch_copy_pad(const int64_t *in, int64_t len, int64_t len_pad, int64_t *out, cudaStream_t s);
+size_t gemm_smem_bytes(int max_ops);
+cudaError_t launch_gemm(const GemmArgs &a, int grid, cudaStream_t s);
+int gemm_max_grid(int max_ops);
+cudaError_t launch_accumulate(const AccArgs &a, cudaStream_t s);
+cudaError_t launch_unpack(const UnpackArgs &a, cudaStream_t s);
+cudaError_t launch_accum_dense_single(const double *M, int64_t ldm, int64_t m, int64_t n, double *C,
+                                      const int64_t *rows, const int64_t *cols, double coeff, cudaStream_t s);
+struct ViewSet {
+  const int64_t *rows[MAX_OPS];
+  const int64_t *cols[MAX_OPS];
+  double coeff[MAX_OPS];
+  int n;
+};
+cudaError_t launch_unpack_views(double *out, int64_t ldo, int64_t m, int64_t n, const double *data,
+                                const ViewSet &vs, cudaStream_t s);
+cudaError_t launch_sq_norms(int ndim, const int64_t *ext, const double *x, const int64_t *xs, int64_t xb,
+                            const double *r, const int64_t *rs, int64_t rb, double *partials, int nblocks,
+                            cudaStream_t s);
+
+}  // namespace stc

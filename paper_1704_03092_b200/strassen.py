@@ -1,0 +1,202 @@
+"""The drop-in entry point: Strassen tensor contraction on the B200.
+
+``contract(spec, a, b, c, level, variant, ...) -> RunStats`` keeps the
+signature, argument meaning and error behaviour of the reference's
+``strassen_tc.contract`` (/root/reference/pkg/src/strassen_tc/strassen.py:141-207):
+
+* C += A.B over the bundles of ``spec`` with an L-level Strassen recursion
+  (7^L leaf products over 4^L quadrants, PAD-padded to a multiple of 2^L);
+* variants ABC (operand sums fused into the DMMA kernel's staging, +/-M fused
+  into its epilogue), AB (dense M per term, then accumulate) and NAIVE (dense
+  operand sums, dense GEMM, accumulate) -- strassen.py:173-203;
+* ``ValueError`` before C is touched for bad extents ("extents") or levels
+  above the cap ("cap"), strassen.py:130-134 / 80-81.
+
+Operands may be reference-style ``DenseTensor`` objects with host (numpy)
+storage -- staged through HBM, C copied back -- or HBM-resident: strided
+float64 CUDA ``torch.Tensor`` or ``DenseTensor`` with CUDA storage.  The work
+itself always runs in ``libstc_b200.so`` (C ABI, include/stc_b200.h); there is
+no CPU path.  ``params`` (CPU blocking) and ``threads`` are accepted and
+ignored: the GPU tiling is fixed (views.TILE).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from enum import Enum
+
+from . import _lib
+from .stats import RunStats, effective_gflops
+from .tensor import ContractionSpec, DenseTensor
+from .views import DEFAULT_BLOCKING, BlockingParams, check_c_targets, make_view, quadrant_views
+
+__all__ = ["MAX_LEVEL", "DEVICE_MAX_LEVEL", "StrassenTerm", "Variant", "contract", "strassen_terms",
+           "problem_of", "quadrant_rc"]
+
+MAX_LEVEL = 2          # reference cap without allow_deep (strassen.py:38)
+DEVICE_MAX_LEVEL = 4   # 2^L views per side must fit the kernel's op tables
+
+
+class Variant(Enum):
+    ABC = "abc"
+    AB = "ab"
+    NAIVE = "naive"
+
+
+@dataclass(frozen=True)
+class StrassenTerm:
+    """Quadrant ids with +/-1 signs per operand (strassen.py:47-53)."""
+
+    a_ops: tuple
+    b_ops: tuple
+    c_ops: tuple
+
+
+# M0..M6 of one Strassen level, quadrants 0=TL 1=TR 2=BL 3=BR (strassen.py:56-65).
+_ONE_LEVEL = (
+    (((0, 1), (3, 1)), ((0, 1), (3, 1)), ((0, 1), (3, 1))),
+    (((2, 1), (3, 1)), ((0, 1),), ((2, 1), (3, -1))),
+    (((0, 1),), ((1, 1), (3, -1)), ((1, 1), (3, 1))),
+    (((3, 1),), ((2, 1), (0, -1)), ((0, 1), (2, 1))),
+    (((0, 1), (1, 1)), ((3, 1),), ((1, 1), (0, -1))),
+    (((2, 1), (0, -1)), ((0, 1), (1, 1)), ((3, 1),)),
+    (((1, 1), (3, -1)), ((2, 1), (3, 1)), ((0, 1),)),
+)
+
+
+def strassen_terms(level: int, allow_deep: bool = False) -> list:
+    """7^L terms over 4^L quadrants; level l substitutes level l-1 into each
+    level-1 operand: (q * 4^(l-1) + q2, s * s2), outer level first
+    (strassen.py:70-94)."""
+    if level < 0:
+        raise ValueError(f"level must be non-negative, got {level}")
+    if level > MAX_LEVEL and not allow_deep:
+        raise ValueError(f"level {level} exceeds the cap of {MAX_LEVEL} (pass allow_deep to override)")
+    table = [(((0, 1),), ((0, 1),), ((0, 1),))]
+    for lev in range(1, level + 1):
+        scale = 4 ** (lev - 1)
+        table = [
+            tuple(tuple((q * scale + q2, s * s2) for q, s in outer[side] for q2, s2 in inner[side]) for side in range(3))
+            for outer in _ONE_LEVEL
+            for inner in table
+        ]
+    return [StrassenTerm(*t) for t in table]
+
+
+def quadrant_rc(q: int, level: int) -> tuple:
+    """Quadrant id -> (row block, col block) in the 2^L x 2^L grid."""
+    r = c = 0
+    for l in range(level):
+        d = (q >> (2 * (level - 1 - l))) & 3
+        r, c = 2 * r + (d >> 1), 2 * c + (d & 1)
+    return r, c
+
+
+def _variant(v) -> Variant:
+    if isinstance(v, Variant):
+        return v
+    if hasattr(v, "value"):
+        v = v.value
+    try:
+        return Variant(str(v).lower())
+    except ValueError:
+        raise ValueError(f"unknown variant {v!r}") from None
+
+
+def _as_dense(t, name: str) -> DenseTensor:
+    if isinstance(t, DenseTensor):
+        return t
+    if type(t).__module__.startswith("torch"):
+        return DenseTensor.from_torch(t)
+    if all(hasattr(t, a) for a in ("extents", "strides", "data", "base_offset")):  # reference DenseTensor
+        return DenseTensor(t.extents, t.strides, t.data, t.base_offset)
+    raise TypeError(f"tensor {name} must be a DenseTensor or a torch.Tensor")
+
+
+def _check_operands(spec: ContractionSpec, a: DenseTensor, b: DenseTensor, c: DenseTensor) -> None:
+    for t, labels, name in ((a, spec.labels_a, "A"), (b, spec.labels_b, "B"), (c, spec.labels_c, "C")):
+        want = spec.tensor_extents(labels)
+        if tuple(t.extents) != want:
+            raise ValueError(f"tensor {name} extents {tuple(t.extents)} do not match spec {want}")
+
+
+def problem_of(spec: ContractionSpec, a: DenseTensor, b: DenseTensor, c: DenseTensor, level: int,
+               variant: Variant, flags: int = 0) -> _lib.Problem:
+    """The C-ABI problem descriptor: the six bundles of the three views."""
+
+    def bundle(labels: str, tensor_labels: str, t: DenseTensor) -> _lib.Bundle:
+        axes = [tensor_labels.index(l) for l in labels]
+        return _lib.Bundle.of([t.extents[x] for x in axes], [t.strides[x] for x in axes])
+
+    p = _lib.Problem()
+    p.a_row, p.a_col = bundle(spec.bundle_i, spec.labels_a, a), bundle(spec.bundle_p, spec.labels_a, a)
+    p.b_row, p.b_col = bundle(spec.bundle_p, spec.labels_b, b), bundle(spec.bundle_j, spec.labels_b, b)
+    p.c_row, p.c_col = bundle(spec.bundle_i, spec.labels_c, c), bundle(spec.bundle_j, spec.labels_c, c)
+    p.a_base, p.b_base, p.c_base = a.base_offset, b.base_offset, c.base_offset
+    p.level = int(level)
+    p.variant = _lib.VARIANT_CODES[variant.value]
+    p.flags = int(flags)
+    return p
+
+
+def _validate_targets(spec, c: DenseTensor, level: int, terms) -> None:
+    """validate=True: every term's C targets pairwise disjoint (driver.py:53-61)."""
+    axes = {lab: i for i, lab in enumerate(spec.labels_c)}
+    v = make_view(c, spec.bundle_i, spec.bundle_j, axes, 8, 4)
+    quads = {0: v} if level == 0 else quadrant_views(v, level)
+    for term in terms:
+        check_c_targets([quads[q] for q, _ in term.c_ops])
+
+
+def contract(spec: ContractionSpec, a, b, c, level: int, variant, params: BlockingParams = DEFAULT_BLOCKING,
+             threads: int = 1, force_slow: bool = False, allow_deep: bool = False, validate: bool = False,
+             reference_tiling: bool = False) -> RunStats:
+    """C += contraction of A and B with an L-level Strassen recursion on the B200.
+
+    Level 0 is the plain block-scatter GEMM.  All variants compute the same
+    result up to floating-point reordering and execute exactly 7^level leaf
+    products.  ``RunStats.seconds`` is the device time of the call (CUDA
+    events on the current stream; host staging excluded).
+    """
+    a, b, c = _as_dense(a, "A"), _as_dense(b, "B"), _as_dense(c, "C")
+    _check_operands(spec, a, b, c)
+    terms = strassen_terms(level, allow_deep)
+    if level > DEVICE_MAX_LEVEL:
+        raise ValueError(f"level {level} exceeds the device cap of {DEVICE_MAX_LEVEL}")
+    variant = _variant(variant)
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device: the B200 contraction path has no CPU fallback")
+    dev = next((t.data.device for t in (c, a, b) if t.on_device), torch.device("cuda", torch.cuda.current_device()))
+    staged = {}
+    for name, t in (("a", a), ("b", b), ("c", c)):
+        staged[name] = t if t.on_device else t.to_device(dev)
+    A, B, C = staged["a"], staged["b"], staged["c"]
+    if validate:
+        _validate_targets(spec, C, level, terms)
+    flags = (_lib.FLAG_FORCE_SLOW if force_slow else 0) | (_lib.FLAG_REFERENCE_TILING if reference_tiling else 0)
+    prob = problem_of(spec, A, B, C, level, variant, flags)
+    L = _lib.lib()
+    stats = RunStats()
+    with torch.cuda.device(dev):
+        need = ctypes.c_size_t()
+        _lib.check(L.stc_workspace_size(ctypes.byref(prob), ctypes.byref(need)))
+        ws = torch.empty(max(int(need.value), 256), dtype=torch.uint8, device=dev)
+        stream = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st = _lib.Stats()
+        e0.record(stream)
+        _lib.check(L.stc_contract(ctypes.byref(prob), ctypes.c_void_p(A.data.data_ptr()),
+                                  ctypes.c_void_p(B.data.data_ptr()), ctypes.c_void_p(C.data.data_ptr()),
+                                  ctypes.c_void_p(ws.data_ptr()), ws.numel(), ctypes.c_void_p(stream.cuda_stream),
+                                  ctypes.byref(st)))
+        e1.record(stream)
+        e1.synchronize()
+        stats.absorb(st)
+        stats.seconds = max(e0.elapsed_time(e1) * 1e-3, 1e-12)
+        if not c.on_device:
+            c.data[:] = C.data.cpu().numpy()
+    stats.effective_gflops = effective_gflops(spec.n_i, spec.n_j, spec.n_p, stats.seconds)
+    return stats
