@@ -8,11 +8,12 @@ is missing or CUDA is unavailable, every compute entry point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import pathlib
 
 __all__ = ["lib", "Bundle", "Problem", "Stats", "check", "MAX_LABELS", "PAD", "LIB_PATH"]
 
-LIB_PATH = pathlib.Path(__file__).resolve().parent / "libstc_b200.so"
+LIB_PATH = pathlib.Path(os.environ.get("STC_LIBRARY", pathlib.Path(__file__).resolve().parent / "libstc_b200.so"))
 MAX_LABELS = 16
 PAD = -(1 << 63)
 

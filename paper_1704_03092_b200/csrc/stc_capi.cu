@@ -288,6 +288,8 @@ struct Plan {
   int batch = 1, nbatches = 1;
   int grid = 1;
   // workspace layout (bytes)
+  int max_ops = 1;  // most views on one side of any term (2^L)
+  size_t off_kbs = 0;
   size_t off_pool = 0, off_vecs = 0, off_tab = 0, off_tickets = 0, off_counters = 0, off_M = 0, off_pa = 0,
          off_pb = 0, off_acc = 0, total = 0;
   size_t tab_bytes = 0, acc_bytes = 0;
@@ -307,7 +309,8 @@ std::vector<int> exec_order(const std::vector<Term> &terms, int window) {
   const int T = (int)terms.size();
   std::vector<int> seq;
   seq.reserve(T);
-  if (window <= 1) {
+  const char *env = getenv("STC_EXEC_ORDER");
+  if (window <= 1 || (env && strcmp(env, "reference") == 0)) {
     for (int i = 0; i < T; ++i) seq.push_back(i);
     return seq;
   }
@@ -400,6 +403,7 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   }
 
   pl.terms = strassen_terms(pl.level);
+  for (const Term &t : pl.terms) pl.max_ops = std::max(pl.max_ops, (int)std::max(t.a.size(), t.b.size()));
   const int T = (int)pl.terms.size();
   const int64_t P = (pl.mq_pad / BM) * (pl.nq_pad / BN);
   if (P * (int64_t)T > INT32_MAX) return fail(STC_EINVAL, "problem too large: %lld work items", (long long)(P * T));
@@ -467,6 +471,8 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   size_t off = 0;
   pl.off_pool = off;
   off = align256(off + (size_t)pl.pool_len * 8);
+  pl.off_kbs = off;
+  off = align256(off + (size_t)(pl.pool_len / BK) * 8);
   pl.off_vecs = off;
   off = align256(off + pl.vecs.size() * sizeof(VecDesc));
   pl.off_tab = off;
@@ -531,7 +537,9 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
   if (int rc = upload(pl.vecs.data(), pl.vecs.size() * sizeof(VecDesc), ws + pl.off_vecs, s)) return rc;
   CU(launch_build_pool(reinterpret_cast<VecDesc *>(ws + pl.off_vecs), (int)pl.vecs.size(), pl.pool_len, pool, s),
      "k_build_pool");
-  ++launches;
+  int64_t *kbs = reinterpret_cast<int64_t *>(ws + pl.off_kbs);
+  CU(launch_chunk_strides(pool, pl.pool_len / BK, kbs, s), "k_chunk_strides");
+  launches += 2;
   // tickets + work counters
   CU(cudaMemsetAsync(ws + pl.off_tickets, 0, pl.off_M - pl.off_tickets, s), "cudaMemsetAsync");
   int32_t *tickets = reinterpret_cast<int32_t *>(ws + pl.off_tickets);
@@ -546,7 +554,10 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
   g.tiles_n = tiles_n;
   g.kchunks = (int)(pl.kq_pad / BK);
   g.group_m = 8;
-  g.max_ops = MAX_OPS;
+  g.max_ops = pl.max_ops;
+  g.nraw = gemm_nraw(pl.max_ops);
+  g.kbs = kbs;
+  g.force_slow = (pl.flags & STC_FLAG_FORCE_SLOW) ? 1 : 0;
   g.tickets = tickets;
 
   if (pl.variant == STC_VARIANT_ABC) {
@@ -772,7 +783,7 @@ int stc_fused_term_workspace_size(int64_t m, int64_t n, int64_t k, int n_a, int 
   const int64_t mp = rup(m, BM), np = rup(n, BN), kp = rup(k, BK);
   size_t pool = (size_t)(n_a * (mp + kp) + n_b * (np + kp) + n_c * (mp + np)) * 8;
   size_t tab = sizeof(TermDesc) + (size_t)(n_a + n_b) * sizeof(OpDesc) + (size_t)n_c * sizeof(TgtDesc);
-  if (bytes) *bytes = align256(pool) + align256(tab) + 256;
+  if (bytes) *bytes = align256(pool) + align256(pool / BK) + align256(tab) + 256;
   return STC_OK;
 }
 
@@ -832,7 +843,9 @@ int stc_fused_term(int64_t m, int64_t n, int64_t k, const double *A, int n_a, co
   td.b_count = n_b;
   td.c_first = 0;
   td.c_count = n_c;
-  char *tab = ws + align256((size_t)at * 8);
+  int64_t *kbs = reinterpret_cast<int64_t *>(ws + align256((size_t)at * 8));
+  CU(launch_chunk_strides(pool, at / BK, kbs, s), "k_chunk_strides");
+  char *tab = ws + align256((size_t)at * 8) + align256((size_t)at);
   std::vector<char> host(sizeof(TermDesc) + ops.size() * sizeof(OpDesc) + tg.size() * sizeof(TgtDesc) + 8);
   size_t o = 0;
   memcpy(host.data() + o, &td, sizeof(td));
@@ -842,7 +855,7 @@ int stc_fused_term(int64_t m, int64_t n, int64_t k, const double *A, int n_a, co
   memcpy(host.data() + o, tg.data(), tg.size() * sizeof(TgtDesc));
   o += tg.size() * sizeof(TgtDesc);
   // counter lives after the tables
-  char *ctr = ws + align256((size_t)at * 8) + align256(o);
+  char *ctr = tab + align256(o);
   if (ctr + 4 > ws + workspace_bytes) return fail(STC_EWORKSPACE, "workspace too small for counters");
   if (int rc = upload(host.data(), o, tab, s)) return rc;
   CU(cudaMemsetAsync(ctr, 0, 4, s), "cudaMemsetAsync");
@@ -864,7 +877,10 @@ int stc_fused_term(int64_t m, int64_t n, int64_t k, const double *A, int n_a, co
   g.dense_out = 0;
   g.use_tickets = 0;
   g.group_m = 8;
-  g.max_ops = MAX_OPS;
+  g.max_ops = std::max(n_a, n_b);
+  g.nraw = gemm_nraw(g.max_ops);
+  g.kbs = kbs;
+  g.force_slow = (flags & STC_FLAG_FORCE_SLOW) ? 1 : 0;
   g.counter = reinterpret_cast<int32_t *>(ctr);
   const int grid = std::min(gemm_max_grid(MAX_OPS), g.total_items);
   CU(launch_gemm(g, grid, s), "k_strassen_gemm(fused_term)");

@@ -16,7 +16,7 @@ constexpr int BM = 128;              // CTA tile rows   (I bundle)
 constexpr int BN = 128;              // CTA tile cols   (J bundle)
 constexpr int BK = 16;               // k-chunk per pipeline stage (P bundle)
 constexpr int LDS = 132;             // smem row stride in doubles (== 4 mod 16: conflict-free fragments)
-constexpr int STAGES = 4;            // smem ring depth
+constexpr int STAGES = 3;            // smem ring depth of summed operand tiles
 constexpr int CONSUMER_WARPS = 8;    // 2 x 4 warps, 64 x 32 warp tiles of m16n8k4 DMMA
 constexpr int PRODUCER_WARPS = 4;    // gather + Strassen operand sums into smem
 constexpr int THREADS = 32 * (CONSUMER_WARPS + PRODUCER_WARPS);
@@ -65,7 +65,11 @@ struct GemmArgs {
   int32_t use_tickets;       // serialise C-tile updates across terms
   int32_t group_m;           // tile rasterisation group
   int32_t max_ops;           // op-table capacity in smem (per side)
-  int32_t force_slow;        // reference force_slow: always take the PAD-checking gather
+  int32_t force_slow;        // reference force_slow: always take the per-element gather
+  int32_t nraw;              // raw cp.async slots in smem (units in flight + 1)
+  int32_t _pad2;
+  const int64_t *kbs;        // chunk strides: kbs[i] = stride of pool[16i .. 16i+15] or INT64_MIN
+  int32_t *debug;            // experiment builds only (nullptr in production)
   double *M;                 // dense out: M + slot*m_stride + row*m_ld + col
   int64_t m_ld, m_stride;
   int32_t *tickets;
@@ -120,6 +124,8 @@ cudaError_t launch_block_vector(const int64_t *scat, int64_t len, int64_t blk, i
                                 cudaStream_t s);
 cudaError_t launch_copy_pad(const int64_t *in, int64_t len, int64_t len_pad, int64_t *out, cudaStream_t s);
 size_t gemm_smem_bytes(int max_ops);
+int gemm_nraw(int max_ops);
+cudaError_t launch_chunk_strides(const int64_t *pool, int64_t nchunks, int64_t *kbs, cudaStream_t s);
 cudaError_t launch_gemm(const GemmArgs &a, int grid, cudaStream_t s);
 int gemm_max_grid(int max_ops);
 cudaError_t launch_accumulate(const AccArgs &a, cudaStream_t s);
