@@ -556,6 +556,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
   g.group_m = 8;
   g.max_ops = pl.max_ops;
   g.nraw = gemm_nraw(pl.max_ops);
+  g.kwin = gemm_kwin(pl.max_ops);
   g.kbs = kbs;
   g.force_slow = (pl.flags & STC_FLAG_FORCE_SLOW) ? 1 : 0;
   g.tickets = tickets;
@@ -879,6 +880,7 @@ int stc_fused_term(int64_t m, int64_t n, int64_t k, const double *A, int n_a, co
   g.group_m = 8;
   g.max_ops = std::max(n_a, n_b);
   g.nraw = gemm_nraw(g.max_ops);
+  g.kwin = gemm_kwin(g.max_ops);
   g.kbs = kbs;
   g.force_slow = (flags & STC_FLAG_FORCE_SLOW) ? 1 : 0;
   g.counter = reinterpret_cast<int32_t *>(ctr);

@@ -47,24 +47,37 @@ struct SmemLayout {
   static constexpr size_t bar_off = b_off + STAGES * stage_bytes;  // full[STAGES], empty[STAGES]
   static constexpr size_t meta_off = bar_off + 2 * STAGES * 8;    // stage_item[STAGES], s_item
   static constexpr size_t tab_off = (meta_off + (STAGES + 4) * 4 + 127) / 128 * 128;
-  // xoffA[ops][BM], xoffB[ops][BN], kstA[ops], kstB[ops], doffA[ops], doffB[ops],
-  // sgnA[ops], sgnB[ops], then raw[nraw][BK][128] (thread-private, see raw_index)
-  __host__ __device__ static size_t tab_bytes(int ops) { return 8 * ((size_t)ops * (BM + BN) + 6 * (size_t)ops); }
-  __host__ __device__ static size_t raw_off(int ops) { return (tab_off + tab_bytes(ops) + 127) / 128 * 128; }
+  // xoffA[ops][BM], xoffB[ops][BN], UnitDesc[2 * ops], then raw[nraw][BK * 128] (thread-private, see raw_index)
+  // k-info window: kwin chunks x 2 buffers x (2 * ops) units x 16 bytes
+  __host__ __device__ static size_t tab_bytes(int ops, int kwin) {
+    return 8 * (size_t)ops * (BM + BN) + 2 * (size_t)ops * 64 + 2 * (2 * (size_t)ops) * (size_t)kwin * 16;
+  }
+  __host__ __device__ static size_t raw_off(int ops, int kwin) { return (tab_off + tab_bytes(ops, kwin) + 127) / 128 * 128; }
   static constexpr size_t raw_doubles = (size_t)BK * 128;  // one thread-private raw slot
-  __host__ __device__ static size_t bytes(int ops, int nraw) { return raw_off(ops) + (size_t)nraw * raw_doubles * 8; }
+  __host__ __device__ static size_t bytes(int ops, int kwin, int nraw) {
+    return raw_off(ops, kwin) + (size_t)nraw * raw_doubles * 8;
+  }
 };
 
 constexpr size_t kMaxSmem = 227 * 1024;
 
+// k-info window (chunks): the largest of 32/16/8 that leaves room for 4 raw slots.
+int gemm_kwin(int max_ops) {
+  int w = 32;
+  while (w > 8 && SmemLayout::bytes(max_ops, w, 4) > kMaxSmem) w /= 2;
+  return w;
+}
+
+// Raw slots (cp.async units in flight + 1): as many as fit, 4..MAX_NRAW.
 int gemm_nraw(int max_ops) {
+  const int w = gemm_kwin(max_ops);
   int n = MAX_NRAW;
   if (const char *e = getenv("STC_NRAW")) n = std::max(4, std::min(MAX_NRAW, atoi(e)));
-  while (n > 4 && SmemLayout::bytes(max_ops, n) > kMaxSmem) --n;
+  while (n > 4 && SmemLayout::bytes(max_ops, w, n) > kMaxSmem) --n;
   return n;
 }
 
-size_t gemm_smem_bytes(int max_ops) { return SmemLayout::bytes(max_ops, gemm_nraw(max_ops)); }
+size_t gemm_smem_bytes(int max_ops) { return SmemLayout::bytes(max_ops, gemm_kwin(max_ops), gemm_nraw(max_ops)); }
 
 __device__ __forceinline__ void tile_of(const GemmArgs &p, int item, int &slot, int &ti, int &tj) {
   const int P = p.tiles_m * p.tiles_n;
@@ -80,51 +93,80 @@ __device__ __forceinline__ void tile_of(const GemmArgs &p, int item, int &slot, 
   tj = r / gsz;
 }
 
-// Element e of a producer thread's 16 in a [BK][LDS] tile:
-//   kfast = 0: x = ptid, k = e (x contiguous in memory)
-//   kfast = 1: k = (ptid & 3) + 4 (e & 3), x = (ptid >> 2) + 32 (e >> 2) (k contiguous)
-__device__ __forceinline__ int tile_index(int kfast, int ptid, int e) {
-  return kfast ? ((ptid & 3) + 4 * (e & 3)) * LDS + (ptid >> 2) + 32 * (e >> 2) : e * LDS + ptid;
+// Producer thread mappings (NP = 256 threads, EPT = 8 elements per unit):
+//   x-contiguous side (kfast = 0): x = t % 128, k = 8 (t / 128) + e
+//   k-contiguous side (kfast = 1): k = (t & 3) + 4 (e & 3), x = (t >> 2) + 64 (e >> 2)
+constexpr int NP = 32 * PRODUCER_WARPS;
+constexpr int EPT = BK * 128 / NP;
+static_assert(NP == 256 && EPT == 8, "producer mapping assumes 256 threads x 8 elements");
+
+__device__ __forceinline__ int tile_index(int kfast, int t, int e) {
+  return kfast ? ((t & 3) + 4 * (e & 3)) * LDS + (t >> 2) + 64 * (e >> 2) : ((t >> 7) * 8 + e) * LDS + (t & 127);
 }
 
 // Raw slots are private to each producer thread, independent of the side's
-// mapping: element e of thread ptid lives at e * 128 + ptid (conflict-free).
-// (A slot alternately holds A- and B-side units whose tile mappings differ, so
-// a tile-position layout would let one thread's cp.async land on data another
-// thread has not read yet.)
-__device__ __forceinline__ int raw_index(int ptid, int e) { return e * 128 + ptid; }
+// mapping: element e of thread t lives at e * NP + t (conflict-free).  A slot
+// alternately holds A- and B-side units whose tile mappings differ, so a
+// tile-position layout would let one thread's cp.async land on data another
+// thread has not read yet.
+__device__ __forceinline__ int raw_index(int t, int e) { return e * NP + t; }
 
-// cp.async one unit into a raw slot (zero-fill for PAD).
-__device__ __forceinline__ void issue_unit(double *__restrict__ dst, const double *__restrict__ D,
-                                           const int64_t *__restrict__ xop, const int64_t *__restrict__ kvec,
-                                           int64_t kstr, int kfast, bool slow, int ptid) {
-  if (!slow && kstr != kIrregular) {
-    const int64_t b0 = kvec[0];
-    if (!kfast) {
-      const int64_t a = xop[ptid];
+// Everything the producer needs about one unit (one view of one side) of the
+// current item, staged in smem at item start.
+struct UnitDesc {
+  const double *D;     // side data + the view's data offset
+  const int64_t *xo;   // the view's x offsets for this tile (smem)
+  int64_t kst;         // pool index of the view's k vector
+  uint64_t signbit;    // sign of the coefficient as a bit (first view of a side)
+  double sign;         // +/-1 (later views)
+  int32_t kfast, is_a, first, last;
+};
+
+static_assert(sizeof(UnitDesc) <= 64, "UnitDesc slot");
+
+// First k offset and chunk stride (kbs entry) of one unit for one chunk; the
+// producer keeps a double-buffered window of KWIN chunks of these in smem so
+// that issuing a unit never waits on a global load.
+struct KInfo {
+  int64_t b0, kstr;
+};
+
+// cp.async one unit of chunk `kc` into a raw slot (zero-fill for PAD).  A
+// chunk whose 16 k entries share one stride (its block-scatter entry at GPU
+// granularity, kbs) is addressed base + k * stride: the reference's fast path
+// (_jit.py:54-65); otherwise every element goes through the scatter vector:
+// the slow path (_jit.py:66-78).
+__device__ __forceinline__ void issue_unit(double *__restrict__ dst, const UnitDesc &u, const int64_t *__restrict__ pool,
+                                           KInfo ki, int kc, bool force_slow, int t) {
+  const int64_t kst = u.kst + (int64_t)kc * BK;
+  const int64_t kstr = force_slow ? kIrregular : ki.kstr;
+  const double *D = u.D;
+  if (kstr != kIrregular) {
+    const int64_t b0 = ki.b0;
+    if (!u.kfast) {
+      const int64_t a = u.xo[t & 127];
       const bool ok = a != kPad;
-      const double *src = ok ? D + a + b0 : D;
+      const double *src = D + (ok ? a + b0 + (t >> 7) * 8 * kstr : 0);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) cp_async8(dst + raw_index(ptid, e), ok ? src + e * kstr : D, ok);
+      for (int e = 0; e < EPT; ++e) cp_async8(dst + raw_index(t, e), ok ? src + e * kstr : D, ok);
     } else {
-      const double *base = D + b0 + (ptid & 3) * kstr;
+      const double *base = D + b0 + (t & 3) * kstr;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t a = xop[(ptid >> 2) + 32 * j];
+      for (int j = 0; j < 2; ++j) {
+        const int64_t a = u.xo[(t >> 2) + 64 * j];
         const bool ok = a != kPad;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          cp_async8(dst + raw_index(ptid, 4 * j + i), ok ? base + a + 4 * i * kstr : D, ok);
+        for (int i = 0; i < 4; ++i) cp_async8(dst + raw_index(t, 4 * j + i), ok ? base + a + 4 * i * kstr : D, ok);
       }
     }
   } else {
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const int x = kfast ? (ptid >> 2) + 32 * (e >> 2) : ptid;
-      const int k = kfast ? (ptid & 3) + 4 * (e & 3) : e;
-      const int64_t a = xop[x], b = __ldg(kvec + k);
+    for (int e = 0; e < EPT; ++e) {
+      const int x = u.kfast ? (t >> 2) + 64 * (e >> 2) : (t & 127);
+      const int k = u.kfast ? (t & 3) + 4 * (e & 3) : (t >> 7) * 8 + e;
+      const int64_t a = u.xo[x], b = __ldg(pool + kst + k);
       const bool ok = a != kPad && b != kPad;
-      cp_async8(dst + raw_index(ptid, e), ok ? D + a + b : D, ok);
+      cp_async8(dst + raw_index(t, e), ok ? D + a + b : D, ok);
     }
   }
 }
@@ -147,22 +189,18 @@ __global__ void __launch_bounds__(THREADS, 1) k_strassen_gemm(const GemmArgs p) 
   int *stage_item = reinterpret_cast<int *>(smem + SmemLayout::meta_off);
   int *s_item = stage_item + STAGES;
   const int mo = p.max_ops;
-  constexpr int nraw = NRAW;
-  double *raw = reinterpret_cast<double *>(smem + SmemLayout::raw_off(mo));
+  const int KWIN = p.kwin;
+  double *raw = reinterpret_cast<double *>(smem + SmemLayout::raw_off(mo, KWIN));
   int64_t *xoffA = reinterpret_cast<int64_t *>(smem + SmemLayout::tab_off);
   int64_t *xoffB = xoffA + mo * BM;
-  int64_t *kstA = xoffB + mo * BN;
-  int64_t *kstB = kstA + mo;
-  int64_t *doffA = kstB + mo;
-  int64_t *doffB = doffA + mo;
-  double *sgnA = reinterpret_cast<double *>(doffB + mo);
-  double *sgnB = sgnA + mo;
+  UnitDesc *units = reinterpret_cast<UnitDesc *>(xoffB + mo * BN);  // [2 * mo]
+  KInfo *kinfo = reinterpret_cast<KInfo *>(units + 2 * mo);          // [2][2 * mo][KWIN]
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 32 * PRODUCER_WARPS);
+      mbar_init(&full[s], NP);
       mbar_init(&empty[s], CONSUMER_WARPS);
     }
   }
@@ -173,18 +211,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_strassen_gemm(const GemmArgs p) 
 #ifndef STC_NO_SETMAXNREG
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
 #endif
-    const int ptid = tid - 32 * CONSUMER_WARPS;
-    const int nprod = 32 * PRODUCER_WARPS;
+    const int t = tid - 32 * CONSUMER_WARPS;
     const bool force_slow = p.force_slow != 0;
     int stage = 0;
     uint32_t phase = 0;
     for (;;) {
-      if (ptid == 0) *s_item = atomicAdd(p.counter, 1);
-      named_bar(1, nprod);
+      if (t == 0) *s_item = atomicAdd(p.counter, 1);
+      named_bar(1, NP);
       const int item = *s_item;
       if (item >= p.total_items) {
         mbar_wait(&empty[stage], phase ^ 1);
-        if (ptid == 0) stage_item[stage] = -1;
+        if (t == 0) stage_item[stage] = -1;
         mbar_arrive(&full[stage]);
         break;
       }
@@ -193,90 +230,112 @@ __global__ void __launch_bounds__(THREADS, 1) k_strassen_gemm(const GemmArgs p) 
       const TermDesc td = p.terms[slot];
       const int na = td.a_count, nb = td.b_count;
       const int U = na + nb;  // units per chunk: every view of A, then of B
-      for (int i = ptid; i < U; i += nprod) {
-        const OpDesc o = p.ops[i < na ? td.a_first + i : td.b_first + i - na];
-        if (i < na) {
-          kstA[i] = o.k_start;
-          doffA[i] = o.data_off;
-          sgnA[i] = o.sign;
-        } else {
-          kstB[i - na] = o.k_start;
-          doffB[i - na] = o.data_off;
-          sgnB[i - na] = o.sign;
-        }
+      if (t < U) {
+        const bool is_a = t < na;
+        const int op = is_a ? t : t - na;
+        const OpDesc o = p.ops[is_a ? td.a_first + op : td.b_first + op];
+        UnitDesc u;
+        u.D = (is_a ? p.A : p.B) + o.data_off;
+        u.xo = is_a ? xoffA + op * BM : xoffB + op * BN;
+        u.kst = o.k_start;
+        u.signbit = o.sign < 0 ? 0x8000000000000000ull : 0ull;
+        u.sign = o.sign;
+        u.kfast = is_a ? p.a_kfast : p.b_kfast;
+        u.is_a = is_a;
+        u.first = op == 0;
+        u.last = op == (is_a ? na : nb) - 1;
+        units[t] = u;
       }
-      for (int idx = ptid; idx < na * BM; idx += nprod) {
+      for (int idx = t; idx < na * BM; idx += NP) {
         const int op = idx / BM, x = idx - op * BM;
         xoffA[idx] = p.pool[p.ops[td.a_first + op].x_start + (int64_t)ti * BM + x];
       }
-      for (int idx = ptid; idx < nb * BN; idx += nprod) {
+      for (int idx = t; idx < nb * BN; idx += NP) {
         const int op = idx / BN, x = idx - op * BN;
         xoffB[idx] = p.pool[p.ops[td.b_first + op].x_start + (int64_t)tj * BN + x];
       }
-      named_bar(1, nprod);
+      const int kchunks = p.kchunks;
+      // k-info window w (chunks [w*KWIN, (w+1)*KWIN)) into buffer w & 1
+      auto fill_kwin = [&](int w) {
+        for (int idx = t; idx < U * KWIN; idx += NP) {
+          const int u = idx / KWIN, c = idx - u * KWIN;
+          const int chunk = w * KWIN + c;
+          if (chunk >= kchunks) continue;
+          const int64_t kst = p.ops[u < na ? td.a_first + u : td.b_first + u - na].k_start + (int64_t)chunk * BK;
+          KInfo ki;
+          ki.b0 = __ldg(p.pool + kst);
+          ki.kstr = __ldg(p.kbs + (kst >> 4));
+          kinfo[((w & 1) * 2 * mo + u) * KWIN + c] = ki;
+        }
+      };
+      fill_kwin(0);  // window 1 follows half-way through window 0
+      named_bar(1, NP);
 
-      const int G = p.kchunks * U;
+      const int G = kchunks * U;
       constexpr int D = NRAW - 1;  // units in flight ahead of the one being summed
       int ig = 0, ic = 0, iu = 0, islot = 0;  // issue cursor
-      int cu = 0, cslot = 0;                  // consume cursor
+      int cc = 0, cu = 0, cslot = 0;          // consume cursor (chunk, unit, raw slot)
       auto issue = [&]() {
         if (ig < G) {
-          const bool is_a = iu < na;
-          const int op = is_a ? iu : iu - na;
-          const int64_t kst = (is_a ? kstA : kstB)[op] + (int64_t)ic * BK;
-          const int64_t kstr = __ldg(p.kbs + (kst >> 4));
-          issue_unit(raw + islot * SmemLayout::raw_doubles, (is_a ? p.A : p.B) + (is_a ? doffA : doffB)[op],
-                     is_a ? xoffA + op * BM : xoffB + op * BN, p.pool + kst, kstr, is_a ? p.a_kfast : p.b_kfast,
-                     force_slow, ptid);
+          issue_unit(raw + islot * SmemLayout::raw_doubles, units[iu], p.pool,
+                     kinfo[(((ic / KWIN) & 1) * 2 * mo + iu) * KWIN + ic % KWIN], ic, force_slow, t);
           if (++iu == U) {
             iu = 0;
             ++ic;
           }
-          if (++islot == nraw) islot = 0;
+          if (++islot == NRAW) islot = 0;
         }
         cp_async_commit();  // empty groups at the tail keep the wait count uniform
         ++ig;
       };
       for (int d = 0; d < D; ++d) issue();
-      double acc[16];
+      double acc[EPT];
       for (int g = 0; g < G; ++g) {
         issue();
         cp_async_wait<D>();  // unit g has landed (this thread's own copies)
-        const bool is_a = cu < na;
-        const int op = is_a ? cu : cu - na;
-        const int kfast = is_a ? p.a_kfast : p.b_kfast;
+        const UnitDesc &u = units[cu];
         const double *src = raw + cslot * SmemLayout::raw_doubles;
-        if (op == 0) {
-          const uint64_t sb = (is_a ? sgnA : sgnB)[0] < 0 ? 0x8000000000000000ull : 0ull;
+        if (u.first) {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) acc[e] = first_term(src[raw_index(ptid, e)], sb);
+          for (int e = 0; e < EPT; ++e) acc[e] = first_term(src[raw_index(t, e)], u.signbit);
         } else {
-          const double s = (is_a ? sgnA : sgnB)[op];
+          const double s = u.sign;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) acc[e] += s * src[raw_index(ptid, e)];
+          for (int e = 0; e < EPT; ++e) {
+#ifdef STC_EXPERIMENT_INTADD
+            acc[e] = __longlong_as_double(__double_as_longlong(acc[e]) + __double_as_longlong(src[raw_index(t, e)]));
+#else
+            acc[e] += s * src[raw_index(t, e)];
+#endif
+          }
         }
-        if (++cslot == nraw) cslot = 0;
-        if (op == (is_a ? na : nb) - 1) {  // side complete: store its sum into the MMA ring
-          if (is_a) mbar_wait(&empty[stage], phase ^ 1);
-          double *S = (is_a ? sA : sB) + stage * SmemLayout::stage_doubles;
+        if (++cslot == NRAW) cslot = 0;
+        if (u.last) {  // side complete: store its sum into the MMA ring
+          if (u.is_a) mbar_wait(&empty[stage], phase ^ 1);
+          double *S = (u.is_a ? sA : sB) + stage * SmemLayout::stage_doubles;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) S[tile_index(kfast, ptid, e)] = acc[e];
+          for (int e = 0; e < EPT; ++e) S[tile_index(u.kfast, t, e)] = acc[e];
         }
         if (++cu == U) {
           cu = 0;
-          if (ptid == 0) stage_item[stage] = item;
+          if (t == 0) stage_item[stage] = item;
           mbar_arrive(&full[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
-#ifdef STC_EXPERIMENT_CHUNKBAR
-          named_bar(1, nprod);
-#endif
+          // half-way through window w, publish window w+1 (its buffer held window
+          // w-1, which every producer thread has finished issuing: producers are at
+          // most STAGES chunks apart)
+          ++cc;
+          if (cc % KWIN == KWIN / 2 && (cc / KWIN + 1) * KWIN < kchunks) {
+            fill_kwin(cc / KWIN + 1);
+            named_bar(1, NP);
+          }
         }
       }
       cp_async_wait<0>();
-      named_bar(1, nprod);  // tables of this item fully used before the next fill
+      named_bar(1, NP);  // tables of this item fully used before the next fill
     }
   } else {
     // ===================== consumer warps: DMMA + epilogue ============
@@ -401,21 +460,17 @@ static GemmKernel kernel_for(int nraw) {
   }
 }
 
+// One persistent CTA per SM: 512 threads x 128 registers fill the register file.
 int gemm_max_grid(int max_ops) {
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int nraw = gemm_nraw(max_ops);
-  const size_t sm = SmemLayout::bytes(max_ops, nraw);
-  GemmKernel k = kernel_for(nraw);
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, sm);
-  if (per_sm < 1) per_sm = 1;
-  return sms * per_sm;
+  (void)max_ops;
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  return sms;
 }
 
 cudaError_t launch_gemm(const GemmArgs &a, int grid, cudaStream_t s) {
-  const size_t sm = SmemLayout::bytes(a.max_ops, a.nraw);
+  const size_t sm = SmemLayout::bytes(a.max_ops, a.kwin, a.nraw);
   GemmKernel k = kernel_for(a.nraw);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;

@@ -18,12 +18,12 @@ constexpr int BK = 16;               // k-chunk per pipeline stage (P bundle)
 constexpr int LDS = 132;             // smem row stride in doubles (== 4 mod 16: conflict-free fragments)
 constexpr int STAGES = 3;            // smem ring depth of summed operand tiles
 constexpr int CONSUMER_WARPS = 8;    // 2 x 4 warps, 64 x 32 warp tiles of m16n8k4 DMMA
-constexpr int PRODUCER_WARPS = 4;    // gather + Strassen operand sums into smem
+constexpr int PRODUCER_WARPS = 8;    // gather + Strassen operand sums into smem
 constexpr int THREADS = 32 * (CONSUMER_WARPS + PRODUCER_WARPS);
-// Register split via setmaxnreg (launch: 65536 / 384 -> 168 per thread):
-// 256 consumer threads x 192 + 128 producer threads x 120 = 64512.
+// Register split via setmaxnreg (launch: 65536 / 512 -> 128 per thread):
+// 256 consumer threads x 192 + 256 producer threads x 64 = 65536.
 constexpr int CONSUMER_REGS = 192;
-constexpr int PRODUCER_REGS = 120;
+constexpr int PRODUCER_REGS = 64;
 constexpr int MAX_OPS = 16;          // views per operand side (2^L, L <= 4)
 
 // One operand view of a term side.  For the A side the tile-fixed dimension x
@@ -67,7 +67,7 @@ struct GemmArgs {
   int32_t max_ops;           // op-table capacity in smem (per side)
   int32_t force_slow;        // reference force_slow: always take the per-element gather
   int32_t nraw;              // raw cp.async slots in smem (units in flight + 1)
-  int32_t _pad2;
+  int32_t kwin;              // producer k-info window (chunks)
   const int64_t *kbs;        // chunk strides: kbs[i] = stride of pool[16i .. 16i+15] or INT64_MIN
   int32_t *debug;            // experiment builds only (nullptr in production)
   double *M;                 // dense out: M + slot*m_stride + row*m_ld + col
@@ -125,6 +125,7 @@ cudaError_t launch_block_vector(const int64_t *scat, int64_t len, int64_t blk, i
 cudaError_t launch_copy_pad(const int64_t *in, int64_t len, int64_t len_pad, int64_t *out, cudaStream_t s);
 size_t gemm_smem_bytes(int max_ops);
 int gemm_nraw(int max_ops);
+int gemm_kwin(int max_ops);
 cudaError_t launch_chunk_strides(const int64_t *pool, int64_t nchunks, int64_t *kbs, cudaStream_t s);
 cudaError_t launch_gemm(const GemmArgs &a, int grid, cudaStream_t s);
 int gemm_max_grid(int max_ops);
