@@ -104,6 +104,13 @@ int stc_workspace_size(const stc_problem *p, size_t *bytes);
 int stc_contract(const stc_problem *p, const double *A, const double *B, double *C, void *workspace,
                  size_t workspace_bytes, void *stream, stc_stats *stats);
 
+/* Profiling hook (no reference counterpart): the next stc_contract call on
+ * this thread records `before` / `after` (cudaEvent_t handles passed as void*)
+ * on its stream immediately around the fused DMMA launch (ABC) or around the
+ * span of its batched DMMA launches (AB / Naive).  Consumed by that call;
+ * pass NULLs to disarm. */
+int stc_set_kernel_events(void *before, void *after);
+
 /* ---- subsystem (1): device-side scatter / block-scatter vectors ---- */
 
 /* make_view's _bundle_scatter (scatter.py:105-112) on the device: out[l] for

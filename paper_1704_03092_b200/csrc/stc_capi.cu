@@ -26,6 +26,7 @@ using namespace stc;
 namespace {
 
 thread_local std::string g_err;
+thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;  // stc_set_kernel_events
 
 int fail(int code, const char *fmt, ...) {
   char buf[512];
@@ -510,6 +511,12 @@ extern "C" {
 const char *stc_last_error(void) { return g_err.c_str(); }
 int stc_abi_version(void) { return STC_ABI_VERSION; }
 
+int stc_set_kernel_events(void *before, void *after) {
+  g_ev_before = reinterpret_cast<cudaEvent_t>(before);
+  g_ev_after = reinterpret_cast<cudaEvent_t>(after);
+  return STC_OK;
+}
+
 int stc_workspace_size(const stc_problem *p, size_t *bytes) {
   Plan pl;
   if (int rc = build_plan(p, pl, 0)) return rc;
@@ -585,7 +592,9 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
     g.use_tickets = T > 1;
     g.counter = counters;
     const int grid = (int)std::min<int64_t>(pl.grid, g.total_items);
+    if (g_ev_before) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
     CU(launch_gemm(g, grid, s), "k_strassen_gemm");
+    if (g_ev_after) CU(cudaEventRecord(g_ev_after, s), "cudaEventRecord");
     ++launches;
     st.fast_updates = 0;
     st.slow_updates = (int64_t)P * (int64_t)pl.tgts.size();
@@ -727,7 +736,9 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       g.m_stride = pl.m_slot;
       g.counter = counters + bi;
       const int grid = (int)std::min<int64_t>(pl.grid, g.total_items);
+      if (g_ev_before && bi == 0) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
       CU(launch_gemm(g, grid, s), "k_strassen_gemm(dense)");
+      if (g_ev_after && bi == pl.nbatches - 1) CU(cudaEventRecord(g_ev_after, s), "cudaEventRecord");
       aa.M = M;
       aa.m_ld = pl.nq_pad;
       aa.m_stride = pl.m_slot;
@@ -747,6 +758,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
   st.work_items = P * T;
   st.kernel_launches = launches;
   if (stats) *stats = st;
+  g_ev_before = g_ev_after = nullptr;
   return STC_OK;
 }
 
