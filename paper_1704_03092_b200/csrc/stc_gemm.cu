@@ -74,7 +74,7 @@ int gemm_nraw(int max_ops) {
   int n = MAX_NRAW;
   if (const char *e = getenv("STC_NRAW")) n = std::max(4, std::min(MAX_NRAW, atoi(e)));
   while (n > 4 && SmemLayout::bytes(max_ops, w, n) > kMaxSmem) --n;
-  return n;
+  return w < 32 ? 4 : n;  // reduced windows are only instantiated with 4 slots
 }
 
 size_t gemm_smem_bytes(int max_ops) { return SmemLayout::bytes(max_ops, gemm_kwin(max_ops), gemm_nraw(max_ops)); }
@@ -115,7 +115,8 @@ __device__ __forceinline__ int raw_index(int t, int e) { return e * NP + t; }
 // current item, staged in smem at item start.
 struct UnitDesc {
   const double *D;     // side data + the view's data offset
-  const int64_t *xo;   // the view's x offsets for this tile (smem)
+  int32_t xo;          // element offset of the view's x offsets in the smem x table
+  int32_t _pad;
   int64_t kst;         // pool index of the view's k vector
   uint64_t signbit;    // sign of the coefficient as a bit (first view of a side)
   double sign;         // +/-1 (later views)
@@ -135,36 +136,41 @@ struct KInfo {
 // chunk whose 16 k entries share one stride (its block-scatter entry at GPU
 // granularity, kbs) is addressed base + k * stride: the reference's fast path
 // (_jit.py:54-65); otherwise every element goes through the scatter vector:
-// the slow path (_jit.py:66-78).
-__device__ __forceinline__ void issue_unit(double *__restrict__ dst, const UnitDesc &u, const int64_t *__restrict__ pool,
-                                           KInfo ki, int kc, bool force_slow, int t) {
-  const int64_t kst = u.kst + (int64_t)kc * BK;
-  const int64_t kstr = force_slow ? kIrregular : ki.kstr;
+// the slow path (_jit.py:66-78).  PAD rows (x) are handled per row: the whole
+// run is zero-filled from a dummy source.
+__device__ __forceinline__ void issue_unit(double *__restrict__ dst, const UnitDesc &u, const int64_t *__restrict__ xtab,
+                                           const int64_t *__restrict__ pool, KInfo ki, int kc, bool force_slow,
+                                           int t) {
   const double *D = u.D;
-  if (kstr != kIrregular) {
-    const int64_t b0 = ki.b0;
+  const int64_t *xo = xtab + u.xo;
+  if (!force_slow && ki.kstr != kIrregular) {
+    const int64_t kstr = ki.kstr;
     if (!u.kfast) {
-      const int64_t a = u.xo[t & 127];
+      const int64_t a = xo[t & 127];
       const bool ok = a != kPad;
-      const double *src = D + (ok ? a + b0 + (t >> 7) * 8 * kstr : 0);
+      const double *src = ok ? D + (a + ki.b0 + (t >> 7) * 8 * kstr) : D;
+      const int64_t step = ok ? kstr : 0;
 #pragma unroll
-      for (int e = 0; e < EPT; ++e) cp_async8(dst + raw_index(t, e), ok ? src + e * kstr : D, ok);
+      for (int e = 0; e < EPT; ++e) cp_async8(dst + raw_index(t, e), src + e * step, ok);
     } else {
-      const double *base = D + b0 + (t & 3) * kstr;
+      const double *base = D + (ki.b0 + (t & 3) * kstr);
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        const int64_t a = u.xo[(t >> 2) + 64 * j];
+        const int64_t a = xo[(t >> 2) + 64 * j];
         const bool ok = a != kPad;
+        const double *src = ok ? base + a : D;
+        const int64_t step = ok ? 4 * kstr : 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) cp_async8(dst + raw_index(t, 4 * j + i), ok ? base + a + 4 * i * kstr : D, ok);
+        for (int i = 0; i < 4; ++i) cp_async8(dst + raw_index(t, 4 * j + i), src + i * step, ok);
       }
     }
   } else {
+    const int64_t kst = u.kst + (int64_t)kc * BK;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       const int x = u.kfast ? (t >> 2) + 64 * (e >> 2) : (t & 127);
       const int k = u.kfast ? (t & 3) + 4 * (e & 3) : (t >> 7) * 8 + e;
-      const int64_t a = u.xo[x], b = __ldg(pool + kst + k);
+      const int64_t a = xo[x], b = __ldg(pool + kst + k);
       const bool ok = a != kPad && b != kPad;
       cp_async8(dst + raw_index(t, e), ok ? D + a + b : D, ok);
     }
@@ -179,7 +185,7 @@ __device__ __forceinline__ double first_term(double v, uint64_t signbit) {
   return __longlong_as_double(static_cast<long long>(b));
 }
 
-template <int NRAW>
+template <int NRAW, int KWIN>
 __global__ void __launch_bounds__(THREADS, 1) k_strassen_gemm(const GemmArgs p) {
   extern __shared__ __align__(128) unsigned char smem[];
   double *sA = reinterpret_cast<double *>(smem + SmemLayout::a_off);
@@ -189,7 +195,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_strassen_gemm(const GemmArgs p) 
   int *stage_item = reinterpret_cast<int *>(smem + SmemLayout::meta_off);
   int *s_item = stage_item + STAGES;
   const int mo = p.max_ops;
-  const int KWIN = p.kwin;
   double *raw = reinterpret_cast<double *>(smem + SmemLayout::raw_off(mo, KWIN));
   int64_t *xoffA = reinterpret_cast<int64_t *>(smem + SmemLayout::tab_off);
   int64_t *xoffB = xoffA + mo * BM;
@@ -236,7 +241,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_strassen_gemm(const GemmArgs p) 
         const OpDesc o = p.ops[is_a ? td.a_first + op : td.b_first + op];
         UnitDesc u;
         u.D = (is_a ? p.A : p.B) + o.data_off;
-        u.xo = is_a ? xoffA + op * BM : xoffB + op * BN;
+        u.xo = is_a ? op * BM : mo * BM + op * BN;
         u.kst = o.k_start;
         u.signbit = o.sign < 0 ? 0x8000000000000000ull : 0ull;
         u.sign = o.sign;
@@ -277,8 +282,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_strassen_gemm(const GemmArgs p) 
       int cc = 0, cu = 0, cslot = 0;          // consume cursor (chunk, unit, raw slot)
       auto issue = [&]() {
         if (ig < G) {
-          issue_unit(raw + islot * SmemLayout::raw_doubles, units[iu], p.pool,
-                     kinfo[(((ic / KWIN) & 1) * 2 * mo + iu) * KWIN + ic % KWIN], ic, force_slow, t);
+          issue_unit(raw + islot * SmemLayout::raw_doubles, units[iu], xoffA, p.pool,
+                     kinfo[(((ic / KWIN) & 1) * 2 * mo + iu) * KWIN + (ic & (KWIN - 1))], ic, force_slow, t);
           if (++iu == U) {
             iu = 0;
             ++ic;
@@ -451,12 +456,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_strassen_gemm(const GemmArgs p) 
 
 using GemmKernel = void (*)(const GemmArgs);
 
-static GemmKernel kernel_for(int nraw) {
+static GemmKernel kernel_for(int nraw, int kwin) {
+  if (kwin == 16) return k_strassen_gemm<4, 16>;
+  if (kwin == 8) return k_strassen_gemm<4, 8>;
   switch (nraw) {
-    case 4: return k_strassen_gemm<4>;
-    case 5: return k_strassen_gemm<5>;
-    case 6: return k_strassen_gemm<6>;
-    default: return k_strassen_gemm<7>;
+    case 4: return k_strassen_gemm<4, 32>;
+    case 5: return k_strassen_gemm<5, 32>;
+    case 6: return k_strassen_gemm<6, 32>;
+    default: return k_strassen_gemm<7, 32>;
   }
 }
 
@@ -471,7 +478,7 @@ int gemm_max_grid(int max_ops) {
 
 cudaError_t launch_gemm(const GemmArgs &a, int grid, cudaStream_t s) {
   const size_t sm = SmemLayout::bytes(a.max_ops, a.kwin, a.nraw);
-  GemmKernel k = kernel_for(a.nraw);
+  GemmKernel k = kernel_for(a.nraw, a.kwin);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   k<<<grid, THREADS, sm, s>>>(a);
