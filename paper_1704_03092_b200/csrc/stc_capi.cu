@@ -796,7 +796,7 @@ int stc_fused_term_workspace_size(int64_t m, int64_t n, int64_t k, int n_a, int 
   const int64_t mp = rup(m, BM), np = rup(n, BN), kp = rup(k, BK);
   size_t pool = (size_t)(n_a * (mp + kp) + n_b * (np + kp) + n_c * (mp + np)) * 8;
   size_t tab = sizeof(TermDesc) + (size_t)(n_a + n_b) * sizeof(OpDesc) + (size_t)n_c * sizeof(TgtDesc);
-  if (bytes) *bytes = align256(pool) + align256(pool / BK) + align256(tab) + 256;
+  if (bytes) *bytes = align256(pool) + align256(pool / BK) + align256(tab) + 256;  // pool, kbs, tables, counter
   return STC_OK;
 }
 
@@ -858,7 +858,7 @@ int stc_fused_term(int64_t m, int64_t n, int64_t k, const double *A, int n_a, co
   td.c_count = n_c;
   int64_t *kbs = reinterpret_cast<int64_t *>(ws + align256((size_t)at * 8));
   CU(launch_chunk_strides(pool, at / BK, kbs, s), "k_chunk_strides");
-  char *tab = ws + align256((size_t)at * 8) + align256((size_t)at);
+  char *tab = ws + align256((size_t)at * 8) + align256((size_t)(at / BK) * 8);
   std::vector<char> host(sizeof(TermDesc) + ops.size() * sizeof(OpDesc) + tg.size() * sizeof(TgtDesc) + 8);
   size_t o = 0;
   memcpy(host.data() + o, &td, sizeof(td));
