@@ -304,14 +304,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_strassen_gemm(const GemmArgs p) 
 #pragma unroll
           for (int e = 0; e < EPT; ++e) acc[e] = first_term(src[raw_index(t, e)], u.signbit);
         } else {
-          const double s = u.sign;
+          // later views: acc + v or acc - v (a DADD; the sign is exact, so this equals
+          // the reference's acc + coeff * v)
+          if (u.signbit == 0) {
 #pragma unroll
-          for (int e = 0; e < EPT; ++e) {
-#ifdef STC_EXPERIMENT_INTADD
-            acc[e] = __longlong_as_double(__double_as_longlong(acc[e]) + __double_as_longlong(src[raw_index(t, e)]));
-#else
-            acc[e] += s * src[raw_index(t, e)];
-#endif
+            for (int e = 0; e < EPT; ++e) acc[e] = __dadd_rn(acc[e], src[raw_index(t, e)]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < EPT; ++e) acc[e] = __dsub_rn(acc[e], src[raw_index(t, e)]);
           }
         }
         if (++cslot == NRAW) cslot = 0;
