@@ -8,6 +8,8 @@
 // and replaces the CPU cache-blocking (driver.py:76-126) with one persistent
 // DMMA launch over all (term, tile) work items (ABC) or batched launches that
 // write dense M slots (AB / Naive).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -277,6 +279,7 @@ struct Plan {
   int64_t Q = 1;  // quadrants per dimension
   int nquads = 1;
   int a_kfast = 0, b_kfast = 0;
+  Tiling ti, tj, tp;  // tile orders of the I, J, P bundles
   std::vector<VecDesc> vecs;
   int64_t pool_len = 0;
   int64_t ar = 0, ac = 0, br = 0, bc = 0, cr = 0, cc = 0;  // pool starts
@@ -290,7 +293,7 @@ struct Plan {
   int grid = 1;
   // workspace layout (bytes)
   int max_ops = 1;  // most views on one side of any term (2^L)
-  size_t off_kbs = 0;
+  size_t off_kbs = 0, off_coords = 0;
   size_t off_pool = 0, off_vecs = 0, off_tab = 0, off_tickets = 0, off_counters = 0, off_M = 0, off_pa = 0,
          off_pb = 0, off_acc = 0, total = 0;
   size_t tab_bytes = 0, acc_bytes = 0;
@@ -379,6 +382,9 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   const Tiling ti = make_tiling(p->a_row, pl.level, key_i, ref);
   const Tiling tj = make_tiling(p->b_col, pl.level, key_j, ref);
   const Tiling tp = make_tiling(p->a_col, pl.level, key_p, ref);
+  pl.ti = ti;
+  pl.tj = tj;
+  pl.tp = tp;
   pl.a_kfast = a_min == 1;
   pl.b_kfast = b_min == 0;
 
@@ -474,6 +480,8 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   off = align256(off + (size_t)pl.pool_len * 8);
   pl.off_kbs = off;
   off = align256(off + (size_t)(pl.pool_len / BK) * 8);
+  pl.off_coords = off;  // fused kernel: int4 map coordinates per 8 pool entries
+  off = align256(off + (size_t)(pl.pool_len / 8) * 16);
   pl.off_vecs = off;
   off = align256(off + pl.vecs.size() * sizeof(VecDesc));
   pl.off_tab = off;
@@ -501,6 +509,306 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   if (pl.variant == STC_VARIANT_NAIVE) off = align256(off + (size_t)pl.batch * pl.pb_slot * 8);
   pl.total = off;
   return STC_OK;
+}
+
+
+// ------------------------------------------------------------ TMA staging
+// A side (A or B) can be staged with tensor-map box loads when every unit --
+// one view's 128-row tile x one 16-deep k-chunk -- is a box of the tensor:
+// the bundles' tile orders (make_tiling) cut tiles and chunks as aligned
+// sub-boxes, the tensor's unit-stride label leads the tile order of its
+// bundle, and the strides meet TMA's rules.  The map's dims are then ordered
+// so that the box lands as raw[k][128] (unit stride in x) or raw[x][16] (unit
+// stride in k, 16-element rows swizzled).  Otherwise the side uses the
+// cp.async gather (always correct; the reference's fast/slow split,
+// _jit.py:54-78, becomes TMA vs gather).
+struct TmaSide {
+  int rank = 0;
+  cuuint64_t dims[5];
+  cuuint64_t strides[4];  // bytes, dims 1..rank-1
+  cuuint32_t box[5];
+  int src[5];
+  int np[2] = {0, 0};
+  int64_t pstr[2][4];
+  int swizzle = 0;  // 0, 64 or 128 (bytes)
+};
+
+// Tile sub-box of a bundle: per label, the extent covered by one tile of
+// `tile` consecutive tile-order indices, and the labels in tile order.
+bool tile_subbox(const stc_bundle &b, const Tiling &t, int64_t tile, int64_t *tb, int *ord, int &nord) {
+  for (int d = 0; d < b.nlab; ++d) tb[d] = 1;
+  nord = 0;
+  int64_t rem = tile;
+  for (int j = 0; j < t.nbox && rem > 1; ++j) {
+    const int d = t.order[j];
+    const int64_t e = t.box_ext[d];
+    if (e == 1) continue;
+    if (rem >= e) {
+      if (rem % e) return false;
+      tb[d] = e;
+      rem /= e;
+    } else {
+      if (e % rem) return false;
+      tb[d] = rem;
+      rem = 1;
+    }
+    ord[nord++] = d;
+  }
+  return rem == 1;
+}
+
+bool plan_tma_side(const stc_bundle &xb, const Tiling &tx, const stc_bundle &kb, const Tiling &tk, int level, int kfast,
+                   const double *data, int64_t base, TmaSide &ts) {
+  if (tx.nbox == 0 || tk.nbox == 0) return false;
+  const int64_t Q = (int64_t)1 << level;
+  if ((bundle_len(xb) / Q) % BM != 0 || (bundle_len(kb) / Q) % BK != 0) return false;
+  int64_t tbx[STC_MAX_LABELS], tbk[STC_MAX_LABELS];
+  int ox[STC_MAX_LABELS], ok_[STC_MAX_LABELS], nox = 0, nok = 0;
+  if (!tile_subbox(xb, tx, BM, tbx, ox, nox) || !tile_subbox(kb, tk, BK, tbk, ok_, nok)) return false;
+  // map dims: the leading part (unit-stride side) in tile order, the other part, then box-1 labels
+  struct Dim {
+    int64_t ext, str, box;
+    bool isx;
+    int lab;
+  };
+  std::vector<Dim> dims;
+  auto push_ordered = [&](const stc_bundle &b, const int64_t *tb, const int *ord, int n, bool isx) {
+    for (int j = 0; j < n; ++j) dims.push_back({b.ext[ord[j]], b.str[ord[j]], tb[ord[j]], isx, ord[j]});
+  };
+  if (kfast) {
+    push_ordered(kb, tbk, ok_, nok, false);
+    push_ordered(xb, tbx, ox, nox, true);
+  } else {
+    push_ordered(xb, tbx, ox, nox, true);
+    push_ordered(kb, tbk, ok_, nok, false);
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    const stc_bundle &b = pass == 0 ? xb : kb;
+    const int64_t *tb = pass == 0 ? tbx : tbk;
+    for (int d = 0; d < b.nlab; ++d)
+      if (b.ext[d] > 1 && tb[d] == 1) dims.push_back({b.ext[d], b.str[d], 1, pass == 0, d});
+  }
+  if (dims.empty() || dims.size() > 5) return false;
+  if (dims[0].str != 1) return false;                          // unit stride leads the box
+  if (kfast && dims[0].box != BK) return false;                // one swizzled 128-byte row per x
+  if (!kfast && (dims[0].box * 8) % 16 != 0) return false;
+  for (size_t d = 0; d < dims.size(); ++d) {
+    if (dims[d].str <= 0 || dims[d].box > 256 || dims[d].ext >= (int64_t)1 << 31) return false;
+    if (d > 0 && ((dims[d].str % 2) != 0 || dims[d].str * 8 >= ((int64_t)1 << 40))) return false;
+  }
+  if ((reinterpret_cast<uintptr_t>(data + base) & 15) != 0) return false;
+  // coordinate parts: labels of each bundle by descending stride, strides nested
+  for (int part = 0; part < 2; ++part) {
+    std::vector<int> idx;
+    for (size_t d = 0; d < dims.size(); ++d)
+      if (dims[d].isx == (part == 0)) idx.push_back((int)d);
+    if (idx.empty() || idx.size() > 4) return false;
+    std::sort(idx.begin(), idx.end(), [&](int a, int b) { return dims[a].str > dims[b].str; });
+    for (size_t i = 0; i + 1 < idx.size(); ++i)
+      if (dims[idx[i]].str < dims[idx[i + 1]].str * dims[idx[i + 1]].ext) return false;
+    ts.np[part] = (int)idx.size();
+    for (size_t i = 0; i < idx.size(); ++i) {
+      ts.pstr[part][i] = dims[idx[i]].str;
+      ts.src[idx[i]] = part * 4 + (int)i;
+    }
+    for (size_t i = idx.size(); i < 4; ++i) ts.pstr[part][i] = 1;
+  }
+  ts.rank = (int)dims.size();
+  for (int d = 0; d < ts.rank; ++d) {
+    ts.dims[d] = (cuuint64_t)dims[d].ext;
+    ts.box[d] = (cuuint32_t)dims[d].box;
+    if (d > 0) ts.strides[d - 1] = (cuuint64_t)(dims[d].str * 8);
+  }
+  for (int d = ts.rank; d < 5; ++d) ts.src[d] = 0;
+  ts.swizzle = kfast ? 128 : 0;
+  return true;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool encode_side(const TmaSide &ts, const double *data, int64_t base, CUtensorMap &map) {
+  PFN_cuTensorMapEncodeTiled_v12000 fn = encode_fn();
+  if (!fn) return false;
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  if (const char *e = getenv("STC_TMA_PROMO"))
+    promo = atoi(e) == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+            : atoi(e) == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+            : atoi(e) == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  const CUresult r = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)ts.rank, (void *)(data + base), ts.dims,
+                        ts.strides, ts.box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        ts.swizzle == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : ts.swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                        promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Both sides of the operand views of `p` (A: I x P, B: P x J) as tensor maps;
+// false (gather path) unless both qualify.  STC_TMA=0 disables.
+bool plan_tma(const stc_problem *p, const Plan &pl, const double *A, const double *B, GemmArgs &g, CUtensorMap maps[2]) {
+  if (const char *e = getenv("STC_TMA"))
+    if (atoi(e) == 0) return false;
+  if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
+  TmaSide sa, sb;
+  if (!plan_tma_side(p->a_row, pl.ti, p->a_col, pl.tp, pl.level, pl.a_kfast, A, p->a_base, sa)) return false;
+  if (!plan_tma_side(p->b_col, pl.tj, p->b_row, pl.tp, pl.level, pl.b_kfast, B, p->b_base, sb)) return false;
+  int nraw = 0, kwin = 0;
+  if (!gemm_tma_config(pl.max_ops, nraw, kwin)) return false;
+  if (!encode_side(sa, A, p->a_base, maps[0]) || !encode_side(sb, B, p->b_base, maps[1])) return false;
+  const TmaSide *ss[2] = {&sa, &sb};
+  for (int sd = 0; sd < 2; ++sd) {
+    g.tm_rank[sd] = ss[sd]->rank;
+    for (int d = 0; d < 5; ++d) g.tm_src[sd][d] = ss[sd]->src[d];
+    for (int part = 0; part < 2; ++part) {
+      g.tm_np[sd][part] = ss[sd]->np[part];
+      for (int i = 0; i < 4; ++i) g.tm_pstr[sd][part][i] = ss[sd]->pstr[part][i];
+    }
+  }
+  // which pool vector carries the tensor's base offset (build_plan: ac for A, bc for B)
+  g.tm_base[0][0] = 0;
+  g.tm_base[0][1] = p->a_base;
+  g.tm_base[1][0] = p->b_base;
+  g.tm_base[1][1] = 0;
+  g.tma = 1;
+  // prefetch distance: what the k-coordinate window keeps ready (KWIN/2 chunks minus the issue lookahead)
+  int pf = std::min(16, (kwin / 2 - 2) * 2);
+  if (const char *e = getenv("STC_TMA_PF")) pf = atoi(e);
+  g.tma_prefetch = std::max(0, pf);
+  g.nraw = nraw;
+  g.kwin = kwin;
+  return true;
+}
+
+
+// ---- fused kernel (stc_fused.cu) -----------------------------------------------
+// Same regularity conditions as plan_tma_side, for 128 x 8 views whose boxes
+// land in the fused kernel's swizzled layouts: unit stride in x -> dims
+// (x_lo 16, k..., x_hi...), 128-byte swizzle; unit stride in k -> dims
+// (k 8, x...), 64-byte swizzle.  The unit-stride label is split into a 16-wide
+// low dim and a high dim when its tile extent exceeds 16.
+constexpr int kFusedK = 8;
+
+bool plan_fused_side(const stc_bundle &xb, const Tiling &tx, const stc_bundle &kb, const Tiling &tk, int level,
+                     int kfast, const double *data, int64_t base, TmaSide &ts) {
+  if (tx.nbox == 0 || tk.nbox == 0) return false;
+  const int64_t Q = (int64_t)1 << level;
+  if ((bundle_len(xb) / Q) % BM != 0 || (bundle_len(kb) / Q) % BK != 0) return false;
+  int64_t tbx[STC_MAX_LABELS], tbk[STC_MAX_LABELS];
+  int ox[STC_MAX_LABELS], ok_[STC_MAX_LABELS], nox = 0, nok = 0;
+  if (!tile_subbox(xb, tx, BM, tbx, ox, nox) || !tile_subbox(kb, tk, kFusedK, tbk, ok_, nok)) return false;
+  struct Dim {
+    int64_t ext, str, box;
+    bool isx;
+  };
+  std::vector<Dim> dims;
+  if (kfast) {
+    if (nok == 0 || kb.str[ok_[0]] != 1 || tbk[ok_[0]] != kFusedK) return false;
+    for (int j = 0; j < nok; ++j) dims.push_back({kb.ext[ok_[j]], kb.str[ok_[j]], tbk[ok_[j]], false});
+    for (int j = 0; j < nox; ++j) dims.push_back({xb.ext[ox[j]], xb.str[ox[j]], tbx[ox[j]], true});
+  } else {
+    if (nox == 0 || xb.str[ox[0]] != 1) return false;
+    const int64_t e0 = xb.ext[ox[0]], b0 = tbx[ox[0]];
+    if (b0 < 16 || b0 % 16 != 0 || (b0 > 16 && e0 % 16 != 0)) return false;
+    dims.push_back({b0 > 16 ? 16 : e0, 1, 16, true});
+    for (int j = 0; j < nok; ++j) dims.push_back({kb.ext[ok_[j]], kb.str[ok_[j]], tbk[ok_[j]], false});
+    if (b0 > 16) dims.push_back({e0 / 16, 16, b0 / 16, true});
+    for (int j = 1; j < nox; ++j) dims.push_back({xb.ext[ox[j]], xb.str[ox[j]], tbx[ox[j]], true});
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    const stc_bundle &b = pass == 0 ? xb : kb;
+    const int64_t *tb = pass == 0 ? tbx : tbk;
+    for (int d = 0; d < b.nlab; ++d)
+      if (b.ext[d] > 1 && tb[d] == 1) dims.push_back({b.ext[d], b.str[d], 1, pass == 0});
+  }
+  if (dims.empty() || dims.size() > 5) return false;
+  for (size_t d = 0; d < dims.size(); ++d) {
+    if (dims[d].str <= 0 || dims[d].box > 256 || dims[d].ext >= (int64_t)1 << 31) return false;
+    if (d > 0 && ((dims[d].str % 2) != 0 || dims[d].str * 8 >= ((int64_t)1 << 40))) return false;
+  }
+  if ((reinterpret_cast<uintptr_t>(data + base) & 15) != 0) return false;
+  for (int part = 0; part < 2; ++part) {
+    std::vector<int> idx;
+    for (size_t d = 0; d < dims.size(); ++d)
+      if (dims[d].isx == (part == 0)) idx.push_back((int)d);
+    if (idx.empty() || idx.size() > 4) return false;
+    std::sort(idx.begin(), idx.end(), [&](int a, int b) { return dims[a].str > dims[b].str; });
+    for (size_t i = 0; i + 1 < idx.size(); ++i)
+      if (dims[idx[i]].str < dims[idx[i + 1]].str * dims[idx[i + 1]].ext) return false;
+    ts.np[part] = (int)idx.size();
+    for (size_t i = 0; i < idx.size(); ++i) {
+      ts.pstr[part][i] = dims[idx[i]].str;
+      ts.src[idx[i]] = part * 4 + (int)i;
+    }
+    for (size_t i = idx.size(); i < 4; ++i) ts.pstr[part][i] = 1;
+  }
+  ts.rank = (int)dims.size();
+  for (int d = 0; d < ts.rank; ++d) {
+    ts.dims[d] = (cuuint64_t)dims[d].ext;
+    ts.box[d] = (cuuint32_t)dims[d].box;
+    if (d > 0) ts.strides[d - 1] = (cuuint64_t)(dims[d].str * 8);
+  }
+  for (int d = ts.rank; d < 5; ++d) ts.src[d] = 0;
+  ts.swizzle = kfast ? 64 : 128;
+  return true;
+}
+
+// Fused-kernel plan for ABC / AB (terms of at most 8 views per chunk: L <= 2):
+// tensor maps, the coordinate-table jobs and the kernel arguments.
+// STC_FUSED=0 disables.
+bool plan_fused(const stc_problem *p, const Plan &pl, const double *A, const double *B, GemmArgs &g, CUtensorMap maps[2],
+                CoordJobs &jobs) {
+  if (const char *e = getenv("STC_FUSED"))
+    if (atoi(e) == 0) return false;
+  if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
+  const int umax = 2 * pl.max_ops;
+  const int S = fused_stages(umax);
+  if (umax > 8 || S < 2) return false;
+  TmaSide sa, sb;
+  if (!plan_fused_side(p->a_row, pl.ti, p->a_col, pl.tp, pl.level, pl.a_kfast, A, p->a_base, sa)) return false;
+  if (!plan_fused_side(p->b_col, pl.tj, p->b_row, pl.tp, pl.level, pl.b_kfast, B, p->b_base, sb)) return false;
+  if (!encode_side(sa, A, p->a_base, maps[0]) || !encode_side(sb, B, p->b_base, maps[1])) return false;
+  const TmaSide *ss[2] = {&sa, &sb};
+  for (int sd = 0; sd < 2; ++sd) {
+    g.tm_rank[sd] = ss[sd]->rank;
+    for (int d = 0; d < 5; ++d) g.tm_src[sd][d] = ss[sd]->src[d];
+    for (int part = 0; part < 2; ++part) {
+      g.tm_np[sd][part] = ss[sd]->np[part];
+      for (int i = 0; i < 4; ++i) g.tm_pstr[sd][part][i] = ss[sd]->pstr[part][i];
+    }
+  }
+  // pool vectors: ar (A x, base 0), ac (A k, base a_base), br (B k, base 0), bc (B x, base b_base)
+  struct V {
+    int64_t start, len;
+    int sd, part;
+    int64_t base;
+  } vs[4] = {{pl.ar, pl.Q * rup(cdiv(bundle_len(p->a_row), pl.Q), BM), 0, 0, 0},
+             {pl.ac, pl.Q * rup(cdiv(bundle_len(p->a_col), pl.Q), BK), 0, 1, p->a_base},
+             {pl.br, pl.Q * rup(cdiv(bundle_len(p->b_row), pl.Q), BK), 1, 1, 0},
+             {pl.bc, pl.Q * rup(cdiv(bundle_len(p->b_col), pl.Q), BN), 1, 0, p->b_base}};
+  jobs.n = 4;
+  for (int j = 0; j < 4; ++j) {
+    CoordJob &jb = jobs.job[j];
+    jb.start = vs[j].start;
+    jb.count = vs[j].len / 8;
+    jb.base = vs[j].base;
+    jb.np = ss[vs[j].sd]->np[vs[j].part];
+    for (int i = 0; i < 4; ++i) jb.str[i] = ss[vs[j].sd]->pstr[vs[j].part][i];
+  }
+  g.tma = 0;
+  g.umax = umax;
+  g.stages = S;
+  g.kchunks = (int)(pl.kq_pad / kFusedK);
+  return true;
 }
 
 }  // namespace
@@ -538,6 +846,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
   char *ws = reinterpret_cast<char *>(workspace);
   int64_t *pool = reinterpret_cast<int64_t *>(ws + pl.off_pool);
   int64_t launches = 0;
+  bool tma = false;  // operand units staged by tensor-map box loads
   stc_stats st{};
 
   // subsystem (1): scatter vectors on the device
@@ -592,8 +901,22 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
     g.use_tickets = T > 1;
     g.counter = counters;
     const int grid = (int)std::min<int64_t>(pl.grid, g.total_items);
-    if (g_ev_before) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
-    CU(launch_gemm(g, grid, s), "k_strassen_gemm");
+    CUtensorMap maps[2];
+    CoordJobs jobs{};
+    GemmArgs gf = g;
+    if (plan_fused(p, pl, A, B, gf, maps, jobs)) {
+      // fused kernel: TMA boxes of 128 x 8, sums in the consumers' fragment loads
+      tma = true;
+      gf.coords = reinterpret_cast<const int4 *>(ws + pl.off_coords);
+      CU(launch_pool_coords(pool, reinterpret_cast<int4 *>(ws + pl.off_coords), jobs, s), "k_pool_coords");
+      ++launches;
+      if (g_ev_before) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
+      CU(launch_fused(gf, grid, s, maps), "k_strassen_fused");
+    } else {
+      tma = plan_tma(p, pl, A, B, g, maps);
+      if (g_ev_before) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
+      CU(launch_gemm(g, grid, s, tma ? maps : nullptr), "k_strassen_gemm");
+    }
     if (g_ev_after) CU(cudaEventRecord(g_ev_after, s), "cudaEventRecord");
     ++launches;
     st.fast_updates = 0;
@@ -753,7 +1076,9 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
     }
   }
   st.total_flops = 2.0 * BM * BN * (double)pl.kq_pad * (double)P * (double)T;
-  st.slow_blocks += 2 * (int64_t)(pl.kq_pad / BK) * P * T;
+  // operand blocks (one view of one side x one k-chunk per tile): TMA-staged
+  // boxes are the reference's fast (constant-stride) blocks
+  (tma ? st.fast_blocks : st.slow_blocks) += 2 * (int64_t)(pl.kq_pad / BK) * P * T;
   st.leaf_multiplies = T;
   st.work_items = P * T;
   st.kernel_launches = launches;

@@ -1,0 +1,438 @@
+// stc_fused.cu -- the TMA Strassen kernel: operand sums fused into the DMMA
+// fragment loads (north-star subsystems 2 + 3, regular layouts).
+//
+// When every view of both operand sides is a regular box of its tensor (host
+// check in stc_capi.cu: plan_fused), one producer warp stages each k-chunk's
+// raw views -- all views of the term's A side and B side, 128 x 8 doubles each
+// -- with one cp.async.bulk.tensor box load per view into a swizzled smem
+// stage, and the eight consumer warps form the Strassen sums (A0 + A3, B1 - B3,
+// ... in the reference's view order and rounding, _jit.py:27-131) directly
+// while loading their mma.sync.m16n8k4 fragments.  Nothing is written back to
+// shared memory and no producer thread touches the FP64 pipe, which the DMMAs
+// occupy; the consumers' own DADDs interleave with their DMMAs in program
+// order.  The epilogue (stc_common.cuh) is shared with the gather kernel.
+//
+// Raw view layouts (element offsets inside one 1024-double view; both read
+// conflict-free by the fragment pattern lanes = (g: 8 x) x (tig: 4 k)):
+//   unit stride in x:  row (k + 8 * (x / 16)) of 16 doubles, 128-byte swizzle
+//   unit stride in k:  row x of 8 doubles, 64-byte swizzle
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "stc_common.cuh"
+#include "stc_internal.cuh"
+#include "stc_ptx.cuh"
+
+namespace stc {
+
+constexpr int FK = 8;                        // k-chunk of the fused kernel
+constexpr int VIEW_DOUBLES = BM * FK;        // one raw view of one chunk (BM == BN)
+constexpr int FUSED_PRODUCER_WARPS = 4;  // one warpgroup (setmaxnreg is warpgroup-wide); warp 0 of it issues
+constexpr int FUSED_THREADS = 32 * (CONSUMER_WARPS + FUSED_PRODUCER_WARPS);
+constexpr int FUSED_CONSUMER_REGS = 232;
+constexpr int FUSED_PRODUCER_REGS = 24;
+constexpr int MAX_FUSED_STAGES = 8;
+
+struct FusedLayout {
+  __host__ __device__ static size_t stage_bytes(int umax) { return (size_t)umax * VIEW_DOUBLES * 8; }
+  __host__ __device__ static size_t bar_off(int umax, int stages) { return (size_t)stages * stage_bytes(umax); }
+  __host__ __device__ static size_t meta_off(int umax, int stages) { return bar_off(umax, stages) + 16 * (size_t)stages; }
+  __host__ __device__ static size_t bytes(int umax, int stages) { return meta_off(umax, stages) + 4 * (size_t)stages + 16; }
+};
+
+constexpr size_t kFusedMaxSmem = 227 * 1024;
+
+// Stages of the fused ring for terms of at most `umax` views per chunk (0: does not fit).
+int fused_stages(int umax) {
+  int s = MAX_FUSED_STAGES;
+  while (s >= 2 && FusedLayout::bytes(umax, s) > kFusedMaxSmem) --s;
+  return s >= 2 ? s : 0;
+}
+
+// Element offset of (x, k) inside a raw view.
+__host__ __device__ __forceinline__ int view_index(int kfast, int x, int k) {
+  if (!kfast) return (k + 8 * (x >> 4)) * 16 + ((((x & 15) >> 1) ^ k) << 1) + (x & 1);
+  return x * 8 + ((((k >> 1) ^ (x >> 1)) & 3) << 1) + (k & 1);
+}
+
+__device__ __forceinline__ void mbar_expect_tx_f(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void tma_box_f(void *dst, const CUtensorMap *map, int rank, const int32_t (&c)[5],
+                                          uint64_t *bar) {
+  const uint32_t d = smem_u32(dst), b = smem_u32(bar);
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  switch (rank) {
+    case 2:
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(d),
+          "l"(m), "r"(c[0]), "r"(c[1]), "r"(b)
+          : "memory");
+      break;
+    case 3:
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(d),
+          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(b)
+          : "memory");
+      break;
+    case 4:
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(d),
+          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(b)
+          : "memory");
+      break;
+    default:
+      asm volatile(
+          "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(d),
+          "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(b)
+          : "memory");
+      break;
+  }
+}
+
+__device__ __forceinline__ int coord_of(const int4 &v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
+// Sum of the views [v0, v0 + n) of one side at the element offsets `off[i]`
+// (I values), in view order: acc = s0 * V0; acc = acc +/- V_v.  The reference's
+// leading 0.0 + (_jit.py:43-65) only turns an operand -0.0 into +0.0, which
+// cannot change C: the DMMA accumulators start at +0.0, and adding a zero
+// product of either sign to them gives the same result.
+__device__ __forceinline__ double flip_sign(double v) {
+  return __hiloint2double(__double2hiint(v) ^ static_cast<int>(0x80000000u), __double2loint(v));
+}
+
+template <int I>
+__device__ __forceinline__ void side_sum(double (&out)[I], const double *st, int v0, int n, uint32_t negmask,
+                                         const int (&off)[I]) {
+  {
+    const double *src = st + v0 * VIEW_DOUBLES;
+#pragma unroll
+    for (int i = 0; i < I; ++i) out[i] = src[off[i]];
+    if ((negmask >> v0) & 1u) {
+#pragma unroll
+      for (int i = 0; i < I; ++i) out[i] = flip_sign(out[i]);
+    }
+  }
+  for (int v = 1; v < n; ++v) {
+    const double *src = st + (v0 + v) * VIEW_DOUBLES;
+    double t[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) t[i] = src[off[i]];
+    if ((negmask >> (v0 + v)) & 1u) {
+#pragma unroll
+      for (int i = 0; i < I; ++i) out[i] = __dsub_rn(out[i], t[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < I; ++i) out[i] = __dadd_rn(out[i], t[i]);
+    }
+  }
+}
+
+
+// One view step of the consumer pipeline (V: view index, KN: k-step of the
+// fragments being built; compile-time): load view V of the next k-step and
+// fold it into the next step's fragments (sign flip for the side's first view,
+// DADD of the signed value otherwise -- the reference's view order), then issue
+// MMA group V of the current k-step.  Loads go in groups of four values to keep
+// the register footprint inside the consumers' budget.
+template <int NA, int NB, int V, int KN, bool MMA>
+__device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (&fa)[8], const double (&fb)[4],
+                                          double (&xa)[8], double (&xb)[4], const double *nst, bool load,
+                                          const int (&offA)[2][2], const int (&offB)[2][2], uint32_t negmask) {
+  constexpr int G = NA + NB;
+  const int fl = static_cast<int>(((negmask >> V) & 1u) << 31);
+  const double *src = nst + V * VIEW_DOUBLES;
+  if (load) {
+    if constexpr (V < NA) {
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {  // mt pairs {0, 1}, {2, 3}
+        double t[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) t[j] = src[offA[KN][j & 1] + 128 * (2 * hh + (j >> 1))];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double sv = __hiloint2double(__double2hiint(t[j]) ^ fl, __double2loint(t[j]));
+          xa[4 * hh + j] = V == 0 ? sv : __dadd_rn(xa[4 * hh + j], sv);
+        }
+      }
+    } else {
+      double t[4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) t[nt] = src[offB[KN][nt & 1] + 128 * (nt >> 1)];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const double sv = __hiloint2double(__double2hiint(t[nt]) ^ fl, __double2loint(t[nt]));
+        xb[nt] = V == NA ? sv : __dadd_rn(xb[nt], sv);
+      }
+    }
+  }
+  if constexpr (MMA) {
+#pragma unroll
+    for (int i = 16 * V / G; i < 16 * (V + 1) / G; ++i)
+      dmma_16x8x4(acc[i >> 2][i & 3], fa[2 * (i >> 2)], fa[2 * (i >> 2) + 1], fb[i & 3]);
+  }
+  if constexpr (V + 1 < G) pipe_view<NA, NB, V + 1, KN, MMA>(acc, fa, fb, xa, xb, nst, load, offA, offB, negmask);
+}
+
+// One work item's main loop for terms with NA A-views and NB B-views
+// (compile-time): a software pipeline over the item's 4-deep k-steps (two per
+// 8-deep chunk, fragments ping-ponging between two register sets).  While the
+// 16 MMAs of one k-step issue in NA + NB groups, the fragments of the next
+// k-step are built one view per group, so no DADD waits on a result it needs
+// right away behind the DMMAs queued on the shared FP64 pipe.  A chunk stage
+// is released as soon as both of its k-steps are in registers.
+template <int NA, int NB>
+__device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const double *stages, int umax, int S,
+                                             uint64_t *full, uint64_t *empty, int &stage, uint32_t &phase, int kchunks,
+                                             uint32_t negmask, const int (&offA)[2][2], const int (&offB)[2][2],
+                                             int lane) {
+  const size_t sstride = (size_t)umax * VIEW_DOUBLES;
+  double fa[8], fb[4], xa[8], xb[4];
+  pipe_view<NA, NB, 0, 0, false>(acc, fa, fb, fa, fb, stages + stage * sstride, true, offA, offB, negmask);
+  for (int c = 0; c < kchunks; ++c) {
+    // k-step 0 of chunk c (fa, fb) -> build k-step 1 of chunk c (xa, xb)
+    pipe_view<NA, NB, 0, 1, true>(acc, fa, fb, xa, xb, stages + stage * sstride, true, offA, offB, negmask);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);  // both k-steps of chunk c are in registers
+    if (++stage == S) {
+      stage = 0;
+      phase ^= 1;
+    }
+    // k-step 1 of chunk c (xa, xb) -> build k-step 0 of chunk c + 1 (fa, fb)
+    const bool more = c + 1 < kchunks;
+    if (more) mbar_wait(&full[stage], phase);
+    pipe_view<NA, NB, 0, 0, true>(acc, xa, xb, fa, fb, stages + stage * sstride, more, offA, offB, negmask);
+  }
+}
+
+template <int AKF, int BKF>
+__global__ void __launch_bounds__(FUSED_THREADS, 1)
+    k_strassen_fused(const GemmArgs p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int umax = p.umax, S = p.stages;
+  double *stages = reinterpret_cast<double *>(smem);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + FusedLayout::bar_off(umax, S));
+  uint64_t *empty = full + S;
+  int *stage_item = reinterpret_cast<int *>(smem + FusedLayout::meta_off(umax, S));
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CONSUMER_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int kchunks = p.kchunks;  // 8-deep chunks
+
+  if (warp >= CONSUMER_WARPS) {
+    // ===================== producer warp: TMA box loads ================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(FUSED_PRODUCER_REGS));
+    if (warp != CONSUMER_WARPS) return;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (;;) {
+      int item = 0;
+      if (lane == 0) item = atomicAdd(p.counter, 1);
+      item = __shfl_sync(0xffffffffu, item, 0);
+      if (item >= p.total_items) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0) {
+          stage_item[stage] = -1;
+          mbar_arrive(&full[stage]);
+        }
+        break;
+      }
+      int slot, ti, tj;
+      tile_of(p, item, slot, ti, tj);
+      const TermDesc td = p.terms[slot];
+      const int na = td.a_count, U = td.a_count + td.b_count;
+      // lane u < U stages view u (A views first, then B views) of every chunk
+      int sd = 0;
+      int64_t kst = 0;
+      int4 xc = make_int4(0, 0, 0, 0);
+      if (lane < U) {
+        sd = lane < na ? 0 : 1;
+        const OpDesc o = p.ops[sd == 0 ? td.a_first + lane : td.b_first + lane - na];
+        xc = p.coords[(o.x_start + (int64_t)(sd == 0 ? ti * BM : tj * BN)) >> 3];
+        kst = o.k_start;
+      }
+      const CUtensorMap *map = sd == 0 ? &tmA : &tmB;
+      const int rank = p.tm_rank[sd];
+      int src[5];
+#pragma unroll
+      for (int d = 0; d < 5; ++d) src[d] = p.tm_src[sd][d];
+      const uint32_t bytes = (uint32_t)U * VIEW_DOUBLES * 8;
+      for (int c = 0; c < kchunks; ++c) {
+        int4 kc = make_int4(0, 0, 0, 0);
+        if (lane < U) kc = p.coords[(kst + (int64_t)c * FK) >> 3];
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0) {
+          stage_item[stage] = item;
+          mbar_expect_tx_f(&full[stage], bytes);
+        }
+        __syncwarp();
+        if (lane < U) {
+          int32_t cc[5];
+#pragma unroll
+          for (int d = 0; d < 5; ++d) cc[d] = src[d] < 4 ? coord_of(xc, src[d]) : coord_of(kc, src[d] - 4);
+          tma_box_f(stages + ((size_t)stage * umax + lane) * VIEW_DOUBLES, map, rank, cc, &full[stage]);
+        }
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===================== consumer warps: sums + DMMA + epilogue =====
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(FUSED_CONSUMER_REGS));
+    const int g = lane >> 2, tig = lane & 3;
+    const int wm = warp & 1, wn = warp >> 1;
+    // Fragment offsets inside a view: A (kk, h) + 128 * mt; B (kk, nt & 1) + 128 * (nt >> 1).
+    // MMA row m of each 16-row block reads tile row pi(m) = (m & 1) + 2 ((m >> 3) & 1) +
+    // 4 ((m >> 1) & 3) (columns likewise within 16-column pairs): with it the 128-byte
+    // swizzle spreads a fragment load over all 16 8-byte bank pairs (the identity
+    // would hit 8); the epilogue maps rows / columns back (epilogue_store<true>).
+    int offA[2][2], offB[2][2];
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int pm = (g & 1) + 2 * h + 4 * (g >> 1);
+        offA[kk][h] = view_index(AKF, wm * 64 + pm, kk * 4 + tig);
+        offB[kk][h] = view_index(BKF, wn * 32 + pm, kk * 4 + tig);
+      }
+    int stage = 0;
+    uint32_t phase = 0;
+    double acc[4][4][4];
+    for (;;) {
+      mbar_wait(&full[stage], phase);
+      const int item = stage_item[stage];
+      if (item < 0) break;
+      int slot, ti, tj;
+      tile_of(p, item, slot, ti, tj);
+      const TermDesc td = p.terms[slot];
+      const int na = td.a_count, nb = td.b_count;
+      uint32_t negmask = 0;
+      for (int u = 0; u < na + nb; ++u) {
+        const double sg = p.ops[u < na ? td.a_first + u : td.b_first + u - na].sign;
+        negmask |= (__double_as_longlong(sg) < 0 ? 1u : 0u) << u;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
+      switch (na * 8 + nb) {
+        case 9: consume_item<1, 1>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        case 10: consume_item<1, 2>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        case 17: consume_item<2, 1>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        case 18: consume_item<2, 2>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        case 12: consume_item<1, 4>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        case 33: consume_item<4, 1>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        case 20: consume_item<2, 4>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        case 34: consume_item<4, 2>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        case 36: consume_item<4, 4>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        default:  // other view counts (not produced by the Strassen recursion)
+          for (int kc = 0; kc < kchunks; ++kc) {
+            if (kc > 0) mbar_wait(&full[stage], phase);
+            const double *st = stages + (size_t)stage * umax * VIEW_DOUBLES;
+            double a[2][8], b[2][4];
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+              int oa[8], ob[4];
+#pragma unroll
+              for (int mt = 0; mt < 4; ++mt) {
+                oa[2 * mt] = offA[kk][0] + 128 * mt;
+                oa[2 * mt + 1] = offA[kk][1] + 128 * mt;
+              }
+#pragma unroll
+              for (int nt = 0; nt < 4; ++nt) ob[nt] = offB[kk][nt & 1] + 128 * (nt >> 1);
+              side_sum<8>(a[kk], st, 0, na, negmask, oa);
+              side_sum<4>(b[kk], st, na, nb, negmask, ob);
+            }
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+              for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt)
+                  dmma_16x8x4(acc[mt][nt], a[kk][2 * mt], a[kk][2 * mt + 1], b[kk][nt]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          break;
+      }
+      epilogue_store<true>(p, acc, item, tid, wm, wn, g, tig);
+    }
+  }
+}
+
+using FusedKernel = void (*)(const GemmArgs, const CUtensorMap, const CUtensorMap);
+
+static FusedKernel fused_for(int akf, int bkf) {
+  if (akf) return bkf ? k_strassen_fused<1, 1> : k_strassen_fused<1, 0>;
+  return bkf ? k_strassen_fused<0, 1> : k_strassen_fused<0, 0>;
+}
+
+cudaError_t launch_fused(const GemmArgs &a, int grid, cudaStream_t s, const void *maps) {
+  const size_t sm = FusedLayout::bytes(a.umax, a.stages);
+  FusedKernel k = fused_for(a.a_kfast, a.b_kfast);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  CUtensorMap m[2];
+  memcpy(m, maps, sizeof(m));
+  k<<<grid, FUSED_THREADS, sm, s>>>(a, m[0], m[1]);
+  return cudaGetLastError();
+}
+
+// ---- coordinate table --------------------------------------------------------
+// coords[i] = tensor-map coordinates (one part: x or k) of pool entry 8 i, for
+// the pool ranges of the operand vectors: the producer warp reads one int4 per
+// view and chunk instead of dividing.
+__global__ void k_pool_coords(const int64_t *__restrict__ pool, int4 *__restrict__ coords, CoordJobs jobs) {
+  for (int j = 0; j < jobs.n; ++j) {
+    const CoordJob &jb = jobs.job[j];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < jb.count; i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t e = jb.start / 8 + i;
+      const int64_t v = pool[e * 8];
+      int32_t c[4] = {0, 0, 0, 0};
+      if (v != kPad) {
+        int64_t off = v - jb.base;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < jb.np) {
+            const int64_t d = off / jb.str[q];
+            c[q] = (int32_t)d;
+            off -= d * jb.str[q];
+          }
+      }
+      coords[e] = make_int4(c[0], c[1], c[2], c[3]);
+    }
+  }
+}
+
+cudaError_t launch_pool_coords(const int64_t *pool, int4 *coords, const CoordJobs &jobs, cudaStream_t s) {
+  int64_t mx = 0;
+  for (int j = 0; j < jobs.n; ++j) mx = std::max(mx, jobs.job[j].count);
+  if (mx == 0) return cudaSuccess;
+  const int threads = 256;
+  const int blocks = (int)std::min<int64_t>((mx + threads - 1) / threads, 148 * 8);
+  k_pool_coords<<<blocks, threads, 0, s>>>(pool, coords, jobs);
+  return cudaGetLastError();
+}
+
+}  // namespace stc

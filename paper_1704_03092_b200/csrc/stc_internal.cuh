@@ -74,6 +74,33 @@ struct GemmArgs {
   int64_t m_ld, m_stride;
   int32_t *tickets;
   int32_t *counter;
+  // TMA box staging (both sides regular; see stc_tma.cu).  A side whose unit
+  // stride is an x label lands as raw[k][128]; one whose unit stride is a k
+  // label lands as raw[x][16] with the 128-byte swizzle.  Map dim d of side s
+  // takes coordinate tm_src[s][d] of the concatenated (x part, k part) vector;
+  // each part is decomposed from its pool offset by descending strides.
+  int32_t tma;
+  int32_t tma_prefetch;      // L2 prefetch distance (units) beyond the raw-slot lookahead
+  int32_t tm_rank[2];
+  int32_t tm_src[2][5];
+  int32_t tm_np[2][2];       // dims in the x / k part
+  int64_t tm_pstr[2][2][4];  // part strides, descending
+  int64_t tm_base[2][2];     // subtracted from the x / k pool entries (the map's base offset)
+  // fused kernel (stc_fused.cu)
+  const int4 *coords;        // coords[i]: map coordinates (one part) of pool entry 8 i
+  int32_t umax, stages;      // views per chunk stage (2 * max_ops), ring depth
+};
+
+// Jobs of k_pool_coords: one per operand pool vector (x or k part of A or B).
+struct CoordJob {
+  int64_t start, count;  // pool index of the first entry (multiple of 8), entries / 8
+  int64_t base;          // subtracted before the decomposition (the map's base offset)
+  int64_t str[4];        // part strides, descending
+  int32_t np, _pad;
+};
+struct CoordJobs {
+  CoordJob job[4];
+  int32_t n, _pad;
 };
 
 // Descriptor of one pool vector built on the device (subsystem 1).
@@ -127,7 +154,11 @@ size_t gemm_smem_bytes(int max_ops);
 int gemm_nraw(int max_ops);
 int gemm_kwin(int max_ops);
 cudaError_t launch_chunk_strides(const int64_t *pool, int64_t nchunks, int64_t *kbs, cudaStream_t s);
-cudaError_t launch_gemm(const GemmArgs &a, int grid, cudaStream_t s);
+cudaError_t launch_gemm(const GemmArgs &a, int grid, cudaStream_t s, const void *maps = nullptr);
+int gemm_tma_config(int max_ops, int &nraw, int &kwin);
+int fused_stages(int umax);
+cudaError_t launch_fused(const GemmArgs &a, int grid, cudaStream_t s, const void *maps);
+cudaError_t launch_pool_coords(const int64_t *pool, int4 *coords, const CoordJobs &jobs, cudaStream_t s);
 int gemm_max_grid(int max_ops);
 cudaError_t launch_accumulate(const AccArgs &a, cudaStream_t s);
 cudaError_t launch_unpack(const UnpackArgs &a, cudaStream_t s);
