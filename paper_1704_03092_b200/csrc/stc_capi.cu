@@ -1059,8 +1059,22 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       g.m_stride = pl.m_slot;
       g.counter = counters + bi;
       const int grid = (int)std::min<int64_t>(pl.grid, g.total_items);
+      CUtensorMap maps[2];
+      CoordJobs jobs{};
+      GemmArgs gf = g;
+      const bool fused = !naive && plan_fused(p, pl, A, B, gf, maps, jobs);
+      if (fused && bi == 0) {
+        CU(launch_pool_coords(pool, reinterpret_cast<int4 *>(ws + pl.off_coords), jobs, s), "k_pool_coords");
+        ++launches;
+      }
       if (g_ev_before && bi == 0) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
-      CU(launch_gemm(g, grid, s), "k_strassen_gemm(dense)");
+      if (fused) {
+        tma = true;
+        gf.coords = reinterpret_cast<const int4 *>(ws + pl.off_coords);
+        CU(launch_fused(gf, grid, s, maps), "k_strassen_fused(dense)");
+      } else {
+        CU(launch_gemm(g, grid, s), "k_strassen_gemm(dense)");
+      }
       if (g_ev_after && bi == pl.nbatches - 1) CU(cudaEventRecord(g_ev_after, s), "cudaEventRecord");
       aa.M = M;
       aa.m_ld = pl.nq_pad;

@@ -1,0 +1,96 @@
+"""GPU parity of the fused TMA kernel (stc_fused.cu) on layouts it accepts.
+
+Each case is a 1024^3 contraction whose views are regular boxes, one per
+combination of unit-stride sides (A unit stride in x or k, B unit stride in x
+or k), so both raw-view layouts (128-byte swizzled x rows, 64-byte swizzled k
+rows) and the fragment permutation are exercised.  Checks:
+  * the fused kernel ran (one extra launch: the coordinate table);
+  * its C equals the gather kernel's C bitwise (same view order, same DMMA
+    k order), for ABC and AB at levels 0..2;
+  * normwise relative error <= 1e-12 against the CPU oracle's classical
+    contraction (the reference suite's bound; the north star's gate is 1e-10).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1704_03092_b200 as stc
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+LAYOUTS = {
+    # A unit stride in x (b), B unit stride in k (e) -- the BASELINE cfg2 pattern
+    "ax_bk": "aibj eafb jfie & a:16;b:64;i:16;j:64;e:64;f:16;",
+    # A unit stride in k (f), B unit stride in x (j) -- the 16384^3 bar pattern
+    "ak_bx": "abij abef efij & a:16;b:64;i:16;j:64;e:16;f:64;",
+    # both unit strides in x
+    "ax_bx": "abij eafb efij & a:16;b:64;i:16;j:64;e:16;f:64;",
+    # both unit strides in k
+    "ak_bk": "abij abef ijef & a:16;b:64;i:16;j:64;e:16;f:64;",
+}
+
+
+def _operands(spec, seed):
+    a = stc.make_dense_tensor(spec.tensor_extents(spec.labels_a), "random", seed)
+    b = stc.make_dense_tensor(spec.tensor_extents(spec.labels_b), "random", seed + 1)
+    c = stc.make_dense_tensor(spec.tensor_extents(spec.labels_c), "random", seed + 2)
+    return a.to_device(), b.to_device(), c
+
+
+def _run(spec, a, b, c0, level, variant, fused):
+    old = os.environ.get("STC_FUSED")
+    os.environ["STC_FUSED"] = "1" if fused else "0"
+    try:
+        c = c0.to_device()
+        st = stc.contract(spec, a, b, c, level, variant)
+        return c.to_host(), st
+    finally:
+        if old is None:
+            del os.environ["STC_FUSED"]
+        else:
+            os.environ["STC_FUSED"] = old
+
+
+@pytest.mark.parametrize("name", sorted(LAYOUTS))
+def test_fused_matches_gather_bitwise_and_classical(name):
+    spec = stc.parse_benchmark_line(LAYOUTS[name])
+    a, b, c0 = _operands(spec, 11)
+    classical = c0.copy()
+    oracle.contract_reference(spec, a.to_host(), b.to_host(), classical)
+    for level in (0, 1, 2):
+        for variant in ("abc", "ab"):
+            cf, stf = _run(spec, a, b, c0, level, variant, True)
+            cg, stg = _run(spec, a, b, c0, level, variant, False)
+            assert stf.kernel_launches == stg.kernel_launches + 1, (name, level, variant)  # coordinate table
+            assert stf.fast_blocks > 0 and stf.slow_blocks == 0, (name, level, variant)
+            assert np.array_equal(cf.data, cg.data), (name, level, variant)
+            assert stc.relative_error(cf, classical) <= TOL, (name, level, variant)
+
+
+def test_fused_matches_oracle_strassen():
+    # the oracle's own L2 ABC Strassen on the same inputs (different summation
+    # order inside the leaf GEMMs, so compared in norm)
+    spec = stc.parse_benchmark_line(LAYOUTS["ax_bk"])
+    a, b, c0 = _operands(spec, 21)
+    ref = c0.copy()
+    oracle.contract(spec, a.to_host(), b.to_host(), ref, 2, "abc")
+    cf, st = _run(spec, a, b, c0, 2, "abc", True)
+    assert st.leaf_multiplies == 49
+    assert stc.relative_error(cf, ref) <= TOL
+
+
+def test_fused_declines_irregular_and_forced_slow():
+    # extents 24: tiles do not cut the bundles into boxes of 16 -> gather kernel
+    spec = stc.parse_benchmark_line("abij abef efij & a:24;b:24;i:24;j:24;e:24;f:24;")
+    a, b, c0 = _operands(spec, 31)
+    _, st = _run(spec, a, b, c0, 1, "abc", True)
+    assert st.fast_blocks == 0 and st.slow_blocks > 0
+    spec = stc.parse_benchmark_line(LAYOUTS["ak_bx"])
+    a, b, c0 = _operands(spec, 32)
+    c = c0.to_device()
+    st = stc.contract(spec, a, b, c, 1, "abc", force_slow=True)
+    assert st.fast_blocks == 0 and st.slow_blocks > 0
