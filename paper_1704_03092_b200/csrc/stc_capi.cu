@@ -293,7 +293,7 @@ struct Plan {
   int grid = 1;
   // workspace layout (bytes)
   int max_ops = 1;  // most views on one side of any term (2^L)
-  size_t off_kbs = 0, off_coords = 0;
+  size_t off_kbs = 0, off_coords = 0, off_mscr = 0;
   size_t off_pool = 0, off_vecs = 0, off_tab = 0, off_tickets = 0, off_counters = 0, off_M = 0, off_pa = 0,
          off_pb = 0, off_acc = 0, total = 0;
   size_t tab_bytes = 0, acc_bytes = 0;
@@ -482,6 +482,8 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   off = align256(off + (size_t)(pl.pool_len / BK) * 8);
   pl.off_coords = off;  // fused kernel: int4 map coordinates per 8 pool entries
   off = align256(off + (size_t)(pl.pool_len / 8) * 16);
+  pl.off_mscr = off;  // fused ABC: two M tiles per CTA for the epilogue warps
+  if (pl.variant == STC_VARIANT_ABC) off = align256(off + (size_t)pl.grid * 2 * BM * BN * 8);
   pl.off_vecs = off;
   off = align256(off + pl.vecs.size() * sizeof(VecDesc));
   pl.off_tab = off;
@@ -827,7 +829,8 @@ int stc_set_kernel_events(void *before, void *after) {
 
 int stc_workspace_size(const stc_problem *p, size_t *bytes) {
   Plan pl;
-  if (int rc = build_plan(p, pl, 0)) return rc;
+  const int sms = gemm_max_grid(MAX_OPS);  // per-CTA scratch is sized by the launch grid (0 without a device)
+  if (int rc = build_plan(p, pl, sms > 0 ? sms : 0)) return rc;
   if (bytes) *bytes = pl.total;
   return STC_OK;
 }
@@ -908,6 +911,10 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       // fused kernel: TMA boxes of 128 x 8, sums in the consumers' fragment loads
       tma = true;
       gf.coords = reinterpret_cast<const int4 *>(ws + pl.off_coords);
+      // opt-in: C updates by the producer warpgroup's idle warps (helps L1 / large
+      // k; at L2 on 4096^3 their DADDs starve behind the DMMAs)
+      if (getenv("STC_EPI_OFFLOAD") && atoi(getenv("STC_EPI_OFFLOAD")) != 0)
+        gf.mscratch = reinterpret_cast<double *>(ws + pl.off_mscr);
       CU(launch_pool_coords(pool, reinterpret_cast<int4 *>(ws + pl.off_coords), jobs, s), "k_pool_coords");
       ++launches;
       if (g_ev_before) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");

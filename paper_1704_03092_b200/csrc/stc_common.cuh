@@ -5,6 +5,12 @@
 #include "stc_internal.cuh"
 #include "stc_ptx.cuh"
 
+#ifdef STC_EXPERIMENT_NOTICKET
+#define STC_NOTICKET 1  // timing experiment only (C-tile updates race)
+#else
+#define STC_NOTICKET 0
+#endif
+
 namespace stc {
 
 __device__ __forceinline__ void tile_of(const GemmArgs &p, int item, int &slot, int &ti, int &tj) {
@@ -27,19 +33,24 @@ __device__ __forceinline__ void tile_of(const GemmArgs &p, int item, int &slot, 
 // (deterministic, no atomics on C) -- replaces store_tile (_jit.py:158-186);
 // or write M densely (AB / Naive).
 //
-// PERM: the fused kernel's fragment-to-tile permutation (stc_fused.cu): MMA row
-// m of a 16-row block holds tile row (m & 1) + 2 ((m >> 3) & 1) + 4 ((m >> 1) & 3),
-// and likewise for columns within each 16-column pair of n8 tiles.
-template <bool PERM>
-__device__ __forceinline__ int epi_row(int mt, int h, int g) {
-  return mt * 16 + (PERM ? (g & 1) + 2 * h + 4 * (g >> 1) : g + 8 * h);
+// PA / PB: fragment-to-tile permutation of rows (A side) / columns (B side):
+// 0 identity (gather kernel); 1 or 2 the fused kernel's (stc_fused.cu,
+// frag_perm) for a side whose unit stride is in x (1) or in k (2).
+__host__ __device__ __forceinline__ int frag_perm(int kind, int g, int h) {  // g: 0..7, h: 0..1 -> 0..15
+  if (kind == 1) return (g & 1) + 8 * ((g >> 1) & 1) + 2 * (g >> 2) + 4 * h;
+  if (kind == 2) return (g & 1) + 2 * h + 4 * (g >> 1);
+  return g + 8 * h;
 }
-template <bool PERM>
-__device__ __forceinline__ int epi_col(int nt, int tig) {  // first of the pair (b = 0, 1)
-  return PERM ? 16 * (nt >> 1) + 2 * (nt & 1) + 4 * tig : nt * 8 + 2 * tig;
+template <int PA>
+__device__ __forceinline__ int epi_row(int mt, int h, int g) {
+  return mt * 16 + frag_perm(PA, g, h);
+}
+template <int PB>
+__device__ __forceinline__ int epi_col(int nt, int tig) {  // first of the pair (b = 0, 1): frag_perm keeps pairs adjacent
+  return 16 * (nt >> 1) + frag_perm(PB, 2 * tig, nt & 1);
 }
 
-template <bool PERM = false>
+template <int PA = 0, int PB = 0, int RB = 1>
 __device__ __forceinline__ void epilogue_store(const GemmArgs &p, const double (&acc)[4][4][4], int item, int tid,
                                                int wm, int wn, int g, int tig) {
   int slot, ti, tj;
@@ -56,8 +67,8 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs &p, const double (
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           double2 v = make_double2(acc[mt][nt][2 * h], acc[mt][nt][2 * h + 1]);
-          *reinterpret_cast<double2 *>(Mt + (int64_t)(row0 + epi_row<PERM>(mt, h, g)) * p.m_ld + col0 +
-                                      epi_col<PERM>(nt, tig)) = v;
+          *reinterpret_cast<double2 *>(Mt + (int64_t)(row0 + epi_row<PA>(mt, h, g)) * p.m_ld + col0 +
+                                      epi_col<PB>(nt, tig)) = v;
         }
     return;
   }
@@ -65,7 +76,7 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs &p, const double (
   for (int j = 0; j < td.c_count; ++j) {
     const TgtDesc tg = p.tgts[td.c_first + j];
     int32_t *ticket = p.tickets + tg.ticket_base + pos;
-    if (p.use_tickets) {
+    if (p.use_tickets && !STC_NOTICKET) {
       if (tid == 0) {
         while (ld_acquire_gpu(ticket) < tg.order) __nanosleep(128);
       }
@@ -75,21 +86,32 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs &p, const double (
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-      for (int b = 0; b < 2; ++b) co[nt * 2 + b] = __ldcg(p.pool + tg.col_start + col0 + epi_col<PERM>(nt, tig) + b);
+      for (int b = 0; b < 2; ++b) co[nt * 2 + b] = __ldcg(p.pool + tg.col_start + col0 + epi_col<PB>(nt, tig) + b);
+    // batches of RB rows (h = 0, 1 of RB / 2 ... 2 / RB mt blocks): all 8 RB loads of a
+    // batch in flight before its stores
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
+    for (int bt = 0; bt < 8 / RB; ++bt) {
+      int64_t ro[RB];
+      double old[RB][8];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t ro = __ldcg(p.pool + tg.row_start + row0 + epi_row<PERM>(mt, h, g));
-        double *Crow = p.C + ro;
-        double old[8];
+      for (int i = 0; i < RB; ++i) {
+        const int rr = bt * RB + i, mt = rr >> 1, h = rr & 1;
+        ro[i] = __ldcg(p.pool + tg.row_start + row0 + epi_row<PA>(mt, h, g));
+      }
 #pragma unroll
-        for (int c = 0; c < 8; ++c) old[c] = (ro == kPad || co[c] == kPad) ? 0.0 : __ldcg(Crow + co[c]);
+      for (int i = 0; i < RB; ++i)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) old[i][c] = (ro[i] == kPad || co[c] == kPad) ? 0.0 : __ldcg(p.C + ro[i] + co[c]);
+#pragma unroll
+      for (int i = 0; i < RB; ++i) {
+        const int rr = bt * RB + i, mt = rr >> 1, h = rr & 1;
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-          if (ro != kPad && co[c] != kPad) __stcg(Crow + co[c], old[c] + tg.sign * acc[mt][c >> 1][2 * h + (c & 1)]);
+          if (ro[i] != kPad && co[c] != kPad)
+            __stcg(p.C + ro[i] + co[c], old[i][c] + tg.sign * acc[mt][c >> 1][2 * h + (c & 1)]);
       }
-    if (p.use_tickets) {
+    }
+    if (p.use_tickets && !STC_NOTICKET) {
       __threadfence();
       named_bar(2, 32 * CONSUMER_WARPS);
       if (tid == 0) st_release_gpu(ticket, tg.order + 1);

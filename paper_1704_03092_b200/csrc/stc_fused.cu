@@ -32,16 +32,27 @@ constexpr int FK = 8;                        // k-chunk of the fused kernel
 constexpr int VIEW_DOUBLES = BM * FK;        // one raw view of one chunk (BM == BN)
 constexpr int FUSED_PRODUCER_WARPS = 4;  // one warpgroup (setmaxnreg is warpgroup-wide); warp 0 of it issues
 constexpr int FUSED_THREADS = 32 * (CONSUMER_WARPS + FUSED_PRODUCER_WARPS);
-constexpr int FUSED_CONSUMER_REGS = 232;
-constexpr int FUSED_PRODUCER_REGS = 24;
+constexpr int FUSED_CONSUMER_REGS = 232;  // 2 x 232 + 40 (x 32 lanes) fits an SMSP's 16 K registers
+constexpr int FUSED_PRODUCER_REGS = 40;
 constexpr int MAX_FUSED_STAGES = 8;
 
+// smem: stages [S][umax][1024 doubles] | full[S], empty[S] | epi_full[2], epi_empty[2]
+//       | stage_item[S], epi_item[2] | epilogue offset tables: rows[128], cols[128] (int64)
 struct FusedLayout {
   __host__ __device__ static size_t stage_bytes(int umax) { return (size_t)umax * VIEW_DOUBLES * 8; }
   __host__ __device__ static size_t bar_off(int umax, int stages) { return (size_t)stages * stage_bytes(umax); }
-  __host__ __device__ static size_t meta_off(int umax, int stages) { return bar_off(umax, stages) + 16 * (size_t)stages; }
-  __host__ __device__ static size_t bytes(int umax, int stages) { return meta_off(umax, stages) + 4 * (size_t)stages + 16; }
+  __host__ __device__ static size_t meta_off(int umax, int stages) {
+    return bar_off(umax, stages) + 16 * (size_t)stages + 32;
+  }
+  __host__ __device__ static size_t epi_tab_off(int umax, int stages) {
+    return (meta_off(umax, stages) + 4 * (size_t)stages + 8 + 15) / 16 * 16;
+  }
+  __host__ __device__ static size_t bytes(int umax, int stages) { return epi_tab_off(umax, stages) + 2 * 128 * 8; }
 };
+
+constexpr int EPI_WARPS = FUSED_PRODUCER_WARPS - 1;  // the producer warpgroup's other warps
+constexpr int EPI_THREADS = 32 * EPI_WARPS;
+constexpr size_t TILE_DOUBLES = (size_t)BM * BN;
 
 constexpr size_t kFusedMaxSmem = 227 * 1024;
 
@@ -211,6 +222,75 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
   }
 }
 
+// Epilogue warps (the producer warpgroup's three other warps; ABC, opt-in with
+// STC_EPI_OFFLOAD=1): for each item's dense M tile in this CTA's scratch
+// buffer, add sign * M into every C target through the scatter layout --
+// ticket-ordered across terms exactly as epilogue_store does, so C is bitwise
+// the same -- while the consumers run the next item's MMAs.
+__device__ __forceinline__ void epilogue_warps(const GemmArgs &p, uint64_t *epi_full, uint64_t *epi_empty,
+                                               const int *epi_item, int64_t *rows, int64_t *cols, int t) {
+  int eb = 0;
+  uint32_t ephase = 0;
+  const int lane = t & 31;
+  for (;;) {
+    mbar_wait(&epi_full[eb], ephase);
+    const int item = epi_item[eb];
+    if (item < 0) break;
+    int slot, ti, tj;
+    tile_of(p, item, slot, ti, tj);
+    const TermDesc td = p.terms[slot];
+    const int pos = item - slot * p.tiles_m * p.tiles_n;
+    const double *Mt = p.mscratch + ((size_t)blockIdx.x * 2 + eb) * TILE_DOUBLES;
+    for (int j = 0; j < td.c_count; ++j) {
+      const TgtDesc tg = p.tgts[td.c_first + j];
+      for (int i = t; i < 128; i += EPI_THREADS) {
+        rows[i] = __ldcg(p.pool + tg.row_start + ti * BM + i);
+        cols[i] = __ldcg(p.pool + tg.col_start + tj * BN + i);
+      }
+      int32_t *ticket = p.tickets + tg.ticket_base + pos;
+      if (p.use_tickets && !STC_NOTICKET) {
+        if (t == 0)
+          while (ld_acquire_gpu(ticket) < tg.order) __nanosleep(64);
+      }
+      named_bar(3, EPI_THREADS);
+      // one warp per row pair at a time, lanes along columns (4 columns per lane);
+      // all loads of the pair are issued before any store
+      int64_t co[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) co[q] = cols[lane + 32 * q];
+      for (int r0 = 2 * (t >> 5); r0 < BM; r0 += 2 * EPI_WARPS) {
+        int64_t ro[2];
+        double m[2][4], c[2][4];
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          ro[rr] = rows[r0 + rr];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const bool ok = ro[rr] != kPad && co[q] != kPad;
+            m[rr][q] = Mt[(size_t)(r0 + rr) * BN + lane + 32 * q];
+            c[rr][q] = ok ? __ldcg(p.C + ro[rr] + co[q]) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (ro[rr] != kPad && co[q] != kPad) __stcg(p.C + ro[rr] + co[q], c[rr][q] + tg.sign * m[rr][q]);
+      }
+      if (p.use_tickets && !STC_NOTICKET) {
+        __threadfence();
+        named_bar(3, EPI_THREADS);
+        if (t == 0) st_release_gpu(ticket, tg.order + 1);
+      }
+      named_bar(3, EPI_THREADS);  // offset tables reused by the next target
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&epi_empty[eb]);
+    eb ^= 1;
+    if (eb == 0) ephase ^= 1;
+  }
+}
+
 template <int AKF, int BKF>
 __global__ void __launch_bounds__(FUSED_THREADS, 1)
     k_strassen_fused(const GemmArgs p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
@@ -219,13 +299,23 @@ __global__ void __launch_bounds__(FUSED_THREADS, 1)
   double *stages = reinterpret_cast<double *>(smem);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + FusedLayout::bar_off(umax, S));
   uint64_t *empty = full + S;
+  uint64_t *epi_full = empty + S;  // M tile b written by the consumers (ABC: C updates offloaded)
+  uint64_t *epi_empty = epi_full + 2;
   int *stage_item = reinterpret_cast<int *>(smem + FusedLayout::meta_off(umax, S));
+  int *epi_item = stage_item + S;
+  int64_t *epi_rows = reinterpret_cast<int64_t *>(smem + FusedLayout::epi_tab_off(umax, S));
+  int64_t *epi_cols = epi_rows + 128;
+  const bool offload = p.mscratch != nullptr;  // ABC: epilogue warps update C from the M tiles
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], CONSUMER_WARPS);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&epi_full[b], CONSUMER_WARPS);
+      mbar_init(&epi_empty[b], EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -235,7 +325,10 @@ __global__ void __launch_bounds__(FUSED_THREADS, 1)
   if (warp >= CONSUMER_WARPS) {
     // ===================== producer warp: TMA box loads ================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(FUSED_PRODUCER_REGS));
-    if (warp != CONSUMER_WARPS) return;
+    if (warp != CONSUMER_WARPS) {
+      if (offload) epilogue_warps(p, epi_full, epi_empty, epi_item, epi_rows, epi_cols, tid - 32 * (CONSUMER_WARPS + 1));
+      return;
+    }
     int stage = 0;
     uint32_t phase = 0;
     for (;;) {
@@ -297,26 +390,35 @@ __global__ void __launch_bounds__(FUSED_THREADS, 1)
     const int g = lane >> 2, tig = lane & 3;
     const int wm = warp & 1, wn = warp >> 1;
     // Fragment offsets inside a view: A (kk, h) + 128 * mt; B (kk, nt & 1) + 128 * (nt >> 1).
-    // MMA row m of each 16-row block reads tile row pi(m) = (m & 1) + 2 ((m >> 3) & 1) +
-    // 4 ((m >> 1) & 3) (columns likewise within 16-column pairs): with it the 128-byte
-    // swizzle spreads a fragment load over all 16 8-byte bank pairs (the identity
-    // would hit 8); the epilogue maps rows / columns back (epilogue_store<true>).
+    // MMA row (column) g + 8 h of each 16-row block (16-column pair) reads tile row
+    // (column) frag_perm(kind, g, h) (stc_common.cuh): with it every half-warp of a
+    // fragment load touches 16 distinct 8-byte bank pairs in the swizzled view (the
+    // identity would need twice the wavefronts); the epilogue maps rows / columns back.
     int offA[2][2], offB[2][2];
 #pragma unroll
     for (int kk = 0; kk < 2; ++kk)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int pm = (g & 1) + 2 * h + 4 * (g >> 1);
-        offA[kk][h] = view_index(AKF, wm * 64 + pm, kk * 4 + tig);
-        offB[kk][h] = view_index(BKF, wn * 32 + pm, kk * 4 + tig);
+        offA[kk][h] = view_index(AKF, wm * 64 + frag_perm(AKF + 1, g, h), kk * 4 + tig);
+        offB[kk][h] = view_index(BKF, wn * 32 + frag_perm(BKF + 1, g, h), kk * 4 + tig);
       }
     int stage = 0;
     uint32_t phase = 0;
+    int eb = 0;  // M scratch buffer (offloaded epilogue)
+    uint32_t ephase = 0;
     double acc[4][4][4];
     for (;;) {
       mbar_wait(&full[stage], phase);
       const int item = stage_item[stage];
-      if (item < 0) break;
+      if (item < 0) {
+        if (offload) {  // tell the epilogue warps to stop
+          mbar_wait(&epi_empty[eb], ephase ^ 1);
+          if (tid == 0) epi_item[eb] = -1;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&epi_full[eb]);
+        }
+        break;
+      }
       int slot, ti, tj;
       tile_of(p, item, slot, ti, tj);
       const TermDesc td = p.terms[slot];
@@ -376,7 +478,42 @@ __global__ void __launch_bounds__(FUSED_THREADS, 1)
           }
           break;
       }
-      epilogue_store<true>(p, acc, item, tid, wm, wn, g, tig);
+      if (offload) {
+        // dense M tile into this CTA's scratch buffer; the epilogue warps add it
+        // into the C targets while the next item's MMAs run
+        mbar_wait(&epi_empty[eb], ephase ^ 1);
+        double *Mt = p.mscratch + ((size_t)blockIdx.x * 2 + eb) * TILE_DOUBLES;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              *reinterpret_cast<double2 *>(Mt + (size_t)(wm * 64 + epi_row<AKF + 1>(mt, h, g)) * BN + wn * 32 +
+                                           epi_col<BKF + 1>(nt, tig)) =
+                  make_double2(acc[mt][nt][2 * h], acc[mt][nt][2 * h + 1]);
+        if (tid == 0) epi_item[eb] = item;
+        __threadfence_block();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&epi_full[eb]);
+        eb ^= 1;
+        if (eb == 0) ephase ^= 1;
+        continue;
+      }
+#ifdef STC_EXPERIMENT_NOEPI
+      {  // timing experiment only: keep every accumulator live, skip the C updates
+        double z = 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) z += acc[i][j][r];
+        if (z == 1.2345e300) p.C[0] = z;
+      }
+#else
+      epilogue_store<AKF + 1, BKF + 1, 2>(p, acc, item, tid, wm, wn, g, tig);
+#endif
     }
   }
 }

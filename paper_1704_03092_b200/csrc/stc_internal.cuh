@@ -89,6 +89,7 @@ struct GemmArgs {
   // fused kernel (stc_fused.cu)
   const int4 *coords;        // coords[i]: map coordinates (one part) of pool entry 8 i
   int32_t umax, stages;      // views per chunk stage (2 * max_ops), ring depth
+  double *mscratch;          // ABC: [grid][2][BM * BN] M tiles handed to the epilogue warps
 };
 
 // Jobs of k_pool_coords: one per operand pool vector (x or k part of A or B).

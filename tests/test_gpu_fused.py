@@ -94,3 +94,19 @@ def test_fused_declines_irregular_and_forced_slow():
     c = c0.to_device()
     st = stc.contract(spec, a, b, c, 1, "abc", force_slow=True)
     assert st.fast_blocks == 0 and st.slow_blocks > 0
+
+
+def test_offloaded_epilogue_is_bitwise_identical():
+    # STC_EPI_OFFLOAD=1: the producer warpgroup's spare warps apply the C updates
+    spec = stc.parse_benchmark_line(LAYOUTS["ak_bx"])
+    a, b, c0 = _operands(spec, 41)
+    outs = []
+    for flag in ("0", "1"):
+        os.environ["STC_EPI_OFFLOAD"] = flag
+        try:
+            for level in (1, 2):
+                c, st = _run(spec, a, b, c0, level, "abc", True)
+                outs.append(c.data)
+        finally:
+            del os.environ["STC_EPI_OFFLOAD"]
+    assert np.array_equal(outs[0], outs[2]) and np.array_equal(outs[1], outs[3])
