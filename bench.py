@@ -277,7 +277,8 @@ def main():
             traffic = None
     roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_TC_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP64_TC_PEAK_TFLOPS, "traffic": traffic,
-                "kernel": "k_strassen_gemm (fused ABC term/tile DMMA kernel)",
+                "kernel": ("k_strassen_fused (TMA views, Strassen sums in the DMMA fragment loads)" if st.fast_blocks
+                           else "k_strassen_gemm (gather producer, Strassen sums in smem)"),
                 "kernel_ms": gemm_avg * 1e3, "kernel_share_of_step": gemm_avg / (elapsed / args.steps),
                 "algorithmic_flops_per_launch": alg_flops,
                 "peak_source": "measured FP64 DMMA peak, tools/fp64_peak.cu, burst (MEASURED_PEAKS.json has no FP64)",
