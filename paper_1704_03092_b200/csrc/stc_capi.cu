@@ -764,11 +764,77 @@ bool plan_fused_side(const stc_bundle &xb, const Tiling &tx, const stc_bundle &k
   return true;
 }
 
+
+// ---- TMA-reduce epilogue (fused ABC) ------------------------------------------
+// C target views as tensor-map boxes of 32 tile rows x 128 tile columns, dims
+// (column low 16, column high..., rows...), 128-byte swizzle: the smem piece is
+// [row][column / 16][column % 16].  Needs the C tensor's unit-stride label to
+// lead the J bundle's tile order.  x part = rows (I), k part = columns (J).
+constexpr int kRedRows = 32;
+
+bool plan_cred_side(const stc_bundle &rb, const Tiling &tr, const stc_bundle &cb, const Tiling &tc, int level,
+                    const double *data, int64_t base, TmaSide &ts) {
+  if (tr.nbox == 0 || tc.nbox == 0) return false;
+  const int64_t Q = (int64_t)1 << level;
+  if ((bundle_len(rb) / Q) % BM != 0 || (bundle_len(cb) / Q) % BN != 0) return false;
+  int64_t tbr[STC_MAX_LABELS], tbc[STC_MAX_LABELS];
+  int orr[STC_MAX_LABELS], oc[STC_MAX_LABELS], nor = 0, noc = 0;
+  if (!tile_subbox(rb, tr, kRedRows, tbr, orr, nor) || !tile_subbox(cb, tc, BN, tbc, oc, noc)) return false;
+  struct Dim {
+    int64_t ext, str, box;
+    bool isx;
+  };
+  std::vector<Dim> dims;
+  if (noc == 0 || cb.str[oc[0]] != 1) return false;
+  const int64_t e0 = cb.ext[oc[0]], b0 = tbc[oc[0]];
+  if (b0 < 16 || b0 % 16 != 0 || (b0 > 16 && e0 % 16 != 0)) return false;
+  dims.push_back({b0 > 16 ? 16 : e0, 1, 16, false});
+  if (b0 > 16) dims.push_back({e0 / 16, 16, b0 / 16, false});
+  for (int j = 1; j < noc; ++j) dims.push_back({cb.ext[oc[j]], cb.str[oc[j]], tbc[oc[j]], false});
+  for (int j = 0; j < nor; ++j) dims.push_back({rb.ext[orr[j]], rb.str[orr[j]], tbr[orr[j]], true});
+  for (int pass = 0; pass < 2; ++pass) {
+    const stc_bundle &b = pass == 0 ? rb : cb;
+    const int64_t *tb = pass == 0 ? tbr : tbc;
+    for (int d = 0; d < b.nlab; ++d)
+      if (b.ext[d] > 1 && tb[d] == 1) dims.push_back({b.ext[d], b.str[d], 1, pass == 0});
+  }
+  if (dims.size() > 5) return false;
+  for (size_t d = 0; d < dims.size(); ++d) {
+    if (dims[d].str <= 0 || dims[d].box > 256 || dims[d].ext >= (int64_t)1 << 31) return false;
+    if (d > 0 && ((dims[d].str % 2) != 0 || dims[d].str * 8 >= ((int64_t)1 << 40))) return false;
+  }
+  if ((reinterpret_cast<uintptr_t>(data + base) & 15) != 0) return false;
+  for (int part = 0; part < 2; ++part) {
+    std::vector<int> idx;
+    for (size_t d = 0; d < dims.size(); ++d)
+      if (dims[d].isx == (part == 0)) idx.push_back((int)d);
+    if (idx.empty() || idx.size() > 4) return false;
+    std::sort(idx.begin(), idx.end(), [&](int a, int b) { return dims[a].str > dims[b].str; });
+    for (size_t i = 0; i + 1 < idx.size(); ++i)
+      if (dims[idx[i]].str < dims[idx[i + 1]].str * dims[idx[i + 1]].ext) return false;
+    ts.np[part] = (int)idx.size();
+    for (size_t i = 0; i < idx.size(); ++i) {
+      ts.pstr[part][i] = dims[idx[i]].str;
+      ts.src[idx[i]] = part * 4 + (int)i;
+    }
+    for (size_t i = idx.size(); i < 4; ++i) ts.pstr[part][i] = 1;
+  }
+  ts.rank = (int)dims.size();
+  for (int d = 0; d < ts.rank; ++d) {
+    ts.dims[d] = (cuuint64_t)dims[d].ext;
+    ts.box[d] = (cuuint32_t)dims[d].box;
+    if (d > 0) ts.strides[d - 1] = (cuuint64_t)(dims[d].str * 8);
+  }
+  for (int d = ts.rank; d < 5; ++d) ts.src[d] = 0;
+  ts.swizzle = 128;
+  return true;
+}
+
 // Fused-kernel plan for ABC / AB (terms of at most 8 views per chunk: L <= 2):
 // tensor maps, the coordinate-table jobs and the kernel arguments.
 // STC_FUSED=0 disables.
-bool plan_fused(const stc_problem *p, const Plan &pl, const double *A, const double *B, GemmArgs &g, CUtensorMap maps[2],
-                CoordJobs &jobs) {
+bool plan_fused(const stc_problem *p, const Plan &pl, const double *A, const double *B, const double *C, GemmArgs &g,
+                CUtensorMap maps[3], CoordJobs &jobs) {
   if (const char *e = getenv("STC_FUSED"))
     if (atoi(e) == 0) return false;
   if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
@@ -806,9 +872,35 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const double *A, const dou
     jb.np = ss[vs[j].sd]->np[vs[j].part];
     for (int i = 0; i < 4; ++i) jb.str[i] = ss[vs[j].sd]->pstr[vs[j].part][i];
   }
+  // ABC: C updates by TMA reduce-add when the C targets are regular boxes (STC_CRED=0 disables)
+  g.cred = 0;
+  TmaSide sc;
+  if (pl.variant == STC_VARIANT_ABC && C && !(getenv("STC_CRED") && atoi(getenv("STC_CRED")) == 0) &&
+      fused_stages_red(umax) >= 2 &&
+      plan_cred_side(p->c_row, pl.ti, p->c_col, pl.tj, pl.level, C, p->c_base, sc) &&
+      encode_side(sc, C, p->c_base, maps[2])) {
+    g.cred = 1;
+    g.tm_rank[2] = sc.rank;
+    for (int d = 0; d < 5; ++d) g.tm_src[2][d] = sc.src[d];
+    for (int part = 0; part < 2; ++part) {
+      g.tm_np[2][part] = sc.np[part];
+      for (int i = 0; i < 4; ++i) g.tm_pstr[2][part][i] = sc.pstr[part][i];
+    }
+    // pool vectors cr (rows, base 0) and cc (columns, base c_base)
+    const int64_t lens[2] = {pl.Q * rup(cdiv(bundle_len(p->c_row), pl.Q), BM), pl.Q * rup(cdiv(bundle_len(p->c_col), pl.Q), BN)};
+    const int64_t starts[2] = {pl.cr, pl.cc}, bases[2] = {0, p->c_base};
+    for (int part = 0; part < 2; ++part) {
+      CoordJob &jb = jobs.job[jobs.n++];
+      jb.start = starts[part];
+      jb.count = lens[part] / 8;
+      jb.base = bases[part];
+      jb.np = sc.np[part];
+      for (int i = 0; i < 4; ++i) jb.str[i] = sc.pstr[part][i];
+    }
+  }
   g.tma = 0;
   g.umax = umax;
-  g.stages = S;
+  g.stages = g.cred ? fused_stages_red(umax) : S;
   g.kchunks = (int)(pl.kq_pad / kFusedK);
   return true;
 }
@@ -904,10 +996,10 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
     g.use_tickets = T > 1;
     g.counter = counters;
     const int grid = (int)std::min<int64_t>(pl.grid, g.total_items);
-    CUtensorMap maps[2];
+    CUtensorMap maps[3];
     CoordJobs jobs{};
     GemmArgs gf = g;
-    if (plan_fused(p, pl, A, B, gf, maps, jobs)) {
+    if (plan_fused(p, pl, A, B, C, gf, maps, jobs)) {
       // fused kernel: TMA boxes of 128 x 8, sums in the consumers' fragment loads
       tma = true;
       gf.coords = reinterpret_cast<const int4 *>(ws + pl.off_coords);
@@ -1066,10 +1158,10 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       g.m_stride = pl.m_slot;
       g.counter = counters + bi;
       const int grid = (int)std::min<int64_t>(pl.grid, g.total_items);
-      CUtensorMap maps[2];
+      CUtensorMap maps[3];
       CoordJobs jobs{};
       GemmArgs gf = g;
-      const bool fused = !naive && plan_fused(p, pl, A, B, gf, maps, jobs);
+      const bool fused = !naive && plan_fused(p, pl, A, B, nullptr, gf, maps, jobs);
       if (fused && bi == 0) {
         CU(launch_pool_coords(pool, reinterpret_cast<int4 *>(ws + pl.off_coords), jobs, s), "k_pool_coords");
         ++launches;

@@ -36,18 +36,26 @@ constexpr int FUSED_CONSUMER_REGS = 232;  // 2 x 232 + 40 (x 32 lanes) fits an S
 constexpr int FUSED_PRODUCER_REGS = 40;
 constexpr int MAX_FUSED_STAGES = 8;
 
-// smem: stages [S][umax][1024 doubles] | full[S], empty[S] | epi_full[2], epi_empty[2]
-//       | stage_item[S], epi_item[2] | epilogue offset tables: rows[128], cols[128] (int64)
+// smem: stages [S][umax][1024 doubles] | (cred) M piece [32][128] | full[S], empty[S] |
+//       epi_full[2], epi_empty[2] | stage_item[S], epi_item[2] | epilogue offset tables:
+//       rows[128], cols[128] (int64)
+constexpr int RED_ROWS = 32;                          // rows of one TMA-reduce piece
+constexpr size_t RED_BYTES = (size_t)RED_ROWS * BN * 8;
 struct FusedLayout {
   __host__ __device__ static size_t stage_bytes(int umax) { return (size_t)umax * VIEW_DOUBLES * 8; }
-  __host__ __device__ static size_t bar_off(int umax, int stages) { return (size_t)stages * stage_bytes(umax); }
-  __host__ __device__ static size_t meta_off(int umax, int stages) {
-    return bar_off(umax, stages) + 16 * (size_t)stages + 32;
+  __host__ __device__ static size_t red_off(int umax, int stages) { return (size_t)stages * stage_bytes(umax); }
+  __host__ __device__ static size_t bar_off(int umax, int stages, bool red) {
+    return red_off(umax, stages) + (red ? RED_BYTES : 0);
   }
-  __host__ __device__ static size_t epi_tab_off(int umax, int stages) {
-    return (meta_off(umax, stages) + 4 * (size_t)stages + 8 + 15) / 16 * 16;
+  __host__ __device__ static size_t meta_off(int umax, int stages, bool red) {
+    return bar_off(umax, stages, red) + 16 * (size_t)stages + 32;
   }
-  __host__ __device__ static size_t bytes(int umax, int stages) { return epi_tab_off(umax, stages) + 2 * 128 * 8; }
+  __host__ __device__ static size_t epi_tab_off(int umax, int stages, bool red) {
+    return (meta_off(umax, stages, red) + 4 * (size_t)stages + 8 + 15) / 16 * 16;
+  }
+  __host__ __device__ static size_t bytes(int umax, int stages, bool red) {
+    return epi_tab_off(umax, stages, red) + 2 * 128 * 8;
+  }
 };
 
 constexpr int EPI_WARPS = FUSED_PRODUCER_WARPS - 1;  // the producer warpgroup's other warps
@@ -59,7 +67,14 @@ constexpr size_t kFusedMaxSmem = 227 * 1024;
 // Stages of the fused ring for terms of at most `umax` views per chunk (0: does not fit).
 int fused_stages(int umax) {
   int s = MAX_FUSED_STAGES;
-  while (s >= 2 && FusedLayout::bytes(umax, s) > kFusedMaxSmem) --s;
+  while (s >= 2 && FusedLayout::bytes(umax, s, false) > kFusedMaxSmem) --s;
+  return s >= 2 ? s : 0;
+}
+
+// Stages when the TMA-reduce epilogue's M piece also lives in smem.
+int fused_stages_red(int umax) {
+  int s = MAX_FUSED_STAGES;
+  while (s >= 2 && FusedLayout::bytes(umax, s, true) > kFusedMaxSmem) --s;
   return s >= 2 ? s : 0;
 }
 
@@ -222,6 +237,104 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
   }
 }
 
+// TMA-reduce epilogue (ABC, C targets regular): for each C target in ticket
+// order, the tile's sign * M goes through a 32 x 128 smem piece (128-byte
+// swizzled, the C map's box) and cp.reduce.async.bulk.tensor adds it into C in
+// L2.  C_new = C_old + (+/-M) is one IEEE add per element, as in
+// epilogue_store, and tickets keep the reference's term order: C is bitwise
+// the same.  No C data passes through the SM.
+__device__ __forceinline__ int red_index(int r, int c) {
+  return r * BN + (c >> 4) * 16 + ((((c & 15) >> 1) ^ (c >> 4)) << 1) + (c & 1);
+}
+
+__device__ __forceinline__ void tma_reduce_add(const CUtensorMap *map, int rank, const int32_t (&c)[5], const void *src) {
+  const uint32_t sa = smem_u32(src);
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  switch (rank) {
+    case 2:
+      asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(m),
+                   "r"(c[0]), "r"(c[1]), "r"(sa)
+                   : "memory");
+      break;
+    case 3:
+      asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(m),
+                   "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(sa)
+                   : "memory");
+      break;
+    case 4:
+      asm volatile(
+          "cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(m),
+          "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(sa)
+          : "memory");
+      break;
+    default:
+      asm volatile(
+          "cp.reduce.async.bulk.tensor.5d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(m),
+          "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(sa)
+          : "memory");
+      break;
+  }
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+template <int PA, int PB>
+__device__ __forceinline__ void epilogue_red(const GemmArgs &p, const double (&acc)[4][4][4], int item, int tid, int wm,
+                                             int wn, int g, int tig, double *buf, const CUtensorMap *tmC) {
+  int slot, ti, tj;
+  tile_of(p, item, slot, ti, tj);
+  const TermDesc td = p.terms[slot];
+  const int pos = item - slot * p.tiles_m * p.tiles_n;
+  for (int j = 0; j < td.c_count; ++j) {
+    const TgtDesc tg = p.tgts[td.c_first + j];
+    int32_t *ticket = p.tickets + tg.ticket_base + pos;
+    if (p.use_tickets && !STC_NOTICKET) {
+      if (tid == 0)
+        while (ld_acquire_gpu(ticket) < tg.order) __nanosleep(64);
+    }
+    for (int pc = 0; pc < BM / RED_ROWS; ++pc) {
+      if (wm == (pc >> 1)) {
+#pragma unroll
+        for (int m2 = 0; m2 < 2; ++m2) {
+          const int mt = 2 * (pc & 1) + m2;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = epi_row<PA>(mt, h, g) - RED_ROWS * (pc & 1);
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+              const int c = wn * 32 + epi_col<PB>(nt, tig);
+              *reinterpret_cast<double2 *>(buf + red_index(r, c)) =
+                  make_double2(tg.sign * acc[mt][nt][2 * h], tg.sign * acc[mt][nt][2 * h + 1]);
+            }
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA reads
+      }
+      named_bar(2, 32 * CONSUMER_WARPS);
+      if (tid == 0) {
+        const int4 rc = p.coords[(tg.row_start + (int64_t)ti * BM + RED_ROWS * pc) >> 3];
+        const int4 cc = p.coords[(tg.col_start + (int64_t)tj * BN) >> 3];
+        int32_t c5[5];
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+          const int src = p.tm_src[2][d];
+          c5[d] = src < 4 ? coord_of(rc, src) : coord_of(cc, src - 4);
+        }
+        tma_reduce_add(tmC, p.tm_rank[2], c5, buf);
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // piece buffer reusable
+      }
+      named_bar(2, 32 * CONSUMER_WARPS);
+    }
+    if (tid == 0) {
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // the adds are performed
+      if (p.use_tickets && !STC_NOTICKET) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence();
+        st_release_gpu(ticket, tg.order + 1);
+      }
+    }
+  }
+}
+
 // Epilogue warps (the producer warpgroup's three other warps; ABC, opt-in with
 // STC_EPI_OFFLOAD=1): for each item's dense M tile in this CTA's scratch
 // buffer, add sign * M into every C target through the scatter layout --
@@ -293,17 +406,20 @@ __device__ __forceinline__ void epilogue_warps(const GemmArgs &p, uint64_t *epi_
 
 template <int AKF, int BKF>
 __global__ void __launch_bounds__(FUSED_THREADS, 1)
-    k_strassen_fused(const GemmArgs p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
+    k_strassen_fused(const GemmArgs p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmC) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const int umax = p.umax, S = p.stages;
+  const bool red = p.cred != 0;
   double *stages = reinterpret_cast<double *>(smem);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + FusedLayout::bar_off(umax, S));
+  double *redbuf = reinterpret_cast<double *>(smem + FusedLayout::red_off(umax, S));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + FusedLayout::bar_off(umax, S, red));
   uint64_t *empty = full + S;
   uint64_t *epi_full = empty + S;  // M tile b written by the consumers (ABC: C updates offloaded)
   uint64_t *epi_empty = epi_full + 2;
-  int *stage_item = reinterpret_cast<int *>(smem + FusedLayout::meta_off(umax, S));
+  int *stage_item = reinterpret_cast<int *>(smem + FusedLayout::meta_off(umax, S, red));
   int *epi_item = stage_item + S;
-  int64_t *epi_rows = reinterpret_cast<int64_t *>(smem + FusedLayout::epi_tab_off(umax, S));
+  int64_t *epi_rows = reinterpret_cast<int64_t *>(smem + FusedLayout::epi_tab_off(umax, S, red));
   int64_t *epi_cols = epi_rows + 128;
   const bool offload = p.mscratch != nullptr;  // ABC: epilogue warps update C from the M tiles
   const int tid = threadIdx.x;
@@ -512,13 +628,16 @@ __global__ void __launch_bounds__(FUSED_THREADS, 1)
         if (z == 1.2345e300) p.C[0] = z;
       }
 #else
-      epilogue_store<AKF + 1, BKF + 1, 2>(p, acc, item, tid, wm, wn, g, tig);
+      if (red)
+        epilogue_red<AKF + 1, BKF + 1>(p, acc, item, tid, wm, wn, g, tig, redbuf, &tmC);
+      else
+        epilogue_store<AKF + 1, BKF + 1, 2>(p, acc, item, tid, wm, wn, g, tig);
 #endif
     }
   }
 }
 
-using FusedKernel = void (*)(const GemmArgs, const CUtensorMap, const CUtensorMap);
+using FusedKernel = void (*)(const GemmArgs, const CUtensorMap, const CUtensorMap, const CUtensorMap);
 
 static FusedKernel fused_for(int akf, int bkf) {
   if (akf) return bkf ? k_strassen_fused<1, 1> : k_strassen_fused<1, 0>;
@@ -526,13 +645,14 @@ static FusedKernel fused_for(int akf, int bkf) {
 }
 
 cudaError_t launch_fused(const GemmArgs &a, int grid, cudaStream_t s, const void *maps) {
-  const size_t sm = FusedLayout::bytes(a.umax, a.stages);
+  const size_t sm = FusedLayout::bytes(a.umax, a.stages, a.cred != 0);
   FusedKernel k = fused_for(a.a_kfast, a.b_kfast);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  CUtensorMap m[2];
-  memcpy(m, maps, sizeof(m));
-  k<<<grid, FUSED_THREADS, sm, s>>>(a, m[0], m[1]);
+  CUtensorMap m[3];
+  memcpy(m, maps, (a.cred ? 3 : 2) * sizeof(CUtensorMap));
+  if (!a.cred) memset(&m[2], 0, sizeof(CUtensorMap));
+  k<<<grid, FUSED_THREADS, sm, s>>>(a, m[0], m[1], m[2]);
   return cudaGetLastError();
 }
 

@@ -81,15 +81,17 @@ struct GemmArgs {
   // each part is decomposed from its pool offset by descending strides.
   int32_t tma;
   int32_t tma_prefetch;      // L2 prefetch distance (units) beyond the raw-slot lookahead
-  int32_t tm_rank[2];
-  int32_t tm_src[2][5];
-  int32_t tm_np[2][2];       // dims in the x / k part
-  int64_t tm_pstr[2][2][4];  // part strides, descending
-  int64_t tm_base[2][2];     // subtracted from the x / k pool entries (the map's base offset)
+  // (index 2: the C map of the fused kernel's TMA-reduce epilogue; x part = rows, k part = columns)
+  int32_t tm_rank[3];
+  int32_t tm_src[3][5];
+  int32_t tm_np[3][2];       // dims in the x / k part
+  int64_t tm_pstr[3][2][4];  // part strides, descending
+  int64_t tm_base[3][2];     // subtracted from the x / k pool entries (the map's base offset)
   // fused kernel (stc_fused.cu)
   const int4 *coords;        // coords[i]: map coordinates (one part) of pool entry 8 i
   int32_t umax, stages;      // views per chunk stage (2 * max_ops), ring depth
   double *mscratch;          // ABC: [grid][2][BM * BN] M tiles handed to the epilogue warps
+  int32_t cred;              // ABC: C updates by TMA reduce-add of M pieces (C views regular)
 };
 
 // Jobs of k_pool_coords: one per operand pool vector (x or k part of A or B).
@@ -100,7 +102,7 @@ struct CoordJob {
   int32_t np, _pad;
 };
 struct CoordJobs {
-  CoordJob job[4];
+  CoordJob job[6];
   int32_t n, _pad;
 };
 
@@ -158,6 +160,7 @@ cudaError_t launch_chunk_strides(const int64_t *pool, int64_t nchunks, int64_t *
 cudaError_t launch_gemm(const GemmArgs &a, int grid, cudaStream_t s, const void *maps = nullptr);
 int gemm_tma_config(int max_ops, int &nraw, int &kwin);
 int fused_stages(int umax);
+int fused_stages_red(int umax);
 cudaError_t launch_fused(const GemmArgs &a, int grid, cudaStream_t s, const void *maps);
 cudaError_t launch_pool_coords(const int64_t *pool, int4 *coords, const CoordJobs &jobs, cudaStream_t s);
 int gemm_max_grid(int max_ops);
