@@ -770,7 +770,7 @@ bool plan_fused_side(const stc_bundle &xb, const Tiling &tx, const stc_bundle &k
 // (column low 16, column high..., rows...), 128-byte swizzle: the smem piece is
 // [row][column / 16][column % 16].  Needs the C tensor's unit-stride label to
 // lead the J bundle's tile order.  x part = rows (I), k part = columns (J).
-constexpr int kRedRows = 32;
+constexpr int kRedRows = 16;
 
 bool plan_cred_side(const stc_bundle &rb, const Tiling &tr, const stc_bundle &cb, const Tiling &tc, int level,
                     const double *data, int64_t base, TmaSide &ts) {

@@ -36,11 +36,11 @@ constexpr int FUSED_CONSUMER_REGS = 232;  // 2 x 232 + 40 (x 32 lanes) fits an S
 constexpr int FUSED_PRODUCER_REGS = 40;
 constexpr int MAX_FUSED_STAGES = 8;
 
-// smem: stages [S][umax][1024 doubles] | (cred) M piece [32][128] | full[S], empty[S] |
+// smem: stages [S][umax][1024 doubles] | (cred) M pieces [2][16][128] | full[S], empty[S] |
 //       epi_full[2], epi_empty[2] | stage_item[S], epi_item[2] | epilogue offset tables:
 //       rows[128], cols[128] (int64)
-constexpr int RED_ROWS = 32;                          // rows of one TMA-reduce piece
-constexpr size_t RED_BYTES = (size_t)RED_ROWS * BN * 8;
+constexpr int RED_ROWS = 16;                          // rows of one TMA-reduce piece (double-buffered)
+constexpr size_t RED_BYTES = 2 * (size_t)RED_ROWS * BN * 8;
 struct FusedLayout {
   __host__ __device__ static size_t stage_bytes(int umax) { return (size_t)umax * VIEW_DOUBLES * 8; }
   __host__ __device__ static size_t red_off(int umax, int stages) { return (size_t)stages * stage_bytes(umax); }
@@ -284,27 +284,27 @@ __device__ __forceinline__ void epilogue_red(const GemmArgs &p, const double (&a
   tile_of(p, item, slot, ti, tj);
   const TermDesc td = p.terms[slot];
   const int pos = item - slot * p.tiles_m * p.tiles_n;
+  int nb = 0;  // piece buffer
   for (int j = 0; j < td.c_count; ++j) {
     const TgtDesc tg = p.tgts[td.c_first + j];
-    int32_t *ticket = p.tickets + tg.ticket_base + pos;
     if (p.use_tickets && !STC_NOTICKET) {
       if (tid == 0)
-        while (ld_acquire_gpu(ticket) < tg.order) __nanosleep(64);
+        while (ld_acquire_gpu(p.tickets + tg.ticket_base + pos) < tg.order) __nanosleep(64);
     }
+    // pieces of 16 tile rows (= one mt block of the warps with wm = pc / 4), two
+    // buffers: the writes of piece pc overlap the TMA read of piece pc - 1
     for (int pc = 0; pc < BM / RED_ROWS; ++pc) {
-      if (wm == (pc >> 1)) {
+      double *pb = buf + (size_t)nb * RED_ROWS * BN;
+      if (wm == (pc >> 2)) {
+        const int mt = pc & 3;
 #pragma unroll
-        for (int m2 = 0; m2 < 2; ++m2) {
-          const int mt = 2 * (pc & 1) + m2;
+        for (int h = 0; h < 2; ++h) {
+          const int r = epi_row<PA>(mt, h, g) - RED_ROWS * mt;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int r = epi_row<PA>(mt, h, g) - RED_ROWS * (pc & 1);
-#pragma unroll
-            for (int nt = 0; nt < 4; ++nt) {
-              const int c = wn * 32 + epi_col<PB>(nt, tig);
-              *reinterpret_cast<double2 *>(buf + red_index(r, c)) =
-                  make_double2(tg.sign * acc[mt][nt][2 * h], tg.sign * acc[mt][nt][2 * h + 1]);
-            }
+          for (int nt = 0; nt < 4; ++nt) {
+            const int c = wn * 32 + epi_col<PB>(nt, tig);
+            *reinterpret_cast<double2 *>(pb + red_index(r, c)) =
+                make_double2(tg.sign * acc[mt][nt][2 * h], tg.sign * acc[mt][nt][2 * h + 1]);
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA reads
@@ -319,17 +319,18 @@ __device__ __forceinline__ void epilogue_red(const GemmArgs &p, const double (&a
           const int src = p.tm_src[2][d];
           c5[d] = src < 4 ? coord_of(rc, src) : coord_of(cc, src - 4);
         }
-        tma_reduce_add(tmC, p.tm_rank[2], c5, buf);
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // piece buffer reusable
+        tma_reduce_add(tmC, p.tm_rank[2], c5, pb);
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // the other buffer is reusable
       }
       named_bar(2, 32 * CONSUMER_WARPS);
+      nb ^= 1;
     }
-    if (tid == 0) {
-      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // the adds are performed
+    if (tid == 0) {  // this target's adds performed: hand the tile to the next term at once
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
       if (p.use_tickets && !STC_NOTICKET) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
         __threadfence();
-        st_release_gpu(ticket, tg.order + 1);
+        st_release_gpu(p.tickets + tg.ticket_base + pos, tg.order + 1);
       }
     }
   }
