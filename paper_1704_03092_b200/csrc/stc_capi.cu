@@ -293,7 +293,8 @@ struct Plan {
   int grid = 1;
   // workspace layout (bytes)
   int max_ops = 1;  // most views on one side of any term (2^L)
-  size_t off_kbs = 0, off_coords = 0, off_mscr = 0;
+  size_t off_kbs = 0, off_coords = 0, off_mscr = 0, off_pka = 0, off_pkb = 0;
+  bool need_pack = false;  // fused kernel on repacked operands (layout not box-regular)
   size_t off_pool = 0, off_vecs = 0, off_tab = 0, off_tickets = 0, off_counters = 0, off_M = 0, off_pa = 0,
          off_pb = 0, off_acc = 0, total = 0;
   size_t tab_bytes = 0, acc_bytes = 0;
@@ -342,6 +343,21 @@ std::vector<int> exec_order(const std::vector<Term> &terms, int window) {
   }
   return seq;
 }
+
+// Operand sides seen by the fused kernel: the original tensors (direct) or
+// their repacked quadrant blocks (packed_sides).
+struct FusedSides {
+  stc_bundle ax, ak, bk, bx;  // A rows (I), A cols (P), B rows (P), B cols (J)
+  Tiling tax, tak, tbk, tbx;
+  int akf = 0, bkf = 0;
+  int64_t a_base = 0, b_base = 0;            // map base offsets (elements)
+  int64_t start[4], len[4], vbase[4];        // pool vectors ar, ac, br, bc: start, length, subtracted base
+};
+
+FusedSides direct_sides(const stc_problem *p, const Plan &pl);
+FusedSides packed_sides(const Plan &pl);
+bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, const double *A, const double *B,
+                const double *C, GemmArgs &g, CUtensorMap maps[3], CoordJobs &jobs);
 
 int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   if (!p) return fail(STC_EINVAL, "null problem");
@@ -484,8 +500,21 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   off = align256(off + (size_t)(pl.pool_len / 8) * 16);
   pl.off_mscr = off;  // fused ABC: two M tiles per CTA for the epilogue warps
   if (pl.variant == STC_VARIANT_ABC) off = align256(off + (size_t)pl.grid * 2 * BM * BN * 8);
+  // fused kernel on repacked operands when the views are not box-regular
+  if (pl.variant != STC_VARIANT_NAIVE) {
+    GemmArgs gd{};
+    CUtensorMap md[3];
+    CoordJobs jd{};
+    const bool direct = plan_fused(p, pl, direct_sides(p, pl), nullptr, nullptr, nullptr, gd, md, jd);
+    pl.need_pack = !direct && plan_fused(p, pl, packed_sides(pl), nullptr, nullptr, nullptr, gd, md, jd) &&
+                   !(getenv("STC_PACK") && atoi(getenv("STC_PACK")) == 0);
+  }
+  pl.off_pka = off;
+  if (pl.need_pack) off = align256(off + (size_t)(pl.Q * pl.Q) * pl.mq_pad * pl.kq_pad * 8);
+  pl.off_pkb = off;
+  if (pl.need_pack) off = align256(off + (size_t)(pl.Q * pl.Q) * pl.nq_pad * pl.kq_pad * 8);
   pl.off_vecs = off;
-  off = align256(off + pl.vecs.size() * sizeof(VecDesc));
+  off = align256(off + (pl.vecs.size() + 4) * sizeof(VecDesc));  // + the packed sides' vectors
   pl.off_tab = off;
   if (pl.variant == STC_VARIANT_ABC) {
     pl.tab_bytes = pl.tdesc.size() * sizeof(TermDesc) + pl.ops.size() * sizeof(OpDesc) + pl.tgts.size() * sizeof(TgtDesc);
@@ -737,7 +766,7 @@ bool plan_fused_side(const stc_bundle &xb, const Tiling &tx, const stc_bundle &k
     if (dims[d].str <= 0 || dims[d].box > 256 || dims[d].ext >= (int64_t)1 << 31) return false;
     if (d > 0 && ((dims[d].str % 2) != 0 || dims[d].str * 8 >= ((int64_t)1 << 40))) return false;
   }
-  if ((reinterpret_cast<uintptr_t>(data + base) & 15) != 0) return false;
+  if (data && (reinterpret_cast<uintptr_t>(data + base) & 15) != 0) return false;
   for (int part = 0; part < 2; ++part) {
     std::vector<int> idx;
     for (size_t d = 0; d < dims.size(); ++d)
@@ -830,21 +859,107 @@ bool plan_cred_side(const stc_bundle &rb, const Tiling &tr, const stc_bundle &cb
   return true;
 }
 
+FusedSides direct_sides(const stc_problem *p, const Plan &pl) {
+  FusedSides f;
+  f.ax = p->a_row;
+  f.ak = p->a_col;
+  f.bk = p->b_row;
+  f.bx = p->b_col;
+  f.tax = pl.ti;
+  f.tak = pl.tp;
+  f.tbk = pl.tp;
+  f.tbx = pl.tj;
+  f.akf = pl.a_kfast;
+  f.bkf = pl.b_kfast;
+  f.a_base = p->a_base;
+  f.b_base = p->b_base;
+  const int64_t st[4] = {pl.ar, pl.ac, pl.br, pl.bc};
+  const int64_t ln[4] = {pl.Q * pl.mq_pad, pl.Q * pl.kq_pad, pl.Q * pl.kq_pad, pl.Q * pl.nq_pad};
+  const int64_t vb[4] = {0, p->a_base, 0, p->b_base};  // build_plan: ac carries a_base, bc carries b_base
+  for (int i = 0; i < 4; ++i) {
+    f.start[i] = st[i];
+    f.len[i] = ln[i];
+    f.vbase[i] = vb[i];
+  }
+  return f;
+}
+
+// Repacked sides: quadrant block (r, c) of A is a dense mq_pad x kq_pad block
+// [k][x] (unit stride in x) or [x][k] (unit stride in k, like the source), block
+// index r * Q + c; B's block (r, c) (P quadrant r, J quadrant c) likewise with
+// nq_pad.  Expressed as two-label bundles (x | quadrant, k | quadrant) so the
+// fused planner treats them like any other tensor.
+void packed_bundle(stc_bundle &b, int64_t len, int64_t stride, int64_t Q, int64_t qstride) {
+  memset(&b, 0, sizeof(b));
+  b.nlab = Q > 1 ? 2 : 1;
+  b.ext[0] = len;
+  b.str[0] = stride;
+  if (Q > 1) {
+    b.ext[1] = Q;
+    b.str[1] = qstride;
+  }
+}
+
+FusedSides packed_sides(const Plan &pl) {
+  FusedSides f;
+  const int64_t Q = pl.Q, mq = pl.mq_pad, nq = pl.nq_pad, kq = pl.kq_pad;
+  const int64_t blkA = mq * kq, blkB = nq * kq;
+  f.akf = pl.a_kfast;
+  f.bkf = pl.b_kfast;
+  // A: x quadrant r (block row), k quadrant c (block column)
+  packed_bundle(f.ax, mq, f.akf ? kq : 1, Q, Q * blkA);
+  packed_bundle(f.ak, kq, f.akf ? 1 : mq, Q, blkA);
+  // B: k quadrant r (block row), x quadrant c (block column)
+  packed_bundle(f.bk, kq, f.bkf ? 1 : nq, Q, Q * blkB);
+  packed_bundle(f.bx, nq, f.bkf ? kq : 1, Q, blkB);
+  const int64_t keyx[2] = {1, 2}, keyk[2] = {1, 2};  // tile order: the block dims in natural order
+  f.tax = make_tiling(f.ax, pl.level, keyx, false);
+  f.tak = make_tiling(f.ak, pl.level, keyk, false);
+  f.tbk = make_tiling(f.bk, pl.level, keyk, false);
+  f.tbx = make_tiling(f.bx, pl.level, keyx, false);
+  const int64_t st[4] = {pl.ar, pl.ac, pl.br, pl.bc};
+  const int64_t ln[4] = {Q * mq, Q * kq, Q * kq, Q * nq};
+  for (int i = 0; i < 4; ++i) {
+    f.start[i] = st[i];
+    f.len[i] = ln[i];
+    f.vbase[i] = 0;
+  }
+  return f;
+}
+
+// The packed sides' pool vectors (mode 2), written over ar, ac, br, bc once the
+// operands are packed (the ops tables then address the packed blocks unchanged).
+void packed_vecs(const Plan &pl, const FusedSides &f, VecDesc out[4]) {
+  const stc_bundle *b[4] = {&f.ax, &f.ak, &f.bk, &f.bx};
+  for (int i = 0; i < 4; ++i) {
+    VecDesc &d = out[i];
+    memset(&d, 0, sizeof(d));
+    d.mode = 2;
+    d.out_start = f.start[i];
+    d.nq = pl.Q;
+    d.q_len = d.q_len_pad = d.len = b[i]->ext[0];
+    d.stride = b[i]->str[0];
+    d.base = pl.Q > 1 ? b[i]->str[1] : 0;
+  }
+}
+
 // Fused-kernel plan for ABC / AB (terms of at most 8 views per chunk: L <= 2):
 // tensor maps, the coordinate-table jobs and the kernel arguments.
-// STC_FUSED=0 disables.
-bool plan_fused(const stc_problem *p, const Plan &pl, const double *A, const double *B, const double *C, GemmArgs &g,
-                CUtensorMap maps[3], CoordJobs &jobs) {
+// STC_FUSED=0 disables.  A / B null: layout check only (no maps).
+bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, const double *A, const double *B,
+                const double *C, GemmArgs &g, CUtensorMap maps[3], CoordJobs &jobs) {
   if (const char *e = getenv("STC_FUSED"))
     if (atoi(e) == 0) return false;
   if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
+  if (pl.variant == STC_VARIANT_NAIVE) return false;
   const int umax = 2 * pl.max_ops;
   const int S = fused_stages(umax);
   if (umax > 8 || S < 2) return false;
   TmaSide sa, sb;
-  if (!plan_fused_side(p->a_row, pl.ti, p->a_col, pl.tp, pl.level, pl.a_kfast, A, p->a_base, sa)) return false;
-  if (!plan_fused_side(p->b_col, pl.tj, p->b_row, pl.tp, pl.level, pl.b_kfast, B, p->b_base, sb)) return false;
-  if (!encode_side(sa, A, p->a_base, maps[0]) || !encode_side(sb, B, p->b_base, maps[1])) return false;
+  if (!plan_fused_side(fs.ax, fs.tax, fs.ak, fs.tak, pl.level, fs.akf, A, fs.a_base, sa)) return false;
+  if (!plan_fused_side(fs.bx, fs.tbx, fs.bk, fs.tbk, pl.level, fs.bkf, B, fs.b_base, sb)) return false;
+  if (!A || !B) return true;
+  if (!encode_side(sa, A, fs.a_base, maps[0]) || !encode_side(sb, B, fs.b_base, maps[1])) return false;
   const TmaSide *ss[2] = {&sa, &sb};
   for (int sd = 0; sd < 2; ++sd) {
     g.tm_rank[sd] = ss[sd]->rank;
@@ -854,24 +969,19 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const double *A, const dou
       for (int i = 0; i < 4; ++i) g.tm_pstr[sd][part][i] = ss[sd]->pstr[part][i];
     }
   }
-  // pool vectors: ar (A x, base 0), ac (A k, base a_base), br (B k, base 0), bc (B x, base b_base)
-  struct V {
-    int64_t start, len;
-    int sd, part;
-    int64_t base;
-  } vs[4] = {{pl.ar, pl.Q * rup(cdiv(bundle_len(p->a_row), pl.Q), BM), 0, 0, 0},
-             {pl.ac, pl.Q * rup(cdiv(bundle_len(p->a_col), pl.Q), BK), 0, 1, p->a_base},
-             {pl.br, pl.Q * rup(cdiv(bundle_len(p->b_row), pl.Q), BK), 1, 1, 0},
-             {pl.bc, pl.Q * rup(cdiv(bundle_len(p->b_col), pl.Q), BN), 1, 0, p->b_base}};
+  // pool vectors ar (A x), ac (A k), br (B k), bc (B x)
+  const int vsd[4] = {0, 0, 1, 1}, vpart[4] = {0, 1, 1, 0};
   jobs.n = 4;
   for (int j = 0; j < 4; ++j) {
     CoordJob &jb = jobs.job[j];
-    jb.start = vs[j].start;
-    jb.count = vs[j].len / 8;
-    jb.base = vs[j].base;
-    jb.np = ss[vs[j].sd]->np[vs[j].part];
-    for (int i = 0; i < 4; ++i) jb.str[i] = ss[vs[j].sd]->pstr[vs[j].part][i];
+    jb.start = fs.start[j];
+    jb.count = fs.len[j] / 8;
+    jb.base = fs.vbase[j];
+    jb.np = ss[vsd[j]]->np[vpart[j]];
+    for (int i = 0; i < 4; ++i) jb.str[i] = ss[vsd[j]]->pstr[vpart[j]][i];
   }
+  g.a_kfast = fs.akf;
+  g.b_kfast = fs.bkf;
   // ABC: C updates by TMA reduce-add when the C targets are regular boxes (STC_CRED=0 disables)
   g.cred = 0;
   TmaSide sc;
@@ -959,6 +1069,44 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
   const int64_t P = (int64_t)tiles_m * tiles_n;
   const int T = (int)pl.terms.size();
 
+  // Fused kernel set-up: the operands' own views when they are box-regular, else
+  // their repacked quadrant blocks (one gather pass per operand, pure copies).
+  bool packed = false;
+  auto prepare_fused = [&](GemmArgs &gf, CUtensorMap *maps, const double *Cp) -> int {
+    CoordJobs jobs{};
+    int ok = plan_fused(p, pl, direct_sides(p, pl), A, B, Cp, gf, maps, jobs) ? 1 : 0;
+    if (!ok && pl.need_pack) {
+      double *PA = reinterpret_cast<double *>(ws + pl.off_pka);
+      double *PB = reinterpret_cast<double *>(ws + pl.off_pkb);
+      PackArgs pa{pl.ar, pl.ac, pl.mq_pad, pl.kq_pad, (int32_t)pl.Q, 1, pl.a_kfast, 0};
+      PackArgs pb{pl.bc, pl.br, pl.nq_pad, pl.kq_pad, (int32_t)pl.Q, 0, pl.b_kfast, 0};
+      CU(launch_pack_views(A, pool, pa, PA, s), "k_pack_views(A)");
+      CU(launch_pack_views(B, pool, pb, PB, s), "k_pack_views(B)");
+      const FusedSides fs = packed_sides(pl);
+      VecDesc pv[4];
+      packed_vecs(pl, fs, pv);
+      VecDesc *d_pv = reinterpret_cast<VecDesc *>(ws + pl.off_vecs) + pl.vecs.size();
+      if (int rc = upload(pv, sizeof(pv), d_pv, s)) return -rc;
+      CU(launch_build_pool(d_pv, 4, pl.pool_len, pool, s), "k_build_pool(packed)");
+      launches += 3;
+      if (!plan_fused(p, pl, fs, PA, PB, Cp, gf, maps, jobs)) return -fail(STC_EINVAL, "internal: packed plan");
+      gf.A = PA;
+      gf.B = PB;
+      ok = 1;
+      packed = true;
+    }
+    if (ok && !packed) {
+      gf.A = A;
+      gf.B = B;
+    }
+    if (ok) {
+      gf.coords = reinterpret_cast<const int4 *>(ws + pl.off_coords);
+      CU(launch_pool_coords(pool, reinterpret_cast<int4 *>(ws + pl.off_coords), jobs, s), "k_pool_coords");
+      ++launches;
+    }
+    return ok;
+  };
+
   GemmArgs g{};
   g.pool = pool;
   g.tiles_m = tiles_m;
@@ -997,18 +1145,16 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
     g.counter = counters;
     const int grid = (int)std::min<int64_t>(pl.grid, g.total_items);
     CUtensorMap maps[3];
-    CoordJobs jobs{};
     GemmArgs gf = g;
-    if (plan_fused(p, pl, A, B, C, gf, maps, jobs)) {
+    const int fz = prepare_fused(gf, maps, C);
+    if (fz < 0) return -fz;
+    if (fz) {
       // fused kernel: TMA boxes of 128 x 8, sums in the consumers' fragment loads
-      tma = true;
-      gf.coords = reinterpret_cast<const int4 *>(ws + pl.off_coords);
+      tma = !packed;
       // opt-in: C updates by the producer warpgroup's idle warps (helps L1 / large
       // k; at L2 on 4096^3 their DADDs starve behind the DMMAs)
       if (getenv("STC_EPI_OFFLOAD") && atoi(getenv("STC_EPI_OFFLOAD")) != 0)
         gf.mscratch = reinterpret_cast<double *>(ws + pl.off_mscr);
-      CU(launch_pool_coords(pool, reinterpret_cast<int4 *>(ws + pl.off_coords), jobs, s), "k_pool_coords");
-      ++launches;
       if (g_ev_before) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
       CU(launch_fused(gf, grid, s, maps), "k_strassen_fused");
     } else {
@@ -1025,6 +1171,9 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
     double *M = reinterpret_cast<double *>(ws + pl.off_M);
     double *PA = reinterpret_cast<double *>(ws + pl.off_pa);
     double *PB = reinterpret_cast<double *>(ws + pl.off_pb);
+    GemmArgs gf_ab = g;  // fused set-up shared by the batches (AB)
+    CUtensorMap maps_ab[3];
+    int fused_ab = 0;
     for (int bi = 0; bi < pl.nbatches; ++bi) {
       const int t0 = bi * pl.batch, t1 = std::min(T, t0 + pl.batch);
       const int nb = t1 - t0;
@@ -1158,19 +1307,36 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       g.m_stride = pl.m_slot;
       g.counter = counters + bi;
       const int grid = (int)std::min<int64_t>(pl.grid, g.total_items);
-      CUtensorMap maps[3];
-      CoordJobs jobs{};
       GemmArgs gf = g;
-      const bool fused = !naive && plan_fused(p, pl, A, B, nullptr, gf, maps, jobs);
-      if (fused && bi == 0) {
-        CU(launch_pool_coords(pool, reinterpret_cast<int4 *>(ws + pl.off_coords), jobs, s), "k_pool_coords");
-        ++launches;
+      if (bi == 0 && !naive) {
+        fused_ab = prepare_fused(gf_ab, maps_ab, nullptr);
+        if (fused_ab < 0) return -fused_ab;
+      }
+      const bool fused = fused_ab > 0;
+      if (fused) {  // per-batch fields over the fused set-up (maps, coordinates, packed operands)
+        const GemmArgs base = gf_ab;
+        gf.A = base.A;
+        gf.B = base.B;
+        gf.a_kfast = base.a_kfast;
+        gf.b_kfast = base.b_kfast;
+        gf.coords = base.coords;
+        gf.umax = base.umax;
+        gf.stages = base.stages;
+        gf.kchunks = base.kchunks;
+        gf.cred = 0;
+        for (int sd = 0; sd < 3; ++sd) {
+          gf.tm_rank[sd] = base.tm_rank[sd];
+          for (int d = 0; d < 5; ++d) gf.tm_src[sd][d] = base.tm_src[sd][d];
+          for (int part = 0; part < 2; ++part) {
+            gf.tm_np[sd][part] = base.tm_np[sd][part];
+            for (int i = 0; i < 4; ++i) gf.tm_pstr[sd][part][i] = base.tm_pstr[sd][part][i];
+          }
+        }
       }
       if (g_ev_before && bi == 0) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
       if (fused) {
-        tma = true;
-        gf.coords = reinterpret_cast<const int4 *>(ws + pl.off_coords);
-        CU(launch_fused(gf, grid, s, maps), "k_strassen_fused(dense)");
+        tma = !packed;
+        CU(launch_fused(gf, grid, s, maps_ab), "k_strassen_fused(dense)");
       } else {
         CU(launch_gemm(g, grid, s), "k_strassen_gemm(dense)");
       }

@@ -121,6 +121,14 @@ struct VecDesc {
   int32_t order[STC_MAX_LABELS];    // tile order of the box dims (order[0] fastest)
 };
 
+// Operand repacking (k_pack_views): pool vectors of the side's x and k views.
+struct PackArgs {
+  int64_t xv, kv;      // pool starts of the x / k vectors (quadrant-major, xlen / klen per quadrant)
+  int64_t xlen, klen;  // padded quadrant lengths
+  int32_t Q, xfirst;   // quadrants per dimension; block y = qa * Q + qb, x quadrant = xfirst ? qa : qb
+  int32_t kfast, _pad; // packed block layout: 0 [k][x], 1 [x][k]
+};
+
 // AB / Naive accumulate: C_q += sum over the quadrant's terms of sign * M_slot.
 struct AccArgs {
   const double *M;
@@ -166,6 +174,7 @@ cudaError_t launch_pool_coords(const int64_t *pool, int4 *coords, const CoordJob
 int gemm_max_grid(int max_ops);
 cudaError_t launch_accumulate(const AccArgs &a, cudaStream_t s);
 cudaError_t launch_unpack(const UnpackArgs &a, cudaStream_t s);
+cudaError_t launch_pack_views(const double *D, const int64_t *pool, const PackArgs &a, double *out, cudaStream_t s);
 cudaError_t launch_accum_dense_single(const double *M, int64_t ldm, int64_t m, int64_t n, double *C,
                                       const int64_t *rows, const int64_t *cols, double coeff, cudaStream_t s);
 struct ViewSet {

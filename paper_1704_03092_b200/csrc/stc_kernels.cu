@@ -34,6 +34,7 @@ __device__ __forceinline__ int64_t pool_entry(const VecDesc &d, int64_t o) {
   const int64_t ip = o - q * d.q_len_pad;
   if (ip >= d.q_len) return kPad;
   if (d.mode == 1) return ip * d.stride;
+  if (d.mode == 2) return q * d.base + ip * d.stride;  // packed quadrant blocks (quadrant stride in `base`)
   // tile order -> quadrant-local reference index
   int64_t i = ip;
   if (d.nbox > 0) {
@@ -209,6 +210,43 @@ cudaError_t launch_unpack(const UnpackArgs &a, cudaStream_t s) {
   int bx = (int)std::min<int64_t>((total + 255) / 256, 2048);
   dim3 grid(bx, a.nterms);
   k_unpack<<<grid, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+
+// ---- operand repacking for the fused kernel (irregular layouts) -------------
+// Block (qa, qb) = (blockIdx.y / Q, blockIdx.y % Q) of one operand side is the
+// view of x-quadrant (xfirst ? qa : qb) and k-quadrant (the other) copied into a
+// dense [k][x] (kfast = 0) or [x][k] (kfast = 1) block, PAD -> 0.  A pure copy:
+// the Strassen sums stay in the fused kernel, in the reference's view order.
+__global__ void k_pack_views(const double *__restrict__ D, const int64_t *__restrict__ pool, PackArgs a,
+                             double *__restrict__ out) {
+  const int qa = blockIdx.y / a.Q, qb = blockIdx.y - qa * a.Q;
+  const int xq = a.xfirst ? qa : qb, kq = a.xfirst ? qb : qa;
+  const int64_t *xv = pool + a.xv + (int64_t)xq * a.xlen;
+  const int64_t *kv = pool + a.kv + (int64_t)kq * a.klen;
+  double *o = out + (int64_t)blockIdx.y * a.xlen * a.klen;
+  const int64_t total = a.xlen * a.klen;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t x, k;
+    if (a.kfast) {
+      x = e / a.klen;
+      k = e - x * a.klen;
+    } else {
+      k = e / a.xlen;
+      x = e - k * a.xlen;
+    }
+    const int64_t xo = __ldg(xv + x), ko = __ldg(kv + k);
+    o[e] = (xo == kPad || ko == kPad) ? 0.0 : __ldg(D + xo + ko);
+  }
+}
+
+cudaError_t launch_pack_views(const double *D, const int64_t *pool, const PackArgs &a, double *out, cudaStream_t s) {
+  const int64_t total = a.xlen * a.klen;
+  if (total <= 0) return cudaSuccess;
+  const int bx = (int)std::min<int64_t>((total + 255) / 256, 1184 / std::max(1, a.Q * a.Q) + 1);
+  dim3 grid(std::max(bx, 4), a.Q * a.Q);
+  k_pack_views<<<grid, 256, 0, s>>>(D, pool, a, out);
   return cudaGetLastError();
 }
 

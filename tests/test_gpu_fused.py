@@ -83,12 +83,8 @@ def test_fused_matches_oracle_strassen():
     assert stc.relative_error(cf, ref) <= TOL
 
 
-def test_fused_declines_irregular_and_forced_slow():
-    # extents 24: tiles do not cut the bundles into boxes of 16 -> gather kernel
-    spec = stc.parse_benchmark_line("abij abef efij & a:24;b:24;i:24;j:24;e:24;f:24;")
-    a, b, c0 = _operands(spec, 31)
-    _, st = _run(spec, a, b, c0, 1, "abc", True)
-    assert st.fast_blocks == 0 and st.slow_blocks > 0
+def test_forced_slow_uses_the_gather_kernel():
+    # force_slow (the reference's per-element packing) always takes the gather kernel
     spec = stc.parse_benchmark_line(LAYOUTS["ak_bx"])
     a, b, c0 = _operands(spec, 32)
     c = c0.to_device()
@@ -110,3 +106,26 @@ def test_offloaded_epilogue_is_bitwise_identical():
         finally:
             del os.environ["STC_EPI_OFFLOAD"]
     assert np.array_equal(outs[0], outs[2]) and np.array_equal(outs[1], outs[3])
+
+
+@pytest.mark.parametrize("line", [
+    # the BASELINE irregular stress pattern, shrunk: odd extents, PAD quadrants
+    "abcij eafbc ifje & a:10;b:7;c:13;i:14;j:9;e:18;f:11;",
+    # permuted regular-looking layout whose tiles are not boxes (extent 24)
+    "abij abef efij & a:24;b:24;i:24;j:24;e:24;f:24;",
+])
+def test_repacked_operands_match_gather_bitwise(line):
+    # irregular views: A and B are repacked into dense quadrant blocks and the
+    # fused kernel runs on those (one extra pack + pool launch per operand);
+    # results must equal the gather kernel's bitwise, and the classical result
+    spec = stc.parse_benchmark_line(line)
+    a, b, c0 = _operands(spec, 51)
+    classical = c0.copy()
+    oracle.contract_reference(spec, a.to_host(), b.to_host(), classical)
+    for level in (0, 1, 2):
+        for variant in ("abc", "ab"):
+            cf, stf = _run(spec, a, b, c0, level, variant, True)
+            cg, stg = _run(spec, a, b, c0, level, variant, False)
+            assert stf.kernel_launches == stg.kernel_launches + 4, (level, variant)  # 2 packs, pool, coordinates
+            assert np.array_equal(cf.data, cg.data), (level, variant)
+            assert stc.relative_error(cf, classical) <= TOL, (level, variant)
