@@ -104,6 +104,13 @@ int stc_workspace_size(const stc_problem *p, size_t *bytes);
 int stc_contract(const stc_problem *p, const double *A, const double *B, double *C, void *workspace,
                  size_t workspace_bytes, void *stream, stc_stats *stats);
 
+/* Overlap hook (no reference counterpart): the next stc_contract call on this
+ * thread makes its kernels wait on the device until *c_ready != 0 (a device
+ * int32 another stream sets once C has arrived) before their first access to
+ * C, so an upload of C can overlap the operand staging and the DMMA main loop.
+ * Consumed by that call; NULL clears it. */
+int stc_set_c_ready(const int32_t *c_ready);
+
 /* Profiling hook (no reference counterpart): the next stc_contract call on
  * this thread records `before` / `after` (cudaEvent_t handles passed as void*)
  * on its stream immediately around the fused DMMA launch (ABC) or around the

@@ -56,7 +56,7 @@ class Stats(ctypes.Structure):
 _EXPORTS = (
     "stc_last_error", "stc_abi_version", "stc_workspace_size", "stc_contract", "stc_bundle_scatter",
     "stc_block_vector", "stc_fused_term_workspace_size", "stc_fused_term", "stc_accumulate_dense",
-    "stc_unpack_sum", "stc_sq_norms", "stc_set_kernel_events",
+    "stc_unpack_sum", "stc_sq_norms", "stc_set_kernel_events", "stc_set_c_ready",
 )
 
 _lib = None
@@ -83,6 +83,7 @@ def _declare(l):
     l.stc_unpack_sum.argtypes = [vp, i64, i64, i64, vp, ctypes.c_int, pp, pp, dp, vp, P(Stats)]
     l.stc_sq_norms.argtypes = [ctypes.c_int, P(i64), vp, P(i64), i64, vp, P(i64), i64, dp, vp]
     l.stc_set_kernel_events.argtypes = [vp, vp]
+    l.stc_set_c_ready.argtypes = [vp]
     for name in _EXPORTS:
         if name not in ("stc_last_error",):
             getattr(l, name).restype = ctypes.c_int if name != "stc_last_error" else ctypes.c_char_p

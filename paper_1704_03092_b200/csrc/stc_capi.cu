@@ -29,6 +29,7 @@ namespace {
 
 thread_local std::string g_err;
 thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;  // stc_set_kernel_events
+thread_local const int32_t *g_c_ready = nullptr;                        // stc_set_c_ready
 
 int fail(int code, const char *fmt, ...) {
   char buf[512];
@@ -1029,6 +1030,11 @@ int stc_set_kernel_events(void *before, void *after) {
   return STC_OK;
 }
 
+int stc_set_c_ready(const int32_t *c_ready) {
+  g_c_ready = c_ready;
+  return STC_OK;
+}
+
 int stc_workspace_size(const stc_problem *p, size_t *bytes) {
   Plan pl;
   const int sms = gemm_max_grid(MAX_OPS);  // per-CTA scratch is sized by the launch grid (0 without a device)
@@ -1107,8 +1113,11 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
     return ok;
   };
 
+  const int32_t *c_ready = g_c_ready;  // consumed by this call
+  g_c_ready = nullptr;
   GemmArgs g{};
   g.pool = pool;
+  g.c_ready = c_ready;
   g.tiles_m = tiles_m;
   g.tiles_n = tiles_n;
   g.kchunks = (int)(pl.kq_pad / BK);
@@ -1260,6 +1269,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         return acc + at;
       };
       AccArgs aa{};
+      aa.c_ready = c_ready;
       aa.list_start = reinterpret_cast<const int32_t *>(aput(lstart.data(), lstart.size() * 4, (pl.nquads + 1) * 4));
       aa.list_slot = reinterpret_cast<const int32_t *>(
           aput(lslot.data(), lslot.size() * 4, (size_t)pl.batch * pl.nquads * 4));

@@ -27,6 +27,16 @@ __device__ __forceinline__ void tile_of(const GemmArgs &p, int item, int &slot, 
   tj = r / gsz;
 }
 
+// stc_set_c_ready: block until C has arrived (thread 0 polls, the consumer
+// warps meet at named barrier 2).  `seen` keeps it to one poll per CTA.
+__device__ __forceinline__ void wait_c_ready(const GemmArgs &p, int tid, bool &seen) {
+  if (!p.c_ready || seen) return;
+  if (tid == 0)
+    while (ld_acquire_gpu(p.c_ready) == 0) __nanosleep(256);
+  named_bar(2, 32 * CONSUMER_WARPS);
+  seen = true;
+}
+
 // Epilogue of one work item (consumer warps 0..7, 64x32 warp tiles of
 // m16n8k4 fragments): add sign * M into each C target through the scatter
 // layout, C-tile updates ordered across terms by per-tile tickets

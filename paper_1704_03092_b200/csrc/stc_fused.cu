@@ -346,10 +346,17 @@ __device__ __forceinline__ void epilogue_warps(const GemmArgs &p, uint64_t *epi_
   int eb = 0;
   uint32_t ephase = 0;
   const int lane = t & 31;
+  bool c_seen = false;
   for (;;) {
     mbar_wait(&epi_full[eb], ephase);
     const int item = epi_item[eb];
     if (item < 0) break;
+    if (p.c_ready && !c_seen) {  // stc_set_c_ready
+      if (t == 0)
+        while (ld_acquire_gpu(p.c_ready) == 0) __nanosleep(256);
+      named_bar(3, EPI_THREADS);
+      c_seen = true;
+    }
     int slot, ti, tj;
     tile_of(p, item, slot, ti, tj);
     const TermDesc td = p.terms[slot];
@@ -523,6 +530,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 1)
     uint32_t phase = 0;
     int eb = 0;  // M scratch buffer (offloaded epilogue)
     uint32_t ephase = 0;
+    bool c_seen = false;  // stc_set_c_ready flag observed
     double acc[4][4][4];
     for (;;) {
       mbar_wait(&full[stage], phase);
@@ -629,6 +637,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 1)
         if (z == 1.2345e300) p.C[0] = z;
       }
 #else
+      if (!p.dense_out) wait_c_ready(p, tid, c_seen);
       if (red)
         epilogue_red<AKF + 1, BKF + 1>(p, acc, item, tid, wm, wn, g, tig, redbuf, &tmC);
       else

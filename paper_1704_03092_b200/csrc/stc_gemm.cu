@@ -684,6 +684,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int wm = warp & 1, wn = warp >> 1;
     int stage = 0;
     uint32_t phase = 0;
+    bool c_seen = false;  // stc_set_c_ready flag observed
     double acc[4][4][4];
     for (;;) {
       mbar_wait(&full[stage], phase);
@@ -728,6 +729,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           phase ^= 1;
         }
       }
+      if (!p.dense_out) wait_c_ready(p, tid, c_seen);
       epilogue_store(p, acc, item, tid, wm, wn, g, tig);
     }
   }

@@ -92,6 +92,7 @@ struct GemmArgs {
   int32_t umax, stages;      // views per chunk stage (2 * max_ops), ring depth
   double *mscratch;          // ABC: [grid][2][BM * BN] M tiles handed to the epilogue warps
   int32_t cred;              // ABC: C updates by TMA reduce-add of M pieces (C views regular)
+  const int32_t *c_ready;    // stc_set_c_ready: wait until *c_ready != 0 before touching C
 };
 
 // Jobs of k_pool_coords: one per operand pool vector (x or k part of A or B).
@@ -140,6 +141,7 @@ struct AccArgs {
   const int32_t *list_start;   // [nquads + 1]
   const int32_t *list_slot;    // M slots in term order
   const double *list_sign;
+  const int32_t *c_ready;      // stc_set_c_ready (see GemmArgs)
   const int64_t *row_start;    // [nquads] pool index of C row vector
   const int64_t *col_start;    // [nquads] pool index of C col vector
 };

@@ -161,6 +161,16 @@ cudaError_t launch_copy_pad(const int64_t *in, int64_t len, int64_t len_pad, int
 // C_q(i,j) += s_1 M_1(i,j) + s_2 M_2(i,j) + ... in term order, one RMW per
 // element (bitwise the reference's per-term accum_dense sequence).
 __global__ void k_accumulate(const AccArgs a) {
+  if (a.c_ready) {  // stc_set_c_ready: C's upload may still be in flight
+    if (threadIdx.x == 0) {
+      int v;
+      do {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(a.c_ready) : "memory");
+        if (v == 0) __nanosleep(256);
+      } while (v == 0);
+    }
+    __syncthreads();
+  }
   const int q = blockIdx.y;
   const int64_t total = a.mq * a.nq;
   const int64_t rs = a.row_start[q], cs = a.col_start[q];
