@@ -420,10 +420,12 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   pl.cc = add(vec_bundle(p->c_col, p->c_base, pl.Q, BN, tj));
   if (pl.variant == STC_VARIANT_NAIVE) {
     // packed operand sums: Apack[k][x] (ld mq_pad), Bpack[k][x] (ld nq_pad)
-    pl.dxa = add(vec_affine(pl.mq_pad, pl.mq_pad, 1));
-    pl.dka = add(vec_affine(pl.kq_pad, pl.kq_pad, pl.mq_pad));
-    pl.dxb = add(vec_affine(pl.nq_pad, pl.nq_pad, 1));
-    pl.dkb = add(vec_affine(pl.kq_pad, pl.kq_pad, pl.nq_pad));
+    // packed operand sums per term slot, oriented like the source (unit stride in k ->
+    // [x][k] slots, else [k][x]) so the unpack reads and writes coalesce
+    pl.dxa = add(vec_affine(pl.mq_pad, pl.mq_pad, pl.a_kfast ? pl.kq_pad : 1));
+    pl.dka = add(vec_affine(pl.kq_pad, pl.kq_pad, pl.a_kfast ? 1 : pl.mq_pad));
+    pl.dxb = add(vec_affine(pl.nq_pad, pl.nq_pad, pl.b_kfast ? pl.kq_pad : 1));
+    pl.dkb = add(vec_affine(pl.kq_pad, pl.kq_pad, pl.b_kfast ? 1 : pl.nq_pad));
   }
 
   pl.terms = strassen_terms(pl.level);
@@ -1290,12 +1292,14 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         ua.x_len = pl.mq_pad;
         ua.k_len = pl.kq_pad;
         ua.slot_stride = pl.pa_slot;
+        ua.kfast = pl.a_kfast;
         CU(launch_unpack(ua, s), "k_unpack(A)");
         ua.D = B;
         ua.out = PB;
         ua.terms = d_ub;
         ua.x_len = pl.nq_pad;
         ua.slot_stride = pl.pb_slot;
+        ua.kfast = pl.b_kfast;
         CU(launch_unpack(ua, s), "k_unpack(B)");
         launches += 2;
         st.slow_blocks += 2 * nb;
@@ -1308,8 +1312,8 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       g.tgts = nullptr;
       g.nterms = nb;
       g.total_items = (int)(P * nb);
-      g.a_kfast = naive ? 0 : pl.a_kfast;
-      g.b_kfast = naive ? 0 : pl.b_kfast;
+      g.a_kfast = pl.a_kfast;  // Naive slots follow the source orientation too
+      g.b_kfast = pl.b_kfast;
       g.dense_out = 1;
       g.use_tickets = 0;
       g.M = M;

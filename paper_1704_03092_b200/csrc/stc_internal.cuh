@@ -153,8 +153,8 @@ struct UnpackArgs {
   const int64_t *pool;
   const TermDesc *terms;  // uses (a_first, a_count) as the side's op range
   const OpDesc *ops;
-  int32_t nterms, _pad;
-  int64_t x_len, k_len;   // padded extents (ld = x_len)
+  int32_t nterms, kfast;  // kfast: slot layout [x][k] (k contiguous, ld = k_len), else [k][x] (ld = x_len)
+  int64_t x_len, k_len;   // padded extents
   int64_t slot_stride;
 };
 

@@ -195,14 +195,23 @@ cudaError_t launch_accumulate(const AccArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// out_slot[k*x_len + x] = sum_op sign * D[x_vec[x] + k_vec[k]]  (view order, PAD -> 0)
+// out_slot[k*x_len + x] (or [x*k_len + k] when kfast) = sum_op sign * D[x_vec[x] + k_vec[k]]
+// (view order, PAD -> 0)
 __global__ void k_unpack(const UnpackArgs a) {
   const int t = blockIdx.y;
   const TermDesc td = a.terms[t];
   double *out = a.out + (int64_t)td.m_slot * a.slot_stride;
   const int64_t total = a.x_len * a.k_len;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = e / a.x_len, x = e - k * a.x_len;
+    // the slot layout follows the source's unit stride, so both sides of the copy coalesce
+    int64_t k, x;
+    if (a.kfast) {
+      x = e / a.k_len;
+      k = e - x * a.k_len;
+    } else {
+      k = e / a.x_len;
+      x = e - k * a.x_len;
+    }
     double acc = 0.0;
     for (int o = 0; o < td.a_count; ++o) {
       const OpDesc op = a.ops[td.a_first + o];

@@ -232,8 +232,9 @@ def contract(spec: ContractionSpec, a, b, c, level: int, variant, params: Blocki
                                   ctypes.byref(st)))
         e1.record(stream)
         stats.absorb(st)
-        if c_ready is not None:
-            stream.wait_stream(side)  # C's upload is complete before it is read back
+        if not c.on_device:
+            if c_ready is not None:
+                stream.wait_stream(side)  # C's upload is complete before it is read back
             c.store_from(C)  # synchronous download of C (host operands)
         elif not synchronize:
             # stream-ordered only: the caller times the stream itself; no per-call seconds
