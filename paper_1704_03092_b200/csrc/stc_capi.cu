@@ -1162,10 +1162,12 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
     if (fz) {
       // fused kernel: TMA boxes of 128 x 8, sums in the consumers' fragment loads
       tma = !packed;
-      // opt-in: C updates by the producer warpgroup's idle warps (helps L1 / large
-      // k; at L2 on 4096^3 their DADDs starve behind the DMMAs)
-      if (getenv("STC_EPI_OFFLOAD") && atoi(getenv("STC_EPI_OFFLOAD")) != 0)
-        gf.mscratch = reinterpret_cast<double *>(ws + pl.off_mscr);
+      // C updates by the producer warpgroup's three spare warps from dense M tiles:
+      // by default with the TMA reduce-add epilogue (no FP64 work in those warps);
+      // opt-in (STC_EPI_OFFLOAD=1) with load/add/store, whose DADDs starve behind the DMMAs
+      const char *eo = getenv("STC_EPI_OFFLOAD");
+      const int offload = eo ? atoi(eo) : (gf.cred ? 1 : 0);
+      if (offload) gf.mscratch = reinterpret_cast<double *>(ws + pl.off_mscr);
       if (g_ev_before) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
       CU(launch_fused(gf, grid, s, maps), "k_strassen_fused");
     } else {

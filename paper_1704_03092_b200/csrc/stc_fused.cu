@@ -412,6 +412,82 @@ __device__ __forceinline__ void epilogue_warps(const GemmArgs &p, uint64_t *epi_
   }
 }
 
+// Epilogue warps with TMA reduce-add (ABC, C targets regular; the default when
+// both apply): per item, the dense M tile in this CTA's scratch buffer is
+// streamed through the 16-row swizzled smem pieces (sign applied by an integer
+// sign-bit flip -- no FP64 work competing with the consumers' DMMAs) and added
+// into each C target in L2 by cp.reduce.async.bulk.tensor, in ticket order.
+// The consumers only write M and go on with the next item.
+__device__ __forceinline__ void epilogue_warps_red(const GemmArgs &p, uint64_t *epi_full, uint64_t *epi_empty,
+                                                   const int *epi_item, double *buf, const CUtensorMap *tmC, int t) {
+  int eb = 0;
+  uint32_t ephase = 0;
+  const int lane = t & 31;
+  bool c_seen = false;
+  for (;;) {
+    mbar_wait(&epi_full[eb], ephase);
+    const int item = epi_item[eb];
+    if (item < 0) break;
+    if (p.c_ready && !c_seen) {  // stc_set_c_ready
+      if (t == 0)
+        while (ld_acquire_gpu(p.c_ready) == 0) __nanosleep(256);
+      c_seen = true;
+    }
+    int slot, ti, tj;
+    tile_of(p, item, slot, ti, tj);
+    const TermDesc td = p.terms[slot];
+    const int pos = item - slot * p.tiles_m * p.tiles_n;
+    const double *Mt = p.mscratch + ((size_t)blockIdx.x * 2 + eb) * TILE_DOUBLES;
+    int nb = 0;
+    for (int j = 0; j < td.c_count; ++j) {
+      const TgtDesc tg = p.tgts[td.c_first + j];
+      const uint32_t flip = __double_as_longlong(tg.sign) < 0 ? 0x80000000u : 0u;
+      if (t == 0 && p.use_tickets && !STC_NOTICKET)
+        while (ld_acquire_gpu(p.tickets + tg.ticket_base + pos) < tg.order) __nanosleep(64);
+      int4 cc = make_int4(0, 0, 0, 0);
+      if (t == 0) cc = p.coords[(tg.col_start + (int64_t)tj * BN) >> 3];
+      for (int pc = 0; pc < BM / RED_ROWS; ++pc) {
+        double *pb = buf + (size_t)nb * RED_ROWS * BN;
+        if (t == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // pb's previous read done
+        named_bar(3, EPI_THREADS);
+        // 16 rows x 128 columns: 1024 double2, ~11 per thread, row-major reads of M
+        for (int e = t; e < RED_ROWS * BN / 2; e += EPI_THREADS) {
+          const int r = e / (BN / 2), c = 2 * (e - r * (BN / 2));
+          double2 v = *reinterpret_cast<const double2 *>(Mt + (size_t)(RED_ROWS * pc + r) * BN + c);
+          v.x = __hiloint2double(__double2hiint(v.x) ^ (int)flip, __double2loint(v.x));
+          v.y = __hiloint2double(__double2hiint(v.y) ^ (int)flip, __double2loint(v.y));
+          *reinterpret_cast<double2 *>(pb + red_index(r, c)) = v;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        named_bar(3, EPI_THREADS);
+        if (t == 0) {
+          const int4 rc = p.coords[(tg.row_start + (int64_t)ti * BM + RED_ROWS * pc) >> 3];
+          int32_t c5[5];
+#pragma unroll
+          for (int d = 0; d < 5; ++d) {
+            const int src = p.tm_src[2][d];
+            c5[d] = src < 4 ? coord_of(rc, src) : coord_of(cc, src - 4);
+          }
+          tma_reduce_add(tmC, p.tm_rank[2], c5, pb);
+        }
+        nb ^= 1;
+      }
+      if (t == 0) {  // this target's adds performed: hand the tile to the next term
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        if (p.use_tickets && !STC_NOTICKET) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          __threadfence();
+          st_release_gpu(p.tickets + tg.ticket_base + pos, tg.order + 1);
+        }
+      }
+    }
+    named_bar(3, EPI_THREADS);  // every warp is done with this M buffer
+    if (lane == 0) mbar_arrive(&epi_empty[eb]);
+    eb ^= 1;
+    if (eb == 0) ephase ^= 1;
+  }
+}
+
 template <int AKF, int BKF>
 __global__ void __launch_bounds__(FUSED_THREADS, 1)
     k_strassen_fused(const GemmArgs p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -450,7 +526,10 @@ __global__ void __launch_bounds__(FUSED_THREADS, 1)
     // ===================== producer warp: TMA box loads ================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(FUSED_PRODUCER_REGS));
     if (warp != CONSUMER_WARPS) {
-      if (offload) epilogue_warps(p, epi_full, epi_empty, epi_item, epi_rows, epi_cols, tid - 32 * (CONSUMER_WARPS + 1));
+      if (offload && red)
+        epilogue_warps_red(p, epi_full, epi_empty, epi_item, redbuf, &tmC, tid - 32 * (CONSUMER_WARPS + 1));
+      else if (offload)
+        epilogue_warps(p, epi_full, epi_empty, epi_item, epi_rows, epi_cols, tid - 32 * (CONSUMER_WARPS + 1));
       return;
     }
     int stage = 0;

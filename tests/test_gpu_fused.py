@@ -92,20 +92,24 @@ def test_forced_slow_uses_the_gather_kernel():
     assert st.fast_blocks == 0 and st.slow_blocks > 0
 
 
-def test_offloaded_epilogue_is_bitwise_identical():
-    # STC_EPI_OFFLOAD=1: the producer warpgroup's spare warps apply the C updates
+def test_epilogue_modes_are_bitwise_identical():
+    # C updates: inline or by the producer warpgroup's spare warps (STC_EPI_OFFLOAD),
+    # with TMA reduce-add (default when the C targets are regular) or load/add/store
+    # (STC_CRED=0); every combination must give the same C
     spec = stc.parse_benchmark_line(LAYOUTS["ak_bx"])
     a, b, c0 = _operands(spec, 41)
-    outs = []
-    for flag in ("0", "1"):
-        os.environ["STC_EPI_OFFLOAD"] = flag
-        try:
-            for level in (1, 2):
-                c, st = _run(spec, a, b, c0, level, "abc", True)
-                outs.append(c.data)
-        finally:
-            del os.environ["STC_EPI_OFFLOAD"]
-    assert np.array_equal(outs[0], outs[2]) and np.array_equal(outs[1], outs[3])
+    outs = {}
+    for cred in ("1", "0"):
+        for off in ("0", "1"):
+            os.environ["STC_CRED"], os.environ["STC_EPI_OFFLOAD"] = cred, off
+            try:
+                outs[cred, off] = [_run(spec, a, b, c0, level, "abc", True)[0].data for level in (1, 2)]
+            finally:
+                del os.environ["STC_CRED"], os.environ["STC_EPI_OFFLOAD"]
+    ref = outs["1", "1"]
+    for key, got in outs.items():
+        for level in range(2):
+            assert np.array_equal(got[level], ref[level]), (key, level + 1)
 
 
 @pytest.mark.parametrize("line", [
