@@ -32,8 +32,13 @@ constexpr int FK = 8;                        // k-chunk of the fused kernel
 constexpr int VIEW_DOUBLES = BM * FK;        // one raw view of one chunk (BM == BN)
 constexpr int FUSED_PRODUCER_WARPS = 4;  // one warpgroup (setmaxnreg is warpgroup-wide); warp 0 of it issues
 constexpr int FUSED_THREADS = 32 * (CONSUMER_WARPS + FUSED_PRODUCER_WARPS);
-constexpr int FUSED_CONSUMER_REGS = 232;  // 2 x 232 + 40 (x 32 lanes) fits an SMSP's 16 K registers
+// setmaxnreg budget: the CTA launches with 168 regs x 384 threads; the consumers'
+// increase (8 warps x 64) must be covered by what the producer warpgroup releases
+// (4 warps x (168 - 40)) or setmaxnreg.inc waits forever -- 40 is the ceiling.
+constexpr int FUSED_CONSUMER_REGS = 232;
 constexpr int FUSED_PRODUCER_REGS = 40;
+static_assert(CONSUMER_WARPS * (FUSED_CONSUMER_REGS - 168) <= FUSED_PRODUCER_WARPS * (168 - FUSED_PRODUCER_REGS),
+              "setmaxnreg: consumer increase exceeds the producer release");
 constexpr int MAX_FUSED_STAGES = 8;
 
 // smem: stages [S][umax][1024 doubles] | (cred) M pieces [2][16][128] | full[S], empty[S] |
