@@ -133,3 +133,24 @@ def test_repacked_operands_match_gather_bitwise(line):
             assert stf.kernel_launches == stg.kernel_launches + 4, (level, variant)  # 2 packs, pool, coordinates
             assert np.array_equal(cf.data, cg.data), (level, variant)
             assert stc.relative_error(cf, classical) <= TOL, (level, variant)
+
+
+def test_host_c_upload_overlap_matches():
+    # STC_C_OVERLAP=1: a host C is uploaded on a side stream while the kernel's
+    # main loop runs; the kernels wait on the device flag (stc_set_c_ready)
+    spec = stc.parse_benchmark_line(LAYOUTS["ax_bk"])
+    a = stc.make_dense_tensor(spec.tensor_extents(spec.labels_a), "random", 61)
+    b = stc.make_dense_tensor(spec.tensor_extents(spec.labels_b), "random", 62)
+    c0 = stc.make_dense_tensor(spec.tensor_extents(spec.labels_c), "random", 63)
+    outs = []
+    for flag in ("0", "1"):
+        os.environ["STC_C_OVERLAP"] = flag
+        try:
+            for variant in ("abc", "ab", "naive"):
+                c = c0.copy()
+                stc.contract(spec, a, b, c, 2, variant)
+                outs.append(c.data.copy())
+        finally:
+            del os.environ["STC_C_OVERLAP"]
+    for i in range(3):
+        assert np.array_equal(outs[i], outs[i + 3])
