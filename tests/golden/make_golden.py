@@ -18,6 +18,11 @@ the tests only read the committed .npz/.json outputs.  What is pinned:
 * cfg1.json     -- BASELINE config 1 (abij-abef-efij, extents 24, row-major,
                    uniform[-1,1] from seed 7 / 8, C = 0): reference L1 ABC output
                    summarised by norms and 4096 sampled entries.
+* full.json     -- BASELINE configs 2 and 4 at full size (cfg2: 4096^3 permuted,
+                   uniform[-1,1], L1 / L2 ABC; cfg4: 4550 x 3150 x 2970 irregular,
+                   normal(0,1), AB and Naive at L1 / L2), row-major, C = 0: the
+                   reference's own outputs summarised by norms and 4096 sampled
+                   entries (gen_full; run with --full, several minutes on 8 threads).
 """
 
 from __future__ import annotations
@@ -152,9 +157,48 @@ def gen_cfg1():
     (OUT / "cfg1.json").write_text(json.dumps(out))
 
 
+FULL = [
+    # (name, line, fill, seeds (A, B), runs)
+    ("cfg2", "aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;", "uniform", (2017, 2018),
+     [(1, "abc"), (2, "abc")]),
+    ("cfg4", "abcij eafbc ifje & a:50;b:7;c:13;i:70;j:45;e:90;f:33;", "normal", (4, 5),
+     [(1, "ab"), (2, "ab"), (1, "naive"), (2, "naive")]),
+]
+
+
+def gen_full():
+    out = []
+    for name, line, fill, (sa, sb), runs in FULL:
+        spec = st.parse_benchmark_line(line)
+
+        def tensor(labels, seed):
+            ext = tuple(spec.extents[x] for x in labels)
+            n = int(np.prod(ext))
+            rng = np.random.default_rng(seed)
+            data = rng.uniform(-1.0, 1.0, n) if fill == "uniform" else rng.standard_normal(n)
+            return st.DenseTensor(ext, row_major_strides(ext), data)
+
+        a, b = tensor(spec.labels_a, sa), tensor(spec.labels_b, sb)
+        ext_c = tuple(spec.extents[x] for x in spec.labels_c)
+        nc = int(np.prod(ext_c))
+        idx = np.random.default_rng(12).choice(nc, 4096, replace=False)
+        for level, variant in runs:
+            c = st.DenseTensor(ext_c, row_major_strides(ext_c), np.zeros(nc))
+            s = st.contract(spec, a, b, c, level, st.Variant(variant), threads=8)
+            out.append(dict(name=name, line=line, fill=fill, seed_a=sa, seed_b=sb, level=level, variant=variant,
+                            seconds=s.seconds, leaf_multiplies=s.leaf_multiplies,
+                            frob=float(np.sqrt(np.sum(c.data ** 2))), sum=float(np.sum(c.data)),
+                            sample_index=idx.tolist(), sample_value=c.data[idx].tolist()))
+            print(name, level, variant, f"{s.seconds:.1f} s", flush=True)
+    (OUT / "full.json").write_text(json.dumps(out))
+
+
 if __name__ == "__main__":
-    gen_views()
-    gen_terms()
-    gen_contract()
-    gen_cfg1()
+    if "--full" in sys.argv:
+        gen_full()
+    else:
+        gen_views()
+        gen_terms()
+        gen_contract()
+        gen_cfg1()
     print("golden fixtures written to", OUT)
