@@ -353,10 +353,12 @@ struct FusedSides {
   int akf = 0, bkf = 0;
   int64_t a_base = 0, b_base = 0;            // map base offsets (elements)
   int64_t start[4], len[4], vbase[4];        // pool vectors ar, ac, br, bc: start, length, subtracted base
+  int64_t qxa = 0, qk = 0, qxb = 0;          // quadrant (or slot) lengths of the A-x, k and B-x bundles
 };
 
 FusedSides direct_sides(const stc_problem *p, const Plan &pl);
 FusedSides packed_sides(const Plan &pl);
+FusedSides naive_sides(const Plan &pl);
 bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, const double *A, const double *B,
                 const double *C, GemmArgs &g, CUtensorMap maps[3], CoordJobs &jobs);
 
@@ -422,9 +424,8 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     // packed operand sums: Apack[k][x] (ld mq_pad), Bpack[k][x] (ld nq_pad)
     // packed operand sums per term slot, oriented like the source (unit stride in k ->
     // [x][k] slots, else [k][x]) so the unpack reads and writes coalesce
-    pl.dxa = add(vec_affine(pl.mq_pad, pl.mq_pad, pl.a_kfast ? pl.kq_pad : 1));
+    // (the x vectors, per term slot, follow once the batch is known)
     pl.dka = add(vec_affine(pl.kq_pad, pl.kq_pad, pl.a_kfast ? 1 : pl.mq_pad));
-    pl.dxb = add(vec_affine(pl.nq_pad, pl.nq_pad, pl.b_kfast ? pl.kq_pad : 1));
     pl.dkb = add(vec_affine(pl.kq_pad, pl.kq_pad, pl.b_kfast ? 1 : pl.nq_pad));
   }
 
@@ -491,6 +492,22 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     pl.m_slot = pl.mq_pad * pl.nq_pad;
     pl.pa_slot = pl.kq_pad * pl.mq_pad;
     pl.pb_slot = pl.kq_pad * pl.nq_pad;
+    if (pl.variant == STC_VARIANT_NAIVE) {
+      // Naive x vectors per term slot (mode 2, slot stride = the slot size): a
+      // term's op addresses its own slot block through the pool alone
+      auto slot_vec = [&](int64_t len, int64_t stride, int64_t slot) {
+        VecDesc d;
+        memset(&d, 0, sizeof(d));
+        d.mode = 2;
+        d.nq = pl.batch;
+        d.q_len = d.q_len_pad = d.len = len;
+        d.stride = stride;
+        d.base = slot;
+        return d;
+      };
+      pl.dxa = add(slot_vec(pl.mq_pad, pl.a_kfast ? pl.kq_pad : 1, pl.pa_slot));
+      pl.dxb = add(slot_vec(pl.nq_pad, pl.b_kfast ? pl.kq_pad : 1, pl.pb_slot));
+    }
   }
 
   // workspace layout
@@ -732,11 +749,10 @@ bool plan_tma(const stc_problem *p, const Plan &pl, const double *A, const doubl
 // low dim and a high dim when its tile extent exceeds 16.
 constexpr int kFusedK = 8;
 
-bool plan_fused_side(const stc_bundle &xb, const Tiling &tx, const stc_bundle &kb, const Tiling &tk, int level,
-                     int kfast, const double *data, int64_t base, TmaSide &ts) {
+bool plan_fused_side(const stc_bundle &xb, const Tiling &tx, const stc_bundle &kb, const Tiling &tk, int64_t qx,
+                     int64_t qk, int kfast, const double *data, int64_t base, TmaSide &ts) {
   if (tx.nbox == 0 || tk.nbox == 0) return false;
-  const int64_t Q = (int64_t)1 << level;
-  if ((bundle_len(xb) / Q) % BM != 0 || (bundle_len(kb) / Q) % BK != 0) return false;
+  if (qx % BM != 0 || qk % BK != 0) return false;  // quadrants cut into whole tiles / chunks
   int64_t tbx[STC_MAX_LABELS], tbk[STC_MAX_LABELS];
   int ox[STC_MAX_LABELS], ok_[STC_MAX_LABELS], nox = 0, nok = 0;
   if (!tile_subbox(xb, tx, BM, tbx, ox, nox) || !tile_subbox(kb, tk, kFusedK, tbk, ok_, nok)) return false;
@@ -884,6 +900,9 @@ FusedSides direct_sides(const stc_problem *p, const Plan &pl) {
     f.len[i] = ln[i];
     f.vbase[i] = vb[i];
   }
+  f.qxa = bundle_len(p->a_row) / pl.Q;
+  f.qk = bundle_len(p->a_col) / pl.Q;
+  f.qxb = bundle_len(p->b_col) / pl.Q;
   return f;
 }
 
@@ -927,6 +946,45 @@ FusedSides packed_sides(const Plan &pl) {
     f.len[i] = ln[i];
     f.vbase[i] = 0;
   }
+  f.qxa = mq;
+  f.qk = kq;
+  f.qxb = nq;
+  return f;
+}
+
+// Naive: the packed operand sums of each term slot ([k][x] or [x][k] blocks,
+// slot stride pa_slot / pb_slot) as bundles (x | slot, k); the slot x vectors
+// dxa / dxb are per-slot (mode 2), so a term's view is its own slot block.
+FusedSides naive_sides(const Plan &pl) {
+  FusedSides f;
+  const int64_t mq = pl.mq_pad, nq = pl.nq_pad, kq = pl.kq_pad, nb = pl.batch;
+  f.akf = pl.a_kfast;
+  f.bkf = pl.b_kfast;
+  packed_bundle(f.ax, mq, f.akf ? kq : 1, nb, pl.pa_slot);
+  packed_bundle(f.ak, kq, f.akf ? 1 : mq, 1, 0);
+  packed_bundle(f.bk, kq, f.bkf ? 1 : nq, 1, 0);
+  packed_bundle(f.bx, nq, f.bkf ? kq : 1, nb, pl.pb_slot);
+  auto natural = [](int64_t len) {
+    Tiling t;
+    t.nbox = 1;
+    t.box_ext[0] = len;
+    t.order[0] = 0;
+    return t;
+  };
+  f.tax = natural(mq);
+  f.tak = natural(kq);
+  f.tbk = natural(kq);
+  f.tbx = natural(nq);
+  const int64_t st[4] = {pl.dxa, pl.dka, pl.dkb, pl.dxb};
+  const int64_t ln[4] = {nb * mq, kq, kq, nb * nq};
+  for (int i = 0; i < 4; ++i) {
+    f.start[i] = st[i];
+    f.len[i] = ln[i];
+    f.vbase[i] = 0;
+  }
+  f.qxa = mq;
+  f.qk = kq;
+  f.qxb = nq;
   return f;
 }
 
@@ -954,13 +1012,12 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
   if (const char *e = getenv("STC_FUSED"))
     if (atoi(e) == 0) return false;
   if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
-  if (pl.variant == STC_VARIANT_NAIVE) return false;
-  const int umax = 2 * pl.max_ops;
+  const int umax = pl.variant == STC_VARIANT_NAIVE ? 2 : 2 * pl.max_ops;  // Naive: one packed view per side
   const int S = fused_stages(umax);
   if (umax > 8 || S < 2) return false;
   TmaSide sa, sb;
-  if (!plan_fused_side(fs.ax, fs.tax, fs.ak, fs.tak, pl.level, fs.akf, A, fs.a_base, sa)) return false;
-  if (!plan_fused_side(fs.bx, fs.tbx, fs.bk, fs.tbk, pl.level, fs.bkf, B, fs.b_base, sb)) return false;
+  if (!plan_fused_side(fs.ax, fs.tax, fs.ak, fs.tak, fs.qxa, fs.qk, fs.akf, A, fs.a_base, sa)) return false;
+  if (!plan_fused_side(fs.bx, fs.tbx, fs.bk, fs.tbk, fs.qxb, fs.qk, fs.bkf, B, fs.b_base, sb)) return false;
   if (!A || !B) return true;
   if (!encode_side(sa, A, fs.a_base, maps[0]) || !encode_side(sb, B, fs.b_base, maps[1])) return false;
   const TmaSide *ss[2] = {&sa, &sb};
@@ -1215,10 +1272,10 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         if (naive) {
           gd.a_first = (int)ops.size();
           gd.a_count = 1;
-          ops.push_back({pl.dxa, pl.dka, slot * pl.pa_slot, 1.0});
+          ops.push_back({pl.dxa + slot * pl.mq_pad, pl.dka, 0, 1.0});
           gd.b_first = (int)ops.size();
           gd.b_count = 1;
-          ops.push_back({pl.dxb, pl.dkb, slot * pl.pb_slot, 1.0});
+          ops.push_back({pl.dxb + slot * pl.nq_pad, pl.dkb, 0, 1.0});
         } else {
           gd.a_first = ua.a_first;
           gd.a_count = ua.a_count;
@@ -1327,6 +1384,17 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       if (bi == 0 && !naive) {
         fused_ab = prepare_fused(gf_ab, maps_ab, nullptr);
         if (fused_ab < 0) return -fused_ab;
+      } else if (bi == 0 && naive) {
+        // Naive: the per-term packed sums (PA, PB) are regular by construction
+        CoordJobs jobs{};
+        if (plan_fused(p, pl, naive_sides(pl), PA, PB, nullptr, gf_ab, maps_ab, jobs)) {
+          gf_ab.A = PA;
+          gf_ab.B = PB;
+          gf_ab.coords = reinterpret_cast<const int4 *>(ws + pl.off_coords);
+          CU(launch_pool_coords(pool, reinterpret_cast<int4 *>(ws + pl.off_coords), jobs, s), "k_pool_coords");
+          ++launches;
+          fused_ab = 1;
+        }
       }
       const bool fused = fused_ab > 0;
       if (fused) {  // per-batch fields over the fused set-up (maps, coordinates, packed operands)
@@ -1351,7 +1419,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       }
       if (g_ev_before && bi == 0) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
       if (fused) {
-        tma = !packed;
+        tma = !packed && !naive;
         CU(launch_fused(gf, grid, s, maps_ab), "k_strassen_fused(dense)");
       } else {
         CU(launch_gemm(g, grid, s), "k_strassen_gemm(dense)");
