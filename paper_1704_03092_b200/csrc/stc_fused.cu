@@ -178,6 +178,7 @@ __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (
                                           const int (&offA)[2][2], const int (&offB)[2][2], uint32_t negmask) {
   constexpr int G = NA + NB;
   const int fl = static_cast<int>(((negmask >> V) & 1u) << 31);
+  const double sgn = __hiloint2double(0x3ff00000 | fl, 0);  // +/-1.0
   const double *src = nst + V * VIEW_DOUBLES;
   if (load) {
     if constexpr (V < NA) {
@@ -186,20 +187,24 @@ __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (
         double t[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) t[j] = src[offA[KN][j & 1] + 128 * (2 * hh + (j >> 1))];
+        if (V == 0) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const double sv = __hiloint2double(__double2hiint(t[j]) ^ fl, __double2loint(t[j]));
-          xa[4 * hh + j] = V == 0 ? sv : __dadd_rn(xa[4 * hh + j], sv);
+          for (int j = 0; j < 4; ++j) xa[4 * hh + j] = __hiloint2double(__double2hiint(t[j]) ^ fl, __double2loint(t[j]));
+        } else {  // acc + (+/-1) * v: one exactly rounded add, no integer sign flip on the way
+#pragma unroll
+          for (int j = 0; j < 4; ++j) xa[4 * hh + j] = __fma_rn(sgn, t[j], xa[4 * hh + j]);
         }
       }
     } else {
       double t[4];
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) t[nt] = src[offB[KN][nt & 1] + 128 * (nt >> 1)];
+      if (V == NA) {
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        const double sv = __hiloint2double(__double2hiint(t[nt]) ^ fl, __double2loint(t[nt]));
-        xb[nt] = V == NA ? sv : __dadd_rn(xb[nt], sv);
+        for (int nt = 0; nt < 4; ++nt) xb[nt] = __hiloint2double(__double2hiint(t[nt]) ^ fl, __double2loint(t[nt]));
+      } else {
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) xb[nt] = __fma_rn(sgn, t[nt], xb[nt]);
       }
     }
   }
