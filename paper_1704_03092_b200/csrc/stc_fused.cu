@@ -228,21 +228,18 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
                                              uint64_t *full, uint64_t *empty, int &stage, uint32_t &phase, int kchunks,
                                              uint32_t negmask, const int (&offA_)[2][2], const int (&offB_)[2][2],
                                              int lane) {
-  // Many views (>= 4 per k-step): keep the fragment offsets in registers through
-  // opaque copies -- otherwise ptxas rematerialises them from %tid (S2R, a
-  // long-latency special-register read) inside the hot loop.  With few views
-  // the rematerialisation is the cheaper choice, so it is left alone.
+  // Keep the fragment offsets in registers through opaque copies: otherwise
+  // ptxas rematerialises them from %tid (S2R, a long-latency special-register
+  // read, plus the swizzle arithmetic) inside the hot loop.
   int oA[2][2] = {{offA_[0][0], offA_[0][1]}, {offA_[1][0], offA_[1][1]}};
   int oB[2][2] = {{offB_[0][0], offB_[0][1]}, {offB_[1][0], offB_[1][1]}};
-  if constexpr (NA + NB >= 4) {
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        asm volatile("mov.b32 %0, %0;" : "+r"(oA[i][j]));
-        asm volatile("mov.b32 %0, %0;" : "+r"(oB[i][j]));
-      }
-  }
+    for (int j = 0; j < 2; ++j) {
+      asm volatile("mov.b32 %0, %0;" : "+r"(oA[i][j]));
+      asm volatile("mov.b32 %0, %0;" : "+r"(oB[i][j]));
+    }
   const int (&offA)[2][2] = oA;
   const int (&offB)[2][2] = oB;
   const size_t sstride = (size_t)umax * VIEW_DOUBLES;
