@@ -180,13 +180,16 @@ __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (
   const int fl = static_cast<int>(((negmask >> V) & 1u) << 31);
   const double sgn = __hiloint2double(0x3ff00000 | fl, 0);  // +/-1.0
   const double *src = nst + V * VIEW_DOUBLES;
+  // one address per fragment column / row pair; the mt / nt blocks are immediates
+  const double *pa0 = src + offA[KN][0], *pa1 = src + offA[KN][1];
+  const double *pb0 = src + offB[KN][0], *pb1 = src + offB[KN][1];
   if (load) {
     if constexpr (V < NA) {
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {  // mt pairs {0, 1}, {2, 3}
         double t[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) t[j] = src[offA[KN][j & 1] + 128 * (2 * hh + (j >> 1))];
+        for (int j = 0; j < 4; ++j) t[j] = (j & 1 ? pa1 : pa0)[128 * (2 * hh + (j >> 1))];  // immediate offsets
         if (V == 0) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) xa[4 * hh + j] = __hiloint2double(__double2hiint(t[j]) ^ fl, __double2loint(t[j]));
@@ -198,7 +201,7 @@ __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (
     } else {
       double t[4];
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) t[nt] = src[offB[KN][nt & 1] + 128 * (nt >> 1)];
+      for (int nt = 0; nt < 4; ++nt) t[nt] = (nt & 1 ? pb1 : pb0)[128 * (nt >> 1)];
       if (V == NA) {
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) xb[nt] = __hiloint2double(__double2hiint(t[nt]) ^ fl, __double2loint(t[nt]));
