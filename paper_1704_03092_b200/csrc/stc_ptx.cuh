@@ -52,10 +52,6 @@ __device__ __forceinline__ double ld_nc(const double *p) {
 
 // 8-byte global->shared async copy; `valid == false` zero-fills without reading.
 __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc, bool valid) {
-#ifdef STC_EXPERIMENT_SYNCCOPY
-  *reinterpret_cast<double *>(smem_dst) = valid ? *reinterpret_cast<const double *>(gsrc) : 0.0;
-  return;
-#endif
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc),
                "r"(valid ? 8 : 0)
                : "memory");
