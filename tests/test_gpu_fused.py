@@ -154,3 +154,57 @@ def test_host_c_upload_overlap_matches():
             del os.environ["STC_C_OVERLAP"]
     for i in range(3):
         assert np.array_equal(outs[i], outs[i + 3])
+
+
+@pytest.mark.parametrize("name", ["ax_bk", "ak_bx"])
+def test_integer_data_exact_on_every_path(name):
+    # integer-valued inputs: every product and partial sum is exact, so C must equal the
+    # classical result bitwise on the fused path (direct and repacked operands, TMA-reduce
+    # and load/add/store epilogues, inline and offloaded) for ABC, AB and Naive at L0..L2
+    spec = stc.parse_benchmark_line(LAYOUTS[name])
+
+    def ints(labels, seed):
+        e = spec.tensor_extents(labels)
+        return stc.DenseTensor(e, tuple(int(np.prod(e[i + 1:])) for i in range(len(e))),
+                               np.random.default_rng(seed).integers(-8, 9, int(np.prod(e))).astype(np.float64))
+
+    a, b, c0 = ints(spec.labels_a, 71), ints(spec.labels_b, 72), ints(spec.labels_c, 73)
+    ref = c0.copy()
+    oracle.contract_reference(spec, a, b, ref, threads=8)
+    ad, bd = a.to_device(), b.to_device()
+    envs = [{}, {"STC_CRED": "0"}, {"STC_EPI_OFFLOAD": "0"}, {"STC_PACK": "1", "STC_FUSED": "1"}]
+    for env in envs:
+        os.environ.update(env)
+        try:
+            for level in (0, 1, 2):
+                for variant in ("abc", "ab", "naive"):
+                    c = c0.to_device()
+                    stc.contract(spec, ad, bd, c, level, variant)
+                    assert np.array_equal(c.to_host().data, ref.data), (env, level, variant)
+        finally:
+            for k in env:
+                del os.environ[k]
+
+
+@pytest.mark.parametrize("offset", [0, 1, 2])
+def test_strided_torch_views(offset):
+    # operands as strided torch views (permuted strides, storage offsets): the fused path
+    # needs 16-byte aligned map bases, so odd offsets take the repacked path; results must
+    # match a classical einsum on the same views
+    import torch
+
+    spec = stc.parse_benchmark_line(LAYOUTS["ax_bk"])
+    g = torch.Generator(device="cuda").manual_seed(81)
+
+    def view(labels):
+        e = spec.tensor_extents(labels)
+        n = int(np.prod(e))
+        flat = torch.rand(n + 8, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+        return torch.as_strided(flat, e, tuple(int(np.prod(e[i + 1:])) for i in range(len(e))), offset)
+
+    a, b, c = view(spec.labels_a), view(spec.labels_b), view(spec.labels_c)
+    ref = c + torch.einsum(f"{spec.labels_a},{spec.labels_b}->{spec.labels_c}", a, b)
+    for level, variant in ((2, "abc"), (1, "ab")):
+        cc = c.clone()
+        stc.contract(spec, a, b, cc, level, variant)
+        assert (torch.linalg.vector_norm(cc - ref) / torch.linalg.vector_norm(ref)).item() <= TOL
