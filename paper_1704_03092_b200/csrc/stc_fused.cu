@@ -654,11 +654,10 @@ __global__ void __launch_bounds__(FUSED_THREADS, 1)
       tile_of(p, item, slot, ti, tj);
       const TermDesc td = p.terms[slot];
       const int na = td.a_count, nb = td.b_count;
-      uint32_t negmask = 0;
-      for (int u = 0; u < na + nb; ++u) {
-        const double sg = p.ops[u < na ? td.a_first + u : td.b_first + u - na].sign;
-        negmask |= (__double_as_longlong(sg) < 0 ? 1u : 0u) << u;
-      }
+      // coefficient signs of the item's views: one load per lane, one ballot
+      bool neg = false;
+      if (lane < na + nb) neg = __double_as_longlong(p.ops[lane < na ? td.a_first + lane : td.b_first + lane - na].sign) < 0;
+      const uint32_t negmask = __ballot_sync(0xffffffffu, neg);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
