@@ -208,3 +208,16 @@ def test_strided_torch_views(offset):
         cc = c.clone()
         stc.contract(spec, a, b, cc, level, variant)
         assert (torch.linalg.vector_norm(cc - ref) / torch.linalg.vector_norm(ref)).item() <= TOL
+
+
+def test_random_contractions_fuzz():
+    # tools/fuzz_gpu.py: random labels / extents / permuted layouts / storage offsets, all
+    # variants and levels, against a classical einsum (a fixed-seed slice of the sweep)
+    import importlib.util
+    import pathlib
+
+    path = pathlib.Path(__file__).resolve().parents[1] / "tools" / "fuzz_gpu.py"
+    spec = importlib.util.spec_from_file_location("fuzz_gpu", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    assert mod.main(24, 7) == 0
