@@ -1,13 +1,16 @@
-// stc_gemm.cu -- the fused Strassen DMMA kernel (north-star subsystems 2 + 3).
+// stc_gemm.cu -- the gather Strassen DMMA kernel (north-star subsystems 2 + 3):
+// the general path (any layout, PAD, L >= 3, force_slow, reference tiling); the
+// fused TMA kernel (stc_fused.cu) takes ABC / AB / Naive at L <= 2 otherwise.
 //
 // One persistent, warp-specialised CTA per SM.  Work items are (term, tile)
 // pairs fetched with an atomic counter.  For each 16-deep k-chunk:
 //
-//   producer warps (4)  stream every view ("unit" = one view of one side for one
-//                       chunk, 16 elements per thread) of the term's A and B
+//   producer warps (8)  stream every view ("unit" = one view of one side for one
+//                       chunk, 8 elements per thread) of the term's A and B
 //                       sides from HBM/L2 into a ring of raw smem slots with
 //                       cp.async (no registers held per load, NRAW-1 units in
-//                       flight per thread, zero-fill for PAD), then form the
+//                       flight per thread, zero-fill for PAD) -- or, for
+//                       regular views, one TMA box per unit -- then form the
 //                       Strassen operand sums (e.g. A0+A3, B1-B3) in registers
 //                       in view order and store them into the MMA smem ring --
 //                       the work of the reference's pack_a_block /
