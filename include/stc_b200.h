@@ -104,6 +104,25 @@ int stc_workspace_size(const stc_problem *p, size_t *bytes);
 int stc_contract(const stc_problem *p, const double *A, const double *B, double *C, void *workspace,
                  size_t workspace_bytes, void *stream, stc_stats *stats);
 
+/* ---- host operands: strassen.contract on host arrays (strassen.py:141-207) ----
+ * The reference computes on host arrays in place.  Here A, B, C are HOST
+ * storage (element 0 = flat index 0; page-locked for the transfers to overlap
+ * the DMMA work, pageable memory works but serialises) and dA, dB, dC are
+ * DEVICE mirrors with the same element offsets (at least max offset + 1
+ * elements each; contents ignored, dC ends equal to the result).  The problem
+ * is cut along one label of the I or J bundle into pieces whose uploads,
+ * contractions (stc_contract) and downloads are pipelined on library streams
+ * (stc_host.cu); STC_HOST_PIECES=n overrides the piece count (1: no split).
+ * Stream-ordered after prior work on `stream`; hC holds the result once
+ * `stream` has completed.  Stats are summed over the pieces (leaf_multiplies
+ * stays 7^L: every piece is an L-level Strassen contraction). */
+int stc_host_workspace_size(const stc_problem *p, size_t *bytes);
+int stc_contract_host(const stc_problem *p, const double *A, const double *B, double *C, double *dA, double *dB,
+                      double *dC, void *workspace, size_t workspace_bytes, void *stream, stc_stats *stats);
+/* The split stc_contract_host would use: side 0 = I bundle (A and C), 1 = J
+ * bundle (B and C); label = index in that bundle; pieces = 1 for no split. */
+int stc_host_plan(const stc_problem *p, int32_t *side, int32_t *label, int32_t *pieces);
+
 /* Overlap hook (no reference counterpart): the next stc_contract call on this
  * thread makes its kernels wait on the device until *c_ready != 0 (a device
  * int32 another stream sets once C has arrived) before their first access to

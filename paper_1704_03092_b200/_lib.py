@@ -57,6 +57,7 @@ _EXPORTS = (
     "stc_last_error", "stc_abi_version", "stc_workspace_size", "stc_contract", "stc_bundle_scatter",
     "stc_block_vector", "stc_fused_term_workspace_size", "stc_fused_term", "stc_accumulate_dense",
     "stc_unpack_sum", "stc_sq_norms", "stc_set_kernel_events", "stc_set_c_ready",
+    "stc_host_workspace_size", "stc_contract_host", "stc_host_plan",
 )
 
 _lib = None
@@ -84,6 +85,9 @@ def _declare(l):
     l.stc_sq_norms.argtypes = [ctypes.c_int, P(i64), vp, P(i64), i64, vp, P(i64), i64, dp, vp]
     l.stc_set_kernel_events.argtypes = [vp, vp]
     l.stc_set_c_ready.argtypes = [vp]
+    l.stc_host_workspace_size.argtypes = [P(Problem), P(sz)]
+    l.stc_contract_host.argtypes = [P(Problem), vp, vp, vp, vp, vp, vp, vp, sz, vp, P(Stats)]
+    l.stc_host_plan.argtypes = [P(Problem), P(ctypes.c_int32), P(ctypes.c_int32), P(ctypes.c_int32)]
     for name in _EXPORTS:
         if name not in ("stc_last_error",):
             getattr(l, name).restype = ctypes.c_int if name != "stc_last_error" else ctypes.c_char_p

@@ -1,0 +1,390 @@
+// stc_host.cu -- host-operand entry point (stc_contract_host): the
+// contraction of tensors that live in host memory, with the PCIe transfers
+// pipelined against the DMMA work.
+//
+// The reference computes on host arrays in place (strassen.contract,
+// strassen.py:141-207).  On the B200 the operands must cross PCIe, which
+// costs about twice the FP64 tensor-core time of the contraction itself
+// (cfg2: 0.4 GB in, 0.13 GB out).  Instead of upload -> compute -> download,
+// the problem is cut along one label of the I or J bundle into S pieces:
+//
+//   C[:, J_s] += A . B[:, J_s]     (J split; the I split is symmetric)
+//
+// Each piece is an independent contraction over the same block-scatter
+// views, run by stc_contract with the piece's extent and base offset (the
+// piece is itself an L-level Strassen contraction; the multi-GPU shard path
+// splits the same way, shard.py).  Streams:
+//   h2d:      shared operand, then (operand piece, C piece) for s = 0..S-1
+//   comp[2]:  piece s on comp[s % 2] after its inputs arrived; alternating
+//             streams let piece s+1's CTAs fill the SMs of piece s's tail
+//   d2h:      C piece s as soon as piece s finished
+// so the copy engines and the tensor cores run concurrently and the call
+// costs about max(H2D) + one piece's compute + one piece's download.
+//
+// Copies are 2-D (cudaMemcpy2DAsync): in a compact tensor (strides a
+// permutation of a dense layout) restricting one label to a range is a set of
+// equal-length runs at a fixed pitch.  The split label is chosen so the runs
+// are long in both tensors it touches; when no label qualifies (small
+// problem, non-compact storage, short runs) S = 1 and the call is the plain
+// upload -> contract -> download sequence on the same streams.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <vector>
+
+#include "stc_internal.cuh"
+
+using namespace stc;
+
+namespace {
+
+int herr(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+int herr(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  return set_error(code, buf);
+}
+
+#define HCU(expr, what)                                                                     \
+  do {                                                                                      \
+    cudaError_t _e = (expr);                                                                \
+    if (_e != cudaSuccess) return herr(STC_ECUDA, "CUDA error in %s: %s", what, cudaGetErrorString(_e)); \
+  } while (0)
+
+constexpr int64_t kMinRunBytes = 4096;          // shortest copy run worth splitting for
+constexpr int64_t kMinSplitBytes = 32ll << 20;  // smaller problems: one piece
+constexpr int kMaxPieces = 16;
+
+// One tensor's labels (row bundle + column bundle).
+struct TensorLabels {
+  int n = 0;
+  int64_t ext[2 * STC_MAX_LABELS], str[2 * STC_MAX_LABELS];
+  int64_t base = 0;
+  void add(const stc_bundle &b) {
+    for (int d = 0; d < b.nlab; ++d) {
+      ext[n] = b.ext[d];
+      str[n] = b.str[d];
+      ++n;
+    }
+  }
+  int64_t elems() const {
+    int64_t e = 1;
+    for (int d = 0; d < n; ++d) e *= ext[d];
+    return e;
+  }
+  // [base, hi): the storage the tensor's elements occupy (non-negative strides)
+  int64_t hi() const {
+    int64_t h = base;
+    for (int d = 0; d < n; ++d) h += (ext[d] - 1) * str[d];
+    return elems() ? h + 1 : base;
+  }
+  // strides a permutation of a dense row-major layout: the elements fill [base, base + elems)
+  bool compact() const {
+    std::vector<std::pair<int64_t, int64_t>> ls;
+    for (int d = 0; d < n; ++d)
+      if (ext[d] > 1) ls.push_back({str[d], ext[d]});
+    std::sort(ls.begin(), ls.end());
+    int64_t run = 1;
+    for (auto &l : ls) {
+      if (l.first != run) return false;
+      run *= l.second;
+    }
+    return true;
+  }
+};
+
+TensorLabels labels_of(const stc_bundle &r, const stc_bundle &c, int64_t base) {
+  TensorLabels t;
+  t.add(r);
+  t.add(c);
+  t.base = base;
+  return t;
+}
+
+// A split of the I (side 0: A and C) or J (side 1: B and C) bundle on label
+// `lab` of that bundle into `pieces` equal ranges.
+struct Split {
+  int side = 0, lab = 0, pieces = 1;
+  int64_t run = 0;  // shortest copy run, bytes
+};
+
+int64_t bundle_elems(const stc_bundle &b) {
+  int64_t n = 1;
+  for (int d = 0; d < b.nlab; ++d) n *= b.ext[d];
+  return n;
+}
+
+Split choose_split(const stc_problem &p) {
+  Split best;
+  const TensorLabels A = labels_of(p.a_row, p.a_col, p.a_base), B = labels_of(p.b_row, p.b_col, p.b_base),
+                     C = labels_of(p.c_row, p.c_col, p.c_base);
+  const int64_t bytes = 8 * (A.elems() + B.elems() + 2 * C.elems());
+  const char *env = getenv("STC_HOST_PIECES");
+  const int want = env ? std::max(1, std::min(kMaxPieces, atoi(env))) : 4;
+  if (want <= 1 || (!env && bytes < kMinSplitBytes) || !C.compact()) return best;
+  const int64_t quad = int64_t(1) << p.level;
+  for (int side = 0; side < 2; ++side) {
+    const stc_bundle &ob = side == 0 ? p.a_row : p.b_col;  // the operand's split bundle
+    const stc_bundle &cb = side == 0 ? p.c_row : p.c_col;
+    if (!(side == 0 ? A : B).compact()) continue;
+    const int64_t blen = bundle_elems(cb);
+    for (int l = 0; l < cb.nlab; ++l) {
+      for (int S = want; S >= 2; S /= 2) {
+        if (cb.ext[l] % S) continue;
+        // each piece keeps at least two 128-wide tiles per quadrant, and copy runs
+        // are long enough for full PCIe rate (STC_HOST_PIECES set: only divisibility)
+        if (!env && blen / S < quad * 256) continue;
+        const int64_t run = 8 * (cb.ext[l] / S) * std::min(ob.str[l], cb.str[l]);
+        if (!env && run < kMinRunBytes) continue;
+        const bool better = S > best.pieces || (S == best.pieces && run > best.run);
+        if (better) best = Split{side, l, S, run};
+        break;
+      }
+    }
+  }
+  return best;
+}
+
+// The sub-problem of piece s: label `lab` of the split bundle restricted to
+// [r0, r0 + len); bases move by r0 * stride in the two tensors it touches.
+stc_problem piece_problem(const stc_problem &p, const Split &sp, int64_t r0, int64_t len) {
+  stc_problem q = p;
+  if (sp.side == 0) {
+    q.a_row.ext[sp.lab] = len;
+    q.c_row.ext[sp.lab] = len;
+    q.a_base += r0 * p.a_row.str[sp.lab];
+    q.c_base += r0 * p.c_row.str[sp.lab];
+  } else {
+    q.b_col.ext[sp.lab] = len;
+    q.c_col.ext[sp.lab] = len;
+    q.b_base += r0 * p.b_col.str[sp.lab];
+    q.c_base += r0 * p.c_col.str[sp.lab];
+  }
+  return q;
+}
+
+// Copy of the elements of compact tensor t with one label (stride lstr,
+// extent lext) restricted to [r0, r0 + len): rows of len * lstr elements at
+// pitch lext * lstr.
+cudaError_t copy_piece(double *dst, const double *src, const TensorLabels &t, int64_t lstr, int64_t lext,
+                       int64_t r0, int64_t len, cudaMemcpyKind kind, cudaStream_t s) {
+  const int64_t pitch = lext * lstr, rows = t.elems() / pitch;
+  const int64_t off = t.base + r0 * lstr;
+  return cudaMemcpy2DAsync(dst + off, pitch * 8, src + off, pitch * 8, len * lstr * 8, rows, kind, s);
+}
+
+cudaError_t copy_span(double *dst, const double *src, const TensorLabels &t, cudaMemcpyKind kind, cudaStream_t s) {
+  const int64_t n = t.hi() - t.base;
+  if (n <= 0) return cudaSuccess;
+  return cudaMemcpyAsync(dst + t.base, src + t.base, n * 8, kind, s);
+}
+
+struct HostStreams {
+  bool init = false;
+  cudaStream_t h2d = nullptr, d2h = nullptr, comp[2] = {nullptr, nullptr};
+};
+HostStreams g_hs[64];
+std::mutex g_hs_mu;
+
+int host_streams(HostStreams *&hs) {
+  int dev = 0;
+  HCU(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(g_hs_mu);
+  hs = &g_hs[dev & 63];
+  if (!hs->init) {
+    HCU(cudaStreamCreateWithFlags(&hs->h2d, cudaStreamNonBlocking), "cudaStreamCreate");
+    HCU(cudaStreamCreateWithFlags(&hs->d2h, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (auto &c : hs->comp) HCU(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking), "cudaStreamCreate");
+    hs->init = true;
+  }
+  return STC_OK;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int piece_workspace(const stc_problem &p, const Split &sp, size_t &per_slot) {
+  const stc_bundle &cb = sp.side == 0 ? p.c_row : p.c_col;
+  const int64_t len = (cb.ext[sp.lab] + sp.pieces - 1) / sp.pieces;
+  stc_problem q = sp.pieces > 1 ? piece_problem(p, sp, 0, len) : p;
+  size_t b = 0;
+  if (int rc = stc_workspace_size(&q, &b)) return rc;
+  per_slot = align256(std::max<size_t>(b, 256));
+  return STC_OK;
+}
+
+// RAII set of events, destroyed after enqueue (the runtime releases them when
+// the work they mark completes).
+struct Events {
+  std::vector<cudaEvent_t> ev;
+  ~Events() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  }
+  cudaError_t make(cudaEvent_t &e) {
+    cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (r == cudaSuccess) ev.push_back(e);
+    return r;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int stc_host_plan(const stc_problem *p, int32_t *side, int32_t *label, int32_t *pieces) {
+  if (!p) return herr(STC_EINVAL, "null problem");
+  const Split sp = choose_split(*p);
+  if (side) *side = sp.side;
+  if (label) *label = sp.lab;
+  if (pieces) *pieces = sp.pieces;
+  return STC_OK;
+}
+
+int stc_host_workspace_size(const stc_problem *p, size_t *bytes) {
+  if (!p) return herr(STC_EINVAL, "null problem");
+  const Split sp = choose_split(*p);
+  size_t per = 0;
+  if (int rc = piece_workspace(*p, sp, per)) return rc;
+  if (bytes) *bytes = per * (sp.pieces > 1 ? 2 : 1);
+  return STC_OK;
+}
+
+int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, double *hC, double *dA, double *dB,
+                      double *dC, void *workspace, size_t workspace_bytes, void *stream, stc_stats *stats) {
+  if (!p) return herr(STC_EINVAL, "null problem");
+  if (!hA || !hB || !hC || !dA || !dB || !dC) return herr(STC_EINVAL, "null operand pointer");
+  const Split sp = choose_split(*p);
+  size_t per = 0;
+  if (int rc = piece_workspace(*p, sp, per)) return rc;
+  const int slots = sp.pieces > 1 ? 2 : 1;
+  if (!workspace || workspace_bytes < per * slots)
+    return herr(STC_EWORKSPACE, "workspace too small: need %zu bytes, got %zu", per * slots, workspace_bytes);
+  if (reinterpret_cast<uintptr_t>(workspace) & 255) return herr(STC_EINVAL, "workspace must be 256-byte aligned");
+  // the pieces: label `lab` of the split bundle cut into equal ranges
+  const stc_bundle &cb = sp.side == 0 ? p->c_row : p->c_col;
+  const stc_bundle &ob = sp.side == 0 ? p->a_row : p->b_col;
+  const int64_t lext = sp.pieces > 1 ? cb.ext[sp.lab] : 1;
+  std::vector<stc_problem> parts;
+  std::vector<int64_t> r0s, lens;
+  for (int s = 0; s < sp.pieces; ++s) {
+    const int64_t r0 = lext * s / sp.pieces, r1 = lext * (s + 1) / sp.pieces;
+    parts.push_back(sp.pieces > 1 ? piece_problem(*p, sp, r0, r1 - r0) : *p);
+    r0s.push_back(r0);
+    lens.push_back(r1 - r0);
+  }
+  HostStreams *hs = nullptr;
+  if (int rc = host_streams(hs)) return rc;
+  // the per-call hooks belong to device-operand calls
+  stc_set_c_ready(nullptr);
+  stc_set_kernel_events(nullptr, nullptr);
+
+  const TensorLabels A = labels_of(p->a_row, p->a_col, p->a_base), B = labels_of(p->b_row, p->b_col, p->b_base),
+                     C = labels_of(p->c_row, p->c_col, p->c_base);
+  const TensorLabels &O = sp.side == 0 ? A : B;  // split operand
+  const double *hO = sp.side == 0 ? hA : hB;
+  double *dO = sp.side == 0 ? dA : dB;
+  cudaStream_t us = reinterpret_cast<cudaStream_t>(stream);
+  Events E;
+  cudaEvent_t start, end;
+  HCU(E.make(start), "cudaEventCreate");
+  HCU(E.make(end), "cudaEventCreate");
+  HCU(cudaEventRecord(start, us), "cudaEventRecord");
+  // STC_HOST_TRACE=1: timing events per piece (inputs in, compute start / end, C out), printed to stderr
+  const bool trace = getenv("STC_HOST_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tr(trace ? 1 + 4 * sp.pieces : 0);
+  for (auto &e : tr) HCU(cudaEventCreate(&e), "cudaEventCreate");
+  if (trace) HCU(cudaEventRecord(tr[0], us), "cudaEventRecord");
+  for (cudaStream_t s : {hs->h2d, hs->d2h, hs->comp[0], hs->comp[1]})
+    HCU(cudaStreamWaitEvent(s, start, 0), "cudaStreamWaitEvent");
+
+  // uploads: the operand all pieces share, then (operand piece, C piece) per piece
+  std::vector<cudaEvent_t> in(sp.pieces), done(sp.pieces);
+  if (sp.pieces == 1) {
+    HCU(copy_span(dA, hA, A, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(A)");
+    HCU(copy_span(dB, hB, B, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(B)");
+    HCU(copy_span(dC, hC, C, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(C)");
+    HCU(E.make(in[0]), "cudaEventCreate");
+    HCU(cudaEventRecord(in[0], hs->h2d), "cudaEventRecord");
+    if (trace) HCU(cudaEventRecord(tr[1], hs->h2d), "cudaEventRecord");
+  } else {
+    if (sp.side == 0)
+      HCU(copy_span(dB, hB, B, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(B)");
+    else
+      HCU(copy_span(dA, hA, A, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(A)");
+    for (int s = 0; s < sp.pieces; ++s) {
+      HCU(copy_piece(dO, hO, O, ob.str[sp.lab], lext, r0s[s], lens[s], cudaMemcpyHostToDevice, hs->h2d),
+          "cudaMemcpy2DAsync(operand piece)");
+      HCU(copy_piece(dC, hC, C, cb.str[sp.lab], lext, r0s[s], lens[s], cudaMemcpyHostToDevice, hs->h2d),
+          "cudaMemcpy2DAsync(C piece)");
+      HCU(E.make(in[s]), "cudaEventCreate");
+      HCU(cudaEventRecord(in[s], hs->h2d), "cudaEventRecord");
+      if (trace) HCU(cudaEventRecord(tr[1 + 4 * s], hs->h2d), "cudaEventRecord");
+    }
+  }
+  // plan every piece before any of them is launched (the uploads above only fill
+  // the caller's device buffers; on an error they are drained before returning)
+  for (int s = 0; s < sp.pieces; ++s) {
+    size_t need = 0;
+    if (int rc = stc_workspace_size(&parts[s], &need)) {
+      cudaStreamSynchronize(hs->h2d);
+      return rc;
+    }
+  }
+  // pieces on alternating compute streams (workspace slot = stream)
+  stc_stats total{};
+  char *ws = reinterpret_cast<char *>(workspace);
+  for (int s = 0; s < sp.pieces; ++s) {
+    cudaStream_t cs = hs->comp[s % slots];
+    HCU(cudaStreamWaitEvent(cs, in[s], 0), "cudaStreamWaitEvent");
+    if (trace) HCU(cudaEventRecord(tr[2 + 4 * s], cs), "cudaEventRecord");
+    stc_stats st{};
+    if (int rc = stc_contract(&parts[s], dA, dB, dC, ws + (s % slots) * per, per, cs, &st)) return rc;
+    HCU(E.make(done[s]), "cudaEventCreate");
+    HCU(cudaEventRecord(done[s], cs), "cudaEventRecord");
+    if (trace) HCU(cudaEventRecord(tr[3 + 4 * s], cs), "cudaEventRecord");
+    total.total_flops += st.total_flops;
+    total.fast_blocks += st.fast_blocks;
+    total.slow_blocks += st.slow_blocks;
+    total.fast_updates += st.fast_updates;
+    total.slow_updates += st.slow_updates;
+    total.leaf_multiplies = std::max(total.leaf_multiplies, st.leaf_multiplies);
+    total.work_items += st.work_items;
+    total.kernel_launches += st.kernel_launches;
+  }
+  // downloads of C, piece by piece as the pieces finish
+  for (int s = 0; s < sp.pieces; ++s) {
+    HCU(cudaStreamWaitEvent(hs->d2h, done[s], 0), "cudaStreamWaitEvent");
+    if (sp.pieces == 1)
+      HCU(copy_span(hC, dC, C, cudaMemcpyDeviceToHost, hs->d2h), "cudaMemcpyAsync(C)");
+    else
+      HCU(copy_piece(hC, dC, C, cb.str[sp.lab], lext, r0s[s], lens[s], cudaMemcpyDeviceToHost, hs->d2h),
+          "cudaMemcpy2DAsync(C piece)");
+    if (trace) HCU(cudaEventRecord(tr[4 + 4 * s], hs->d2h), "cudaEventRecord");
+  }
+  HCU(cudaEventRecord(end, hs->d2h), "cudaEventRecord");
+  if (trace) {
+    cudaEventSynchronize(end);
+    float t = 0;
+    fprintf(stderr, "[stc host] pieces=%d side=%d label=%d:", sp.pieces, sp.side, sp.lab);
+    for (int s = 0; s < sp.pieces; ++s) {
+      fprintf(stderr, " |%d", s);
+      for (int k = 0; k < 4; ++k) {
+        cudaEventElapsedTime(&t, tr[0], tr[1 + 4 * s + k]);
+        fprintf(stderr, " %.2f", t);
+      }
+    }
+    fprintf(stderr, "  (in, kstart, kend, out ms)\n");
+    for (cudaEvent_t e : tr) cudaEventDestroy(e);
+  }
+  HCU(cudaStreamWaitEvent(us, end, 0), "cudaStreamWaitEvent");
+  if (stats) *stats = total;
+  return STC_OK;
+}
+
+}  // extern "C"

@@ -159,6 +159,9 @@ struct UnpackArgs {
 };
 
 // ---- launchers (stc_kernels.cu) -------------------------------------------
+int set_error(int code, const char *msg);
+cudaError_t launch_stage(const void *host_src, void *dst, size_t bytes, void *zero, size_t zero_bytes,
+                         cudaStream_t s);  // stc_last_error() text for this thread
 cudaError_t launch_build_pool(const VecDesc *d_descs, int ndesc, int64_t total, int64_t *pool, cudaStream_t s);
 cudaError_t launch_block_vector(const int64_t *scat, int64_t len, int64_t blk, int64_t unit, int64_t *out,
                                 cudaStream_t s);

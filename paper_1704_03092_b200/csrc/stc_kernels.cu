@@ -150,6 +150,38 @@ __global__ void k_copy_pad(const int64_t *__restrict__ in, int64_t len, int64_t 
     out[i] = i < len ? in[i] : kPad;
 }
 
+// Staged upload of a host table: SMs read the page-locked staging buffer over
+// PCIe (UVA pointer) and write HBM.  Kept off the copy engines on purpose: a
+// cudaMemcpyAsync of a few KB would queue behind any bulk host->device
+// transfer in flight (stc_contract_host's operand uploads), stalling the
+// launch that needs the table.  Optionally zeroes a second device range.
+__global__ void k_stage(const uint8_t *__restrict__ src, uint8_t *__restrict__ dst, size_t n, uint8_t *z, size_t zn) {
+  const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x, step = (size_t)gridDim.x * blockDim.x;
+  size_t done = 0;
+  if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
+    const size_t n16 = n / 16;
+    for (size_t i = t; i < n16; i += step) reinterpret_cast<uint4 *>(dst)[i] = reinterpret_cast<const uint4 *>(src)[i];
+    done = n16 * 16;
+  }
+  for (size_t i = done + t; i < n; i += step) dst[i] = src[i];
+  done = 0;
+  if (((uintptr_t)z & 15) == 0) {
+    const size_t z16 = zn / 16;
+    for (size_t i = t; i < z16; i += step) reinterpret_cast<uint4 *>(z)[i] = make_uint4(0, 0, 0, 0);
+    done = z16 * 16;
+  }
+  for (size_t i = done + t; i < zn; i += step) z[i] = 0;
+}
+
+cudaError_t launch_stage(const void *host_src, void *dst, size_t bytes, void *zero, size_t zero_bytes,
+                         cudaStream_t s) {
+  const size_t work = std::max(bytes, zero_bytes) / 16 + 1;
+  const int blocks = (int)std::min<size_t>((work + 255) / 256, 64);
+  k_stage<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint8_t *>(host_src), reinterpret_cast<uint8_t *>(dst),
+                                 bytes, reinterpret_cast<uint8_t *>(zero), zero_bytes);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_copy_pad(const int64_t *in, int64_t len, int64_t len_pad, int64_t *out, cudaStream_t s) {
   if (len_pad <= 0) return cudaSuccess;
   int blocks = (int)std::min<int64_t>((len_pad + 255) / 256, 148 * 8);

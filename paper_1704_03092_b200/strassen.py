@@ -27,6 +27,8 @@ import os
 from dataclasses import dataclass
 from enum import Enum
 
+import numpy as np
+
 from . import _lib
 from .stats import RunStats, effective_gflops
 from .tensor import ContractionSpec, DenseTensor
@@ -150,6 +152,55 @@ def _validate_targets(spec, c: DenseTensor, level: int, terms) -> None:
         check_c_targets([quads[q] for q, _ in term.c_ops])
 
 
+def _flat_host(t: DenseTensor):
+    """(pointer, elements) of a contiguous float64 host storage, else None."""
+    import torch
+
+    d = t.data
+    if torch.is_tensor(d):
+        if d.dtype != torch.float64 or not d.is_contiguous():
+            return None
+        return d.data_ptr(), d.numel()
+    if not isinstance(d, np.ndarray) or d.dtype != np.float64 or not d.flags.c_contiguous or not d.flags.writeable:
+        return None
+    return d.ctypes.data, d.size
+
+
+def _contract_host(spec, a, b, c, level, variant, force_slow, reference_tiling, validate, terms, dev) -> RunStats:
+    """Host operands: stc_contract_host pipelines the uploads, the piecewise
+    contraction and the download of C (stc_host.cu).  ``seconds`` covers the
+    whole call (transfers included)."""
+    import torch
+
+    if validate:
+        _validate_targets(spec, c, level, terms)
+    flags = (_lib.FLAG_FORCE_SLOW if force_slow else 0) | (_lib.FLAG_REFERENCE_TILING if reference_tiling else 0)
+    prob = problem_of(spec, a, b, c, level, variant, flags)
+    L = _lib.lib()
+    stats = RunStats()
+    (pa, na), (pb, nb), (pc, nc) = _flat_host(a), _flat_host(b), _flat_host(c)
+    with torch.cuda.device(dev):
+        need = ctypes.c_size_t()
+        _lib.check(L.stc_host_workspace_size(ctypes.byref(prob), ctypes.byref(need)))
+        ws = torch.empty(max(int(need.value), 256), dtype=torch.uint8, device=dev)
+        da, db, dc = (torch.empty(max(n, 1), dtype=torch.float64, device=dev) for n in (na, nb, nc))
+        stream = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st = _lib.Stats()
+        e0.record(stream)
+        _lib.check(L.stc_contract_host(ctypes.byref(prob), ctypes.c_void_p(pa), ctypes.c_void_p(pb),
+                                       ctypes.c_void_p(pc), ctypes.c_void_p(da.data_ptr()),
+                                       ctypes.c_void_p(db.data_ptr()), ctypes.c_void_p(dc.data_ptr()),
+                                       ctypes.c_void_p(ws.data_ptr()), ws.numel(), ctypes.c_void_p(stream.cuda_stream),
+                                       ctypes.byref(st)))
+        e1.record(stream)
+        e1.synchronize()  # C is host memory: complete before returning
+        stats.absorb(st)
+        stats.seconds = max(e0.elapsed_time(e1) * 1e-3, 1e-12)
+    stats.effective_gflops = effective_gflops(spec.n_i, spec.n_j, spec.n_p, stats.seconds)
+    return stats
+
+
 _SIDE = {}
 
 
@@ -184,11 +235,15 @@ def contract(spec: ContractionSpec, a, b, c, level: int, variant, params: Blocki
     if not torch.cuda.is_available():
         raise RuntimeError("no CUDA device: the B200 contraction path has no CPU fallback")
     dev = next((t.data.device for t in (c, a, b) if t.on_device), torch.device("cuda", torch.cuda.current_device()))
-    # Host operands are staged through HBM.  Opt-in (STC_C_OVERLAP=1): a host C is
-    # uploaded on a side stream under the DMMA main loop, the kernels waiting on
-    # the device for its ready flag before their first C update (stc_set_c_ready).
-    # Off by default: every CTA's first epilogue comes ~0.2 ms into the kernel, so
-    # the wait only moves the upload (measured: 12.5 ms/call sequential, 14.9 overlapped).
+    # All operands in host memory (contiguous float64 storage): stc_contract_host
+    # pipelines the uploads, the piecewise contraction and the download of C
+    # (STC_HOST_PIPELINE=0 disables it).  Otherwise host operands are staged
+    # through HBM; opt-in (STC_C_OVERLAP=1) a host C is uploaded on a side stream
+    # under the DMMA main loop, the kernels waiting on the device for its ready
+    # flag before their first C update (stc_set_c_ready).
+    if not (a.on_device or b.on_device or c.on_device) and kernel_events is None \
+            and os.environ.get("STC_HOST_PIPELINE", "1") != "0" and all(_flat_host(t) is not None for t in (a, b, c)):
+        return _contract_host(spec, a, b, c, level, variant, force_slow, reference_tiling, validate, terms, dev)
     c_ready = None
     main = torch.cuda.current_stream(dev)
     A = a if a.on_device else a.to_device(dev)

@@ -130,7 +130,8 @@ def test_repacked_operands_match_gather_bitwise(line):
         for variant in ("abc", "ab"):
             cf, stf = _run(spec, a, b, c0, level, variant, True)
             cg, stg = _run(spec, a, b, c0, level, variant, False)
-            assert stf.kernel_launches == stg.kernel_launches + 4, (level, variant)  # 2 packs, pool, coordinates
+            # 2 packs, pool, coordinates, the packed vectors' table upload
+            assert stf.kernel_launches == stg.kernel_launches + 5, (level, variant)
             assert np.array_equal(cf.data, cg.data), (level, variant)
             assert stc.relative_error(cf, classical) <= TOL, (level, variant)
 
@@ -143,6 +144,7 @@ def test_host_c_upload_overlap_matches():
     b = stc.make_dense_tensor(spec.tensor_extents(spec.labels_b), "random", 62)
     c0 = stc.make_dense_tensor(spec.tensor_extents(spec.labels_c), "random", 63)
     outs = []
+    os.environ["STC_HOST_PIPELINE"] = "0"  # the staged path (host operands uploaded whole)
     for flag in ("0", "1"):
         os.environ["STC_C_OVERLAP"] = flag
         try:
@@ -152,6 +154,7 @@ def test_host_c_upload_overlap_matches():
                 outs.append(c.data.copy())
         finally:
             del os.environ["STC_C_OVERLAP"]
+    del os.environ["STC_HOST_PIPELINE"]
     for i in range(3):
         assert np.array_equal(outs[i], outs[i + 3])
 

@@ -1,0 +1,125 @@
+"""GPU parity of the host-operand entry point (stc_contract_host, stc_host.cu).
+
+Host operands are uploaded, contracted piece by piece (the I or J bundle cut
+along one label) and downloaded with the transfers pipelined against the DMMA
+work.  Checks, against the CPU oracle's classical contraction:
+  * integer-valued data: exact for every piece count, variant and level;
+  * random data: normwise error <= 1e-12 (the reference suite's bound);
+  * J-side splits, pinned and pageable storage, base offsets and a
+    non-compact C (which disables the split);
+  * the staged path (STC_HOST_PIPELINE=0) agrees.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1704_03092_b200 as stc
+from paper_1704_03092_b200 import _lib
+from paper_1704_03092_b200.strassen import Variant, problem_of
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+# I bundle split on a (A and C), J bundle split on j (B outermost j; C: j ahead of i)
+LINES = {
+    "i_split": "aibj eafb jfie & a:32;b:64;i:16;j:64;e:32;f:32;",
+    "j_split": "jiab eafb jfie & a:16;b:64;i:32;j:64;e:32;f:32;",
+}
+
+
+def _row_major(e):
+    return tuple(int(np.prod(e[i + 1:])) for i in range(len(e)))
+
+
+def _tensor(spec, labels, seed, ints, pad=0):
+    e = spec.tensor_extents(labels)
+    n = int(np.prod(e))
+    rng = np.random.default_rng(seed)
+    data = rng.integers(-8, 9, n + pad).astype(np.float64) if ints else rng.uniform(-1, 1, n + pad)
+    return stc.DenseTensor(e, _row_major(e), data, pad)
+
+
+def _plan(spec, a, b, c, level):
+    p = problem_of(spec, a, b, c, level, Variant.ABC)
+    s, l, n = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _lib.check(_lib.lib().stc_host_plan(ctypes.byref(p), ctypes.byref(s), ctypes.byref(l), ctypes.byref(n)))
+    return s.value, l.value, n.value
+
+
+def _with_env(env, fn):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return fn()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("name", sorted(LINES))
+def test_host_pipeline_integer_exact(name):
+    spec = stc.parse_benchmark_line(LINES[name])
+    a, b, c0 = (_tensor(spec, l, s, True) for l, s in ((spec.labels_a, 1), (spec.labels_b, 2), (spec.labels_c, 3)))
+    ref = c0.copy()
+    oracle.contract_reference(spec, a, b, ref, threads=8)
+    side = {"i_split": 0, "j_split": 1}[name]
+    for pieces in ("1", "2", "4"):
+        assert _with_env({"STC_HOST_PIECES": pieces}, lambda: _plan(spec, a, b, c0, 2))[::2] == \
+            ((side if pieces != "1" else 0), int(pieces))
+        for level in (0, 1, 2):
+            for variant in ("abc", "ab", "naive"):
+                c = c0.copy()
+                st = _with_env({"STC_HOST_PIECES": pieces}, lambda: stc.contract(spec, a, b, c, level, variant))
+                assert st.leaf_multiplies == 7 ** level
+                assert np.array_equal(c.data, ref.data), (pieces, level, variant)
+
+
+def test_host_pipeline_random_pinned_and_offsets():
+    import torch
+
+    spec = stc.parse_benchmark_line(LINES["i_split"])
+    a, b, c0 = (_tensor(spec, l, s, False, pad=3) for l, s in ((spec.labels_a, 4), (spec.labels_b, 5),
+                                                              (spec.labels_c, 6)))
+    ref = c0.copy()
+    oracle.contract_reference(spec, a, b, ref, threads=8)
+    outs = []
+    for pinned in (False, True):
+        for env in ({}, {"STC_HOST_PIECES": "8"}, {"STC_HOST_PIPELINE": "0"}):
+            c = c0.copy()
+            aa, bb = a, b
+            if pinned:
+                aa, bb, c = (stc.DenseTensor(t.extents, t.strides, torch.from_numpy(t.data).pin_memory(),
+                                             t.base_offset) for t in (a, b, c))
+            _with_env(env, lambda: stc.contract(spec, aa, bb, c, 2, "abc"))
+            got = c.data.numpy() if torch.is_tensor(c.data) else c.data
+            assert np.array_equal(got[:3], c0.data[:3])  # storage ahead of base_offset untouched
+            outs.append(got)
+            err = np.linalg.norm(got - ref.data) / np.linalg.norm(ref.data)
+            assert err <= TOL, (pinned, env, err)
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0]) or np.linalg.norm(o - outs[0]) / np.linalg.norm(outs[0]) <= TOL
+
+
+def test_host_pipeline_non_compact_c_is_not_split():
+    # C stored with a gap between its rows: not compact, so one piece; the gap is preserved
+    spec = stc.parse_benchmark_line(LINES["i_split"])
+    a, b = _tensor(spec, spec.labels_a, 7, True), _tensor(spec, spec.labels_b, 8, True)
+    e = spec.tensor_extents(spec.labels_c)
+    strides = list(_row_major(e))
+    strides[0] += 5  # gap after every outermost slice
+    size = (e[0] - 1) * strides[0] + strides[1] * e[1]
+    data = np.random.default_rng(9).integers(-8, 9, size).astype(np.float64)
+    c0 = stc.DenseTensor(e, tuple(strides), data)
+    assert _plan(spec, a, b, c0, 2)[2] == 1
+    ref = c0.copy()
+    oracle.contract_reference(spec, a, b, ref, threads=8)
+    c = c0.copy()
+    stc.contract(spec, a, b, c, 2, "abc")
+    assert np.array_equal(c.data, ref.data)
