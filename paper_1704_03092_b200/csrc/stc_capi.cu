@@ -64,32 +64,45 @@ int64_t bundle_len(const stc_bundle &b) {
 // ---------------------------------------------------------------- staging
 // Pinned host staging for the small plan tables, double-buffered and fenced
 // by events so uploads never force a stream synchronisation.
-constexpr int kStagingSlots = 8;
+// Page-locked staging ring for the plan tables.  A slot is reused once the
+// k_stage launch that read it has run; when every slot is still pending (a
+// stream parked behind transfers, as in stc_contract_host) the ring grows
+// instead of blocking the host, up to kStagingMax slots.
+constexpr int kStagingMax = 64;
 struct Staging {
-  void *host[kStagingSlots] = {};
-  size_t cap[kStagingSlots] = {};
-  cudaEvent_t ev[kStagingSlots] = {};
-  bool used[kStagingSlots] = {};
-  int next = 0;
+  void *host[kStagingMax] = {};
+  size_t cap[kStagingMax] = {};
+  cudaEvent_t ev[kStagingMax] = {};
+  bool used[kStagingMax] = {};
+  int nslots = 0, next = 0;
   std::mutex mu;
 };
 Staging g_staging[64];
 thread_local int64_t g_stage_launches = 0;  // k_stage launches of the current call
 
-// Host table -> device, read by a k_stage launch from a page-locked ring slot
-// (reused once the launch that read it has run); optionally zeroes
-// [zero, zero + zero_bytes) in the same launch.
+// Host table -> device, read by a k_stage launch from a staging slot;
+// optionally zeroes [zero, zero + zero_bytes) in the same launch.
 int upload(const void *src, size_t bytes, void *dst, cudaStream_t s, void *zero = nullptr, size_t zero_bytes = 0) {
   if (bytes == 0 && zero_bytes == 0) return STC_OK;
   int dev = 0;
   CU(cudaGetDevice(&dev), "cudaGetDevice");
   Staging &st = g_staging[dev & 63];
   std::lock_guard<std::mutex> lk(st.mu);
-  const int i = st.next;
-  st.next = (st.next + 1) % kStagingSlots;
+  int i = -1;
+  for (int t = 0; t < st.nslots && i < 0; ++t) {  // a free slot, oldest first
+    const int c = (st.next + t) % st.nslots;
+    if (!st.used[c] || cudaEventQuery(st.ev[c]) == cudaSuccess) i = c;
+  }
+  cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error here
+  if (i < 0 && st.nslots < kStagingMax) i = st.nslots++;
+  if (i < 0) {  // ring full: wait for the oldest
+    i = st.next % st.nslots;
+    CU(cudaEventSynchronize(st.ev[i]), "cudaEventSynchronize");
+  }
+  st.next = (i + 1) % std::max(st.nslots, 1);
   if (!st.ev[i]) CU(cudaEventCreateWithFlags(&st.ev[i], cudaEventDisableTiming), "cudaEventCreate");
-  if (st.used[i]) CU(cudaEventSynchronize(st.ev[i]), "cudaEventSynchronize");
   if (st.cap[i] < bytes) {
+    if (st.used[i]) CU(cudaEventSynchronize(st.ev[i]), "cudaEventSynchronize");
     if (st.host[i]) cudaFreeHost(st.host[i]);
     st.host[i] = nullptr;
     size_t c = std::max<size_t>(bytes, 1 << 16);

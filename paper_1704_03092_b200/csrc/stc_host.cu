@@ -336,6 +336,22 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
       return rc;
     }
   }
+  // download of piece s's C once the piece finished
+  auto download = [&](int s) -> int {
+    HCU(cudaStreamWaitEvent(hs->d2h, done[s], 0), "cudaStreamWaitEvent");
+    if (sp.pieces == 1)
+      HCU(copy_span(hC, dC, C, cudaMemcpyDeviceToHost, hs->d2h), "cudaMemcpyAsync(C)");
+    else
+      HCU(copy_piece(hC, dC, C, cb.str[sp.lab], lext, r0s[s], lens[s], cudaMemcpyDeviceToHost, hs->d2h),
+          "cudaMemcpy2DAsync(C piece)");
+    if (trace) HCU(cudaEventRecord(tr[4 + 4 * s], hs->d2h), "cudaEventRecord");
+    return STC_OK;
+  };
+  // page-locked C: each download is enqueued right behind its piece (asynchronous);
+  // pageable C: after all pieces (such copies block the host until they ran)
+  cudaPointerAttributes pa{};
+  const bool locked = cudaPointerGetAttributes(&pa, hC) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();  // a failed query leaves an error code behind
   // pieces on alternating compute streams (workspace slot = stream)
   stc_stats total{};
   char *ws = reinterpret_cast<char *>(workspace);
@@ -356,17 +372,12 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
     total.leaf_multiplies = std::max(total.leaf_multiplies, st.leaf_multiplies);
     total.work_items += st.work_items;
     total.kernel_launches += st.kernel_launches;
+    if (locked)
+      if (int rc = download(s)) return rc;
   }
-  // downloads of C, piece by piece as the pieces finish
-  for (int s = 0; s < sp.pieces; ++s) {
-    HCU(cudaStreamWaitEvent(hs->d2h, done[s], 0), "cudaStreamWaitEvent");
-    if (sp.pieces == 1)
-      HCU(copy_span(hC, dC, C, cudaMemcpyDeviceToHost, hs->d2h), "cudaMemcpyAsync(C)");
-    else
-      HCU(copy_piece(hC, dC, C, cb.str[sp.lab], lext, r0s[s], lens[s], cudaMemcpyDeviceToHost, hs->d2h),
-          "cudaMemcpy2DAsync(C piece)");
-    if (trace) HCU(cudaEventRecord(tr[4 + 4 * s], hs->d2h), "cudaEventRecord");
-  }
+  if (!locked)
+    for (int s = 0; s < sp.pieces; ++s)
+      if (int rc = download(s)) return rc;
   HCU(cudaEventRecord(end, hs->d2h), "cudaEventRecord");
   if (trace) {
     cudaEventSynchronize(end);
