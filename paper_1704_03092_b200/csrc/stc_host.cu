@@ -61,6 +61,25 @@ int herr(int code, const char *fmt, ...) {
 constexpr int64_t kMinRunBytes = 4096;          // shortest copy run worth splitting for
 constexpr int64_t kMinSplitBytes = 32ll << 20;  // smaller problems: one piece
 constexpr int kMaxPieces = 16;
+constexpr size_t kFlagBytes = 256;  // per-piece "C piece arrived" flags, after the piece workspaces
+
+// Page-locked constants the flags are copied from: kMaxPieces zeros, then kMaxPieces ones.
+// The flags are written by the copy engine, in order behind the C uploads on the h2d
+// stream: a kernel launch (cudaMemsetAsync, fill) could not get an SM while the pieces'
+// persistent kernels, spinning on those flags, occupy all of them.
+const int32_t *pinned_flag_values() {
+  static std::once_flag once;
+  static int32_t *v = nullptr;
+  std::call_once(once, [] {
+    if (cudaHostAlloc(reinterpret_cast<void **>(&v), 2 * kMaxPieces * sizeof(int32_t), cudaHostAllocPortable) !=
+        cudaSuccess) {
+      v = nullptr;
+      return;
+    }
+    for (int i = 0; i < 2 * kMaxPieces; ++i) v[i] = i >= kMaxPieces;
+  });
+  return v;
+}
 
 // One tensor's labels (row bundle + column bundle).
 struct TensorLabels {
@@ -251,7 +270,7 @@ int stc_host_workspace_size(const stc_problem *p, size_t *bytes) {
   const Split sp = choose_split(*p);
   size_t per = 0;
   if (int rc = piece_workspace(*p, sp, per)) return rc;
-  if (bytes) *bytes = per * (sp.pieces > 1 ? 2 : 1);
+  if (bytes) *bytes = per * (sp.pieces > 1 ? 2 : 1) + kFlagBytes;
   return STC_OK;
 }
 
@@ -263,8 +282,9 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
   size_t per = 0;
   if (int rc = piece_workspace(*p, sp, per)) return rc;
   const int slots = sp.pieces > 1 ? 2 : 1;
-  if (!workspace || workspace_bytes < per * slots)
-    return herr(STC_EWORKSPACE, "workspace too small: need %zu bytes, got %zu", per * slots, workspace_bytes);
+  if (!workspace || workspace_bytes < per * slots + kFlagBytes)
+    return herr(STC_EWORKSPACE, "workspace too small: need %zu bytes, got %zu", per * slots + kFlagBytes,
+                workspace_bytes);
   if (reinterpret_cast<uintptr_t>(workspace) & 255) return herr(STC_EINVAL, "workspace must be 256-byte aligned");
   // the pieces: label `lab` of the split bundle cut into equal ranges
   const stc_bundle &cb = sp.side == 0 ? p->c_row : p->c_col;
@@ -303,15 +323,29 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
   for (cudaStream_t s : {hs->h2d, hs->d2h, hs->comp[0], hs->comp[1]})
     HCU(cudaStreamWaitEvent(s, start, 0), "cudaStreamWaitEvent");
 
-  // uploads: the operand all pieces share, then (operand piece, C piece) per piece
-  std::vector<cudaEvent_t> in(sp.pieces), done(sp.pieces);
+  // uploads: the operand all pieces share, then (operand piece, C piece, flag) per piece.
+  // A piece's kernels start once its operands are in (event opin) and wait on the
+  // device for its flag before their first access to C (stc_set_c_ready), so the
+  // C upload overlaps the piece's first MMAs.
+  const int32_t *pf = pinned_flag_values();
+  if (!pf) return herr(STC_ECUDA, "cudaHostAlloc failed for the piece flags");
+  int32_t *flags = reinterpret_cast<int32_t *>(reinterpret_cast<char *>(workspace) + per * slots);
+  HCU(cudaMemcpyAsync(flags, pf, sp.pieces * sizeof(int32_t), cudaMemcpyHostToDevice, hs->h2d),
+      "cudaMemcpyAsync(flags)");
+  std::vector<cudaEvent_t> opin(sp.pieces), done(sp.pieces);
+  auto c_arrived = [&](int s) -> int {
+    HCU(cudaMemcpyAsync(flags + s, pf + kMaxPieces, sizeof(int32_t), cudaMemcpyHostToDevice, hs->h2d),
+        "cudaMemcpyAsync(flag)");
+    if (trace) HCU(cudaEventRecord(tr[1 + 4 * s], hs->h2d), "cudaEventRecord");
+    return STC_OK;
+  };
   if (sp.pieces == 1) {
     HCU(copy_span(dA, hA, A, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(A)");
     HCU(copy_span(dB, hB, B, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(B)");
+    HCU(E.make(opin[0]), "cudaEventCreate");
+    HCU(cudaEventRecord(opin[0], hs->h2d), "cudaEventRecord");
     HCU(copy_span(dC, hC, C, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(C)");
-    HCU(E.make(in[0]), "cudaEventCreate");
-    HCU(cudaEventRecord(in[0], hs->h2d), "cudaEventRecord");
-    if (trace) HCU(cudaEventRecord(tr[1], hs->h2d), "cudaEventRecord");
+    if (int rc = c_arrived(0)) return rc;
   } else {
     if (sp.side == 0)
       HCU(copy_span(dB, hB, B, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(B)");
@@ -320,11 +354,11 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
     for (int s = 0; s < sp.pieces; ++s) {
       HCU(copy_piece(dO, hO, O, ob.str[sp.lab], lext, r0s[s], lens[s], cudaMemcpyHostToDevice, hs->h2d),
           "cudaMemcpy2DAsync(operand piece)");
+      HCU(E.make(opin[s]), "cudaEventCreate");
+      HCU(cudaEventRecord(opin[s], hs->h2d), "cudaEventRecord");
       HCU(copy_piece(dC, hC, C, cb.str[sp.lab], lext, r0s[s], lens[s], cudaMemcpyHostToDevice, hs->h2d),
           "cudaMemcpy2DAsync(C piece)");
-      HCU(E.make(in[s]), "cudaEventCreate");
-      HCU(cudaEventRecord(in[s], hs->h2d), "cudaEventRecord");
-      if (trace) HCU(cudaEventRecord(tr[1 + 4 * s], hs->h2d), "cudaEventRecord");
+      if (int rc = c_arrived(s)) return rc;
     }
   }
   // plan every piece before any of them is launched (the uploads above only fill
@@ -357,10 +391,14 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
   char *ws = reinterpret_cast<char *>(workspace);
   for (int s = 0; s < sp.pieces; ++s) {
     cudaStream_t cs = hs->comp[s % slots];
-    HCU(cudaStreamWaitEvent(cs, in[s], 0), "cudaStreamWaitEvent");
+    HCU(cudaStreamWaitEvent(cs, opin[s], 0), "cudaStreamWaitEvent");
     if (trace) HCU(cudaEventRecord(tr[2 + 4 * s], cs), "cudaEventRecord");
     stc_stats st{};
-    if (int rc = stc_contract(&parts[s], dA, dB, dC, ws + (s % slots) * per, per, cs, &st)) return rc;
+    stc_set_c_ready(flags + s);
+    if (int rc = stc_contract(&parts[s], dA, dB, dC, ws + (s % slots) * per, per, cs, &st)) {
+      stc_set_c_ready(nullptr);
+      return rc;
+    }
     HCU(E.make(done[s]), "cudaEventCreate");
     HCU(cudaEventRecord(done[s], cs), "cudaEventRecord");
     if (trace) HCU(cudaEventRecord(tr[3 + 4 * s], cs), "cudaEventRecord");
@@ -390,7 +428,7 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
         fprintf(stderr, " %.2f", t);
       }
     }
-    fprintf(stderr, "  (in, kstart, kend, out ms)\n");
+    fprintf(stderr, "  (C in, kstart, kend, out ms)\n");
     for (cudaEvent_t e : tr) cudaEventDestroy(e);
   }
   HCU(cudaStreamWaitEvent(us, end, 0), "cudaStreamWaitEvent");

@@ -202,6 +202,16 @@ def _contract_host(spec, a, b, c, level, variant, force_slow, reference_tiling, 
 
 
 _SIDE = {}
+_ONE = []
+
+
+def _pinned_one():
+    """A page-locked int32 1 (source of the c_ready flag copy)."""
+    import torch
+
+    if not _ONE:
+        _ONE.append(torch.ones(1, dtype=torch.int32).pin_memory())
+    return _ONE[0]
 
 
 def _side_stream(dev):
@@ -258,7 +268,9 @@ def contract(spec: ContractionSpec, a, b, c, level: int, variant, params: Blocki
         side.wait_stream(main)
         with torch.cuda.stream(side):
             cd.copy_(src, non_blocking=src.is_pinned())
-            c_ready.fill_(1)
+            # by the copy engine, not a fill kernel: the contraction's persistent CTAs
+            # occupy every SM while they spin on this flag
+            c_ready.copy_(_pinned_one(), non_blocking=True)
         C = DenseTensor(c.extents, c.strides, cd, c.base_offset)
     else:
         C = c if c.on_device else c.to_device(dev)
