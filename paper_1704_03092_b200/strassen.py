@@ -172,13 +172,15 @@ def _contract_host(spec, a, b, c, level, variant, force_slow, reference_tiling, 
     whole call (transfers included)."""
     import torch
 
-    if validate:
-        _validate_targets(spec, c, level, terms)
+    (pa, na), (pb, nb), (pc, nc) = _flat_host(a), _flat_host(b), _flat_host(c)
+    if validate:  # the check needs C's geometry only: an uninitialised device stand-in
+        stand_in = torch.empty(max(nc, 1), dtype=torch.float64, device=dev)
+        _validate_targets(spec, DenseTensor(c.extents, c.strides, stand_in, c.base_offset), level, terms)
+        del stand_in
     flags = (_lib.FLAG_FORCE_SLOW if force_slow else 0) | (_lib.FLAG_REFERENCE_TILING if reference_tiling else 0)
     prob = problem_of(spec, a, b, c, level, variant, flags)
     L = _lib.lib()
     stats = RunStats()
-    (pa, na), (pb, nb), (pc, nc) = _flat_host(a), _flat_host(b), _flat_host(c)
     with torch.cuda.device(dev):
         need = ctypes.c_size_t()
         _lib.check(L.stc_host_workspace_size(ctypes.byref(prob), ctypes.byref(need)))

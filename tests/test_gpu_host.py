@@ -123,3 +123,57 @@ def test_host_pipeline_non_compact_c_is_not_split():
     c = c0.copy()
     stc.contract(spec, a, b, c, 2, "abc")
     assert np.array_equal(c.data, ref.data)
+
+
+def test_host_pipeline_irregular_pieces_integer_exact():
+    # odd extents: pieces of 25 along a (PAD quadrants, repacked operands)
+    spec = stc.parse_benchmark_line("abcij eafbc ifje & a:50;b:7;c:13;i:14;j:9;e:18;f:11;")
+    a, b, c0 = (_tensor(spec, l, s, True) for l, s in ((spec.labels_a, 11), (spec.labels_b, 12), (spec.labels_c, 13)))
+    ref = c0.copy()
+    oracle.contract_reference(spec, a, b, ref, threads=8)
+    for pieces in ("2", "5"):
+        for level, variant in ((1, "abc"), (2, "abc"), (2, "ab"), (2, "naive")):
+            c = c0.copy()
+            _with_env({"STC_HOST_PIECES": pieces}, lambda: stc.contract(spec, a, b, c, level, variant))
+            assert np.array_equal(c.data, ref.data), (pieces, level, variant)
+
+
+def test_host_pipeline_torch_cpu_storage_and_validate():
+    import torch
+
+    spec = stc.parse_benchmark_line(LINES["j_split"])
+    a, b, c0 = (_tensor(spec, l, s, True) for l, s in ((spec.labels_a, 14), (spec.labels_b, 15), (spec.labels_c, 16)))
+    ref = c0.copy()
+    oracle.contract_reference(spec, a, b, ref, threads=8)
+    ta, tb, tc = (stc.DenseTensor(t.extents, t.strides, torch.from_numpy(t.data.copy()), t.base_offset)
+                  for t in (a, b, c0))
+    st = stc.contract(spec, ta, tb, tc, 2, "abc", validate=True)
+    assert st.leaf_multiplies == 49 and st.seconds > 0
+    assert np.array_equal(tc.data.numpy(), ref.data)
+
+
+def test_host_pipeline_errors_leave_c_untouched():
+    # C-ABI errors come before any transfer: C's host storage is unchanged
+    import torch
+
+    spec = stc.parse_benchmark_line(LINES["i_split"])
+    a, b, c0 = (_tensor(spec, l, s, False) for l, s in ((spec.labels_a, 17), (spec.labels_b, 18), (spec.labels_c, 19)))
+    c = c0.copy()
+    p = problem_of(spec, a, b, c, 2, Variant.ABC)
+    p.c_row.ext[0] += 1  # I extents of A and C differ
+    L = _lib.lib()
+    d = [torch.empty(t.data.size + 64, dtype=torch.float64, device="cuda") for t in (a, b, c)]
+    ws = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    rc = L.stc_contract_host(ctypes.byref(p), ctypes.c_void_p(a.data.ctypes.data), ctypes.c_void_p(b.data.ctypes.data),
+                             ctypes.c_void_p(c.data.ctypes.data), *(ctypes.c_void_p(x.data_ptr()) for x in d),
+                             ctypes.c_void_p(ws.data_ptr()), ws.numel(), None, None)
+    torch.cuda.synchronize()
+    assert rc == _lib.STC_EINVAL and b"extents" in L.stc_last_error()
+    assert np.array_equal(c.data, c0.data)
+    # workspace too small
+    p = problem_of(spec, a, b, c, 2, Variant.ABC)
+    rc = L.stc_contract_host(ctypes.byref(p), ctypes.c_void_p(a.data.ctypes.data), ctypes.c_void_p(b.data.ctypes.data),
+                             ctypes.c_void_p(c.data.ctypes.data), *(ctypes.c_void_p(x.data_ptr()) for x in d),
+                             ctypes.c_void_p(ws.data_ptr()), 256, None, None)
+    assert rc == _lib.STC_EWORKSPACE
+    assert np.array_equal(c.data, c0.data)

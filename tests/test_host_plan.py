@@ -1,0 +1,93 @@
+"""Host-side planning of the host-operand pipeline (stc_host_plan, csrc/stc_host.cu): which
+bundle label the problem is cut along and into how many pieces.  Pure host logic, no GPU."""
+
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+import paper_1704_03092_b200 as stc
+from paper_1704_03092_b200 import _lib
+from paper_1704_03092_b200.strassen import Variant, problem_of
+
+
+def _row_major(e):
+    return tuple(int(np.prod(e[i + 1:])) for i in range(len(e)))
+
+
+def _plan(line, level=2, c_strides=None, env=None):
+    spec = stc.parse_benchmark_line(line)
+
+    def t(labels, strides=None):
+        e = spec.tensor_extents(labels)
+        st = strides or _row_major(e)
+        size = sum((x - 1) * s for x, s in zip(e, st)) + 1
+        return stc.DenseTensor(e, st, np.zeros(size))
+
+    p = problem_of(spec, t(spec.labels_a), t(spec.labels_b), t(spec.labels_c, c_strides), level, Variant.ABC)
+    s, l, n = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    old = os.environ.get("STC_HOST_PIECES")
+    if env is not None:
+        os.environ["STC_HOST_PIECES"] = env
+    try:
+        _lib.check(_lib.lib().stc_host_plan(ctypes.byref(p), ctypes.byref(s), ctypes.byref(l), ctypes.byref(n)))
+    finally:
+        if env is not None:
+            if old is None:
+                del os.environ["STC_HOST_PIECES"]
+            else:
+                os.environ["STC_HOST_PIECES"] = old
+    return s.value, l.value, n.value
+
+
+def test_cfg2_cuts_the_i_bundle_on_a_into_four():
+    # C[a,i,b,j], A[e,a,f,b]: label a has the longest runs in both A and C
+    assert _plan("aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;") == (0, 0, 4)
+
+
+def test_j_bundle_cut_when_its_runs_are_longer():
+    # C[j,i,a,b], B[j,f,i,e]: j is outermost in both B and C
+    line = "jiab eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;"
+    side, label, pieces = _plan(line)
+    assert (side, pieces) == (1, 4)
+    assert stc.parse_benchmark_line(line).bundle_j[label] == "j"
+
+
+def test_small_problems_are_not_cut():
+    assert _plan("aibj eafb jfie & a:16;b:16;i:16;j:16;e:16;f:16;")[2] == 1
+
+
+def test_pieces_keep_two_tiles_per_quadrant():
+    # m = 1024 at L2: an I cut would leave quadrants of < 256 rows -> the J bundle (4096) is cut
+    assert _plan("aibj eafb jfie & a:16;b:64;i:64;j:64;e:64;f:64;") == (1, 0, 4)
+    # both bundles 1024 at L2: two pieces at most
+    assert _plan("aibj eafb jfie & a:16;b:64;i:16;j:64;e:64;f:64;")[2] <= 2
+
+
+def test_non_compact_c_is_not_cut():
+    spec = stc.parse_benchmark_line("aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;")
+    e = spec.tensor_extents(spec.labels_c)
+    st = list(_row_major(e))
+    st[0] += 8  # a gap after every outermost slice
+    assert _plan("aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;", c_strides=tuple(st))[2] == 1
+
+
+@pytest.mark.parametrize("n", ["1", "2", "8"])
+def test_piece_count_override(n):
+    assert _plan("aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;", env=n)[2] == int(n)
+
+
+def test_host_workspace_covers_two_piece_slots():
+    spec = stc.parse_benchmark_line("aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;")
+
+    def t(labels):
+        e = spec.tensor_extents(labels)
+        return stc.DenseTensor(e, _row_major(e), np.zeros(int(np.prod(e))))
+
+    p = problem_of(spec, t(spec.labels_a), t(spec.labels_b), t(spec.labels_c), 2, Variant.ABC)
+    whole, host = ctypes.c_size_t(), ctypes.c_size_t()
+    L = _lib.lib()
+    _lib.check(L.stc_workspace_size(ctypes.byref(p), ctypes.byref(whole)))
+    _lib.check(L.stc_host_workspace_size(ctypes.byref(p), ctypes.byref(host)))
+    assert host.value > 0 and host.value < 2 * whole.value  # two quarter-size piece slots + flags
