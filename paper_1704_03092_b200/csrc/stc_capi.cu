@@ -1063,9 +1063,13 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
   g.b_kfast = fs.bkf;
   // ABC: C updates by TMA reduce-add when the C targets are regular boxes (STC_CRED=0 disables)
   g.cred = 0;
+  // summed-operand mode (a summing warpgroup) when some side has more than one
+  // view per chunk (L >= 1); STC_PRESUM=0 keeps the sums in the consumers
+  const bool ps = umax > 2 && !(getenv("STC_PRESUM") && atoi(getenv("STC_PRESUM")) == 0);
+  int nsum = 0;
   TmaSide sc;
   if (pl.variant == STC_VARIANT_ABC && C && !(getenv("STC_CRED") && atoi(getenv("STC_CRED")) == 0) &&
-      fused_stages_red(umax) >= 2 &&
+      (ps ? fused_stages_ps(umax, true, nsum) : fused_stages_red(umax)) >= 2 &&
       plan_cred_side(p->c_row, pl.ti, p->c_col, pl.tj, pl.level, C, p->c_base, sc) &&
       encode_side(sc, C, p->c_base, maps[2])) {
     g.cred = 1;
@@ -1090,6 +1094,14 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
   g.tma = 0;
   g.umax = umax;
   g.stages = g.cred ? fused_stages_red(umax) : S;
+  g.sstages = 0;
+  if (ps) {
+    const int sr = fused_stages_ps(umax, g.cred != 0, nsum);
+    if (sr >= 2) {
+      g.stages = sr;
+      g.sstages = nsum;
+    }
+  }
   g.kchunks = (int)(pl.kq_pad / kFusedK);
   return true;
 }
@@ -1484,6 +1496,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         gf.coords = base.coords;
         gf.umax = base.umax;
         gf.stages = base.stages;
+        gf.sstages = base.sstages;
         gf.kchunks = base.kchunks;
         gf.cred = 0;
         for (int sd = 0; sd < 3; ++sd) {

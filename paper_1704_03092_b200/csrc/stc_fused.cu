@@ -40,26 +40,43 @@ constexpr int FUSED_PRODUCER_REGS = 40;
 static_assert(CONSUMER_WARPS * (FUSED_CONSUMER_REGS - 168) <= FUSED_PRODUCER_WARPS * (168 - FUSED_PRODUCER_REGS),
               "setmaxnreg: consumer increase exceeds the producer release");
 constexpr int MAX_FUSED_STAGES = 8;
+// Summed-operand mode (GemmArgs::sstages > 0, L >= 1): a fourth warpgroup forms
+// the Strassen sums once per CTA into a second ring of summed tiles, and the
+// consumers run the plain one-view-per-side DMMA loop.  512 threads launch at
+// 128 registers: consumers 8 warps x 208 + producer warpgroup 4 x 40 + summing
+// warpgroup 4 x 56 = 65536.
+constexpr int SUM_WARPS = 4;
+constexpr int FUSED_THREADS_PS = FUSED_THREADS + 32 * SUM_WARPS;
+constexpr int PS_CONSUMER_REGS = 208;
+constexpr int PS_SUM_REGS = 56;
+static_assert(CONSUMER_WARPS * (PS_CONSUMER_REGS - 128) <=
+                  FUSED_PRODUCER_WARPS * (128 - FUSED_PRODUCER_REGS) + SUM_WARPS * (128 - PS_SUM_REGS),
+              "setmaxnreg: consumer increase exceeds the producer + summer release");
+constexpr int MAX_SUM_STAGES = 4;
 
-// smem: stages [S][umax][1024 doubles] | (cred) M pieces [2][16][128] | full[S], empty[S] |
-//       epi_full[2], epi_empty[2] | stage_item[S], epi_item[2] | epilogue offset tables:
-//       rows[128], cols[128] (int64)
+// smem: raw stages [S][umax][1024 doubles] | summed stages [Ss][2][1024 doubles] |
+//       (cred) M pieces [2][16][128] | full[S], empty[S], sfull[Ss], sempty[Ss],
+//       epi_full[2], epi_empty[2] | stage_item[S], sum_item[Ss], epi_item[2] |
+//       epilogue offset tables: rows[128], cols[128] (int64)
 constexpr int RED_ROWS = 16;                          // rows of one TMA-reduce piece (double-buffered)
 constexpr size_t RED_BYTES = 2 * (size_t)RED_ROWS * BN * 8;
 struct FusedLayout {
   __host__ __device__ static size_t stage_bytes(int umax) { return (size_t)umax * VIEW_DOUBLES * 8; }
-  __host__ __device__ static size_t red_off(int umax, int stages) { return (size_t)stages * stage_bytes(umax); }
-  __host__ __device__ static size_t bar_off(int umax, int stages, bool red) {
-    return red_off(umax, stages) + (red ? RED_BYTES : 0);
+  __host__ __device__ static size_t sum_off(int umax, int stages) { return (size_t)stages * stage_bytes(umax); }
+  __host__ __device__ static size_t red_off(int umax, int stages, int ss) {
+    return sum_off(umax, stages) + (size_t)ss * stage_bytes(2);
   }
-  __host__ __device__ static size_t meta_off(int umax, int stages, bool red) {
-    return bar_off(umax, stages, red) + 16 * (size_t)stages + 32;
+  __host__ __device__ static size_t bar_off(int umax, int stages, int ss, bool red) {
+    return red_off(umax, stages, ss) + (red ? RED_BYTES : 0);
   }
-  __host__ __device__ static size_t epi_tab_off(int umax, int stages, bool red) {
-    return (meta_off(umax, stages, red) + 4 * (size_t)stages + 8 + 15) / 16 * 16;
+  __host__ __device__ static size_t meta_off(int umax, int stages, int ss, bool red) {
+    return bar_off(umax, stages, ss, red) + 16 * (size_t)(stages + ss) + 32;
   }
-  __host__ __device__ static size_t bytes(int umax, int stages, bool red) {
-    return epi_tab_off(umax, stages, red) + 2 * 128 * 8;
+  __host__ __device__ static size_t epi_tab_off(int umax, int stages, int ss, bool red) {
+    return (meta_off(umax, stages, ss, red) + 4 * (size_t)(stages + ss) + 8 + 15) / 16 * 16;
+  }
+  __host__ __device__ static size_t bytes(int umax, int stages, int ss, bool red) {
+    return epi_tab_off(umax, stages, ss, red) + 2 * 128 * 8;
   }
 };
 
@@ -72,15 +89,30 @@ constexpr size_t kFusedMaxSmem = 227 * 1024;
 // Stages of the fused ring for terms of at most `umax` views per chunk (0: does not fit).
 int fused_stages(int umax) {
   int s = MAX_FUSED_STAGES;
-  while (s >= 2 && FusedLayout::bytes(umax, s, false) > kFusedMaxSmem) --s;
+  while (s >= 2 && FusedLayout::bytes(umax, s, 0, false) > kFusedMaxSmem) --s;
   return s >= 2 ? s : 0;
 }
 
 // Stages when the TMA-reduce epilogue's M piece also lives in smem.
 int fused_stages_red(int umax) {
   int s = MAX_FUSED_STAGES;
-  while (s >= 2 && FusedLayout::bytes(umax, s, true) > kFusedMaxSmem) --s;
+  while (s >= 2 && FusedLayout::bytes(umax, s, 0, true) > kFusedMaxSmem) --s;
   return s >= 2 ? s : 0;
+}
+
+// Summed-operand mode: raw stages (returned) and summed stages (sstages) that
+// fit; the summed ring gets MAX_SUM_STAGES unless only fewer leave two raw stages.
+int fused_stages_ps(int umax, bool red, int &sstages) {
+  for (int ss = MAX_SUM_STAGES; ss >= 2; --ss) {
+    int s = MAX_FUSED_STAGES;
+    while (s >= 2 && FusedLayout::bytes(umax, s, ss, red) > kFusedMaxSmem) --s;
+    if (s >= 2) {
+      sstages = ss;
+      return s;
+    }
+  }
+  sstages = 0;
+  return 0;
 }
 
 // Element offset of (x, k) inside a raw view.
@@ -172,7 +204,7 @@ __device__ __forceinline__ void side_sum(double (&out)[I], const double *st, int
 // DADD of the signed value otherwise -- the reference's view order), then issue
 // MMA group V of the current k-step.  Loads go in groups of four values to keep
 // the register footprint inside the consumers' budget.
-template <int NA, int NB, int V, int KN, bool MMA>
+template <int NA, int NB, int V, int KN, bool MMA, bool SGN = true>
 __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (&fa)[8], const double (&fb)[4],
                                           double (&xa)[8], double (&xb)[4], const double *nst, bool load,
                                           const int (&offA)[2][2], const int (&offB)[2][2], uint32_t negmask) {
@@ -190,7 +222,10 @@ __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (
         double t[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) t[j] = (j & 1 ? pa1 : pa0)[128 * (2 * hh + (j >> 1))];  // immediate offsets
-        if (V == 0) {
+        if (V == 0 && !SGN) {  // summed tile: the signs are already applied
+#pragma unroll
+          for (int j = 0; j < 4; ++j) xa[4 * hh + j] = t[j];
+        } else if (V == 0) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) xa[4 * hh + j] = __hiloint2double(__double2hiint(t[j]) ^ fl, __double2loint(t[j]));
         } else {  // acc + (+/-1) * v: one exactly rounded add, no integer sign flip on the way
@@ -202,7 +237,10 @@ __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (
       double t[4];
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) t[nt] = (nt & 1 ? pb1 : pb0)[128 * (nt >> 1)];
-      if (V == NA) {
+      if (V == NA && !SGN) {
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) xb[nt] = t[nt];
+      } else if (V == NA) {
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) xb[nt] = __hiloint2double(__double2hiint(t[nt]) ^ fl, __double2loint(t[nt]));
       } else {
@@ -216,7 +254,7 @@ __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (
     for (int i = 16 * V / G; i < 16 * (V + 1) / G; ++i)
       dmma_16x8x4(acc[i >> 2][i & 3], fa[2 * (i >> 2)], fa[2 * (i >> 2) + 1], fb[i & 3]);
   }
-  if constexpr (V + 1 < G) pipe_view<NA, NB, V + 1, KN, MMA>(acc, fa, fb, xa, xb, nst, load, offA, offB, negmask);
+  if constexpr (V + 1 < G) pipe_view<NA, NB, V + 1, KN, MMA, SGN>(acc, fa, fb, xa, xb, nst, load, offA, offB, negmask);
 }
 
 // One work item's main loop for terms with NA A-views and NB B-views
@@ -226,7 +264,7 @@ __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (
 // k-step are built one view per group, so no DADD waits on a result it needs
 // right away behind the DMMAs queued on the shared FP64 pipe.  A chunk stage
 // is released as soon as both of its k-steps are in registers.
-template <int NA, int NB>
+template <int NA, int NB, bool SGN = true>
 __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const double *stages, int umax, int S,
                                              uint64_t *full, uint64_t *empty, int &stage, uint32_t &phase, int kchunks,
                                              uint32_t negmask, const int (&offA_)[2][2], const int (&offB_)[2][2],
@@ -247,10 +285,10 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
   const int (&offB)[2][2] = oB;
   const size_t sstride = (size_t)umax * VIEW_DOUBLES;
   double fa[8], fb[4], xa[8], xb[4];
-  pipe_view<NA, NB, 0, 0, false>(acc, fa, fb, fa, fb, stages + stage * sstride, true, offA, offB, negmask);
+  pipe_view<NA, NB, 0, 0, false, SGN>(acc, fa, fb, fa, fb, stages + stage * sstride, true, offA, offB, negmask);
   for (int c = 0; c < kchunks; ++c) {
     // k-step 0 of chunk c (fa, fb) -> build k-step 1 of chunk c (xa, xb)
-    pipe_view<NA, NB, 0, 1, true>(acc, fa, fb, xa, xb, stages + stage * sstride, true, offA, offB, negmask);
+    pipe_view<NA, NB, 0, 1, true, SGN>(acc, fa, fb, xa, xb, stages + stage * sstride, true, offA, offB, negmask);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);  // both k-steps of chunk c are in registers
     if (++stage == S) {
@@ -260,7 +298,7 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
     // k-step 1 of chunk c (xa, xb) -> build k-step 0 of chunk c + 1 (fa, fb)
     const bool more = c + 1 < kchunks;
     if (more) mbar_wait(&full[stage], phase);
-    pipe_view<NA, NB, 0, 0, true>(acc, xa, xb, fa, fb, stages + stage * sstride, more, offA, offB, negmask);
+    pipe_view<NA, NB, 0, 0, true, SGN>(acc, xa, xb, fa, fb, stages + stage * sstride, more, offA, offB, negmask);
   }
 }
 
@@ -515,22 +553,123 @@ __device__ __forceinline__ void epilogue_warps_red(const GemmArgs &p, uint64_t *
   }
 }
 
-template <int AKF, int BKF>
-__global__ void __launch_bounds__(FUSED_THREADS, 1)
+// One side of one k-chunk in the summed-operand mode: dst = s0 * V_v0 +/- ... in
+// view order (sign flip of the first view, one DADD / DSUB per later view: the
+// same roundings as the consumers' fragment-load sums and the reference's
+// _jit.py:43-65).  Raw and summed tiles share the swizzled view layout, so
+// thread t handles the double2 elements t, t + 128, ... of every view.
+__device__ __forceinline__ void sum_side(double2 *__restrict__ dst, const double2 *__restrict__ src, int v0, int n,
+                                         uint32_t negmask, int t) {
+  constexpr int VD2 = VIEW_DOUBLES / 2;
+  constexpr int PER = VD2 / (32 * SUM_WARPS);
+  double2 a[PER];
+  const int fl = static_cast<int>(((negmask >> v0) & 1u) << 31);
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const double2 v = src[v0 * VD2 + t + 32 * SUM_WARPS * i];
+    a[i].x = __hiloint2double(__double2hiint(v.x) ^ fl, __double2loint(v.x));
+    a[i].y = __hiloint2double(__double2hiint(v.y) ^ fl, __double2loint(v.y));
+  }
+  for (int v = v0 + 1; v < v0 + n; ++v) {
+    double2 b[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) b[i] = src[v * VD2 + t + 32 * SUM_WARPS * i];
+    if ((negmask >> v) & 1u) {
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        a[i].x = __dsub_rn(a[i].x, b[i].x);
+        a[i].y = __dsub_rn(a[i].y, b[i].y);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        a[i].x = __dadd_rn(a[i].x, b[i].x);
+        a[i].y = __dadd_rn(a[i].y, b[i].y);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PER; ++i) dst[t + 32 * SUM_WARPS * i] = a[i];
+}
+
+// Summing warpgroup (summed-operand mode): per raw chunk stage of the producer
+// ring, write the A-side sum and the B-side sum into one stage of the summed
+// ring, which the consumers read as a one-view-per-side chunk.  Each element is
+// summed once per CTA (the consumers' fragment-load sums repeat A 4x and B 2x
+// across the warps sharing them), and the summers' stalls on the FP64 unit
+// never hold up a DMMA issue.
+__device__ __forceinline__ void summer_warps(const GemmArgs &p, const double *stages, int umax, int S, uint64_t *full,
+                                             uint64_t *empty, const int *stage_item, double *sums, int Ss,
+                                             uint64_t *sfull, uint64_t *sempty, int *sum_item, int t) {
+  const int lane = t & 31;
+  int rs = 0, ss = 0;
+  uint32_t rph = 0, sph = 0;
+  int cur = -1, na = 0, nb = 0;
+  uint32_t negmask = 0;
+  for (;;) {
+    mbar_wait(&full[rs], rph);
+    const int item = stage_item[rs];
+    mbar_wait(&sempty[ss], sph ^ 1);
+    if (item < 0) {
+      if (t == 0) sum_item[ss] = -1;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sfull[ss]);
+      break;
+    }
+    if (item != cur) {
+      cur = item;
+      int slot, ti, tj;
+      tile_of(p, item, slot, ti, tj);
+      const TermDesc td = p.terms[slot];
+      na = td.a_count;
+      nb = td.b_count;
+      bool neg = false;
+      if (lane < na + nb)
+        neg = __double_as_longlong(p.ops[lane < na ? td.a_first + lane : td.b_first + lane - na].sign) < 0;
+      negmask = __ballot_sync(0xffffffffu, neg);
+    }
+    const double2 *src = reinterpret_cast<const double2 *>(stages + (size_t)rs * umax * VIEW_DOUBLES);
+    double2 *dst = reinterpret_cast<double2 *>(sums + (size_t)ss * 2 * VIEW_DOUBLES);
+    sum_side(dst, src, 0, na, negmask, t);
+    sum_side(dst + VIEW_DOUBLES / 2, src, na, nb, negmask, t);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[rs]);  // raw stage read
+    if (t == 0) sum_item[ss] = item;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sfull[ss]);
+    if (++rs == S) {
+      rs = 0;
+      rph ^= 1;
+    }
+    if (++ss == Ss) {
+      ss = 0;
+      sph ^= 1;
+    }
+  }
+}
+
+// PS: summed-operand mode (a summing warpgroup, p.sstages > 0); otherwise the
+// consumers form the sums in their fragment loads.
+template <int AKF, int BKF, bool PS>
+__global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
     k_strassen_fused(const GemmArgs p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  const int umax = p.umax, S = p.stages;
+  const int umax = p.umax, S = p.stages, Ss = PS ? p.sstages : 0;
   const bool red = p.cred != 0;
   double *stages = reinterpret_cast<double *>(smem);
-  double *redbuf = reinterpret_cast<double *>(smem + FusedLayout::red_off(umax, S));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + FusedLayout::bar_off(umax, S, red));
+  double *sums = reinterpret_cast<double *>(smem + FusedLayout::sum_off(umax, S));
+  double *redbuf = reinterpret_cast<double *>(smem + FusedLayout::red_off(umax, S, Ss));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + FusedLayout::bar_off(umax, S, Ss, red));
   uint64_t *empty = full + S;
-  uint64_t *epi_full = empty + S;  // M tile b written by the consumers (ABC: C updates offloaded)
+  uint64_t *sfull = empty + S;  // summed ring (PS)
+  uint64_t *sempty = sfull + Ss;
+  uint64_t *epi_full = sempty + Ss;  // M tile b written by the consumers (ABC: C updates offloaded)
   uint64_t *epi_empty = epi_full + 2;
-  int *stage_item = reinterpret_cast<int *>(smem + FusedLayout::meta_off(umax, S, red));
-  int *epi_item = stage_item + S;
-  int64_t *epi_rows = reinterpret_cast<int64_t *>(smem + FusedLayout::epi_tab_off(umax, S, red));
+  int *stage_item = reinterpret_cast<int *>(smem + FusedLayout::meta_off(umax, S, Ss, red));
+  int *sum_item = stage_item + S;
+  int *epi_item = sum_item + Ss;
+  int64_t *epi_rows = reinterpret_cast<int64_t *>(smem + FusedLayout::epi_tab_off(umax, S, Ss, red));
   int64_t *epi_cols = epi_rows + 128;
   const bool offload = p.mscratch != nullptr;  // ABC: epilogue warps update C from the M tiles
   const int tid = threadIdx.x;
@@ -538,7 +677,11 @@ __global__ void __launch_bounds__(FUSED_THREADS, 1)
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CONSUMER_WARPS);
+      mbar_init(&empty[s], PS ? SUM_WARPS : CONSUMER_WARPS);
+    }
+    for (int s = 0; s < Ss; ++s) {
+      mbar_init(&sfull[s], SUM_WARPS);
+      mbar_init(&sempty[s], CONSUMER_WARPS);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&epi_full[b], CONSUMER_WARPS);
@@ -549,7 +692,12 @@ __global__ void __launch_bounds__(FUSED_THREADS, 1)
   __syncthreads();
   const int kchunks = p.kchunks;  // 8-deep chunks
 
-  if (warp >= CONSUMER_WARPS) {
+  if (PS && warp >= CONSUMER_WARPS + FUSED_PRODUCER_WARPS) {
+    // ===================== summing warpgroup (PS) ======================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PS_SUM_REGS));
+    summer_warps(p, stages, umax, S, full, empty, stage_item, sums, Ss, sfull, sempty, sum_item,
+                 tid - 32 * (CONSUMER_WARPS + FUSED_PRODUCER_WARPS));
+  } else if (warp >= CONSUMER_WARPS) {
     // ===================== producer warp: TMA box loads ================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(FUSED_PRODUCER_REGS));
     if (warp != CONSUMER_WARPS) {
@@ -616,7 +764,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 1)
     }
   } else {
     // ===================== consumer warps: sums + DMMA + epilogue =====
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(FUSED_CONSUMER_REGS));
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(PS ? PS_CONSUMER_REGS : FUSED_CONSUMER_REGS));
     const int g = lane >> 2, tig = lane & 3;
     const int wm = warp & 1, wn = warp >> 1;
     // Fragment offsets inside a view: A (kk, h) + 128 * mt; B (kk, nt & 1) + 128 * (nt >> 1).
@@ -638,9 +786,15 @@ __global__ void __launch_bounds__(FUSED_THREADS, 1)
     uint32_t ephase = 0;
     bool c_seen = false;  // stc_set_c_ready flag observed
     double acc[4][4][4];
+    // the ring the consumers read: raw views, or (PS) the summed tiles
+    const double *cst = PS ? sums : stages;
+    const int cum = PS ? 2 : umax, CS = PS ? Ss : S;
+    uint64_t *cfull = PS ? sfull : full;
+    uint64_t *cempty = PS ? sempty : empty;
+    const int *citem = PS ? sum_item : stage_item;
     for (;;) {
-      mbar_wait(&full[stage], phase);
-      const int item = stage_item[stage];
+      mbar_wait(&cfull[stage], phase);
+      const int item = citem[stage];
       if (item < 0) {
         if (offload) {  // tell the epilogue warps to stop
           mbar_wait(&epi_empty[eb], ephase ^ 1);
@@ -654,16 +808,19 @@ __global__ void __launch_bounds__(FUSED_THREADS, 1)
       tile_of(p, item, slot, ti, tj);
       const TermDesc td = p.terms[slot];
       const int na = td.a_count, nb = td.b_count;
-      // coefficient signs of the item's views: one load per lane, one ballot
-      bool neg = false;
-      if (lane < na + nb) neg = __double_as_longlong(p.ops[lane < na ? td.a_first + lane : td.b_first + lane - na].sign) < 0;
-      const uint32_t negmask = __ballot_sync(0xffffffffu, neg);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
           for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
+      if constexpr (PS) {
+        consume_item<1, 1, false>(acc, cst, cum, CS, cfull, cempty, stage, phase, kchunks, 0u, offA, offB, lane);
+      } else {
+      // coefficient signs of the item's views: one load per lane, one ballot
+      bool neg = false;
+      if (lane < na + nb) neg = __double_as_longlong(p.ops[lane < na ? td.a_first + lane : td.b_first + lane - na].sign) < 0;
+      const uint32_t negmask = __ballot_sync(0xffffffffu, neg);
       switch (na * 8 + nb) {
         case 9: consume_item<1, 1>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
         case 10: consume_item<1, 2>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
@@ -708,6 +865,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 1)
           }
           break;
       }
+      }  // !PS
       if (offload) {
         // dense M tile into this CTA's scratch buffer; the epilogue warps add it
         // into the C targets while the next item's MMAs run
@@ -754,20 +912,25 @@ __global__ void __launch_bounds__(FUSED_THREADS, 1)
 
 using FusedKernel = void (*)(const GemmArgs, const CUtensorMap, const CUtensorMap, const CUtensorMap);
 
-static FusedKernel fused_for(int akf, int bkf) {
-  if (akf) return bkf ? k_strassen_fused<1, 1> : k_strassen_fused<1, 0>;
-  return bkf ? k_strassen_fused<0, 1> : k_strassen_fused<0, 0>;
+static FusedKernel fused_for(int akf, int bkf, bool ps) {
+  if (ps) {
+    if (akf) return bkf ? k_strassen_fused<1, 1, true> : k_strassen_fused<1, 0, true>;
+    return bkf ? k_strassen_fused<0, 1, true> : k_strassen_fused<0, 0, true>;
+  }
+  if (akf) return bkf ? k_strassen_fused<1, 1, false> : k_strassen_fused<1, 0, false>;
+  return bkf ? k_strassen_fused<0, 1, false> : k_strassen_fused<0, 0, false>;
 }
 
 cudaError_t launch_fused(const GemmArgs &a, int grid, cudaStream_t s, const void *maps) {
-  const size_t sm = FusedLayout::bytes(a.umax, a.stages, a.cred != 0);
-  FusedKernel k = fused_for(a.a_kfast, a.b_kfast);
+  const bool ps = a.sstages > 0;
+  const size_t sm = FusedLayout::bytes(a.umax, a.stages, ps ? a.sstages : 0, a.cred != 0);
+  FusedKernel k = fused_for(a.a_kfast, a.b_kfast, ps);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   CUtensorMap m[3];
   memcpy(m, maps, (a.cred ? 3 : 2) * sizeof(CUtensorMap));
   if (!a.cred) memset(&m[2], 0, sizeof(CUtensorMap));
-  k<<<grid, FUSED_THREADS, sm, s>>>(a, m[0], m[1], m[2]);
+  k<<<grid, ps ? FUSED_THREADS_PS : FUSED_THREADS, sm, s>>>(a, m[0], m[1], m[2]);
   return cudaGetLastError();
 }
 

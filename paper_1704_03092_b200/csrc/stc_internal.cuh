@@ -90,6 +90,8 @@ struct GemmArgs {
   // fused kernel (stc_fused.cu)
   const int4 *coords;        // coords[i]: map coordinates (one part) of pool entry 8 i
   int32_t umax, stages;      // views per chunk stage (2 * max_ops), ring depth
+  int32_t sstages;           // > 0: summing warps form the operand sums into a ring of this depth
+                             // (stc_fused.cu); 0: the consumers form them in their fragment loads
   double *mscratch;          // ABC: [grid][2][BM * BN] M tiles handed to the epilogue warps
   int32_t cred;              // ABC: C updates by TMA reduce-add of M pieces (C views regular)
   const int32_t *c_ready;    // stc_set_c_ready: wait until *c_ready != 0 before touching C
@@ -174,6 +176,7 @@ cudaError_t launch_gemm(const GemmArgs &a, int grid, cudaStream_t s, const void 
 int gemm_tma_config(int max_ops, int &nraw, int &kwin);
 int fused_stages(int umax);
 int fused_stages_red(int umax);
+int fused_stages_ps(int umax, bool red, int &sstages);
 cudaError_t launch_fused(const GemmArgs &a, int grid, cudaStream_t s, const void *maps);
 cudaError_t launch_pool_coords(const int64_t *pool, int4 *coords, const CoordJobs &jobs, cudaStream_t s);
 int gemm_max_grid(int max_ops);

@@ -71,6 +71,36 @@ def test_fused_matches_gather_bitwise_and_classical(name):
             assert stc.relative_error(cf, classical) <= TOL, (name, level, variant)
 
 
+def _run_env(spec, a, b, c0, level, variant, env):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        c = c0.to_device()
+        st = stc.contract(spec, a, b, c, level, variant)
+        return c.to_host(), st
+    finally:
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("name", sorted(LAYOUTS))
+def test_summing_warpgroup_matches_fragment_sums_bitwise(name):
+    # L >= 1: the operand sums are formed once per CTA by the summing warpgroup
+    # (default) or in the consumers' fragment loads (STC_PRESUM=0); same view
+    # order and roundings, so C must be bitwise equal, with every epilogue mode
+    spec = stc.parse_benchmark_line(LAYOUTS[name])
+    a, b, c0 = _operands(spec, 61)
+    for level in (1, 2):
+        for variant in ("abc", "ab"):
+            for epi in ({}, {"STC_CRED": "0"}, {"STC_EPI_OFFLOAD": "0"}):
+                cs, _ = _run_env(spec, a, b, c0, level, variant, {"STC_PRESUM": "1", **epi})
+                cf, _ = _run_env(spec, a, b, c0, level, variant, {"STC_PRESUM": "0", **epi})
+                assert np.array_equal(cs.data, cf.data), (name, level, variant, epi)
+
+
 def test_fused_matches_oracle_strassen():
     # the oracle's own L2 ABC Strassen on the same inputs (different summation
     # order inside the leaf GEMMs, so compared in norm)
