@@ -283,7 +283,7 @@ def main():
             traffic = None
     roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_TC_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP64_TC_PEAK_TFLOPS, "traffic": traffic,
-                "kernel": ("k_strassen_fused (TMA views, Strassen sums in the DMMA fragment loads)" if st.fast_blocks
+                "kernel": ("k_strassen_fused (TMA views; A sums by the summing warpgroup, B sums in the DMMA fragment loads)" if st.fast_blocks
                            else "k_strassen_gemm (gather producer, Strassen sums in smem)"),
                 "kernel_ms": gemm_avg * 1e3, "kernel_share_of_step": gemm_avg / (elapsed / args.steps),
                 "algorithmic_flops_per_launch": alg_flops,

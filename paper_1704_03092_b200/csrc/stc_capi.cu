@@ -537,8 +537,8 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   off = align256(off + (size_t)(pl.pool_len / BK) * 8);
   pl.off_coords = off;  // fused kernel: int4 map coordinates per 8 pool entries
   off = align256(off + (size_t)(pl.pool_len / 8) * 16);
-  pl.off_mscr = off;  // fused ABC: two M tiles per CTA for the epilogue warps
-  if (pl.variant == STC_VARIANT_ABC) off = align256(off + (size_t)pl.grid * 2 * BM * BN * 8);
+  pl.off_mscr = off;  // fused ABC: EPI_BUFS M tiles per CTA for the epilogue warps
+  if (pl.variant == STC_VARIANT_ABC) off = align256(off + (size_t)pl.grid * EPI_BUFS * BM * BN * 8);
   // fused kernel on repacked operands when the views are not box-regular
   if (pl.variant != STC_VARIANT_NAIVE) {
     GemmArgs gd{};
@@ -1063,13 +1063,9 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
   g.b_kfast = fs.bkf;
   // ABC: C updates by TMA reduce-add when the C targets are regular boxes (STC_CRED=0 disables)
   g.cred = 0;
-  // summed-operand mode (a summing warpgroup) when some side has more than one
-  // view per chunk (L >= 1); STC_PRESUM=0 keeps the sums in the consumers
-  const bool ps = umax > 2 && !(getenv("STC_PRESUM") && atoi(getenv("STC_PRESUM")) == 0);
-  int nsum = 0;
   TmaSide sc;
   if (pl.variant == STC_VARIANT_ABC && C && !(getenv("STC_CRED") && atoi(getenv("STC_CRED")) == 0) &&
-      (ps ? fused_stages_ps(umax, true, nsum) : fused_stages_red(umax)) >= 2 &&
+      fused_stages_red(umax) >= 2 &&
       plan_cred_side(p->c_row, pl.ti, p->c_col, pl.tj, pl.level, C, p->c_base, sc) &&
       encode_side(sc, C, p->c_base, maps[2])) {
     g.cred = 1;
@@ -1094,13 +1090,13 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
   g.tma = 0;
   g.umax = umax;
   g.stages = g.cred ? fused_stages_red(umax) : S;
-  g.sstages = 0;
-  if (ps) {
-    const int sr = fused_stages_ps(umax, g.cred != 0, nsum);
-    if (sr >= 2) {
-      g.stages = sr;
-      g.sstages = nsum;
-    }
+  // summing warpgroup when some side has more than one view per chunk (L >= 1):
+  // STC_PRESUM = 0 (the consumers form every sum), 1 (A side; default), 3 (both sides)
+  g.psum = 0;
+  if (umax > 2) {
+    const char *e = getenv("STC_PRESUM");
+    g.psum = e ? atoi(e) & 3 : 1;
+    if (g.psum == 2) g.psum = 3;
   }
   g.kchunks = (int)(pl.kq_pad / kFusedK);
   return true;
@@ -1122,7 +1118,7 @@ constexpr size_t kPlanCache = 32;
 
 std::string plan_env() {
   static const char *knobs[] = {"STC_WORKSPACE_CAP_MB", "STC_EXEC_ORDER", "STC_PACK", "STC_TMA_PROMO",
-                                "STC_TMA", "STC_TMA_PF", "STC_FUSED", "STC_CRED"};
+                                "STC_TMA", "STC_TMA_PF", "STC_FUSED", "STC_CRED", "STC_PRESUM"};
   std::string key;
   for (const char *k : knobs) {
     const char *v = getenv(k);
@@ -1496,7 +1492,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         gf.coords = base.coords;
         gf.umax = base.umax;
         gf.stages = base.stages;
-        gf.sstages = base.sstages;
+        gf.psum = base.psum;
         gf.kchunks = base.kchunks;
         gf.cred = 0;
         for (int sd = 0; sd < 3; ++sd) {

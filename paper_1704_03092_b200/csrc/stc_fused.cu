@@ -40,10 +40,13 @@ constexpr int FUSED_PRODUCER_REGS = 40;
 static_assert(CONSUMER_WARPS * (FUSED_CONSUMER_REGS - 168) <= FUSED_PRODUCER_WARPS * (168 - FUSED_PRODUCER_REGS),
               "setmaxnreg: consumer increase exceeds the producer release");
 constexpr int MAX_FUSED_STAGES = 8;
-// Summed-operand mode (GemmArgs::sstages > 0, L >= 1): a fourth warpgroup forms
-// the Strassen sums once per CTA into a second ring of summed tiles, and the
-// consumers run the plain one-view-per-side DMMA loop.  512 threads launch at
-// 128 registers: consumers 8 warps x 208 + producer warpgroup 4 x 40 + summing
+// Summing warpgroup (GemmArgs::psum != 0, L >= 1): a fourth warpgroup forms
+// Strassen operand sums once per CTA, in place in the raw chunk stage (the sum
+// of a side's views overwrites its first view), before the consumers read the
+// stage.  psum bit 0: the A side (shared by the four warps along N, whose
+// fragment-load sums would repeat it 4x); bit 1: the B side too (else the
+// consumers sum B in their fragment loads, 2x).  512 threads launch at 128
+// registers: consumers 8 warps x 208 + producer warpgroup 4 x 40 + summing
 // warpgroup 4 x 56 = 65536.
 constexpr int SUM_WARPS = 4;
 constexpr int FUSED_THREADS_PS = FUSED_THREADS + 32 * SUM_WARPS;
@@ -52,31 +55,26 @@ constexpr int PS_SUM_REGS = 56;
 static_assert(CONSUMER_WARPS * (PS_CONSUMER_REGS - 128) <=
                   FUSED_PRODUCER_WARPS * (128 - FUSED_PRODUCER_REGS) + SUM_WARPS * (128 - PS_SUM_REGS),
               "setmaxnreg: consumer increase exceeds the producer + summer release");
-constexpr int MAX_SUM_STAGES = 4;
 
-// smem: raw stages [S][umax][1024 doubles] | summed stages [Ss][2][1024 doubles] |
-//       (cred) M pieces [2][16][128] | full[S], empty[S], sfull[Ss], sempty[Ss],
-//       epi_full[2], epi_empty[2] | stage_item[S], sum_item[Ss], epi_item[2] |
-//       epilogue offset tables: rows[128], cols[128] (int64)
+// smem: stages [S][umax][1024 doubles] | (cred) M pieces [2][16][128] |
+//       full[S], empty[S], summed[S], epi_full[EPI_BUFS], epi_empty[EPI_BUFS] |
+//       stage_item[S], epi_item[EPI_BUFS] | epilogue offset tables: rows[128], cols[128] (int64)
 constexpr int RED_ROWS = 16;                          // rows of one TMA-reduce piece (double-buffered)
 constexpr size_t RED_BYTES = 2 * (size_t)RED_ROWS * BN * 8;
 struct FusedLayout {
   __host__ __device__ static size_t stage_bytes(int umax) { return (size_t)umax * VIEW_DOUBLES * 8; }
-  __host__ __device__ static size_t sum_off(int umax, int stages) { return (size_t)stages * stage_bytes(umax); }
-  __host__ __device__ static size_t red_off(int umax, int stages, int ss) {
-    return sum_off(umax, stages) + (size_t)ss * stage_bytes(2);
+  __host__ __device__ static size_t red_off(int umax, int stages) { return (size_t)stages * stage_bytes(umax); }
+  __host__ __device__ static size_t bar_off(int umax, int stages, bool red) {
+    return red_off(umax, stages) + (red ? RED_BYTES : 0);
   }
-  __host__ __device__ static size_t bar_off(int umax, int stages, int ss, bool red) {
-    return red_off(umax, stages, ss) + (red ? RED_BYTES : 0);
+  __host__ __device__ static size_t meta_off(int umax, int stages, bool red) {
+    return bar_off(umax, stages, red) + 24 * (size_t)stages + 16 * EPI_BUFS;
   }
-  __host__ __device__ static size_t meta_off(int umax, int stages, int ss, bool red) {
-    return bar_off(umax, stages, ss, red) + 16 * (size_t)(stages + ss) + 32;
+  __host__ __device__ static size_t epi_tab_off(int umax, int stages, bool red) {
+    return (meta_off(umax, stages, red) + 4 * (size_t)stages + 4 * EPI_BUFS + 15) / 16 * 16;
   }
-  __host__ __device__ static size_t epi_tab_off(int umax, int stages, int ss, bool red) {
-    return (meta_off(umax, stages, ss, red) + 4 * (size_t)(stages + ss) + 8 + 15) / 16 * 16;
-  }
-  __host__ __device__ static size_t bytes(int umax, int stages, int ss, bool red) {
-    return epi_tab_off(umax, stages, ss, red) + 2 * 128 * 8;
+  __host__ __device__ static size_t bytes(int umax, int stages, bool red) {
+    return epi_tab_off(umax, stages, red) + 2 * 128 * 8;
   }
 };
 
@@ -89,30 +87,15 @@ constexpr size_t kFusedMaxSmem = 227 * 1024;
 // Stages of the fused ring for terms of at most `umax` views per chunk (0: does not fit).
 int fused_stages(int umax) {
   int s = MAX_FUSED_STAGES;
-  while (s >= 2 && FusedLayout::bytes(umax, s, 0, false) > kFusedMaxSmem) --s;
+  while (s >= 2 && FusedLayout::bytes(umax, s, false) > kFusedMaxSmem) --s;
   return s >= 2 ? s : 0;
 }
 
 // Stages when the TMA-reduce epilogue's M piece also lives in smem.
 int fused_stages_red(int umax) {
   int s = MAX_FUSED_STAGES;
-  while (s >= 2 && FusedLayout::bytes(umax, s, 0, true) > kFusedMaxSmem) --s;
+  while (s >= 2 && FusedLayout::bytes(umax, s, true) > kFusedMaxSmem) --s;
   return s >= 2 ? s : 0;
-}
-
-// Summed-operand mode: raw stages (returned) and summed stages (sstages) that
-// fit; the summed ring gets MAX_SUM_STAGES unless only fewer leave two raw stages.
-int fused_stages_ps(int umax, bool red, int &sstages) {
-  for (int ss = MAX_SUM_STAGES; ss >= 2; --ss) {
-    int s = MAX_FUSED_STAGES;
-    while (s >= 2 && FusedLayout::bytes(umax, s, ss, red) > kFusedMaxSmem) --s;
-    if (s >= 2) {
-      sstages = ss;
-      return s;
-    }
-  }
-  sstages = 0;
-  return 0;
 }
 
 // Element offset of (x, k) inside a raw view.
@@ -207,11 +190,12 @@ __device__ __forceinline__ void side_sum(double (&out)[I], const double *st, int
 template <int NA, int NB, int V, int KN, bool MMA, bool SGN = true>
 __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (&fa)[8], const double (&fb)[4],
                                           double (&xa)[8], double (&xb)[4], const double *nst, bool load,
-                                          const int (&offA)[2][2], const int (&offB)[2][2], uint32_t negmask) {
+                                          const int (&offA)[2][2], const int (&offB)[2][2], uint32_t negmask,
+                                          int bsh) {
   constexpr int G = NA + NB;
   const int fl = static_cast<int>(((negmask >> V) & 1u) << 31);
   const double sgn = __hiloint2double(0x3ff00000 | fl, 0);  // +/-1.0
-  const double *src = nst + V * VIEW_DOUBLES;
+  const double *src = nst + V * VIEW_DOUBLES + (V >= NA ? bsh : 0);  // bsh: B views' slot shift (summing warps)
   // one address per fragment column / row pair; the mt / nt blocks are immediates
   const double *pa0 = src + offA[KN][0], *pa1 = src + offA[KN][1];
   const double *pb0 = src + offB[KN][0], *pb1 = src + offB[KN][1];
@@ -254,7 +238,7 @@ __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (
     for (int i = 16 * V / G; i < 16 * (V + 1) / G; ++i)
       dmma_16x8x4(acc[i >> 2][i & 3], fa[2 * (i >> 2)], fa[2 * (i >> 2) + 1], fb[i & 3]);
   }
-  if constexpr (V + 1 < G) pipe_view<NA, NB, V + 1, KN, MMA, SGN>(acc, fa, fb, xa, xb, nst, load, offA, offB, negmask);
+  if constexpr (V + 1 < G) pipe_view<NA, NB, V + 1, KN, MMA, SGN>(acc, fa, fb, xa, xb, nst, load, offA, offB, negmask, bsh);
 }
 
 // One work item's main loop for terms with NA A-views and NB B-views
@@ -268,7 +252,7 @@ template <int NA, int NB, bool SGN = true>
 __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const double *stages, int umax, int S,
                                              uint64_t *full, uint64_t *empty, int &stage, uint32_t &phase, int kchunks,
                                              uint32_t negmask, const int (&offA_)[2][2], const int (&offB_)[2][2],
-                                             int lane) {
+                                             int lane, int bsh = 0) {
   // Keep the fragment offsets in registers through opaque copies: otherwise
   // ptxas rematerialises them from %tid (S2R, a long-latency special-register
   // read, plus the swizzle arithmetic) inside the hot loop.
@@ -285,10 +269,10 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
   const int (&offB)[2][2] = oB;
   const size_t sstride = (size_t)umax * VIEW_DOUBLES;
   double fa[8], fb[4], xa[8], xb[4];
-  pipe_view<NA, NB, 0, 0, false, SGN>(acc, fa, fb, fa, fb, stages + stage * sstride, true, offA, offB, negmask);
+  pipe_view<NA, NB, 0, 0, false, SGN>(acc, fa, fb, fa, fb, stages + stage * sstride, true, offA, offB, negmask, bsh);
   for (int c = 0; c < kchunks; ++c) {
     // k-step 0 of chunk c (fa, fb) -> build k-step 1 of chunk c (xa, xb)
-    pipe_view<NA, NB, 0, 1, true, SGN>(acc, fa, fb, xa, xb, stages + stage * sstride, true, offA, offB, negmask);
+    pipe_view<NA, NB, 0, 1, true, SGN>(acc, fa, fb, xa, xb, stages + stage * sstride, true, offA, offB, negmask, bsh);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);  // both k-steps of chunk c are in registers
     if (++stage == S) {
@@ -298,7 +282,7 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
     // k-step 1 of chunk c (xa, xb) -> build k-step 0 of chunk c + 1 (fa, fb)
     const bool more = c + 1 < kchunks;
     if (more) mbar_wait(&full[stage], phase);
-    pipe_view<NA, NB, 0, 0, true, SGN>(acc, xa, xb, fa, fb, stages + stage * sstride, more, offA, offB, negmask);
+    pipe_view<NA, NB, 0, 0, true, SGN>(acc, xa, xb, fa, fb, stages + stage * sstride, more, offA, offB, negmask, bsh);
   }
 }
 
@@ -426,7 +410,7 @@ __device__ __forceinline__ void epilogue_warps(const GemmArgs &p, uint64_t *epi_
     tile_of(p, item, slot, ti, tj);
     const TermDesc td = p.terms[slot];
     const int pos = item - slot * p.tiles_m * p.tiles_n;
-    const double *Mt = p.mscratch + ((size_t)blockIdx.x * 2 + eb) * TILE_DOUBLES;
+    const double *Mt = p.mscratch + ((size_t)blockIdx.x * EPI_BUFS + eb) * TILE_DOUBLES;
     for (int j = 0; j < td.c_count; ++j) {
       const TgtDesc tg = p.tgts[td.c_first + j];
       for (int i = t; i < 128; i += EPI_THREADS) {
@@ -472,8 +456,10 @@ __device__ __forceinline__ void epilogue_warps(const GemmArgs &p, uint64_t *epi_
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&epi_empty[eb]);
-    eb ^= 1;
-    if (eb == 0) ephase ^= 1;
+    if (++eb == EPI_BUFS) {
+      eb = 0;
+      ephase ^= 1;
+    }
   }
 }
 
@@ -502,7 +488,7 @@ __device__ __forceinline__ void epilogue_warps_red(const GemmArgs &p, uint64_t *
     tile_of(p, item, slot, ti, tj);
     const TermDesc td = p.terms[slot];
     const int pos = item - slot * p.tiles_m * p.tiles_n;
-    const double *Mt = p.mscratch + ((size_t)blockIdx.x * 2 + eb) * TILE_DOUBLES;
+    const double *Mt = p.mscratch + ((size_t)blockIdx.x * EPI_BUFS + eb) * TILE_DOUBLES;
     int nb = 0;
     for (int j = 0; j < td.c_count; ++j) {
       const TgtDesc tg = p.tgts[td.c_first + j];
@@ -548,32 +534,34 @@ __device__ __forceinline__ void epilogue_warps_red(const GemmArgs &p, uint64_t *
     }
     named_bar(3, EPI_THREADS);  // every warp is done with this M buffer
     if (lane == 0) mbar_arrive(&epi_empty[eb]);
-    eb ^= 1;
-    if (eb == 0) ephase ^= 1;
+    if (++eb == EPI_BUFS) {
+      eb = 0;
+      ephase ^= 1;
+    }
   }
 }
 
-// One side of one k-chunk in the summed-operand mode: dst = s0 * V_v0 +/- ... in
-// view order (sign flip of the first view, one DADD / DSUB per later view: the
-// same roundings as the consumers' fragment-load sums and the reference's
-// _jit.py:43-65).  Raw and summed tiles share the swizzled view layout, so
-// thread t handles the double2 elements t, t + 128, ... of every view.
-__device__ __forceinline__ void sum_side(double2 *__restrict__ dst, const double2 *__restrict__ src, int v0, int n,
-                                         uint32_t negmask, int t) {
+// One side of one k-chunk, summed in place by the summing warpgroup: view v0
+// becomes s0 * V_v0 +/- V_v0+1 ... in view order (sign flip of the first view,
+// one DADD / DSUB per later view: the roundings of the consumers' fragment-load
+// sums and of the reference's packing, _jit.py:43-65).  All views share the
+// swizzled layout, so thread t owns the double2 elements t, t + 128, ... of
+// every view of the side.
+__device__ __forceinline__ void sum_side(double2 *__restrict__ st, int v0, int n, uint32_t negmask, int t) {
   constexpr int VD2 = VIEW_DOUBLES / 2;
   constexpr int PER = VD2 / (32 * SUM_WARPS);
   double2 a[PER];
   const int fl = static_cast<int>(((negmask >> v0) & 1u) << 31);
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
-    const double2 v = src[v0 * VD2 + t + 32 * SUM_WARPS * i];
+    const double2 v = st[v0 * VD2 + t + 32 * SUM_WARPS * i];
     a[i].x = __hiloint2double(__double2hiint(v.x) ^ fl, __double2loint(v.x));
     a[i].y = __hiloint2double(__double2hiint(v.y) ^ fl, __double2loint(v.y));
   }
   for (int v = v0 + 1; v < v0 + n; ++v) {
     double2 b[PER];
 #pragma unroll
-    for (int i = 0; i < PER; ++i) b[i] = src[v * VD2 + t + 32 * SUM_WARPS * i];
+    for (int i = 0; i < PER; ++i) b[i] = st[v * VD2 + t + 32 * SUM_WARPS * i];
     if ((negmask >> v) & 1u) {
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
@@ -589,87 +577,80 @@ __device__ __forceinline__ void sum_side(double2 *__restrict__ dst, const double
     }
   }
 #pragma unroll
-  for (int i = 0; i < PER; ++i) dst[t + 32 * SUM_WARPS * i] = a[i];
+  for (int i = 0; i < PER; ++i) st[v0 * VD2 + t + 32 * SUM_WARPS * i] = a[i];
 }
 
-// Summing warpgroup (summed-operand mode): per raw chunk stage of the producer
-// ring, write the A-side sum and the B-side sum into one stage of the summed
-// ring, which the consumers read as a one-view-per-side chunk.  Each element is
-// summed once per CTA (the consumers' fragment-load sums repeat A 4x and B 2x
-// across the warps sharing them), and the summers' stalls on the FP64 unit
-// never hold up a DMMA issue.
-__device__ __forceinline__ void summer_warps(const GemmArgs &p, const double *stages, int umax, int S, uint64_t *full,
-                                             uint64_t *empty, const int *stage_item, double *sums, int Ss,
-                                             uint64_t *sfull, uint64_t *sempty, int *sum_item, int t) {
+// Summing warpgroup: per chunk stage (after the TMA loads land), sum the A side
+// (and with psum bit 1 the B side) in place, then release the stage to the
+// consumers (summed[stage]).  Each element is summed once per CTA -- the
+// consumers' fragment-load sums repeat A 4x and B 2x across the warps sharing
+// the fragments -- and the summers' waits for the FP64 unit, which the DMMAs
+// occupy, never hold up a DMMA issue.
+__device__ __forceinline__ void summer_warps(const GemmArgs &p, double *stages, int umax, int S, uint64_t *full,
+                                             uint64_t *summed, const int *stage_item, int t) {
   const int lane = t & 31;
-  int rs = 0, ss = 0;
-  uint32_t rph = 0, sph = 0;
+  const bool sum_b = (p.psum & 2) != 0;
+  int rs = 0;
+  uint32_t rph = 0;
   int cur = -1, na = 0, nb = 0;
   uint32_t negmask = 0;
+  bool do_a = false, do_b = false;
   for (;;) {
     mbar_wait(&full[rs], rph);
     const int item = stage_item[rs];
-    mbar_wait(&sempty[ss], sph ^ 1);
-    if (item < 0) {
-      if (t == 0) sum_item[ss] = -1;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sfull[ss]);
-      break;
+    if (item >= 0) {
+      if (item != cur) {
+        cur = item;
+        int slot, ti, tj;
+        tile_of(p, item, slot, ti, tj);
+        const TermDesc td = p.terms[slot];
+        na = td.a_count;
+        nb = td.b_count;
+        bool neg = false;
+        if (lane < na + nb)
+          neg = __double_as_longlong(p.ops[lane < na ? td.a_first + lane : td.b_first + lane - na].sign) < 0;
+        negmask = __ballot_sync(0xffffffffu, neg);
+        do_a = na > 1 || (negmask & 1u);
+        do_b = sum_b && (nb > 1 || ((negmask >> na) & 1u));
+#ifdef STC_EXPERIMENT_NOSUM
+        do_a = do_b = false;  // timing experiment only: no sums formed
+#endif
+      }
+      double2 *st = reinterpret_cast<double2 *>(stages + (size_t)rs * umax * VIEW_DOUBLES);
+      if (do_a) sum_side(st, 0, na, negmask, t);
+      if (do_b) sum_side(st, na, nb, negmask, t);
+      // generic writes before the async proxy (TMA) refills this stage
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    if (item != cur) {
-      cur = item;
-      int slot, ti, tj;
-      tile_of(p, item, slot, ti, tj);
-      const TermDesc td = p.terms[slot];
-      na = td.a_count;
-      nb = td.b_count;
-      bool neg = false;
-      if (lane < na + nb)
-        neg = __double_as_longlong(p.ops[lane < na ? td.a_first + lane : td.b_first + lane - na].sign) < 0;
-      negmask = __ballot_sync(0xffffffffu, neg);
-    }
-    const double2 *src = reinterpret_cast<const double2 *>(stages + (size_t)rs * umax * VIEW_DOUBLES);
-    double2 *dst = reinterpret_cast<double2 *>(sums + (size_t)ss * 2 * VIEW_DOUBLES);
-    sum_side(dst, src, 0, na, negmask, t);
-    sum_side(dst + VIEW_DOUBLES / 2, src, na, nb, negmask, t);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[rs]);  // raw stage read
-    if (t == 0) sum_item[ss] = item;
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sfull[ss]);
+    if (lane == 0) mbar_arrive(&summed[rs]);
+    if (item < 0) break;
     if (++rs == S) {
       rs = 0;
       rph ^= 1;
     }
-    if (++ss == Ss) {
-      ss = 0;
-      sph ^= 1;
-    }
   }
 }
 
-// PS: summed-operand mode (a summing warpgroup, p.sstages > 0); otherwise the
-// consumers form the sums in their fragment loads.
+// PS: a summing warpgroup forms (some of) the operand sums in place (p.psum);
+// otherwise the consumers form them all in their fragment loads.
 template <int AKF, int BKF, bool PS>
 __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
     k_strassen_fused(const GemmArgs p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  const int umax = p.umax, S = p.stages, Ss = PS ? p.sstages : 0;
+  const int umax = p.umax, S = p.stages;
   const bool red = p.cred != 0;
   double *stages = reinterpret_cast<double *>(smem);
-  double *sums = reinterpret_cast<double *>(smem + FusedLayout::sum_off(umax, S));
-  double *redbuf = reinterpret_cast<double *>(smem + FusedLayout::red_off(umax, S, Ss));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + FusedLayout::bar_off(umax, S, Ss, red));
+  double *redbuf = reinterpret_cast<double *>(smem + FusedLayout::red_off(umax, S));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + FusedLayout::bar_off(umax, S, red));
   uint64_t *empty = full + S;
-  uint64_t *sfull = empty + S;  // summed ring (PS)
-  uint64_t *sempty = sfull + Ss;
-  uint64_t *epi_full = sempty + Ss;  // M tile b written by the consumers (ABC: C updates offloaded)
-  uint64_t *epi_empty = epi_full + 2;
-  int *stage_item = reinterpret_cast<int *>(smem + FusedLayout::meta_off(umax, S, Ss, red));
-  int *sum_item = stage_item + S;
-  int *epi_item = sum_item + Ss;
-  int64_t *epi_rows = reinterpret_cast<int64_t *>(smem + FusedLayout::epi_tab_off(umax, S, Ss, red));
+  uint64_t *summed = empty + S;  // PS: the stage's sums are formed (the consumers' full barrier)
+  uint64_t *epi_full = summed + S;  // M tile b written by the consumers (ABC: C updates offloaded)
+  uint64_t *epi_empty = epi_full + EPI_BUFS;
+  int *stage_item = reinterpret_cast<int *>(smem + FusedLayout::meta_off(umax, S, red));
+  int *epi_item = stage_item + S;
+  int64_t *epi_rows = reinterpret_cast<int64_t *>(smem + FusedLayout::epi_tab_off(umax, S, red));
   int64_t *epi_cols = epi_rows + 128;
   const bool offload = p.mscratch != nullptr;  // ABC: epilogue warps update C from the M tiles
   const int tid = threadIdx.x;
@@ -677,13 +658,10 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], PS ? SUM_WARPS : CONSUMER_WARPS);
+      mbar_init(&empty[s], CONSUMER_WARPS);
+      mbar_init(&summed[s], SUM_WARPS);
     }
-    for (int s = 0; s < Ss; ++s) {
-      mbar_init(&sfull[s], SUM_WARPS);
-      mbar_init(&sempty[s], CONSUMER_WARPS);
-    }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < EPI_BUFS; ++b) {
       mbar_init(&epi_full[b], CONSUMER_WARPS);
       mbar_init(&epi_empty[b], EPI_WARPS);
     }
@@ -695,8 +673,7 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
   if (PS && warp >= CONSUMER_WARPS + FUSED_PRODUCER_WARPS) {
     // ===================== summing warpgroup (PS) ======================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PS_SUM_REGS));
-    summer_warps(p, stages, umax, S, full, empty, stage_item, sums, Ss, sfull, sempty, sum_item,
-                 tid - 32 * (CONSUMER_WARPS + FUSED_PRODUCER_WARPS));
+    summer_warps(p, stages, umax, S, full, summed, stage_item, tid - 32 * (CONSUMER_WARPS + FUSED_PRODUCER_WARPS));
   } else if (warp >= CONSUMER_WARPS) {
     // ===================== producer warp: TMA box loads ================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(FUSED_PRODUCER_REGS));
@@ -740,7 +717,11 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
       int src[5];
 #pragma unroll
       for (int d = 0; d < 5; ++d) src[d] = p.tm_src[sd][d];
+#ifdef STC_EXPERIMENT_TWOVIEWS
+      const uint32_t bytes = 2u * VIEW_DOUBLES * 8;
+#else
       const uint32_t bytes = (uint32_t)U * VIEW_DOUBLES * 8;
+#endif
       for (int c = 0; c < kchunks; ++c) {
         int4 kc = make_int4(0, 0, 0, 0);
         if (lane < U) kc = p.coords[(kst + (int64_t)c * FK) >> 3];
@@ -750,7 +731,12 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
           mbar_expect_tx_f(&full[stage], bytes);
         }
         __syncwarp();
+#ifdef STC_EXPERIMENT_TWOVIEWS
+        // timing experiment only: the first view of each side is loaded, the other slots are stale
+        if (lane == 0 || lane == na) {
+#else
         if (lane < U) {
+#endif
           int32_t cc[5];
 #pragma unroll
           for (int d = 0; d < 5; ++d) cc[d] = src[d] < 4 ? coord_of(xc, src[d]) : coord_of(kc, src[d] - 4);
@@ -786,15 +772,11 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
     uint32_t ephase = 0;
     bool c_seen = false;  // stc_set_c_ready flag observed
     double acc[4][4][4];
-    // the ring the consumers read: raw views, or (PS) the summed tiles
-    const double *cst = PS ? sums : stages;
-    const int cum = PS ? 2 : umax, CS = PS ? Ss : S;
-    uint64_t *cfull = PS ? sfull : full;
-    uint64_t *cempty = PS ? sempty : empty;
-    const int *citem = PS ? sum_item : stage_item;
+    // PS: a stage is ready for the consumers once its sums are formed
+    uint64_t *cfull = PS ? summed : full;
     for (;;) {
       mbar_wait(&cfull[stage], phase);
-      const int item = citem[stage];
+      const int item = stage_item[stage];
       if (item < 0) {
         if (offload) {  // tell the epilogue warps to stop
           mbar_wait(&epi_empty[eb], ephase ^ 1);
@@ -815,7 +797,24 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
 #pragma unroll
           for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
       if constexpr (PS) {
-        consume_item<1, 1, false>(acc, cst, cum, CS, cfull, cempty, stage, phase, kchunks, 0u, offA, offB, lane);
+        // the A sum sits in view slot 0 and the B views from slot na on
+        const int bsh = (na - 1) * VIEW_DOUBLES;
+        if (p.psum & 2) {  // B summed too (slot na)
+          consume_item<1, 1, false>(acc, stages, umax, S, cfull, empty, stage, phase, kchunks, 0u, offA, offB, lane, bsh);
+        } else {  // B views summed in the fragment loads: their signs at bits 1..nb
+          bool neg = false;
+          if (lane < nb) neg = __double_as_longlong(p.ops[td.b_first + lane].sign) < 0;
+          const uint32_t negmask = __ballot_sync(0xffffffffu, neg) << 1;
+#ifdef STC_EXPERIMENT_NOBSUM
+          switch (1) {  // timing experiment only: the consumers read one B view
+#else
+          switch (nb) {
+#endif
+            case 1: consume_item<1, 1>(acc, stages, umax, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bsh); break;
+            case 2: consume_item<1, 2>(acc, stages, umax, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bsh); break;
+            default: consume_item<1, 4>(acc, stages, umax, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bsh); break;
+          }
+        }
       } else {
       // coefficient signs of the item's views: one load per lane, one ballot
       bool neg = false;
@@ -870,7 +869,7 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
         // dense M tile into this CTA's scratch buffer; the epilogue warps add it
         // into the C targets while the next item's MMAs run
         mbar_wait(&epi_empty[eb], ephase ^ 1);
-        double *Mt = p.mscratch + ((size_t)blockIdx.x * 2 + eb) * TILE_DOUBLES;
+        double *Mt = p.mscratch + ((size_t)blockIdx.x * EPI_BUFS + eb) * TILE_DOUBLES;
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -884,8 +883,10 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
         __threadfence_block();
         __syncwarp();
         if (lane == 0) mbar_arrive(&epi_full[eb]);
-        eb ^= 1;
-        if (eb == 0) ephase ^= 1;
+        if (++eb == EPI_BUFS) {
+          eb = 0;
+          ephase ^= 1;
+        }
         continue;
       }
 #ifdef STC_EXPERIMENT_NOEPI
@@ -922,8 +923,8 @@ static FusedKernel fused_for(int akf, int bkf, bool ps) {
 }
 
 cudaError_t launch_fused(const GemmArgs &a, int grid, cudaStream_t s, const void *maps) {
-  const bool ps = a.sstages > 0;
-  const size_t sm = FusedLayout::bytes(a.umax, a.stages, ps ? a.sstages : 0, a.cred != 0);
+  const bool ps = a.psum != 0;
+  const size_t sm = FusedLayout::bytes(a.umax, a.stages, a.cred != 0);
   FusedKernel k = fused_for(a.a_kfast, a.b_kfast, ps);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;

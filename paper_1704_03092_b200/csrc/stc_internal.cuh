@@ -24,7 +24,11 @@ constexpr int THREADS = 32 * (CONSUMER_WARPS + PRODUCER_WARPS);
 // 256 consumer threads x 192 + 256 producer threads x 64 = 65536.
 constexpr int CONSUMER_REGS = 192;
 constexpr int PRODUCER_REGS = 64;
-constexpr int MAX_OPS = 16;          // views per operand side (2^L, L <= 4)
+constexpr int MAX_OPS = 16;
+#ifndef STC_EPI_BUFS
+#define STC_EPI_BUFS 2
+#endif
+constexpr int EPI_BUFS = STC_EPI_BUFS;  // fused ABC: M tiles per CTA in flight to the epilogue warps          // views per operand side (2^L, L <= 4)
 
 // One operand view of a term side.  For the A side the tile-fixed dimension x
 // is rows (I) and k is columns (P); for the B side x is columns (J) and k rows.
@@ -90,8 +94,8 @@ struct GemmArgs {
   // fused kernel (stc_fused.cu)
   const int4 *coords;        // coords[i]: map coordinates (one part) of pool entry 8 i
   int32_t umax, stages;      // views per chunk stage (2 * max_ops), ring depth
-  int32_t sstages;           // > 0: summing warps form the operand sums into a ring of this depth
-                             // (stc_fused.cu); 0: the consumers form them in their fragment loads
+  int32_t psum;              // summing warpgroup (stc_fused.cu): bit 0 sums the A side, bit 1 the B
+                             // side in place; 0: the consumers form every sum in their fragment loads
   double *mscratch;          // ABC: [grid][2][BM * BN] M tiles handed to the epilogue warps
   int32_t cred;              // ABC: C updates by TMA reduce-add of M pieces (C views regular)
   const int32_t *c_ready;    // stc_set_c_ready: wait until *c_ready != 0 before touching C
@@ -176,7 +180,6 @@ cudaError_t launch_gemm(const GemmArgs &a, int grid, cudaStream_t s, const void 
 int gemm_tma_config(int max_ops, int &nraw, int &kwin);
 int fused_stages(int umax);
 int fused_stages_red(int umax);
-int fused_stages_ps(int umax, bool red, int &sstages);
 cudaError_t launch_fused(const GemmArgs &a, int grid, cudaStream_t s, const void *maps);
 cudaError_t launch_pool_coords(const int64_t *pool, int4 *coords, const CoordJobs &jobs, cudaStream_t s);
 int gemm_max_grid(int max_ops);

@@ -89,16 +89,18 @@ def _run_env(spec, a, b, c0, level, variant, env):
 @pytest.mark.parametrize("name", sorted(LAYOUTS))
 def test_summing_warpgroup_matches_fragment_sums_bitwise(name):
     # L >= 1: the operand sums are formed once per CTA by the summing warpgroup
-    # (default) or in the consumers' fragment loads (STC_PRESUM=0); same view
-    # order and roundings, so C must be bitwise equal, with every epilogue mode
+    # (STC_PRESUM=3: both sides; 1: the A side, B in the consumers' fragment
+    # loads) or all in the fragment loads (0); same view order and roundings,
+    # so C must be bitwise equal, with every epilogue mode
     spec = stc.parse_benchmark_line(LAYOUTS[name])
     a, b, c0 = _operands(spec, 61)
     for level in (1, 2):
         for variant in ("abc", "ab"):
             for epi in ({}, {"STC_CRED": "0"}, {"STC_EPI_OFFLOAD": "0"}):
-                cs, _ = _run_env(spec, a, b, c0, level, variant, {"STC_PRESUM": "1", **epi})
                 cf, _ = _run_env(spec, a, b, c0, level, variant, {"STC_PRESUM": "0", **epi})
-                assert np.array_equal(cs.data, cf.data), (name, level, variant, epi)
+                for ps in ("1", "3"):
+                    cs, _ = _run_env(spec, a, b, c0, level, variant, {"STC_PRESUM": ps, **epi})
+                    assert np.array_equal(cs.data, cf.data), (name, level, variant, epi, ps)
 
 
 def test_fused_matches_oracle_strassen():

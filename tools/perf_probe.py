@@ -28,6 +28,8 @@ CONFIGS = {
     "cfg2h": ("aibj eafb jfie & a:32;b:64;i:64;j:64;e:64;f:64;", [(2, "abc"), (1, "abc")]),
     "cfg2q": ("aibj eafb jfie & a:16;b:64;i:64;j:64;e:64;f:64;", [(2, "abc"), (1, "abc")]),
     "cfg2e": ("aibj eafb jfie & a:8;b:64;i:64;j:64;e:64;f:64;", [(2, "abc"), (1, "abc")]),
+    "cfg2L2": ("aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;", [(2, "abc")]),
+    "barL2": ("abij abef efij & a:128;b:128;i:128;j:128;e:128;f:128;", [(2, "abc")]),
     "bar": ("abij abef efij & a:128;b:128;i:128;j:128;e:128;f:128;", [(2, "abc"), (1, "abc"), (0, "abc")]),
     # cfg5 per-GPU shards of the 8-GPU n-split (i: 32 / G), G = 8 and G = 1 (the full 32768^3)
     "cfg5s8": ("abcijk abcefg efgijk & a:32;b:32;c:32;i:4;j:32;k:32;e:32;f:32;g:32;", [(2, "abc"), (1, "abc")]),

@@ -1,0 +1,39 @@
+"""List local-memory spills (STL/LDL) of one kernel by source line, with their distance to the
+nearest DMMA (spills inside the MMA loops show up with small distances).
+
+Usage: python tools/spill_lines.py build/stc_fused.o <kernel-name-substring>...
+"""
+import collections
+import os
+import re
+import subprocess
+import sys
+import tempfile
+
+obj, pats = sys.argv[1], sys.argv[2:]
+with tempfile.TemporaryDirectory() as d:
+    subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=d, check=True, capture_output=True)
+    cub = [f for f in os.listdir(d) if f.endswith(".cubin")][0]
+    txt = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, cub)], capture_output=True, text=True).stdout
+parts = re.split(r"\n\s*\.text\.(\S+):", txt)
+for i in range(1, len(parts), 2):
+    name, body = parts[i], parts[i + 1]
+    if not all(p in name for p in pats):
+        continue
+    ins, cur = [], None
+    for line in body.split("\n"):
+        m = re.search(r'//## File "([^"]+)", line (\d+)', line)
+        if m:
+            cur = (m.group(1).split("/")[-1], int(m.group(2)))
+            continue
+        if re.search(r"/\*[0-9a-f]{4,}\*/", line):
+            ins.append((cur, line))
+    dmma = [k for k, (_, l) in enumerate(ins) if "DMMA" in l]
+    spills = collections.Counter()
+    near = 0
+    for k, (src, l) in enumerate(ins):
+        if re.search(r"\b(STL|LDL)", l):
+            dist = min((abs(k - j) for j in dmma), default=10**9)
+            spills[src] += 1
+            near += dist < 40
+    print(name, f"instructions {len(ins)}  DMMA {len(dmma)}  spills {sum(spills.values())}  within 40 of a DMMA {near}")
