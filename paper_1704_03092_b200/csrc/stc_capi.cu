@@ -315,6 +315,11 @@ struct Plan {
   int max_ops = 1;  // most views on one side of any term (2^L)
   size_t off_kbs = 0, off_coords = 0, off_mscr = 0, off_pka = 0, off_pkb = 0;
   bool need_pack = false;  // fused kernel on repacked operands (layout not box-regular)
+  // ABC with C updated straight from the kernel, ticket-ordered per C tile; false for AB,
+  // Naive and the dense-M ABC mode (many terms in flight per tile: dense M slots, then one
+  // ordered accumulate pass -- the same additions in the same order, without ticket chains)
+  bool ticketed = false;
+  std::vector<int> seq;  // term order of the dense-M batches and accumulate lists
   size_t off_pool = 0, off_vecs = 0, off_tab = 0, off_tickets = 0, off_counters = 0, off_M = 0, off_pa = 0,
          off_pb = 0, off_acc = 0, total = 0;
   size_t tab_bytes = 0, acc_bytes = 0;
@@ -455,9 +460,23 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   if (P * (int64_t)T > INT32_MAX) return fail(STC_EINVAL, "problem too large: %lld work items", (long long)(P * T));
   pl.grid = grid_hint > 0 ? grid_hint : 148;
 
+  pl.seq.resize(T);
+  for (int t = 0; t < T; ++t) pl.seq[t] = t;
   if (pl.variant == STC_VARIANT_ABC) {
+    // C-tile update order (tickets, or the dense-M accumulate order): terms
+    // that run concurrently should write disjoint quadrants
     const int window = (int)std::min<int64_t>(T, cdiv(pl.grid, P) + 1);
-    const std::vector<int> seq = exec_order(pl.terms, window);
+    pl.seq = exec_order(pl.terms, window);
+    // dense-M mode when many terms per C tile would be in flight at once: the
+    // ticket chains then serialise (cfg2 pieces of m = 1024: 9 terms in flight,
+    // 1.56 ms ticketed vs 1.21 ms dense; 576^3 L2: 0.60 vs 0.15 ms).
+    // STC_ABC_DENSE = 0 / 1 forces either.
+    const char *de = getenv("STC_ABC_DENSE");
+    const bool dense = T > 1 && (de ? atoi(de) != 0 : pl.grid >= 4 * P);
+    pl.ticketed = !dense;
+  }
+  if (pl.ticketed) {
+    const std::vector<int> &seq = pl.seq;
     std::vector<int> writers(pl.nquads, 0);
     for (int t : seq) {
       const Term &tm = pl.terms[t];
@@ -538,7 +557,7 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   pl.off_coords = off;  // fused kernel: int4 map coordinates per 8 pool entries
   off = align256(off + (size_t)(pl.pool_len / 8) * 16);
   pl.off_mscr = off;  // fused ABC: EPI_BUFS M tiles per CTA for the epilogue warps
-  if (pl.variant == STC_VARIANT_ABC) off = align256(off + (size_t)pl.grid * EPI_BUFS * BM * BN * 8);
+  if (pl.ticketed) off = align256(off + (size_t)pl.grid * EPI_BUFS * BM * BN * 8);
   // fused kernel on repacked operands when the views are not box-regular
   if (pl.variant != STC_VARIANT_NAIVE) {
     GemmArgs gd{};
@@ -555,7 +574,7 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   pl.off_vecs = off;
   off = align256(off + (pl.vecs.size() + 4) * sizeof(VecDesc));  // + the packed sides' vectors
   pl.off_tab = off;
-  if (pl.variant == STC_VARIANT_ABC) {
+  if (pl.ticketed) {
     pl.tab_bytes = pl.tdesc.size() * sizeof(TermDesc) + pl.ops.size() * sizeof(OpDesc) + pl.tgts.size() * sizeof(TgtDesc);
   } else {
     // per batch: TermDesc[batch] + OpDesc (<= 2*Q per side per term) + accumulate lists
@@ -564,15 +583,15 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     pl.acc_bytes = align256((size_t)(pl.nquads + 1) * 4) + align256((size_t)pl.batch * pl.nquads * 4) +
                    align256((size_t)pl.batch * pl.nquads * 8) + 2 * align256((size_t)pl.nquads * 8);
   }
-  off = align256(off + pl.tab_bytes * (pl.variant == STC_VARIANT_ABC ? 1 : pl.nbatches));
+  off = align256(off + pl.tab_bytes * (pl.ticketed ? 1 : pl.nbatches));
   pl.off_acc = off;
-  off = align256(off + pl.acc_bytes * (pl.variant == STC_VARIANT_ABC ? 0 : pl.nbatches));
+  off = align256(off + pl.acc_bytes * (pl.ticketed ? 0 : pl.nbatches));
   pl.off_tickets = off;
   off = align256(off + (size_t)pl.ntickets * 4);
   pl.off_counters = off;
   off = align256(off + (size_t)pl.ncounters * 4);
   pl.off_M = off;
-  if (pl.variant != STC_VARIANT_ABC) off = align256(off + (size_t)pl.batch * pl.m_slot * 8);
+  if (!pl.ticketed) off = align256(off + (size_t)pl.batch * pl.m_slot * 8);
   pl.off_pa = off;
   if (pl.variant == STC_VARIANT_NAIVE) off = align256(off + (size_t)pl.batch * pl.pa_slot * 8);
   pl.off_pb = off;
@@ -1118,7 +1137,8 @@ constexpr size_t kPlanCache = 32;
 
 std::string plan_env() {
   static const char *knobs[] = {"STC_WORKSPACE_CAP_MB", "STC_EXEC_ORDER", "STC_PACK", "STC_TMA_PROMO",
-                                "STC_TMA", "STC_TMA_PF", "STC_FUSED", "STC_CRED", "STC_PRESUM"};
+                                "STC_TMA", "STC_TMA_PF", "STC_FUSED", "STC_CRED", "STC_PRESUM",
+                                "STC_ABC_DENSE"};
   std::string key;
   for (const char *k : knobs) {
     const char *v = getenv(k);
@@ -1157,6 +1177,15 @@ namespace stc {
 int set_error(int code, const char *msg) {
   g_err = msg;
   return code;
+}
+
+// Whether stc_contract runs the problem ticketed (ABC, C updated by the kernel)
+// rather than through dense M slots and an accumulate kernel (stc_host.cu).
+bool plan_ticketed(const stc_problem *p) {
+  Plan pl;
+  const int sms = gemm_max_grid(MAX_OPS);
+  if (cached_plan(p, pl, sms > 0 ? sms : 0)) return false;
+  return pl.ticketed;
 }
 }  // namespace stc
 
@@ -1274,7 +1303,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
   g.force_slow = (pl.flags & STC_FLAG_FORCE_SLOW) ? 1 : 0;
   g.tickets = tickets;
 
-  if (pl.variant == STC_VARIANT_ABC) {
+  if (pl.ticketed) {
     char *tab = ws + pl.off_tab;
     std::vector<char> host(pl.tab_bytes);
     size_t o = 0;
@@ -1337,7 +1366,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       std::vector<TermDesc> gterms(nb), uA(nb), uB(nb);
       std::vector<OpDesc> ops;
       for (int t = t0; t < t1; ++t) {
-        const Term &tm = pl.terms[t];
+        const Term &tm = pl.terms[pl.seq[t]];
         const int slot = t - t0;
         TermDesc ua{}, ub{}, gd{};
         ua.a_first = (int)ops.size();
@@ -1379,7 +1408,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       for (int q = 0; q < pl.nquads; ++q) {
         lstart[q] = (int32_t)lslot.size();
         for (int t = t0; t < t1; ++t)
-          for (const Op &op : pl.terms[t].c)
+          for (const Op &op : pl.terms[pl.seq[t]].c)
             if (op.q == q) {
               lslot.push_back(t - t0);
               lsign.push_back((double)op.s);

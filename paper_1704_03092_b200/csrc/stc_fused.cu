@@ -28,6 +28,9 @@
 
 namespace stc {
 
+#ifndef STC_BSUM_BATCH
+#define STC_BSUM_BATCH 1  // B views of a k-step folded in one DFMA run (0: one view per MMA group)
+#endif
 constexpr int FK = 8;                        // k-chunk of the fused kernel
 constexpr int VIEW_DOUBLES = BM * FK;        // one raw view of one chunk (BM == BN)
 constexpr int FUSED_PRODUCER_WARPS = 4;  // one warpgroup (setmaxnreg is warpgroup-wide); warp 0 of it issues
@@ -51,7 +54,7 @@ constexpr int MAX_FUSED_STAGES = 8;
 constexpr int SUM_WARPS = 4;
 constexpr int FUSED_THREADS_PS = FUSED_THREADS + 32 * SUM_WARPS;
 constexpr int PS_CONSUMER_REGS = 208;
-constexpr int PS_SUM_REGS = 56;
+constexpr int PS_SUM_REGS = 56;  // 40 (for 216-register consumers) measured slower: the summers pace the consumers
 static_assert(CONSUMER_WARPS * (PS_CONSUMER_REGS - 128) <=
                   FUSED_PRODUCER_WARPS * (128 - FUSED_PRODUCER_REGS) + SUM_WARPS * (128 - PS_SUM_REGS),
               "setmaxnreg: consumer increase exceeds the producer + summer release");
@@ -215,6 +218,23 @@ __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (
         } else {  // acc + (+/-1) * v: one exactly rounded add, no integer sign flip on the way
 #pragma unroll
           for (int j = 0; j < 4; ++j) xa[4 * hh + j] = __fma_rn(sgn, t[j], xa[4 * hh + j]);
+        }
+      }
+    } else if (STC_BSUM_BATCH && NB > 1 && SGN) {
+      // all B views of the k-step loaded first, then one run of DFMAs (one FP64 pipe switch)
+      if constexpr (V == NA) {
+        double t[NB][4];
+#pragma unroll
+        for (int w = 0; w < NB; ++w)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) t[w][nt] = ((nt & 1 ? pb1 : pb0) + w * VIEW_DOUBLES)[128 * (nt >> 1)];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) xb[nt] = __hiloint2double(__double2hiint(t[0][nt]) ^ fl, __double2loint(t[0][nt]));
+#pragma unroll
+        for (int w = 1; w < NB; ++w) {
+          const double sw = __hiloint2double(0x3ff00000 | static_cast<int>(((negmask >> (V + w)) & 1u) << 31), 0);
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) xb[nt] = __fma_rn(sw, t[w][nt], xb[nt]);
         }
       }
     } else {
@@ -550,8 +570,8 @@ __device__ __forceinline__ void epilogue_warps_red(const GemmArgs &p, uint64_t *
 __device__ __forceinline__ void sum_side(double2 *__restrict__ st, int v0, int n, uint32_t negmask, int t) {
   constexpr int VD2 = VIEW_DOUBLES / 2;
   constexpr int PER = VD2 / (32 * SUM_WARPS);
-  double2 a[PER];
   const int fl = static_cast<int>(((negmask >> v0) & 1u) << 31);
+  double2 a[PER];
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     const double2 v = st[v0 * VD2 + t + 32 * SUM_WARPS * i];

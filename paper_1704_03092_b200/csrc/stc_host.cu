@@ -386,11 +386,15 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
   cudaPointerAttributes pa{};
   const bool locked = cudaPointerGetAttributes(&pa, hC) == cudaSuccess && pa.type == cudaMemoryTypeHost;
   cudaGetLastError();  // a failed query leaves an error code behind
-  // pieces on alternating compute streams (workspace slot = stream)
+  // pieces on alternating compute streams (workspace slot = stream), so piece s+1's
+  // CTAs fill the SMs of piece s's last wave -- unless the pieces run through dense M
+  // slots (stc_contract's dense-M ABC mode, AB, Naive): their accumulate kernels would
+  // then wait behind the next piece's persistent kernel, and one stream is faster
+  const bool alternate = plan_ticketed(&parts[0]);
   stc_stats total{};
   char *ws = reinterpret_cast<char *>(workspace);
   for (int s = 0; s < sp.pieces; ++s) {
-    cudaStream_t cs = hs->comp[s % slots];
+    cudaStream_t cs = hs->comp[alternate ? s % slots : 0];
     HCU(cudaStreamWaitEvent(cs, opin[s], 0), "cudaStreamWaitEvent");
     if (trace) HCU(cudaEventRecord(tr[2 + 4 * s], cs), "cudaEventRecord");
     stc_stats st{};

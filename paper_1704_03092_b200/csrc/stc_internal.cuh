@@ -183,6 +183,7 @@ int fused_stages_red(int umax);
 cudaError_t launch_fused(const GemmArgs &a, int grid, cudaStream_t s, const void *maps);
 cudaError_t launch_pool_coords(const int64_t *pool, int4 *coords, const CoordJobs &jobs, cudaStream_t s);
 int gemm_max_grid(int max_ops);
+bool plan_ticketed(const stc_problem *p);  // stc_capi.cu
 cudaError_t launch_accumulate(const AccArgs &a, cudaStream_t s);
 cudaError_t launch_unpack(const UnpackArgs &a, cudaStream_t s);
 cudaError_t launch_pack_views(const double *D, const int64_t *pool, const PackArgs &a, double *out, cudaStream_t s);

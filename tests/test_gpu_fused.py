@@ -103,6 +103,26 @@ def test_summing_warpgroup_matches_fragment_sums_bitwise(name):
                     assert np.array_equal(cs.data, cf.data), (name, level, variant, epi, ps)
 
 
+@pytest.mark.parametrize("line", [
+    LAYOUTS["ax_bk"],
+    "abij abef efij & a:24;b:24;i:24;j:24;e:24;f:24;",  # cfg1 (576^3): dense by default
+    "abcij eafbc ifje & a:10;b:7;c:13;i:14;j:9;e:18;f:11;",  # irregular, PAD quadrants
+])
+def test_abc_dense_m_matches_ticketed_bitwise(line):
+    # ABC's C updates: straight from the kernel in ticket order, or (many terms in
+    # flight per C tile) dense M slots + one accumulate pass in the same order
+    # (STC_ABC_DENSE forces either): the same additions, so C must be bitwise equal
+    spec = stc.parse_benchmark_line(line)
+    a, b, c0 = _operands(spec, 71)
+    for level in (1, 2):
+        ct, _ = _run_env(spec, a, b, c0, level, "abc", {"STC_ABC_DENSE": "0"})
+        cd, _ = _run_env(spec, a, b, c0, level, "abc", {"STC_ABC_DENSE": "1"})
+        assert np.array_equal(ct.data, cd.data), (line, level)
+        for fused in ("0",):  # the gather kernel takes the same two paths
+            cg, _ = _run_env(spec, a, b, c0, level, "abc", {"STC_ABC_DENSE": "1", "STC_FUSED": fused})
+            assert np.array_equal(cg.data, cd.data), (line, level)
+
+
 def test_fused_matches_oracle_strassen():
     # the oracle's own L2 ABC Strassen on the same inputs (different summation
     # order inside the leaf GEMMs, so compared in norm)

@@ -81,13 +81,20 @@ def test_piece_count_override(n):
 def test_host_workspace_covers_two_piece_slots():
     spec = stc.parse_benchmark_line("aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;")
 
-    def t(labels):
-        e = spec.tensor_extents(labels)
+    def t(labels, sp=spec):
+        e = sp.tensor_extents(labels)
         return stc.DenseTensor(e, _row_major(e), np.zeros(int(np.prod(e))))
 
     p = problem_of(spec, t(spec.labels_a), t(spec.labels_b), t(spec.labels_c), 2, Variant.ABC)
-    whole, host = ctypes.c_size_t(), ctypes.c_size_t()
+    # one piece: the I bundle cut on a into four (a:16); it runs in the dense-M ABC
+    # mode (16 tiles per term, 9 terms in flight per C tile), the whole problem ticketed
+    pspec = stc.parse_benchmark_line("aibj eafb jfie & a:16;b:64;i:64;j:64;e:64;f:64;")
+    pp = problem_of(pspec, t(pspec.labels_a, pspec), t(pspec.labels_b, pspec), t(pspec.labels_c, pspec), 2,
+                    Variant.ABC)
+    whole, host, piece = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
     L = _lib.lib()
     _lib.check(L.stc_workspace_size(ctypes.byref(p), ctypes.byref(whole)))
+    _lib.check(L.stc_workspace_size(ctypes.byref(pp), ctypes.byref(piece)))
     _lib.check(L.stc_host_workspace_size(ctypes.byref(p), ctypes.byref(host)))
-    assert host.value > 0 and host.value < 2 * whole.value  # two quarter-size piece slots + flags
+    assert piece.value > 49 * 256 * 1024 * 8  # the dense M slots of 49 terms
+    assert 2 * piece.value <= host.value <= 2 * piece.value + 4096  # two piece slots + flags

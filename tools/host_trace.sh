@@ -1,4 +1,4 @@
-for P in 1 2 4 8; do STC_HOST_TRACE=1 STC_HOST_PIECES=$P python - <<'PY'
+for P in ${PIECES:-1 2 4 8}; do STC_HOST_TRACE=1 STC_HOST_PIECES=$P python - <<'PY'
 import sys, pathlib
 sys.path.insert(0, "tools")
 import numpy as np, torch

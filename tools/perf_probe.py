@@ -15,7 +15,7 @@ sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
 import paper_1704_03092_b200 as stc  # noqa: E402
 
 CONFIGS = {
-    "cfg1": ("abij abef efij & a:24;b:24;i:24;j:24;e:24;f:24;", [(1, "abc"), (2, "abc"), (0, "abc")]),
+    "cfg1": ("abij abef efij & a:24;b:24;i:24;j:24;e:24;f:24;", [(1, "abc"), (2, "abc"), (0, "abc"), (1, "ab"), (2, "ab")]),
     "cfg2": ("aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;", [(2, "abc"), (1, "abc"), (0, "abc"), (2, "ab"),
                                                                  (2, "naive")]),
     "cfg3a": ("abij abef efij & a:16;b:16;i:16;j:16;e:64;f:64;", [(1, "abc"), (2, "abc")]),
@@ -26,7 +26,7 @@ CONFIGS = {
                                                                   (2, "naive")]),
     # cfg2 pieces of the host pipeline (I bundle cut on a into 2 / 4 / 8)
     "cfg2h": ("aibj eafb jfie & a:32;b:64;i:64;j:64;e:64;f:64;", [(2, "abc"), (1, "abc")]),
-    "cfg2q": ("aibj eafb jfie & a:16;b:64;i:64;j:64;e:64;f:64;", [(2, "abc"), (1, "abc")]),
+    "cfg2q": ("aibj eafb jfie & a:16;b:64;i:64;j:64;e:64;f:64;", [(2, "abc"), (1, "abc"), (2, "ab"), (1, "ab")]),
     "cfg2e": ("aibj eafb jfie & a:8;b:64;i:64;j:64;e:64;f:64;", [(2, "abc"), (1, "abc")]),
     "cfg2L2": ("aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;", [(2, "abc")]),
     "barL2": ("abij abef efij & a:128;b:128;i:128;j:128;e:128;f:128;", [(2, "abc")]),
