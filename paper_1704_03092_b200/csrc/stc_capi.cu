@@ -1294,6 +1294,10 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
   g.c_ready = c_ready;
   g.tiles_m = tiles_m;
   g.tiles_n = tiles_n;
+  g.rows_valid = (int32_t)pl.mq;
+  g.cols_valid = (int32_t)pl.nq;
+  // row-padding warp tiles (the last row tile at most half valid) but no column ones
+  g.warp_map = (pl.mq % BM != 0 && pl.mq % BM <= 64) && !(pl.nq % BN != 0 && pl.nq % BN <= 96);
   g.kchunks = (int)(pl.kq_pad / BK);
   g.group_m = 8;
   g.max_ops = pl.max_ops;

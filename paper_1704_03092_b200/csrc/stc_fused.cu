@@ -652,6 +652,24 @@ __device__ __forceinline__ void summer_warps(const GemmArgs &p, double *stages, 
   }
 }
 
+// A consumer warp whose 64 x 32 tile lies wholly in the quadrant's tile padding
+// (rows past p.rows_valid or columns past p.cols_valid: PAD, never stored) keeps
+// the stage protocol of consume_item but issues no loads or MMAs, so the other
+// warps of its SM sub-partition get the DMMA pipe (m or n = 64 per quadrant:
+// half of every tile is padding).
+__device__ __forceinline__ void skip_item(int S, uint64_t *full, uint64_t *empty, int &stage, uint32_t &phase,
+                                          int kchunks, int lane) {
+  for (int c = 0; c < kchunks; ++c) {
+    if (c > 0) mbar_wait(&full[stage], phase);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == S) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+}
+
 // PS: a summing warpgroup forms (some of) the operand sums in place (p.psum);
 // otherwise the consumers form them all in their fragment loads.
 template <int AKF, int BKF, bool PS>
@@ -772,7 +790,10 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
     // ===================== consumer warps: sums + DMMA + epilogue =====
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(PS ? PS_CONSUMER_REGS : FUSED_CONSUMER_REGS));
     const int g = lane >> 2, tig = lane & 3;
-    const int wm = warp & 1, wn = warp >> 1;
+    // warp -> (wm, wn): the warps of one SM sub-partition (warp % 4) differ in wn by
+    // default; with warp_map = 1 in wm, so the warps left when the wm = 1 row half of
+    // a tile is padding (skip_item) still cover all four sub-partitions
+    const int wm = p.warp_map ? warp >> 2 : warp & 1, wn = p.warp_map ? warp & 3 : warp >> 1;
     // Fragment offsets inside a view: A (kk, h) + 128 * mt; B (kk, nt & 1) + 128 * (nt >> 1).
     // MMA row (column) g + 8 h of each 16-row block (16-column pair) reads tile row
     // (column) frag_perm(kind, g, h) (stc_common.cuh): with it every half-warp of a
@@ -816,7 +837,11 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
         for (int j = 0; j < 4; ++j)
 #pragma unroll
           for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
-      if constexpr (PS) {
+      const bool pad_tile = (p.rows_valid > 0 && ti * BM + wm * 64 >= p.rows_valid) ||
+                            (p.cols_valid > 0 && tj * BN + wn * 32 >= p.cols_valid);
+      if (pad_tile) {
+        skip_item(S, cfull, empty, stage, phase, kchunks, lane);
+      } else if constexpr (PS) {
         // the A sum sits in view slot 0 and the B views from slot na on
         const int bsh = (na - 1) * VIEW_DOUBLES;
         if (p.psum & 2) {  // B summed too (slot na)

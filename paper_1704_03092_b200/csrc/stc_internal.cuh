@@ -63,6 +63,8 @@ struct GemmArgs {
   const OpDesc *ops;
   const TgtDesc *tgts;
   int32_t nterms, tiles_m, tiles_n, kchunks;
+  int32_t rows_valid, cols_valid;  // valid rows / columns per quadrant (0: all): warp tiles past them are PAD
+  int32_t warp_map;                // fused kernel: 0 wm = warp & 1 (default), 1 wm = warp >> 2 (row-PAD tiles)
   int32_t total_items;
   int32_t a_kfast, b_kfast;  // producer thread mapping per side (1: k contiguous)
   int32_t dense_out;         // 1: write M_slot densely instead of C targets

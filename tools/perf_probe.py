@@ -25,6 +25,7 @@ CONFIGS = {
     "cfg2s": ("aibj eafb jfie & a:32;b:64;i:32;j:64;e:32;f:64;", [(2, "abc"), (1, "abc"), (0, "abc"), (2, "ab"),
                                                                   (2, "naive")]),
     # cfg2 pieces of the host pipeline (I bundle cut on a into 2 / 4 / 8)
+    "cfg3l16": ("abij abef efij & a:16;b:16;i:1024;j:1024;e:64;f:64;", [(2, "abc")]),
     "cfg2h": ("aibj eafb jfie & a:32;b:64;i:64;j:64;e:64;f:64;", [(2, "abc"), (1, "abc")]),
     "cfg2q": ("aibj eafb jfie & a:16;b:64;i:64;j:64;e:64;f:64;", [(2, "abc"), (1, "abc"), (2, "ab"), (1, "ab")]),
     "cfg2e": ("aibj eafb jfie & a:8;b:64;i:64;j:64;e:64;f:64;", [(2, "abc"), (1, "abc")]),
