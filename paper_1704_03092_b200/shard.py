@@ -1,21 +1,28 @@
-"""Multi-GPU n-bundle split (north-star subsystem 5).
+"""Multi-GPU splits (north-star subsystem 5).
 
-The J bundle (columns of B and C) of a contraction is split into contiguous
-ranges of one of its labels; every rank contracts its range independently --
-A is shared, B and C are sliced -- so there is no reduction.  One process per
-GPU, torch.distributed for the plumbing; the only collective is the optional
-all-gather of the C shards (NCCL over NVLink on GPUs, gloo on CPUs).  The
-reference has no distributed path; the paper's MPI/CTF runs are the
-analogue.
+n-split: the J bundle (columns of B and C) of a contraction is split into
+contiguous ranges of one of its labels; every rank contracts its range
+independently -- A is shared, B and C are sliced -- so there is no reduction.
+2-D split (plan_grid / contract_grid): an I label and a J label are split on a
+gm x gn rank grid, so a rank holds A[I_r, :], B[:, J_c] and C[I_r, J_c] -- the
+operand replication of the n-split (all of A on every rank) drops to 1/gm of A
+and 1/gn of B; still no reduction, since every C element is owned by one rank.
+One process per GPU, torch.distributed for the plumbing; the only collective
+is the optional all-gather of the C blocks (NCCL over NVLink on GPUs, gloo on
+CPUs).  The reference has no distributed path; the
+paper's MPI/CTF runs are the analogue.
 """
 
 from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
+
 from .tensor import ContractionSpec, DenseTensor
 
-__all__ = ["Shard", "plan_shards", "shard_tensor", "shard_spec", "contract_sharded", "gather_shards"]
+__all__ = ["Shard", "plan_shards", "shard_tensor", "shard_spec", "contract_sharded", "gather_shards", "Block",
+           "plan_grid", "block_spec", "block_tensor", "contract_grid", "gather_blocks"]
 
 
 @dataclass(frozen=True)
@@ -113,3 +120,108 @@ def gather_shards(spec: ContractionSpec, c: DenseTensor, rank: int, world: int, 
     for s, blk in zip(shards, blocks):
         v = shard_tensor(c, spec.labels_c, s)
         torch.as_strided(data, v.extents, v.strides, v.base_offset).copy_(blk)
+
+
+# ---------------------------------------------------------------- 2-D split
+@dataclass(frozen=True)
+class Block:
+    """One rank's block of a gm x gn grid: a range of an I label and of a J label."""
+    row: Shard   # I-bundle label range (rows of A and C)
+    col: Shard   # J-bundle label range (columns of B and C)
+
+
+def _pick(spec: ContractionSpec, t: DenseTensor, labels: str, bundle: str, parts: int, what: str) -> str:
+    cand = [l for l in bundle if spec.extents[l] >= parts]
+    if not cand:
+        raise ValueError(f"no {what} label has extent >= {parts}")
+    stride = lambda l: abs(t.strides[labels.index(l)])
+    return max(cand, key=lambda l: (spec.extents[l] % parts == 0, stride(l)))
+
+
+def _ranges(label: str, ext: int, parts: int) -> list:
+    base, extra = divmod(ext, parts)
+    out, s = [], 0
+    for r in range(parts):
+        n = base + (1 if r < extra else 0)
+        out.append(Shard(label, s, s + n))
+        s += n
+    return out
+
+
+def plan_grid(spec: ContractionSpec, c: DenseTensor, gm: int, gn: int, row_label: str | None = None,
+              col_label: str | None = None) -> list:
+    """Blocks of a gm x gn grid, rank r -> (r // gn, r % gn): an I label cut into gm
+    contiguous ranges and a J label into gn (sizes within 1).  Default labels: the
+    largest C stride among the bundle's labels with extent >= the part count,
+    preferring divisible extents (as plan_shards)."""
+    if gm < 1 or gn < 1:
+        raise ValueError("grid dimensions must be positive")
+    if gm > 1 and not spec.bundle_i:
+        raise ValueError("the I bundle is empty: nothing to split")
+    if gn > 1 and not spec.bundle_j:
+        raise ValueError("the J bundle is empty: nothing to split")
+    if gm > 1 or row_label is not None:
+        row_label = row_label or _pick(spec, c, spec.labels_c, spec.bundle_i, gm, "I")
+        if row_label not in spec.bundle_i:
+            raise ValueError(f"label {row_label!r} is not in the I bundle {spec.bundle_i!r}")
+    if gn > 1 or col_label is not None:
+        col_label = col_label or _pick(spec, c, spec.labels_c, spec.bundle_j, gn, "J")
+        if col_label not in spec.bundle_j:
+            raise ValueError(f"label {col_label!r} is not in the J bundle {spec.bundle_j!r}")
+    rows = _ranges(row_label, spec.extents[row_label], gm) if row_label else [Shard("", 0, 0)] * gm
+    cols = _ranges(col_label, spec.extents[col_label], gn) if col_label else [Shard("", 0, 0)] * gn
+    return [Block(rows[r // gn], cols[r % gn]) for r in range(gm * gn)]
+
+
+def block_spec(spec: ContractionSpec, blk: Block) -> ContractionSpec:
+    ext = dict(spec.extents)
+    for sh in (blk.row, blk.col):
+        if sh.label:
+            ext[sh.label] = sh.stop - sh.start
+    return ContractionSpec(spec.labels_c, spec.labels_a, spec.labels_b, ext)
+
+
+def block_tensor(t: DenseTensor, labels: str, blk: Block) -> DenseTensor:
+    """View of `t` restricted to the block's label ranges it carries (same storage)."""
+    for sh in (blk.row, blk.col):
+        if sh.label:
+            t = shard_tensor(t, labels, sh)
+    return t
+
+
+def contract_grid(spec: ContractionSpec, a: DenseTensor, b: DenseTensor, c: DenseTensor, level: int, variant,
+                  rank: int, gm: int, gn: int, row_label: str | None = None, col_label: str | None = None,
+                  contract_fn=None, **kw):
+    """Contract this rank's block of C (in place): A rows, B columns and C block of
+    the rank's grid cell.  `contract_fn` as in contract_sharded; returns (block, stats)."""
+    if contract_fn is None:
+        from .strassen import contract as contract_fn
+    blk = plan_grid(spec, c, gm, gn, row_label, col_label)[rank]
+    st = contract_fn(block_spec(spec, blk), block_tensor(a, spec.labels_a, blk), block_tensor(b, spec.labels_b, blk),
+                     block_tensor(c, spec.labels_c, blk), level, variant, **kw)
+    return blk, st
+
+
+def gather_blocks(spec: ContractionSpec, c: DenseTensor, rank: int, gm: int, gn: int, row_label: str | None = None,
+                  col_label: str | None = None, group=None) -> None:
+    """All-gather every rank's C block into this rank's full C (in place)."""
+    import torch
+    import torch.distributed as dist
+
+    blocks = plan_grid(spec, c, gm, gn, row_label, col_label)
+    data = c.data if isinstance(c.data, torch.Tensor) else torch.from_numpy(c.data)
+
+    def dense(blk):
+        v = block_tensor(c, spec.labels_c, blk)
+        return torch.as_strided(data, v.extents, v.strides, v.base_offset)
+
+    mine = dense(blocks[rank]).contiguous()
+    # all_gather needs equal sizes: pad every block to the largest one
+    size = max(int(np.prod(block_tensor(c, spec.labels_c, b).extents)) for b in blocks)
+    flat = torch.zeros(size, dtype=mine.dtype, device=mine.device)
+    flat[: mine.numel()] = mine.reshape(-1)
+    bufs = [torch.empty_like(flat) for _ in blocks]
+    dist.all_gather(bufs, flat, group=group)
+    for blk, buf in zip(blocks, bufs):
+        d = dense(blk)
+        d.copy_(buf[: d.numel()].reshape(d.shape))

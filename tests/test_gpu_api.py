@@ -237,3 +237,17 @@ def test_sharded_path_on_one_gpu_matches_unsharded():
     for rank in range(4):
         shard.contract_sharded(spec, a, b, c, 2, "abc", rank, 4)
     assert stc.relative_error(c, full) < 1e-12
+
+
+def test_grid_blocks_on_one_gpu_match_unsharded():
+    """2-D split: the 2 x 2 grid's blocks run one after another on
+    this GPU; every C element is owned by one block, no reduction."""
+    spec = stc.parse_benchmark_line("abcijk abcefg efgijk & a:8;b:8;c:8;i:8;j:8;k:8;e:8;f:8;g:8;")
+    a, b, c0 = _tensors(spec, 19, device=True)
+    full = c0.copy()
+    stc.contract(spec, a, b, full, 2, "abc")
+    for gm, gn in ((2, 2), (4, 1), (1, 2)):
+        c = c0.copy()
+        for rank in range(gm * gn):
+            shard.contract_grid(spec, a, b, c, 2, "abc", rank, gm, gn)
+        assert stc.relative_error(c, full) < 1e-12, (gm, gn)

@@ -89,3 +89,60 @@ def test_shard_views_address_the_right_elements():
         assert stc.element_at(cv, idx) == stc.element_at(c, full)
     bv = shard.shard_tensor(b, spec.labels_b, sh)  # B = [j, f, i, e]
     assert stc.element_at(bv, (0, 1, 2, 1)) == stc.element_at(b, (2, 1, 2, 1))
+
+
+def _grid_worker(rank, world, port, line, gm, gn, ret):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    spec = stc.parse_benchmark_line(line)
+    a, b, c = _operands(spec)
+    shard.contract_grid(spec, a, b, c, 2, "abc", rank, gm, gn, contract_fn=_oracle_classical)
+    shard.gather_blocks(spec, c, rank, gm, gn)
+    ret[rank] = c.data.copy()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("gm,gn", [(2, 1), (1, 2), (2, 2)])
+def test_grid_split_gloo(gm, gn):
+    # the 2-D split over gloo: each rank its (I range, J range) block with the oracle
+    # standing in for the device kernel, then the blocks all-gathered (unequal block
+    # sizes: extents 5 and 3 split in two)
+    line = "abij abef efij & a:5;b:2;i:3;j:4;e:3;f:2;"
+    world = gm * gn
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_grid_worker, args=(world, _free_port(), line, gm, gn, ret), nprocs=world, join=True)
+    spec = stc.parse_benchmark_line(line)
+    a, b, c = _operands(spec)
+    oracle.contract_reference(spec, a, b, c)
+    for r in range(world):
+        assert np.array_equal(ret[r], c.data), r
+
+
+def test_plan_grid_tiles_c_exactly():
+    spec = stc.parse_benchmark_line("abcijk abcefg efgijk & a:3;b:2;c:5;i:5;j:3;k:4;e:2;f:2;g:2;")
+    _, _, c = _operands(spec)
+    for gm, gn in ((1, 1), (2, 1), (1, 3), (3, 2), (2, 4)):
+        blocks = shard.plan_grid(spec, c, gm, gn)
+        assert len(blocks) == gm * gn
+        seen = np.zeros(c.extents, dtype=int)
+        for blk in blocks:
+            v = shard.block_tensor(c, spec.labels_c, blk)
+            idx = [slice(None)] * len(c.extents)
+            for sh in (blk.row, blk.col):
+                if sh.label:
+                    idx[spec.labels_c.index(sh.label)] = slice(sh.start, sh.stop)
+            seen[tuple(idx)] += 1
+            assert v.extents == seen[tuple(idx)].shape
+        assert (seen == 1).all(), (gm, gn)
+        if gm > 1:
+            assert blocks[0].row.label in spec.bundle_i
+        if gn > 1:
+            assert blocks[0].col.label in spec.bundle_j
+    with pytest.raises(ValueError, match="I bundle"):
+        shard.plan_grid(spec, c, 2, 1, row_label="i")
+    with pytest.raises(ValueError, match="extent"):
+        shard.plan_grid(spec, c, 7, 1)
