@@ -640,7 +640,9 @@ __device__ __forceinline__ void summer_warps(const GemmArgs &p, double *stages, 
       if (do_a) sum_side(st, 0, na, negmask, t);
       if (do_b) sum_side(st, na, nb, negmask, t);
       // generic writes before the async proxy (TMA) refills this stage
+#ifndef STC_EXPERIMENT_NOPROXYFENCE
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&summed[rs]);

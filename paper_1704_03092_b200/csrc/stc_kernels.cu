@@ -270,33 +270,38 @@ cudaError_t launch_unpack(const UnpackArgs &a, cudaStream_t s) {
 // view of x-quadrant (xfirst ? qa : qb) and k-quadrant (the other) copied into a
 // dense [k][x] (kfast = 0) or [x][k] (kfast = 1) block, PAD -> 0.  A pure copy:
 // the Strassen sums stay in the fused kernel, in the reference's view order.
-__global__ void k_pack_views(const double *__restrict__ D, const int64_t *__restrict__ pool, PackArgs a,
-                             double *__restrict__ out) {
-  const int qa = blockIdx.y / a.Q, qb = blockIdx.y - qa * a.Q;
+constexpr int UNPACK_ROWS = 4;  // k_pack_views: rows of the slow dimension per block
+
+__global__ void __launch_bounds__(256) k_pack_views(const double *__restrict__ D, const int64_t *__restrict__ pool,
+                                                    PackArgs a, double *__restrict__ out) {
+  // block: 256 positions along the packed block's contiguous dimension x
+  // UNPACK_ROWS of the other (as k_unpack); blockIdx.z = quadrant pair
+  const int qa = blockIdx.z / a.Q, qb = blockIdx.z - qa * a.Q;
   const int xq = a.xfirst ? qa : qb, kq = a.xfirst ? qb : qa;
   const int64_t *xv = pool + a.xv + (int64_t)xq * a.xlen;
   const int64_t *kv = pool + a.kv + (int64_t)kq * a.klen;
-  double *o = out + (int64_t)blockIdx.y * a.xlen * a.klen;
-  const int64_t total = a.xlen * a.klen;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t x, k;
-    if (a.kfast) {
-      x = e / a.klen;
-      k = e - x * a.klen;
-    } else {
-      k = e / a.xlen;
-      x = e - k * a.xlen;
-    }
-    const int64_t xo = __ldg(xv + x), ko = __ldg(kv + k);
-    o[e] = (xo == kPad || ko == kPad) ? 0.0 : __ldg(D + xo + ko);
+  double *o = out + (int64_t)blockIdx.z * a.xlen * a.klen;
+  const int64_t fast_len = a.kfast ? a.klen : a.xlen, slow_len = a.kfast ? a.xlen : a.klen;
+  const int64_t *fv = a.kfast ? kv : xv, *sv = a.kfast ? xv : kv;
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= fast_len) return;
+  const int64_t fo = __ldg(fv + f);
+  const int64_t s0 = (int64_t)blockIdx.y * UNPACK_ROWS;
+#pragma unroll 4
+  for (int r = 0; r < UNPACK_ROWS; ++r) {
+    const int64_t sl = s0 + r;
+    if (sl >= slow_len) break;
+    const int64_t so = __ldg(sv + sl);
+    o[sl * fast_len + f] = (fo == kPad || so == kPad) ? 0.0 : __ldg(D + fo + so);
   }
 }
 
 cudaError_t launch_pack_views(const double *D, const int64_t *pool, const PackArgs &a, double *out, cudaStream_t s) {
-  const int64_t total = a.xlen * a.klen;
-  if (total <= 0) return cudaSuccess;
-  const int bx = (int)std::min<int64_t>((total + 255) / 256, 1184 / std::max(1, a.Q * a.Q) + 1);
-  dim3 grid(std::max(bx, 4), a.Q * a.Q);
+  const int64_t fast_len = a.kfast ? a.klen : a.xlen, slow_len = a.kfast ? a.xlen : a.klen;
+  if (fast_len <= 0 || slow_len <= 0) return cudaSuccess;
+  const int64_t gy = (slow_len + UNPACK_ROWS - 1) / UNPACK_ROWS;
+  if (gy > 65535 || a.Q * a.Q > 65535) return cudaErrorInvalidConfiguration;
+  dim3 grid((unsigned)((fast_len + 255) / 256), (unsigned)gy, (unsigned)(a.Q * a.Q));
   k_pack_views<<<grid, 256, 0, s>>>(D, pool, a, out);
   return cudaGetLastError();
 }
