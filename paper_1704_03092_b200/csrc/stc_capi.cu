@@ -380,6 +380,10 @@ struct FusedSides {
   int64_t qxa = 0, qk = 0, qxb = 0;          // quadrant (or slot) lengths of the A-x, k and B-x bundles
 };
 
+struct TmaSide;
+bool plan_cred_side(const stc_bundle &rb, const Tiling &tr, const stc_bundle &cb, const Tiling &tc, int level,
+                    const double *data, int64_t base, TmaSide &ts);
+bool c_boxes_regular(const stc_problem *p, const Tiling &ti, const Tiling &tj, int level);
 FusedSides direct_sides(const stc_problem *p, const Plan &pl);
 FusedSides packed_sides(const Plan &pl);
 FusedSides naive_sides(const Plan &pl);
@@ -471,8 +475,11 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     // ticket chains then serialise (cfg2 pieces of m = 1024: 9 terms in flight,
     // 1.56 ms ticketed vs 1.21 ms dense; 576^3 L2: 0.60 vs 0.15 ms).
     // STC_ABC_DENSE = 0 / 1 forces either.
+    // Also when the C targets are not regular boxes: the kernel's C updates would then
+    // be load/add/store scatters in the consumers (cfg4 L2: 5.2 ms ticketed, 3.2 dense).
     const char *de = getenv("STC_ABC_DENSE");
-    const bool dense = T > 1 && (de ? atoi(de) != 0 : pl.grid >= 4 * P);
+    const bool dense = T > 1 && (de ? atoi(de) != 0
+                                    : (pl.grid >= 4 * P || !c_boxes_regular(p, pl.ti, pl.tj, pl.level)));
     pl.ticketed = !dense;
   }
   if (pl.ticketed) {
@@ -914,6 +921,13 @@ bool plan_cred_side(const stc_bundle &rb, const Tiling &tr, const stc_bundle &cb
   for (int d = ts.rank; d < 5; ++d) ts.src[d] = 0;
   ts.swizzle = 128;
   return true;
+}
+
+// C quadrant tiles are boxes the TMA-reduce epilogue can address (alignment of
+// the actual pointer aside): the fused kernel's ABC C updates stay off the SMs.
+bool c_boxes_regular(const stc_problem *p, const Tiling &ti, const Tiling &tj, int level) {
+  TmaSide sc;
+  return plan_cred_side(p->c_row, ti, p->c_col, tj, level, nullptr, p->c_base, sc);
 }
 
 FusedSides direct_sides(const stc_problem *p, const Plan &pl) {
