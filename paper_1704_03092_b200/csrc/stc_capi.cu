@@ -30,6 +30,7 @@ namespace {
 thread_local std::string g_err;
 thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;  // stc_set_kernel_events
 thread_local const int32_t *g_c_ready = nullptr;                        // stc_set_c_ready
+thread_local const stc::PieceGate *g_gate = nullptr;                     // stc::set_piece_gate
 
 int fail(int code, const char *fmt, ...) {
   char buf[512];
@@ -1201,6 +1202,87 @@ bool plan_ticketed(const stc_problem *p) {
   if (cached_plan(p, pl, sms > 0 ? sms : 0)) return false;
   return pl.ticketed;
 }
+
+void set_piece_gate(const PieceGate *g) { g_gate = g; }
+
+// Label `lab` index of entry o of an I/J pool vector (mode 0, as k_build_pool
+// decodes it: tile order -> quadrant-local reference index -> labels), -1 for PAD.
+static int64_t vec_label_index(const VecDesc &d, int64_t o, int lab) {
+  const int64_t q = o / d.q_len_pad, ip = o - q * d.q_len_pad;
+  if (ip >= d.q_len) return -1;
+  int64_t i = ip;
+  if (d.nbox > 0) {
+    int64_t digit[STC_MAX_LABELS], rem = ip;
+    for (int j = 0; j < d.nbox; ++j) {
+      const int dim = d.order[j];
+      digit[dim] = rem % d.box_ext[dim];
+      rem /= d.box_ext[dim];
+    }
+    i = 0;
+    int64_t mult = 1;
+    for (int dim = 0; dim < d.nbox; ++dim) {
+      i += digit[dim] * mult;
+      mult *= d.box_ext[dim];
+    }
+  }
+  const int64_t l = q * d.q_len + i;
+  if (l >= d.len) return -1;
+  int64_t rem = l;
+  for (int j = 0; j < lab; ++j) rem /= d.ext[j];
+  return rem % d.ext[lab];
+}
+
+// Gated host pieces (stc_host.cu): can the I-bundle split of label `lab` into S
+// equal ranges run as ONE ticketed fused launch whose items are ordered by piece?
+// Needs the direct (non-repacked) fused kernel and every tile row of every
+// quadrant inside one piece, the pieces in tile-row order.  Fills lo[0..S] (tile
+// rows) and items[s] (work items of piece s).
+bool plan_gate(const stc_problem *p, int lab, int S, int32_t *lo, int64_t *items) {
+  if (S < 2 || S > kMaxGatedPieces || p->variant != STC_VARIANT_ABC || lab < 0 || lab >= p->c_row.nlab) return false;
+  Plan pl;
+  const int sms = gemm_max_grid(MAX_OPS);
+  if (cached_plan(p, pl, sms > 0 ? sms : 0) || !pl.ticketed) return false;
+  if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
+  {
+    GemmArgs g{};
+    CUtensorMap maps[3];
+    CoordJobs jobs{};
+    if (!plan_fused(p, pl, direct_sides(p, pl), nullptr, nullptr, nullptr, g, maps, jobs)) return false;
+  }
+  const int64_t ext = p->c_row.ext[lab];
+  if (ext % S) return false;
+  const int64_t plen = ext / S;
+  const VecDesc d = vec_bundle(p->c_row, 0, pl.Q, BM, pl.ti);
+  const int tiles_m = (int)(pl.mq_pad / BM), tiles_n = (int)(pl.nq_pad / BN);
+  std::vector<int> piece(tiles_m, -1);
+  for (int64_t q = 0; q < pl.Q; ++q)
+    for (int ti = 0; ti < tiles_m; ++ti)
+      for (int r = 0; r < BM; ++r) {
+        const int64_t idx = vec_label_index(d, q * d.q_len_pad + (int64_t)ti * BM + r, lab);
+        if (idx < 0) continue;
+        const int sp = (int)(idx / plen);
+        if (piece[ti] < 0) piece[ti] = sp;
+        else if (piece[ti] != sp) return false;  // a tile row straddles two pieces
+      }
+  int prev = 0;
+  for (int ti = 0; ti < tiles_m; ++ti) {
+    if (piece[ti] < 0) piece[ti] = prev;  // all-padding rows ride with the previous piece
+    if (piece[ti] < prev) return false;    // pieces out of tile-row order
+    prev = piece[ti];
+  }
+  const int T = (int)pl.terms.size();
+  for (int sp = 0; sp <= S; ++sp) lo[sp] = tiles_m;
+  for (int ti = tiles_m - 1; ti >= 0; --ti) lo[piece[ti]] = ti;
+  for (int sp = S - 1; sp >= 0; --sp) {
+    if (lo[sp] > lo[sp + 1]) lo[sp] = lo[sp + 1];
+    items[sp] = 0;
+  }
+  for (int sp = 0; sp < S; ++sp) {
+    if (lo[sp + 1] <= lo[sp]) return false;  // every piece owns tile rows
+    items[sp] = (int64_t)T * (lo[sp + 1] - lo[sp]) * tiles_n;
+  }
+  return lo[0] == 0;
+}
 }  // namespace stc
 
 // ======================================================================== ABI
@@ -1303,6 +1385,10 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
 
   const int32_t *c_ready = g_c_ready;  // consumed by this call
   g_c_ready = nullptr;
+  const PieceGate *gate = g_gate;
+  g_gate = nullptr;
+  if (gate && (!pl.ticketed || gate->n > kMaxGatedPieces))
+    return fail(STC_EINVAL, "internal: gated pieces need the ticketed ABC plan");
   GemmArgs g{};
   g.pool = pool;
   g.c_ready = c_ready;
@@ -1349,6 +1435,14 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
     GemmArgs gf = g;
     const int fz = prepare_fused(gf, maps, C);
     if (fz < 0) return -fz;
+    if (gate && (!fz || packed)) return fail(STC_EINVAL, "internal: gated pieces need the direct fused kernel");
+    if (gate) {
+      gf.npieces = gate->n;
+      for (int i = 0; i <= gate->n; ++i) gf.piece_lo[i] = gate->lo[i];
+      gf.piece_ready = gate->ready;
+      gf.piece_done = gate->done;
+      gf.c_ready = nullptr;
+    }
     if (fz) {
       // fused kernel: TMA boxes of 128 x 8, sums in the consumers' fragment loads
       tma = !packed;

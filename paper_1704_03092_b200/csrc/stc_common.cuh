@@ -13,18 +13,53 @@
 
 namespace stc {
 
-__device__ __forceinline__ void tile_of(const GemmArgs &p, int item, int &slot, int &ti, int &tj) {
-  const int P = p.tiles_m * p.tiles_n;
+// Work item -> (term slot, tile row ti, tile column tj, tile id pos).  pos numbers
+// the quadrant's tiles the same way for every term (per-tile tickets).
+__device__ __forceinline__ void tile_of(const GemmArgs &p, int item, int &slot, int &ti, int &tj, int &pos,
+                                        int &piece) {
+  int r0 = 0, rows = p.tiles_m;
+  piece = 0;
+  if (p.npieces > 1) {  // piece-major: every piece is (terms) x (its tile rows) x (all tile columns)
+    for (;;) {
+      rows = p.piece_lo[piece + 1] - p.piece_lo[piece];
+      const int n = p.nterms * rows * p.tiles_n;
+      if (item < n || piece + 1 == p.npieces) break;
+      item -= n;
+      ++piece;
+    }
+    r0 = p.piece_lo[piece];
+  }
+  const int P = rows * p.tiles_n;
   slot = item / P;
-  const int pos = item - slot * P;
+  const int local = item - slot * P;
   // grouped rasterisation: group_m tile-rows share the B panels in L2
-  const int per_group = p.group_m * p.tiles_n;
-  const int g = pos / per_group;
-  const int first = g * p.group_m;
-  const int gsz = min(p.tiles_m - first, p.group_m);
-  const int r = pos - g * per_group;
-  ti = first + r % gsz;
+  const int gm = min(p.group_m, rows);
+  const int per_group = gm * p.tiles_n;
+  const int g = local / per_group;
+  const int first = g * gm;
+  const int gsz = min(rows - first, gm);
+  const int r = local - g * per_group;
+  ti = r0 + first + r % gsz;
   tj = r / gsz;
+  pos = ti * p.tiles_n + tj;
+}
+__device__ __forceinline__ void tile_of(const GemmArgs &p, int item, int &slot, int &ti, int &tj) {
+  int pos, piece;
+  tile_of(p, item, slot, ti, tj, pos, piece);
+}
+
+// Gated pieces: wait until piece s's operands and C rows are in HBM (thread 0 of
+// the caller polls), then order the TMA (async proxy) accesses after it.
+__device__ __forceinline__ void wait_piece(const GemmArgs &p, int piece) {
+  if (!p.piece_ready) return;
+  while (ld_acquire_gpu(p.piece_ready + piece) == 0) __nanosleep(256);
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// Gated pieces: one more finished item of piece s (after all its C updates).
+__device__ __forceinline__ void piece_item_done(const GemmArgs &p, int piece) {
+  if (!p.piece_done) return;
+  __threadfence();
+  atomicAdd(p.piece_done + piece, 1);
 }
 
 // stc_set_c_ready: block until C has arrived (thread 0 polls, the consumer
@@ -63,8 +98,8 @@ __device__ __forceinline__ int epi_col(int nt, int tig) {  // first of the pair 
 template <int PA = 0, int PB = 0, int RB = 1>
 __device__ __forceinline__ void epilogue_store(const GemmArgs &p, const double (&acc)[4][4][4], int item, int tid,
                                                int wm, int wn, int g, int tig) {
-  int slot, ti, tj;
-  tile_of(p, item, slot, ti, tj);
+  int slot, ti, tj, pos, piece;
+  tile_of(p, item, slot, ti, tj, pos, piece);
   const TermDesc td = p.terms[slot];
   const int row0 = ti * BM + wm * 64;
   const int col0 = tj * BN + wn * 32;
@@ -82,7 +117,10 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs &p, const double (
         }
     return;
   }
-  const int pos = item - slot * p.tiles_m * p.tiles_n;
+  if (p.piece_ready) {  // gated pieces: C rows of this piece uploaded
+    if (tid == 0) wait_piece(p, piece);
+    named_bar(2, 32 * CONSUMER_WARPS);
+  }
   for (int j = 0; j < td.c_count; ++j) {
     const TgtDesc tg = p.tgts[td.c_first + j];
     int32_t *ticket = p.tickets + tg.ticket_base + pos;
@@ -126,6 +164,11 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs &p, const double (
       named_bar(2, 32 * CONSUMER_WARPS);
       if (tid == 0) st_release_gpu(ticket, tg.order + 1);
     }
+  }
+  if (p.piece_done) {
+    __threadfence();
+    named_bar(2, 32 * CONSUMER_WARPS);
+    if (tid == 0) piece_item_done(p, piece);
   }
 }
 

@@ -349,10 +349,13 @@ __device__ __forceinline__ void tma_reduce_add(const CUtensorMap *map, int rank,
 template <int PA, int PB>
 __device__ __forceinline__ void epilogue_red(const GemmArgs &p, const double (&acc)[4][4][4], int item, int tid, int wm,
                                              int wn, int g, int tig, double *buf, const CUtensorMap *tmC) {
-  int slot, ti, tj;
-  tile_of(p, item, slot, ti, tj);
+  int slot, ti, tj, pos, piece;
+  tile_of(p, item, slot, ti, tj, pos, piece);
   const TermDesc td = p.terms[slot];
-  const int pos = item - slot * p.tiles_m * p.tiles_n;
+  if (p.piece_ready) {  // gated pieces: C rows of this piece uploaded
+    if (tid == 0) wait_piece(p, piece);
+    named_bar(2, 32 * CONSUMER_WARPS);
+  }
   int nb = 0;  // piece buffer
   for (int j = 0; j < td.c_count; ++j) {
     const TgtDesc tg = p.tgts[td.c_first + j];
@@ -403,6 +406,10 @@ __device__ __forceinline__ void epilogue_red(const GemmArgs &p, const double (&a
       }
     }
   }
+  if (tid == 0 && p.piece_done) {
+    asm volatile("cp.async.bulk.wait_group 0;\nfence.proxy.async.global;" ::: "memory");
+    piece_item_done(p, piece);
+  }
 }
 
 // Epilogue warps (the producer warpgroup's three other warps; ABC, opt-in with
@@ -426,10 +433,13 @@ __device__ __forceinline__ void epilogue_warps(const GemmArgs &p, uint64_t *epi_
       named_bar(3, EPI_THREADS);
       c_seen = true;
     }
-    int slot, ti, tj;
-    tile_of(p, item, slot, ti, tj);
+    int slot, ti, tj, pos, piece;
+    tile_of(p, item, slot, ti, tj, pos, piece);
     const TermDesc td = p.terms[slot];
-    const int pos = item - slot * p.tiles_m * p.tiles_n;
+    if (p.piece_ready) {  // gated pieces: C rows of this piece uploaded
+      if (t == 0) wait_piece(p, piece);
+      named_bar(3, EPI_THREADS);
+    }
     const double *Mt = p.mscratch + ((size_t)blockIdx.x * EPI_BUFS + eb) * TILE_DOUBLES;
     for (int j = 0; j < td.c_count; ++j) {
       const TgtDesc tg = p.tgts[td.c_first + j];
@@ -474,6 +484,7 @@ __device__ __forceinline__ void epilogue_warps(const GemmArgs &p, uint64_t *epi_
       }
       named_bar(3, EPI_THREADS);  // offset tables reused by the next target
     }
+    if (t == 0) piece_item_done(p, piece);
     __syncwarp();
     if (lane == 0) mbar_arrive(&epi_empty[eb]);
     if (++eb == EPI_BUFS) {
@@ -504,10 +515,10 @@ __device__ __forceinline__ void epilogue_warps_red(const GemmArgs &p, uint64_t *
         while (ld_acquire_gpu(p.c_ready) == 0) __nanosleep(256);
       c_seen = true;
     }
-    int slot, ti, tj;
-    tile_of(p, item, slot, ti, tj);
+    int slot, ti, tj, pos, piece;
+    tile_of(p, item, slot, ti, tj, pos, piece);
     const TermDesc td = p.terms[slot];
-    const int pos = item - slot * p.tiles_m * p.tiles_n;
+    if (t == 0 && p.piece_ready) wait_piece(p, piece);  // gated pieces: C rows uploaded
     const double *Mt = p.mscratch + ((size_t)blockIdx.x * EPI_BUFS + eb) * TILE_DOUBLES;
     int nb = 0;
     for (int j = 0; j < td.c_count; ++j) {
@@ -551,6 +562,10 @@ __device__ __forceinline__ void epilogue_warps_red(const GemmArgs &p, uint64_t *
           st_release_gpu(p.tickets + tg.ticket_base + pos, tg.order + 1);
         }
       }
+    }
+    if (t == 0 && p.piece_done) {
+      asm volatile("cp.async.bulk.wait_group 0;\nfence.proxy.async.global;" ::: "memory");
+      piece_item_done(p, piece);
     }
     named_bar(3, EPI_THREADS);  // every warp is done with this M buffer
     if (lane == 0) mbar_arrive(&epi_empty[eb]);
@@ -726,6 +741,7 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
     }
     int stage = 0;
     uint32_t phase = 0;
+    int ready_piece = -1;
     for (;;) {
       int item = 0;
       if (lane == 0) item = atomicAdd(p.counter, 1);
@@ -738,8 +754,13 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
         }
         break;
       }
-      int slot, ti, tj;
-      tile_of(p, item, slot, ti, tj);
+      int slot, ti, tj, pos, piece;
+      tile_of(p, item, slot, ti, tj, pos, piece);
+      if (p.piece_ready && piece != ready_piece) {  // gated pieces: operands of this piece in HBM
+        if (lane == 0) wait_piece(p, piece);
+        __syncwarp();
+        ready_piece = piece;
+      }
       const TermDesc td = p.terms[slot];
       const int na = td.a_count, U = td.a_count + td.b_count;
       // lane u < U stages view u (A views first, then B views) of every chunk

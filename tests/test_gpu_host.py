@@ -177,3 +177,38 @@ def test_host_pipeline_errors_leave_c_untouched():
                              ctypes.c_void_p(ws.data_ptr()), 256, None, None)
     assert rc == _lib.STC_EWORKSPACE
     assert np.array_equal(c.data, c0.data)
+
+
+def _pinned(t):
+    import torch
+
+    return stc.DenseTensor(t.extents, t.strides, torch.from_numpy(t.data).pin_memory(), t.base_offset)
+
+
+@pytest.mark.parametrize("pieces", ["2", "4"])
+def test_host_pipeline_gated_single_launch_bitwise_equals_device_path(pieces):
+    # STC_HOST_GATED=1, page-locked operands, I split: the pieces run as ONE ticketed launch over the whole
+    # problem (items gated per piece on copy-engine-written flags, downloads behind
+    # device-side item counters), so C equals the device-operand path bitwise
+    import torch
+
+    spec = stc.parse_benchmark_line("aibj eafb jfie & a:32;b:64;i:32;j:64;e:32;f:32;")
+    a, b, c0 = (_tensor(spec, l, s, False) for l, s in ((spec.labels_a, 7), (spec.labels_b, 8), (spec.labels_c, 9)))
+    dev = stc.DenseTensor(c0.extents, c0.strides, torch.from_numpy(c0.data.copy()).cuda(), 0)
+    stc.contract(spec, a.to_device(), b.to_device(), dev, 2, "abc")
+    want = dev.data.cpu().numpy()
+    ha, hb, hc = _pinned(a), _pinned(b), _pinned(c0.copy())
+    env = {"STC_HOST_PIECES": pieces, "STC_ABC_DENSE": "0", "STC_HOST_GATED": "1"}  # the gate needs the ticketed plan
+    st = _with_env(env, lambda: stc.contract(spec, ha, hb, hc, 2, "abc"))
+    assert st.kernel_launches < 10, st  # one contraction, not one per piece
+    assert np.array_equal(hc.data.numpy(), want), pieces
+    # the per-piece contractions (STC_HOST_GATED=0) agree in norm
+    hc2 = _pinned(c0.copy())
+    _with_env({**env, "STC_HOST_GATED": "0"}, lambda: stc.contract(spec, ha, hb, hc2, 2, "abc"))  # per piece
+    assert np.linalg.norm(hc2.data.numpy() - want) / np.linalg.norm(want) <= TOL
+    # repeated calls reuse the flags and counters (zeroed per call)
+    hc3 = _pinned(c0.copy())
+    for _ in range(2):
+        hc3 = _pinned(c0.copy())
+        _with_env(env, lambda: stc.contract(spec, ha, hb, hc3, 2, "abc"))
+    assert np.array_equal(hc3.data.numpy(), want)
