@@ -316,6 +316,8 @@ struct Plan {
   int max_ops = 1;  // most views on one side of any term (2^L)
   size_t off_kbs = 0, off_coords = 0, off_mscr = 0, off_pka = 0, off_pkb = 0;
   bool need_pack = false;  // fused kernel on repacked operands (layout not box-regular)
+  int tshape = 0;          // fused kernel CTA tile shape (stc_fused.cu Shape): 0 128 x 128, 1 64 x 256, 2 256 x 64
+  int64_t tm = BM, tn = BN;  // its tile rows / columns (quadrants padded to them)
   // ABC with C updated straight from the kernel, ticket-ordered per C tile; false for AB,
   // Naive and the dense-M ABC mode (many terms in flight per tile: dense M slots, then one
   // ordered accumulate pass -- the same additions in the same order, without ticket chains)
@@ -415,8 +417,27 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   pl.mq = cdiv(pl.m, pl.Q);
   pl.nq = cdiv(pl.n, pl.Q);
   pl.kq = cdiv(pl.k, pl.Q);
-  pl.mq_pad = rup(pl.mq, BM);
-  pl.nq_pad = rup(pl.nq, BN);
+  // CTA tile shape: 64 x 256 (256 x 64) when the I (J) quadrants are at most 64 past a
+  // multiple of 128 -- a 128-row tile would be half padding -- for the dense-M launches
+  // with the summing warpgroup (AB, ABC with such C tiles, L >= 1); see shape_usable
+  pl.tshape = 0;
+  {
+    const char *ts = getenv("STC_TSHAPE");
+    // (A / B base offsets even: TMA needs 16-byte aligned views of the 256-byte aligned
+    // allocations; the shaped plan has no gather-kernel fallback)
+    const bool allowed = (!ts || atoi(ts) != 0) && pl.level >= 1 && pl.variant != STC_VARIANT_NAIVE &&
+                         p->a_base % 2 == 0 && p->b_base % 2 == 0 &&
+                         !(p->flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) &&
+                         !(getenv("STC_FUSED") && atoi(getenv("STC_FUSED")) == 0) &&
+                         !(getenv("STC_PRESUM") && atoi(getenv("STC_PRESUM")) != 1) &&
+                         !(pl.variant == STC_VARIANT_ABC && getenv("STC_ABC_DENSE") && atoi(getenv("STC_ABC_DENSE")) == 0);
+    if (allowed && pl.mq % BM != 0 && pl.mq % BM <= 64 && pl.nq >= 256) pl.tshape = 1;
+    else if (allowed && pl.nq % BN != 0 && pl.nq % BN <= 64 && pl.mq >= 256) pl.tshape = 2;
+  }
+  pl.tm = pl.tshape == 1 ? 64 : pl.tshape == 2 ? 256 : BM;
+  pl.tn = pl.tshape == 1 ? 256 : pl.tshape == 2 ? 64 : BN;
+  pl.mq_pad = rup(pl.mq, pl.tm);
+  pl.nq_pad = rup(pl.nq, pl.tn);
   pl.kq_pad = rup(pl.kq, BK);
 
   // tile orders per bundle (see make_tiling)
@@ -435,6 +456,18 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   pl.tp = tp;
   pl.a_kfast = a_min == 1;
   pl.b_kfast = b_min == 0;
+  if (pl.tshape != 0) {  // the direct fused layout must cut the new tiles as boxes
+    GemmArgs gd{};
+    CUtensorMap md[3];
+    CoordJobs jd{};
+    if (!plan_fused(p, pl, direct_sides(p, pl), nullptr, nullptr, nullptr, gd, md, jd)) {
+      pl.tshape = 0;
+      pl.tm = BM;
+      pl.tn = BN;
+      pl.mq_pad = rup(pl.mq, BM);
+      pl.nq_pad = rup(pl.nq, BN);
+    }
+  }
 
   // pool vectors (subsystem 1)
   auto add = [&](VecDesc d) {
@@ -443,12 +476,12 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     pl.vecs.push_back(d);
     return d.out_start;
   };
-  pl.ar = add(vec_bundle(p->a_row, 0, pl.Q, BM, ti));
+  pl.ar = add(vec_bundle(p->a_row, 0, pl.Q, pl.tm, ti));
   pl.ac = add(vec_bundle(p->a_col, p->a_base, pl.Q, BK, tp));
   pl.br = add(vec_bundle(p->b_row, 0, pl.Q, BK, tp));
-  pl.bc = add(vec_bundle(p->b_col, p->b_base, pl.Q, BN, tj));
-  pl.cr = add(vec_bundle(p->c_row, 0, pl.Q, BM, ti));
-  pl.cc = add(vec_bundle(p->c_col, p->c_base, pl.Q, BN, tj));
+  pl.bc = add(vec_bundle(p->b_col, p->b_base, pl.Q, pl.tn, tj));
+  pl.cr = add(vec_bundle(p->c_row, 0, pl.Q, pl.tm, ti));
+  pl.cc = add(vec_bundle(p->c_col, p->c_base, pl.Q, pl.tn, tj));
   if (pl.variant == STC_VARIANT_NAIVE) {
     // packed operand sums: Apack[k][x] (ld mq_pad), Bpack[k][x] (ld nq_pad)
     // packed operand sums per term slot, oriented like the source (unit stride in k ->
@@ -461,7 +494,7 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   pl.terms = strassen_terms(pl.level);
   for (const Term &t : pl.terms) pl.max_ops = std::max(pl.max_ops, (int)std::max(t.a.size(), t.b.size()));
   const int T = (int)pl.terms.size();
-  const int64_t P = (pl.mq_pad / BM) * (pl.nq_pad / BN);
+  const int64_t P = (pl.mq_pad / pl.tm) * (pl.nq_pad / pl.tn);
   if (P * (int64_t)T > INT32_MAX) return fail(STC_EINVAL, "problem too large: %lld work items", (long long)(P * T));
   pl.grid = grid_hint > 0 ? grid_hint : 148;
 
@@ -796,12 +829,12 @@ bool plan_tma(const stc_problem *p, const Plan &pl, const double *A, const doubl
 constexpr int kFusedK = 8;
 
 bool plan_fused_side(const stc_bundle &xb, const Tiling &tx, const stc_bundle &kb, const Tiling &tk, int64_t qx,
-                     int64_t qk, int kfast, const double *data, int64_t base, TmaSide &ts) {
+                     int64_t qk, int kfast, const double *data, int64_t base, TmaSide &ts, int64_t tile) {
   if (tx.nbox == 0 || tk.nbox == 0) return false;
-  if (qx % BM != 0 || qk % BK != 0) return false;  // quadrants cut into whole tiles / chunks
+  if (qx % tile != 0 || qk % BK != 0) return false;  // quadrants cut into whole tiles / chunks
   int64_t tbx[STC_MAX_LABELS], tbk[STC_MAX_LABELS];
   int ox[STC_MAX_LABELS], ok_[STC_MAX_LABELS], nox = 0, nok = 0;
-  if (!tile_subbox(xb, tx, BM, tbx, ox, nox) || !tile_subbox(kb, tk, kFusedK, tbk, ok_, nok)) return false;
+  if (!tile_subbox(xb, tx, tile, tbx, ox, nox) || !tile_subbox(kb, tk, kFusedK, tbk, ok_, nok)) return false;
   struct Dim {
     int64_t ext, str, box;
     bool isx;
@@ -1066,11 +1099,12 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
     if (atoi(e) == 0) return false;
   if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
   const int umax = pl.variant == STC_VARIANT_NAIVE ? 2 : 2 * pl.max_ops;  // Naive: one packed view per side
-  const int S = fused_stages(umax);
+  const size_t sd = fused_stage_doubles(umax / 2, pl.tshape);
+  const int S = fused_stages(sd);
   if (umax > 8 || S < 2) return false;
   TmaSide sa, sb;
-  if (!plan_fused_side(fs.ax, fs.tax, fs.ak, fs.tak, fs.qxa, fs.qk, fs.akf, A, fs.a_base, sa)) return false;
-  if (!plan_fused_side(fs.bx, fs.tbx, fs.bk, fs.tbk, fs.qxb, fs.qk, fs.bkf, B, fs.b_base, sb)) return false;
+  if (!plan_fused_side(fs.ax, fs.tax, fs.ak, fs.tak, fs.qxa, fs.qk, fs.akf, A, fs.a_base, sa, pl.tm)) return false;
+  if (!plan_fused_side(fs.bx, fs.tbx, fs.bk, fs.tbk, fs.qxb, fs.qk, fs.bkf, B, fs.b_base, sb, pl.tn)) return false;
   if (!A || !B) return true;
   if (!encode_side(sa, A, fs.a_base, maps[0]) || !encode_side(sb, B, fs.b_base, maps[1])) return false;
   const TmaSide *ss[2] = {&sa, &sb};
@@ -1099,7 +1133,7 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
   g.cred = 0;
   TmaSide sc;
   if (pl.variant == STC_VARIANT_ABC && C && !(getenv("STC_CRED") && atoi(getenv("STC_CRED")) == 0) &&
-      fused_stages_red(umax) >= 2 &&
+      fused_stages_red(sd) >= 2 &&
       plan_cred_side(p->c_row, pl.ti, p->c_col, pl.tj, pl.level, C, p->c_base, sc) &&
       encode_side(sc, C, p->c_base, maps[2])) {
     g.cred = 1;
@@ -1123,7 +1157,9 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
   }
   g.tma = 0;
   g.umax = umax;
-  g.stages = g.cred ? fused_stages_red(umax) : S;
+  g.stages = g.cred ? fused_stages_red(sd) : S;
+  g.stage_dbl = (int32_t)sd;
+  g.tshape = pl.tshape;
   // summing warpgroup when some side has more than one view per chunk (L >= 1):
   // STC_PRESUM = 0 (the consumers form every sum), 1 (A side; default), 3 (both sides)
   g.psum = 0;
@@ -1153,7 +1189,7 @@ constexpr size_t kPlanCache = 32;
 std::string plan_env() {
   static const char *knobs[] = {"STC_WORKSPACE_CAP_MB", "STC_EXEC_ORDER", "STC_PACK", "STC_TMA_PROMO",
                                 "STC_TMA", "STC_TMA_PF", "STC_FUSED", "STC_CRED", "STC_PRESUM",
-                                "STC_ABC_DENSE"};
+                                "STC_ABC_DENSE", "STC_TSHAPE"};
   std::string key;
   for (const char *k : knobs) {
     const char *v = getenv(k);
@@ -1341,7 +1377,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
   // tickets + work counters
   int32_t *tickets = reinterpret_cast<int32_t *>(ws + pl.off_tickets);
   int32_t *counters = reinterpret_cast<int32_t *>(ws + pl.off_counters);
-  const int tiles_m = (int)(pl.mq_pad / BM), tiles_n = (int)(pl.nq_pad / BN);
+  const int tiles_m = (int)(pl.mq_pad / pl.tm), tiles_n = (int)(pl.nq_pad / pl.tn);
   const int64_t P = (int64_t)tiles_m * tiles_n;
   const int T = (int)pl.terms.size();
 
@@ -1633,6 +1669,8 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         gf.coords = base.coords;
         gf.umax = base.umax;
         gf.stages = base.stages;
+        gf.stage_dbl = base.stage_dbl;
+        gf.tshape = base.tshape;
         gf.psum = base.psum;
         gf.kchunks = base.kchunks;
         gf.cred = 0;
@@ -1650,6 +1688,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         tma = !packed && !naive;
         CU(launch_fused(gf, grid, s, maps_ab), "k_strassen_fused(dense)");
       } else {
+        if (pl.tshape != 0) return fail(STC_EINVAL, "internal: tile shape %d needs the fused kernel", pl.tshape);
         CU(launch_gemm(g, grid, s), "k_strassen_gemm(dense)");
       }
       if (g_ev_after && bi == pl.nbatches - 1) CU(cudaEventRecord(g_ev_after, s), "cudaEventRecord");

@@ -95,14 +95,14 @@ __device__ __forceinline__ int epi_col(int nt, int tig) {  // first of the pair 
   return 16 * (nt >> 1) + frag_perm(PB, 2 * tig, nt & 1);
 }
 
-template <int PA = 0, int PB = 0, int RB = 1>
+template <int PA = 0, int PB = 0, int RB = 1, int TBM = BM, int TBN = BN>
 __device__ __forceinline__ void epilogue_store(const GemmArgs &p, const double (&acc)[4][4][4], int item, int tid,
                                                int wm, int wn, int g, int tig) {
   int slot, ti, tj, pos, piece;
   tile_of(p, item, slot, ti, tj, pos, piece);
   const TermDesc td = p.terms[slot];
-  const int row0 = ti * BM + wm * 64;
-  const int col0 = tj * BN + wn * 32;
+  const int row0 = ti * TBM + wm * 64;
+  const int col0 = tj * TBN + wn * 32;
   if (p.dense_out) {
     double *Mt = p.M + (int64_t)td.m_slot * p.m_stride;
 #pragma unroll

@@ -33,6 +33,19 @@ namespace stc {
 #endif
 constexpr int FK = 8;                        // k-chunk of the fused kernel
 constexpr int VIEW_DOUBLES = BM * FK;        // one raw view of one chunk (BM == BN)
+
+// CTA tile shapes (GemmArgs::tshape): the 8 consumer warps keep their 64 x 32 warp
+// tiles and are arranged WM x WN.  0: 128 x 128 (the default); 1: 64 x 256 and 2:
+// 256 x 64 for quadrants that are 64 wide in I or J (cfg3 at m or n = 256, L2), whose
+// 128-wide tiles would be half padding.  Shapes 1 and 2 run with dense M output and
+// the summing warpgroup only.  A views hold BMT x 8, B views BNT x 8 doubles.
+template <int TS>
+struct Shape {
+  static constexpr int WM = TS == 1 ? 1 : TS == 2 ? 4 : 2;
+  static constexpr int WN = CONSUMER_WARPS / WM;
+  static constexpr int BMT = 64 * WM, BNT = 32 * WN;
+  static constexpr int AV = BMT * FK, BV = BNT * FK;
+};
 constexpr int FUSED_PRODUCER_WARPS = 4;  // one warpgroup (setmaxnreg is warpgroup-wide); warp 0 of it issues
 constexpr int FUSED_THREADS = 32 * (CONSUMER_WARPS + FUSED_PRODUCER_WARPS);
 // setmaxnreg budget: the CTA launches with 168 regs x 384 threads; the consumers'
@@ -59,25 +72,21 @@ static_assert(CONSUMER_WARPS * (PS_CONSUMER_REGS - 128) <=
                   FUSED_PRODUCER_WARPS * (128 - FUSED_PRODUCER_REGS) + SUM_WARPS * (128 - PS_SUM_REGS),
               "setmaxnreg: consumer increase exceeds the producer + summer release");
 
-// smem: stages [S][umax][1024 doubles] | (cred) M pieces [2][16][128] |
-//       full[S], empty[S], summed[S], epi_full[EPI_BUFS], epi_empty[EPI_BUFS] |
-//       stage_item[S], epi_item[EPI_BUFS] | epilogue offset tables: rows[128], cols[128] (int64)
+// smem (fixed offsets up front, so the hot loops address the barriers without
+// registers): full[8], empty[8], summed[8], epi_full[EPI_BUFS], epi_empty[EPI_BUFS] |
+// stage_item[8], epi_item[EPI_BUFS] | epilogue offset tables rows[128], cols[128] (int64) |
+// stages [S][sd doubles: na A views of AV, then nb B views of BV] (1024-byte aligned:
+// swizzled TMA boxes) | (cred) M pieces [2][16][128]
 constexpr int RED_ROWS = 16;                          // rows of one TMA-reduce piece (double-buffered)
 constexpr size_t RED_BYTES = 2 * (size_t)RED_ROWS * BN * 8;
 struct FusedLayout {
-  __host__ __device__ static size_t stage_bytes(int umax) { return (size_t)umax * VIEW_DOUBLES * 8; }
-  __host__ __device__ static size_t red_off(int umax, int stages) { return (size_t)stages * stage_bytes(umax); }
-  __host__ __device__ static size_t bar_off(int umax, int stages, bool red) {
-    return red_off(umax, stages) + (red ? RED_BYTES : 0);
-  }
-  __host__ __device__ static size_t meta_off(int umax, int stages, bool red) {
-    return bar_off(umax, stages, red) + 24 * (size_t)stages + 16 * EPI_BUFS;
-  }
-  __host__ __device__ static size_t epi_tab_off(int umax, int stages, bool red) {
-    return (meta_off(umax, stages, red) + 4 * (size_t)stages + 4 * EPI_BUFS + 15) / 16 * 16;
-  }
-  __host__ __device__ static size_t bytes(int umax, int stages, bool red) {
-    return epi_tab_off(umax, stages, red) + 2 * 128 * 8;
+  static constexpr size_t kBars = 0, kMeta = 256, kEpiTab = 512, kStages = 3072;
+  static_assert(8 * (3 * MAX_FUSED_STAGES + 2 * EPI_BUFS) <= kMeta, "barriers");
+  static_assert(kMeta + 4 * (MAX_FUSED_STAGES + EPI_BUFS) <= kEpiTab, "meta");
+  static_assert(kEpiTab + 2 * 128 * 8 <= kStages && kStages % 1024 == 0, "tables");
+  __host__ __device__ static size_t red_off(size_t sd, int stages) { return kStages + (size_t)stages * sd * 8; }
+  __host__ __device__ static size_t bytes(size_t sd, int stages, bool red) {
+    return red_off(sd, stages) + (red ? RED_BYTES : 0);
   }
 };
 
@@ -87,18 +96,25 @@ constexpr size_t TILE_DOUBLES = (size_t)BM * BN;
 
 constexpr size_t kFusedMaxSmem = 227 * 1024;
 
-// Stages of the fused ring for terms of at most `umax` views per chunk (0: does not fit).
-int fused_stages(int umax) {
+// Stages of the fused ring for stages of `sd` doubles (0: does not fit).
+int fused_stages(size_t sd) {
   int s = MAX_FUSED_STAGES;
-  while (s >= 2 && FusedLayout::bytes(umax, s, false) > kFusedMaxSmem) --s;
+  while (s >= 2 && FusedLayout::bytes(sd, s, false) > kFusedMaxSmem) --s;
   return s >= 2 ? s : 0;
 }
 
 // Stages when the TMA-reduce epilogue's M piece also lives in smem.
-int fused_stages_red(int umax) {
+int fused_stages_red(size_t sd) {
   int s = MAX_FUSED_STAGES;
-  while (s >= 2 && FusedLayout::bytes(umax, s, true) > kFusedMaxSmem) --s;
+  while (s >= 2 && FusedLayout::bytes(sd, s, true) > kFusedMaxSmem) --s;
   return s >= 2 ? s : 0;
+}
+
+// Doubles per stage for terms of at most max_ops views per side, tile shape ts.
+size_t fused_stage_doubles(int max_ops, int ts) {
+  const int av = ts == 1 ? Shape<1>::AV : ts == 2 ? Shape<2>::AV : Shape<0>::AV;
+  const int bv = ts == 1 ? Shape<1>::BV : ts == 2 ? Shape<2>::BV : Shape<0>::BV;
+  return (size_t)max_ops * (av + bv);
 }
 
 // Element offset of (x, k) inside a raw view.
@@ -190,15 +206,17 @@ __device__ __forceinline__ void side_sum(double (&out)[I], const double *st, int
 // DADD of the signed value otherwise -- the reference's view order), then issue
 // MMA group V of the current k-step.  Loads go in groups of four values to keep
 // the register footprint inside the consumers' budget.
-template <int NA, int NB, int V, int KN, bool MMA, bool SGN = true>
+template <int NA, int NB, int V, int KN, bool MMA, bool SGN = true, int AV = VIEW_DOUBLES, int BV = VIEW_DOUBLES>
 __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (&fa)[8], const double (&fb)[4],
                                           double (&xa)[8], double (&xb)[4], const double *nst, bool load,
                                           const int (&offA)[2][2], const int (&offB)[2][2], uint32_t negmask,
-                                          int bsh) {
+                                          int bbase) {
   constexpr int G = NA + NB;
   const int fl = static_cast<int>(((negmask >> V) & 1u) << 31);
   const double sgn = __hiloint2double(0x3ff00000 | fl, 0);  // +/-1.0
-  const double *src = nst + V * VIEW_DOUBLES + (V >= NA ? bsh : 0);  // bsh: B views' slot shift (summing warps)
+  // A view V at V * AV; B view V - NA at bbase + (V - NA) * BV (bbase: the stage's B views)
+  const double *src = AV == BV ? nst + V * AV + (V >= NA ? bbase - NA * AV : 0)
+                               : (V < NA ? nst + V * AV : nst + bbase + (V - NA) * BV);
   // one address per fragment column / row pair; the mt / nt blocks are immediates
   const double *pa0 = src + offA[KN][0], *pa1 = src + offA[KN][1];
   const double *pb0 = src + offB[KN][0], *pb1 = src + offB[KN][1];
@@ -227,7 +245,7 @@ __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (
 #pragma unroll
         for (int w = 0; w < NB; ++w)
 #pragma unroll
-          for (int nt = 0; nt < 4; ++nt) t[w][nt] = ((nt & 1 ? pb1 : pb0) + w * VIEW_DOUBLES)[128 * (nt >> 1)];
+          for (int nt = 0; nt < 4; ++nt) t[w][nt] = ((nt & 1 ? pb1 : pb0) + w * BV)[128 * (nt >> 1)];
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) xb[nt] = __hiloint2double(__double2hiint(t[0][nt]) ^ fl, __double2loint(t[0][nt]));
 #pragma unroll
@@ -258,7 +276,8 @@ __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (
     for (int i = 16 * V / G; i < 16 * (V + 1) / G; ++i)
       dmma_16x8x4(acc[i >> 2][i & 3], fa[2 * (i >> 2)], fa[2 * (i >> 2) + 1], fb[i & 3]);
   }
-  if constexpr (V + 1 < G) pipe_view<NA, NB, V + 1, KN, MMA, SGN>(acc, fa, fb, xa, xb, nst, load, offA, offB, negmask, bsh);
+  if constexpr (V + 1 < G)
+    pipe_view<NA, NB, V + 1, KN, MMA, SGN, AV, BV>(acc, fa, fb, xa, xb, nst, load, offA, offB, negmask, bbase);
 }
 
 // One work item's main loop for terms with NA A-views and NB B-views
@@ -268,11 +287,11 @@ __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (
 // k-step are built one view per group, so no DADD waits on a result it needs
 // right away behind the DMMAs queued on the shared FP64 pipe.  A chunk stage
 // is released as soon as both of its k-steps are in registers.
-template <int NA, int NB, bool SGN = true>
-__device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const double *stages, int umax, int S,
+template <int NA, int NB, bool SGN = true, int AV = VIEW_DOUBLES, int BV = VIEW_DOUBLES>
+__device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const double *stages, int sstride, int S,
                                              uint64_t *full, uint64_t *empty, int &stage, uint32_t &phase, int kchunks,
                                              uint32_t negmask, const int (&offA_)[2][2], const int (&offB_)[2][2],
-                                             int lane, int bsh = 0) {
+                                             int lane, int bbase = NA * AV) {
   // Keep the fragment offsets in registers through opaque copies: otherwise
   // ptxas rematerialises them from %tid (S2R, a long-latency special-register
   // read, plus the swizzle arithmetic) inside the hot loop.
@@ -287,12 +306,13 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
     }
   const int (&offA)[2][2] = oA;
   const int (&offB)[2][2] = oB;
-  const size_t sstride = (size_t)umax * VIEW_DOUBLES;
   double fa[8], fb[4], xa[8], xb[4];
-  pipe_view<NA, NB, 0, 0, false, SGN>(acc, fa, fb, fa, fb, stages + stage * sstride, true, offA, offB, negmask, bsh);
+  pipe_view<NA, NB, 0, 0, false, SGN, AV, BV>(acc, fa, fb, fa, fb, stages + stage * sstride, true, offA, offB, negmask,
+                                              bbase);
   for (int c = 0; c < kchunks; ++c) {
     // k-step 0 of chunk c (fa, fb) -> build k-step 1 of chunk c (xa, xb)
-    pipe_view<NA, NB, 0, 1, true, SGN>(acc, fa, fb, xa, xb, stages + stage * sstride, true, offA, offB, negmask, bsh);
+    pipe_view<NA, NB, 0, 1, true, SGN, AV, BV>(acc, fa, fb, xa, xb, stages + stage * sstride, true, offA, offB, negmask,
+                                               bbase);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);  // both k-steps of chunk c are in registers
     if (++stage == S) {
@@ -302,7 +322,8 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
     // k-step 1 of chunk c (xa, xb) -> build k-step 0 of chunk c + 1 (fa, fb)
     const bool more = c + 1 < kchunks;
     if (more) mbar_wait(&full[stage], phase);
-    pipe_view<NA, NB, 0, 0, true, SGN>(acc, xa, xb, fa, fb, stages + stage * sstride, more, offA, offB, negmask, bsh);
+    pipe_view<NA, NB, 0, 0, true, SGN, AV, BV>(acc, xa, xb, fa, fb, stages + stage * sstride, more, offA, offB, negmask,
+                                               bbase);
   }
 }
 
@@ -582,8 +603,9 @@ __device__ __forceinline__ void epilogue_warps_red(const GemmArgs &p, uint64_t *
 // sums and of the reference's packing, _jit.py:43-65).  All views share the
 // swizzled layout, so thread t owns the double2 elements t, t + 128, ... of
 // every view of the side.
+template <int VD>
 __device__ __forceinline__ void sum_side(double2 *__restrict__ st, int v0, int n, uint32_t negmask, int t) {
-  constexpr int VD2 = VIEW_DOUBLES / 2;
+  constexpr int VD2 = VD / 2;
   constexpr int PER = VD2 / (32 * SUM_WARPS);
   const int fl = static_cast<int>(((negmask >> v0) & 1u) << 31);
   double2 a[PER];
@@ -621,8 +643,10 @@ __device__ __forceinline__ void sum_side(double2 *__restrict__ st, int v0, int n
 // consumers' fragment-load sums repeat A 4x and B 2x across the warps sharing
 // the fragments -- and the summers' waits for the FP64 unit, which the DMMAs
 // occupy, never hold up a DMMA issue.
-__device__ __forceinline__ void summer_warps(const GemmArgs &p, double *stages, int umax, int S, uint64_t *full,
+template <int TS>
+__device__ __forceinline__ void summer_warps(const GemmArgs &p, double *stages, int sstride, int S, uint64_t *full,
                                              uint64_t *summed, const int *stage_item, int t) {
+  using SH = Shape<TS>;
   const int lane = t & 31;
   const bool sum_b = (p.psum & 2) != 0;
   int rs = 0;
@@ -651,9 +675,10 @@ __device__ __forceinline__ void summer_warps(const GemmArgs &p, double *stages, 
         do_a = do_b = false;  // timing experiment only: no sums formed
 #endif
       }
-      double2 *st = reinterpret_cast<double2 *>(stages + (size_t)rs * umax * VIEW_DOUBLES);
-      if (do_a) sum_side(st, 0, na, negmask, t);
-      if (do_b) sum_side(st, na, nb, negmask, t);
+      double *st = stages + (size_t)rs * sstride;
+      if (do_a) sum_side<SH::AV>(reinterpret_cast<double2 *>(st), 0, na, negmask, t);
+      if constexpr (TS == 0)  // shapes 1, 2 run with psum = 1
+        if (do_b) sum_side<SH::BV>(reinterpret_cast<double2 *>(st + na * SH::AV), 0, nb, negmask >> na, t);
       // generic writes before the async proxy (TMA) refills this stage
 #ifndef STC_EXPERIMENT_NOPROXYFENCE
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -689,23 +714,26 @@ __device__ __forceinline__ void skip_item(int S, uint64_t *full, uint64_t *empty
 
 // PS: a summing warpgroup forms (some of) the operand sums in place (p.psum);
 // otherwise the consumers form them all in their fragment loads.
-template <int AKF, int BKF, bool PS>
+// TS: CTA tile shape (Shape<TS>; 1 and 2 only with PS and dense M output).
+template <int AKF, int BKF, bool PS, int TS>
 __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
     k_strassen_fused(const GemmArgs p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC) {
+  using SH = Shape<TS>;
   extern __shared__ __align__(1024) unsigned char smem[];
-  const int umax = p.umax, S = p.stages;
+  const int S = p.stages;
+  const int sstride = p.stage_dbl;  // doubles per stage
   const bool red = p.cred != 0;
-  double *stages = reinterpret_cast<double *>(smem);
-  double *redbuf = reinterpret_cast<double *>(smem + FusedLayout::red_off(umax, S));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + FusedLayout::bar_off(umax, S, red));
-  uint64_t *empty = full + S;
-  uint64_t *summed = empty + S;  // PS: the stage's sums are formed (the consumers' full barrier)
-  uint64_t *epi_full = summed + S;  // M tile b written by the consumers (ABC: C updates offloaded)
+  double *stages = reinterpret_cast<double *>(smem + FusedLayout::kStages);
+  double *redbuf = reinterpret_cast<double *>(smem + FusedLayout::red_off(sstride, S));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + FusedLayout::kBars);
+  uint64_t *empty = full + MAX_FUSED_STAGES;
+  uint64_t *summed = empty + MAX_FUSED_STAGES;  // PS: the stage's sums are formed (the consumers' full barrier)
+  uint64_t *epi_full = summed + MAX_FUSED_STAGES;  // M tile b written by the consumers (ABC: C updates offloaded)
   uint64_t *epi_empty = epi_full + EPI_BUFS;
-  int *stage_item = reinterpret_cast<int *>(smem + FusedLayout::meta_off(umax, S, red));
-  int *epi_item = stage_item + S;
-  int64_t *epi_rows = reinterpret_cast<int64_t *>(smem + FusedLayout::epi_tab_off(umax, S, red));
+  int *stage_item = reinterpret_cast<int *>(smem + FusedLayout::kMeta);
+  int *epi_item = stage_item + MAX_FUSED_STAGES;
+  int64_t *epi_rows = reinterpret_cast<int64_t *>(smem + FusedLayout::kEpiTab);
   int64_t *epi_cols = epi_rows + 128;
   const bool offload = p.mscratch != nullptr;  // ABC: epilogue warps update C from the M tiles
   const int tid = threadIdx.x;
@@ -728,7 +756,7 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
   if (PS && warp >= CONSUMER_WARPS + FUSED_PRODUCER_WARPS) {
     // ===================== summing warpgroup (PS) ======================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PS_SUM_REGS));
-    summer_warps(p, stages, umax, S, full, summed, stage_item, tid - 32 * (CONSUMER_WARPS + FUSED_PRODUCER_WARPS));
+    summer_warps<TS>(p, stages, sstride, S, full, summed, stage_item, tid - 32 * (CONSUMER_WARPS + FUSED_PRODUCER_WARPS));
   } else if (warp >= CONSUMER_WARPS) {
     // ===================== producer warp: TMA box loads ================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(FUSED_PRODUCER_REGS));
@@ -770,7 +798,7 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
       if (lane < U) {
         sd = lane < na ? 0 : 1;
         const OpDesc o = p.ops[sd == 0 ? td.a_first + lane : td.b_first + lane - na];
-        xc = p.coords[(o.x_start + (int64_t)(sd == 0 ? ti * BM : tj * BN)) >> 3];
+        xc = p.coords[(o.x_start + (int64_t)(sd == 0 ? ti * SH::BMT : tj * SH::BNT)) >> 3];
         kst = o.k_start;
       }
       const CUtensorMap *map = sd == 0 ? &tmA : &tmB;
@@ -779,10 +807,12 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
 #pragma unroll
       for (int d = 0; d < 5; ++d) src[d] = p.tm_src[sd][d];
 #ifdef STC_EXPERIMENT_TWOVIEWS
-      const uint32_t bytes = 2u * VIEW_DOUBLES * 8;
+      const uint32_t bytes = (uint32_t)(SH::AV + SH::BV) * 8;
 #else
-      const uint32_t bytes = (uint32_t)U * VIEW_DOUBLES * 8;
+      const uint32_t bytes = (uint32_t)(na * SH::AV + (U - na) * SH::BV) * 8;
 #endif
+      // stage layout: A view u at u * AV, B view w at na * AV + w * BV
+      const size_t vofs = lane < na ? (size_t)lane * SH::AV : (size_t)na * SH::AV + (size_t)(lane - na) * SH::BV;
       for (int c = 0; c < kchunks; ++c) {
         int4 kc = make_int4(0, 0, 0, 0);
         if (lane < U) kc = p.coords[(kst + (int64_t)c * FK) >> 3];
@@ -801,7 +831,7 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
           int32_t cc[5];
 #pragma unroll
           for (int d = 0; d < 5; ++d) cc[d] = src[d] < 4 ? coord_of(xc, src[d]) : coord_of(kc, src[d] - 4);
-          tma_box_f(stages + ((size_t)stage * umax + lane) * VIEW_DOUBLES, map, rank, cc, &full[stage]);
+          tma_box_f(stages + (size_t)stage * sstride + vofs, map, rank, cc, &full[stage]);
         }
         if (++stage == S) {
           stage = 0;
@@ -816,7 +846,9 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
     // warp -> (wm, wn): the warps of one SM sub-partition (warp % 4) differ in wn by
     // default; with warp_map = 1 in wm, so the warps left when the wm = 1 row half of
     // a tile is padding (skip_item) still cover all four sub-partitions
-    const int wm = p.warp_map ? warp >> 2 : warp & 1, wn = p.warp_map ? warp & 3 : warp >> 1;
+    // shapes 1 / 2: warp = wn (WM = 1) or wm + 4 wn (WM = 4): all sub-partitions busy either way
+    const int wm = TS == 1 ? 0 : TS == 2 ? warp & 3 : p.warp_map ? warp >> 2 : warp & 1;
+    const int wn = TS == 1 ? warp : TS == 2 ? warp >> 2 : p.warp_map ? warp & 3 : warp >> 1;
     // Fragment offsets inside a view: A (kk, h) + 128 * mt; B (kk, nt & 1) + 128 * (nt >> 1).
     // MMA row (column) g + 8 h of each 16-row block (16-column pair) reads tile row
     // (column) frag_perm(kind, g, h) (stc_common.cuh): with it every half-warp of a
@@ -860,15 +892,16 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
         for (int j = 0; j < 4; ++j)
 #pragma unroll
           for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
-      const bool pad_tile = (p.rows_valid > 0 && ti * BM + wm * 64 >= p.rows_valid) ||
-                            (p.cols_valid > 0 && tj * BN + wn * 32 >= p.cols_valid);
+      const bool pad_tile = (p.rows_valid > 0 && ti * SH::BMT + wm * 64 >= p.rows_valid) ||
+                            (p.cols_valid > 0 && tj * SH::BNT + wn * 32 >= p.cols_valid);
       if (pad_tile) {
         skip_item(S, cfull, empty, stage, phase, kchunks, lane);
       } else if constexpr (PS) {
-        // the A sum sits in view slot 0 and the B views from slot na on
-        const int bsh = (na - 1) * VIEW_DOUBLES;
-        if (p.psum & 2) {  // B summed too (slot na)
-          consume_item<1, 1, false>(acc, stages, umax, S, cfull, empty, stage, phase, kchunks, 0u, offA, offB, lane, bsh);
+        // the A sum sits in view slot 0 and the B views from na * AV on
+        const int bbase = na * SH::AV;
+        if (TS == 0 && (p.psum & 2)) {  // B summed too (first B view)
+          consume_item<1, 1, false>(acc, stages, sstride, S, cfull, empty, stage, phase, kchunks, 0u, offA, offB, lane,
+                                    bbase);
         } else {  // B views summed in the fragment loads: their signs at bits 1..nb
           bool neg = false;
           if (lane < nb) neg = __double_as_longlong(p.ops[td.b_first + lane].sign) < 0;
@@ -878,9 +911,9 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
 #else
           switch (nb) {
 #endif
-            case 1: consume_item<1, 1>(acc, stages, umax, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bsh); break;
-            case 2: consume_item<1, 2>(acc, stages, umax, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bsh); break;
-            default: consume_item<1, 4>(acc, stages, umax, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bsh); break;
+            case 1: consume_item<1, 1, true, SH::AV, SH::BV>(acc, stages, sstride, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bbase); break;
+            case 2: consume_item<1, 2, true, SH::AV, SH::BV>(acc, stages, sstride, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bbase); break;
+            default: consume_item<1, 4, true, SH::AV, SH::BV>(acc, stages, sstride, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bbase); break;
           }
         }
       } else {
@@ -889,19 +922,19 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
       if (lane < na + nb) neg = __double_as_longlong(p.ops[lane < na ? td.a_first + lane : td.b_first + lane - na].sign) < 0;
       const uint32_t negmask = __ballot_sync(0xffffffffu, neg);
       switch (na * 8 + nb) {
-        case 9: consume_item<1, 1>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
-        case 10: consume_item<1, 2>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
-        case 17: consume_item<2, 1>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
-        case 18: consume_item<2, 2>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
-        case 12: consume_item<1, 4>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
-        case 33: consume_item<4, 1>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
-        case 20: consume_item<2, 4>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
-        case 34: consume_item<4, 2>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
-        case 36: consume_item<4, 4>(acc, stages, umax, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        case 9: consume_item<1, 1>(acc, stages, sstride, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        case 10: consume_item<1, 2>(acc, stages, sstride, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        case 17: consume_item<2, 1>(acc, stages, sstride, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        case 18: consume_item<2, 2>(acc, stages, sstride, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        case 12: consume_item<1, 4>(acc, stages, sstride, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        case 33: consume_item<4, 1>(acc, stages, sstride, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        case 20: consume_item<2, 4>(acc, stages, sstride, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        case 34: consume_item<4, 2>(acc, stages, sstride, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
+        case 36: consume_item<4, 4>(acc, stages, sstride, S, full, empty, stage, phase, kchunks, negmask, offA, offB, lane); break;
         default:  // other view counts (not produced by the Strassen recursion)
           for (int kc = 0; kc < kchunks; ++kc) {
             if (kc > 0) mbar_wait(&full[stage], phase);
-            const double *st = stages + (size_t)stage * umax * VIEW_DOUBLES;
+            const double *st = stages + (size_t)stage * sstride;
             double a[2][8], b[2][4];
 #pragma unroll
             for (int kk = 0; kk < 2; ++kk) {
@@ -933,7 +966,7 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
           break;
       }
       }  // !PS
-      if (offload) {
+      if (TS == 0 && offload) {
         // dense M tile into this CTA's scratch buffer; the epilogue warps add it
         // into the C targets while the next item's MMAs run
         mbar_wait(&epi_empty[eb], ephase ^ 1);
@@ -969,11 +1002,15 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
         if (z == 1.2345e300) p.C[0] = z;
       }
 #else
-      if (!p.dense_out) wait_c_ready(p, tid, c_seen);
-      if (red)
-        epilogue_red<AKF + 1, BKF + 1>(p, acc, item, tid, wm, wn, g, tig, redbuf, &tmC);
-      else
-        epilogue_store<AKF + 1, BKF + 1, 2>(p, acc, item, tid, wm, wn, g, tig);
+      if constexpr (TS != 0) {  // shapes 1, 2: dense M output only
+        epilogue_store<AKF + 1, BKF + 1, 2, SH::BMT, SH::BNT>(p, acc, item, tid, wm, wn, g, tig);
+      } else {
+        if (!p.dense_out) wait_c_ready(p, tid, c_seen);
+        if (red)
+          epilogue_red<AKF + 1, BKF + 1>(p, acc, item, tid, wm, wn, g, tig, redbuf, &tmC);
+        else
+          epilogue_store<AKF + 1, BKF + 1, 2>(p, acc, item, tid, wm, wn, g, tig);
+      }
 #endif
     }
   }
@@ -981,19 +1018,23 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
 
 using FusedKernel = void (*)(const GemmArgs, const CUtensorMap, const CUtensorMap, const CUtensorMap);
 
-static FusedKernel fused_for(int akf, int bkf, bool ps) {
-  if (ps) {
-    if (akf) return bkf ? k_strassen_fused<1, 1, true> : k_strassen_fused<1, 0, true>;
-    return bkf ? k_strassen_fused<0, 1, true> : k_strassen_fused<0, 0, true>;
-  }
-  if (akf) return bkf ? k_strassen_fused<1, 1, false> : k_strassen_fused<1, 0, false>;
-  return bkf ? k_strassen_fused<0, 1, false> : k_strassen_fused<0, 0, false>;
+template <bool PS, int TS>
+static FusedKernel fused_for_ts(int akf, int bkf) {
+  if (akf) return bkf ? k_strassen_fused<1, 1, PS, TS> : k_strassen_fused<1, 0, PS, TS>;
+  return bkf ? k_strassen_fused<0, 1, PS, TS> : k_strassen_fused<0, 0, PS, TS>;
+}
+
+static FusedKernel fused_for(int akf, int bkf, bool ps, int ts) {
+  if (ps) return ts == 1 ? fused_for_ts<true, 1>(akf, bkf) : ts == 2 ? fused_for_ts<true, 2>(akf, bkf)
+                                                             : fused_for_ts<true, 0>(akf, bkf);
+  return fused_for_ts<false, 0>(akf, bkf);
 }
 
 cudaError_t launch_fused(const GemmArgs &a, int grid, cudaStream_t s, const void *maps) {
   const bool ps = a.psum != 0;
-  const size_t sm = FusedLayout::bytes(a.umax, a.stages, a.cred != 0);
-  FusedKernel k = fused_for(a.a_kfast, a.b_kfast, ps);
+  if (a.tshape != 0 && (!ps || !a.dense_out || (a.psum & 2))) return cudaErrorInvalidValue;
+  const size_t sm = FusedLayout::bytes((size_t)a.stage_dbl, a.stages, a.cred != 0);
+  FusedKernel k = fused_for(a.a_kfast, a.b_kfast, ps, a.tshape);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   CUtensorMap m[3];

@@ -97,6 +97,8 @@ struct GemmArgs {
   // fused kernel (stc_fused.cu)
   const int4 *coords;        // coords[i]: map coordinates (one part) of pool entry 8 i
   int32_t umax, stages;      // views per chunk stage (2 * max_ops), ring depth
+  int32_t stage_dbl;         // doubles per stage (max_ops x (A view + B view))
+  int32_t tshape;            // CTA tile shape: 0 128 x 128, 1 64 x 256, 2 256 x 64 (stc_fused.cu Shape)
   int32_t psum;              // summing warpgroup (stc_fused.cu): bit 0 sums the A side, bit 1 the B
                              // side in place; 0: the consumers form every sum in their fragment loads
   double *mscratch;          // ABC: [grid][2][BM * BN] M tiles handed to the epilogue warps
@@ -189,8 +191,9 @@ int gemm_kwin(int max_ops);
 cudaError_t launch_chunk_strides(const int64_t *pool, int64_t nchunks, int64_t *kbs, cudaStream_t s);
 cudaError_t launch_gemm(const GemmArgs &a, int grid, cudaStream_t s, const void *maps = nullptr);
 int gemm_tma_config(int max_ops, int &nraw, int &kwin);
-int fused_stages(int umax);
-int fused_stages_red(int umax);
+int fused_stages(size_t stage_doubles);
+int fused_stages_red(size_t stage_doubles);
+size_t fused_stage_doubles(int max_ops, int tshape);
 cudaError_t launch_fused(const GemmArgs &a, int grid, cudaStream_t s, const void *maps);
 cudaError_t launch_pool_coords(const int64_t *pool, int4 *coords, const CoordJobs &jobs, cudaStream_t s);
 int gemm_max_grid(int max_ops);

@@ -123,6 +123,28 @@ def test_abc_dense_m_matches_ticketed_bitwise(line):
             assert np.array_equal(cg.data, cd.data), (line, level)
 
 
+@pytest.mark.parametrize("line,shape", [
+    # I quadrants 64 wide at L2 (m = 256): 64 x 256 tiles; J quadrants 64 wide: 256 x 64
+    ("abij abef efij & a:16;b:16;i:32;j:64;e:32;f:16;", 1),
+    ("abij abef efij & a:64;b:32;i:16;j:16;e:32;f:16;", 2),
+    ("aibj eafb jfie & a:16;b:16;i:16;j:128;e:16;f:32;", 1),
+])
+def test_tile_shapes_match_square_tiles_bitwise(line, shape):
+    # the 64 x 256 / 256 x 64 CTA tiles (dense-M launches with the summing warpgroup) give
+    # every M element the same k order and sums as the 128 x 128 tiles (STC_TSHAPE=0)
+    spec = stc.parse_benchmark_line(line)
+    a, b, c0 = _operands(spec, 81)
+    classical = c0.copy()
+    oracle.contract_reference(spec, a.to_host(), b.to_host(), classical)
+    for level, variant in ((2, "ab"), (2, "abc"), (1, "ab")):
+        cs, ss = _run_env(spec, a, b, c0, level, variant, {})
+        cq, sq = _run_env(spec, a, b, c0, level, variant, {"STC_TSHAPE": "0"})
+        assert np.array_equal(cs.data, cq.data), (line, level, variant)
+        assert stc.relative_error(cs, classical) <= TOL
+        if level == 2:  # the shaped launch has half the padded work items
+            assert ss.work_items < sq.work_items, (ss.work_items, sq.work_items)
+
+
 def test_fused_matches_oracle_strassen():
     # the oracle's own L2 ABC Strassen on the same inputs (different summation
     # order inside the leaf GEMMs, so compared in norm)
