@@ -606,35 +606,40 @@ __device__ __forceinline__ void epilogue_warps_red(const GemmArgs &p, uint64_t *
 template <int VD>
 __device__ __forceinline__ void sum_side(double2 *__restrict__ st, int v0, int n, uint32_t negmask, int t) {
   constexpr int VD2 = VD / 2;
-  constexpr int PER = VD2 / (32 * SUM_WARPS);
+  // at most 4 double2 per thread at a time (the summing warps' 56 registers)
+  constexpr int PER = VD2 / (32 * SUM_WARPS) < 4 ? VD2 / (32 * SUM_WARPS) : 4;
+  constexpr int STEP = 32 * SUM_WARPS * PER;
   const int fl = static_cast<int>(((negmask >> v0) & 1u) << 31);
-  double2 a[PER];
+#pragma unroll 1
+  for (int base = 0; base < VD2; base += STEP) {
+    double2 a[PER];
 #pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    const double2 v = st[v0 * VD2 + t + 32 * SUM_WARPS * i];
-    a[i].x = __hiloint2double(__double2hiint(v.x) ^ fl, __double2loint(v.x));
-    a[i].y = __hiloint2double(__double2hiint(v.y) ^ fl, __double2loint(v.y));
-  }
-  for (int v = v0 + 1; v < v0 + n; ++v) {
-    double2 b[PER];
+    for (int i = 0; i < PER; ++i) {
+      const double2 v = st[v0 * VD2 + base + t + 32 * SUM_WARPS * i];
+      a[i].x = __hiloint2double(__double2hiint(v.x) ^ fl, __double2loint(v.x));
+      a[i].y = __hiloint2double(__double2hiint(v.y) ^ fl, __double2loint(v.y));
+    }
+    for (int v = v0 + 1; v < v0 + n; ++v) {
+      double2 b[PER];
 #pragma unroll
-    for (int i = 0; i < PER; ++i) b[i] = st[v * VD2 + t + 32 * SUM_WARPS * i];
-    if ((negmask >> v) & 1u) {
+      for (int i = 0; i < PER; ++i) b[i] = st[v * VD2 + base + t + 32 * SUM_WARPS * i];
+      if ((negmask >> v) & 1u) {
 #pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        a[i].x = __dsub_rn(a[i].x, b[i].x);
-        a[i].y = __dsub_rn(a[i].y, b[i].y);
-      }
-    } else {
+        for (int i = 0; i < PER; ++i) {
+          a[i].x = __dsub_rn(a[i].x, b[i].x);
+          a[i].y = __dsub_rn(a[i].y, b[i].y);
+        }
+      } else {
 #pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        a[i].x = __dadd_rn(a[i].x, b[i].x);
-        a[i].y = __dadd_rn(a[i].y, b[i].y);
+        for (int i = 0; i < PER; ++i) {
+          a[i].x = __dadd_rn(a[i].x, b[i].x);
+          a[i].y = __dadd_rn(a[i].y, b[i].y);
+        }
       }
     }
-  }
 #pragma unroll
-  for (int i = 0; i < PER; ++i) st[v0 * VD2 + t + 32 * SUM_WARPS * i] = a[i];
+    for (int i = 0; i < PER; ++i) st[v0 * VD2 + base + t + 32 * SUM_WARPS * i] = a[i];
+  }
 }
 
 // Summing warpgroup: per chunk stage (after the TMA loads land), sum the A side
