@@ -31,6 +31,13 @@ def rand_case(rng):
         for group in (li, lj, lp):
             while np.prod([ext[l] for l in group]) < 512:
                 ext[rng.choice(group)] *= 2
+        if rng.random() < 0.3:  # an I or J bundle of 256: 64-wide quadrants at L2 (64 x 256 / 256 x 64 tiles)
+            group = li if rng.random() < 0.5 else lj
+            for l in group:
+                ext[l] = 1
+            ext[group[0]] = 256 if len(group) == 1 else 16
+            if len(group) > 1:
+                ext[group[1]] = 16
     # keep the problem moderate
     while np.prod([ext[l] for l in li]) * np.prod([ext[l] for l in lj]) * np.prod([ext[l] for l in lp]) > 2 ** 28:
         l = rng.choice(li + lj + lp)
