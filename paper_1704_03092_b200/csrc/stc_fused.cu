@@ -79,15 +79,37 @@ static_assert(CONSUMER_WARPS * (PS_CONSUMER_REGS - 128) <=
 // swizzled TMA boxes) | (cred) M pieces [2][16][128]
 constexpr int RED_ROWS = 16;                          // rows of one TMA-reduce piece (double-buffered)
 constexpr size_t RED_BYTES = 2 * (size_t)RED_ROWS * BN * 8;
+#ifndef STC_LAYOUT_TAIL
+#define STC_LAYOUT_TAIL 1
+#endif
 struct FusedLayout {
+#if STC_LAYOUT_TAIL
+  // stages at 0, then the M pieces, then barriers / meta / tables
+  static constexpr size_t kStages = 0;
+  __host__ __device__ static size_t red_off(size_t sd, int stages) { return (size_t)stages * sd * 8; }
+  __host__ __device__ static size_t bar_off(size_t sd, int stages, bool red) {
+    return red_off(sd, stages) + (red ? RED_BYTES : 0);
+  }
+  __host__ __device__ static size_t meta_off(size_t sd, int stages, bool red) {
+    return bar_off(sd, stages, red) + 8 * (3 * MAX_FUSED_STAGES + 2 * EPI_BUFS);
+  }
+  __host__ __device__ static size_t tab_off(size_t sd, int stages, bool red) {
+    return (meta_off(sd, stages, red) + 4 * (MAX_FUSED_STAGES + EPI_BUFS) + 15) / 16 * 16;
+  }
+  __host__ __device__ static size_t bytes(size_t sd, int stages, bool red) { return tab_off(sd, stages, red) + 2 * 128 * 8; }
+#else
   static constexpr size_t kBars = 0, kMeta = 256, kEpiTab = 512, kStages = 3072;
   static_assert(8 * (3 * MAX_FUSED_STAGES + 2 * EPI_BUFS) <= kMeta, "barriers");
   static_assert(kMeta + 4 * (MAX_FUSED_STAGES + EPI_BUFS) <= kEpiTab, "meta");
   static_assert(kEpiTab + 2 * 128 * 8 <= kStages && kStages % 1024 == 0, "tables");
   __host__ __device__ static size_t red_off(size_t sd, int stages) { return kStages + (size_t)stages * sd * 8; }
+  __host__ __device__ static size_t bar_off(size_t, int, bool) { return kBars; }
+  __host__ __device__ static size_t meta_off(size_t, int, bool) { return kMeta; }
+  __host__ __device__ static size_t tab_off(size_t, int, bool) { return kEpiTab; }
   __host__ __device__ static size_t bytes(size_t sd, int stages, bool red) {
     return red_off(sd, stages) + (red ? RED_BYTES : 0);
   }
+#endif
 };
 
 constexpr int EPI_WARPS = FUSED_PRODUCER_WARPS - 1;  // the producer warpgroup's other warps
@@ -731,18 +753,22 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
   const bool red = p.cred != 0;
   double *stages = reinterpret_cast<double *>(smem + FusedLayout::kStages);
   double *redbuf = reinterpret_cast<double *>(smem + FusedLayout::red_off(sstride, S));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + FusedLayout::kBars);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + FusedLayout::bar_off(sstride, S, red));
   uint64_t *empty = full + MAX_FUSED_STAGES;
   uint64_t *summed = empty + MAX_FUSED_STAGES;  // PS: the stage's sums are formed (the consumers' full barrier)
   uint64_t *epi_full = summed + MAX_FUSED_STAGES;  // M tile b written by the consumers (ABC: C updates offloaded)
   uint64_t *epi_empty = epi_full + EPI_BUFS;
-  int *stage_item = reinterpret_cast<int *>(smem + FusedLayout::kMeta);
+  int *stage_item = reinterpret_cast<int *>(smem + FusedLayout::meta_off(sstride, S, red));
   int *epi_item = stage_item + MAX_FUSED_STAGES;
-  int64_t *epi_rows = reinterpret_cast<int64_t *>(smem + FusedLayout::kEpiTab);
+  int64_t *epi_rows = reinterpret_cast<int64_t *>(smem + FusedLayout::tab_off(sstride, S, red));
   int64_t *epi_cols = epi_rows + 128;
   const bool offload = p.mscratch != nullptr;  // ABC: epilogue warps update C from the M tiles
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+#ifdef STC_EXPERIMENT_ALIGNCHECK
+  if (tid == 0 && (smem_u32(stages) & 1023) != 0)
+    printf("[align] block %d smem base %u stages %u\n", blockIdx.x, smem_u32(smem), smem_u32(stages));
+#endif
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);

@@ -286,6 +286,8 @@ def contract(spec: ContractionSpec, a, b, c, level: int, variant, params: Blocki
         need = ctypes.c_size_t()
         _lib.check(L.stc_workspace_size(ctypes.byref(prob), ctypes.byref(need)))
         ws = torch.empty(max(int(need.value), 256), dtype=torch.uint8, device=dev)
+        if os.environ.get("STC_DEBUG_POISON"):  # debugging aid: the library must not read stale workspace
+            ws.fill_(int(os.environ["STC_DEBUG_POISON"]) & 255)
         stream = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         st = _lib.Stats()
