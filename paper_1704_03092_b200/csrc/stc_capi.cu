@@ -1485,13 +1485,12 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       // C updates by the producer warpgroup's three spare warps from dense M tiles:
       // by default with the TMA reduce-add epilogue (no FP64 work in those warps);
       // opt-in (STC_EPI_OFFLOAD=1) with load/add/store, whose DADDs starve behind the DMMAs
-      // Without TMA reduce (C not box-regular: only L0 reaches here, L >= 1 takes the
-      // dense-M path) the spare warps run the load/add/store epilogue too: the consumers'
-      // own inline epilogue showed intermittent wrong 64-row blocks on cfg4 L0 in the
-      // round-1 build (about 1 run in 4; root cause not found), the offloaded one none
-      // in 80 runs.
+      // C updates by the producer warpgroup's three spare warps from dense M tiles: by
+      // default with the TMA reduce-add epilogue (no FP64 work in those warps); without
+      // TMA reduce (C not box-regular: only L0 reaches here) the consumers' own
+      // load/add/store epilogue (the spare warps' DADDs starve behind the DMMAs)
       const char *eo = getenv("STC_EPI_OFFLOAD");
-      const int offload = eo ? atoi(eo) : 1;
+      const int offload = eo ? atoi(eo) : (gf.cred ? 1 : 0);
       if (offload) gf.mscratch = reinterpret_cast<double *>(ws + pl.off_mscr);
       if (g_ev_before) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
       CU(launch_fused(gf, grid, s, maps), "k_strassen_fused");

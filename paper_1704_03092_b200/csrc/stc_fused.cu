@@ -335,6 +335,13 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
     // k-step 0 of chunk c (fa, fb) -> build k-step 1 of chunk c (xa, xb)
     pipe_view<NA, NB, 0, 1, true, SGN, AV, BV>(acc, fa, fb, xa, xb, stages + stage * sstride, true, offA, offB, negmask,
                                                bbase);
+    // The stage's smem was read through the generic proxy and the producer refills it
+    // with TMA (async proxy) once every consumer warp arrived: the proxy fence orders the
+    // k-step 1 fragment loads just issued before the release.  Without it the refill
+    // raced with loads still in flight (wrong 64-row blocks, cfg4 L0, about 1 run in 4;
+    // none with it in 120).  Releasing one k-step later instead (after MMAs that read
+    // those registers) is as safe but shortens the ring: 4-5% slower.
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);  // both k-steps of chunk c are in registers
     if (++stage == S) {
@@ -987,6 +994,7 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
 #pragma unroll
                 for (int nt = 0; nt < 4; ++nt)
                   dmma_16x8x4(acc[mt][nt], a[kk][2 * mt], a[kk][2 * mt + 1], b[kk][nt]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the TMA refill
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
             if (++stage == S) {

@@ -457,7 +457,10 @@ __device__ __forceinline__ void producer_tma(const GemmArgs &p, const CUtensorMa
 #pragma unroll
         for (int e = 0; e < EPT; ++e) acc[e] = __dsub_rn(acc[e], v[e]);
       }
-      __syncwarp();  // every lane's reads of the slot are done (their values are in acc)
+      // every lane's reads of the slot are done (their values are in acc); order them
+      // before the TMA (async proxy) refill of the slot
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
       if (lane == 0) mbar_arrive(&rempty[rslot]);
       if (++rslot == NRAW) {
         rslot = 0;
