@@ -1,25 +1,36 @@
 """Benchmark of the B200 Strassen tensor-contraction path (one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1], the config the headline metric is quoted on):
-  2-level ABC Strassen, float64, permuted non-unit-stride layouts
-  C[a,i,b,j] += sum_{e,f} A[e,a,f,b] * B[j,f,i,e], all extents 64 (m = n = k = 4096),
-  row-major storage in the label order written, entries uniform[-1, 1] from numpy
-  default_rng(seed) (A: seed, B: seed + 1), C = 0.  Synthetic data with the
-  benchmark's shapes and distribution (there is no dataset for this path).
+Headline workload: BASELINE.json configs[4] (cfg5), the config the north star
+quotes at 1/2/4/8 GPUs -- 2-level ABC Strassen in FP64,
+  C[a,b,c,i,j,k] += sum_{e,f,g} A[a,b,c,e,f,g] * B[e,f,g,i,j,k], all extents 32
+  (m = n = k = 32768, 8 GiB per operand), row-major, entries uniform[-1,1) from a
+  seed (A: 2017, B: 2018; the counter-based generator stc_fill_uniform, so each
+  rank generates exactly its part in HBM), C = 0 before the warm-up.
+Synthetic data with the config's shapes and distribution (there is no dataset).
 
-A "step" is one contract(spec, A, B, C, level=2, variant=ABC) call.
-  value  -- effective GFLOP/s = 2 m n k * steps * ranks / (max over ranks of the
-            device time of the timed steps), inputs resident in HBM (384 MiB of
-            operands per rank > 126 MB L2, so no explicit L2 flush).
+A "step" is one contract(spec, A, B, C, level=2, variant=ABC) call over the
+rank's part of the problem.  At N GPUs (torchrun, one process per GPU) the n
+bundle is split on its label i (32 / N values per rank, shard.plan_shards):
+every rank holds all of A, its slice of B and the full C storage, and contracts
+its shard of C -- no data-path collective (strong scaling of one problem).
+  value  -- effective GFLOP/s = 2 m n k * steps / (max over ranks of the device
+            time of the timed steps): the whole problem's classical flops.
+            Operands (24 GiB at N = 1) are far larger than the 126 MB L2: no flush.
+  allgather (N > 1) -- the optional NCCL all-gather of the C shards
+            (shard.gather_shards), timed separately, and the value with it.
   e2e    -- the same metric through the public API with HOST operands in pinned
-            memory: every step uploads A, B, C, contracts and downloads C.
-Multi-GPU (torchrun, one process per GPU): the n bundle of an N-times wider
-problem is split into N independent shards, one cfg2-sized contraction per rank,
-no data-path collective (weak scaling).
+            memory: every step uploads the rank's A, B shard and C shard,
+            contracts and downloads the C shard (stc_contract_host pipeline).
+  secondary (N = 1) -- the north star's bar point (m = n = k = 16384,
+            abij-abef-efij, extents 128, L2 ABC) and cfg2 (4096^3 permuted
+            layouts, L2 ABC), device-resident.
+  roofline -- the fused DMMA kernel's own CUDA events over the timed steps.
 
---impl reference times the reference algorithm on the host CPU (the C restatement
-in oracle/, OpenMP over the jr loop like the reference's thread pool, all host
-cores) on a bounded n-shard sample of the same workload.
+--impl reference times the reference's own CPU implementation (strassen_tc,
+installed under baseline/_ref; the oracle/ C port when it cannot be imported),
+all host cores, on a bounded sample of cfg5: the sub-problem a < 2, i < 1,
+j < 8 (m = 2048, n = 256, k = 32768, 34.4 GFLOP, the full k), with the full
+tensors' values.  Its rate is reported as measured on that sample.
 """
 
 from __future__ import annotations
@@ -38,14 +49,19 @@ import numpy as np
 ROOT = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-SPEC_LINE = "aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;"
+CFG5 = "abcijk abcefg efgijk & a:32;b:32;c:32;i:32;j:32;k:32;e:32;f:32;g:32;"
+BAR = "abij abef efij & a:128;b:128;i:128;j:128;e:128;f:128;"
+CFG2 = "aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;"
+SHARD_LABEL = "i"
 LEVEL, VARIANT = 2, "abc"
-SEED = 2017
+SEED_A, SEED_B = 2017, 2018
+# CPU sample of cfg5: the leading ranges of a, i and j (full k): m = 2048, n = 256
+CPU_SAMPLE = {"a": 2, "i": 1, "j": 8}
 # FP64 tensor-core (DMMA) peak of this pool's B200, measured with tools/fp64_peak.cu
-# (register-resident mma.sync.m8n8k4/m16n8k4/m16n8k16 f64 loops, 148 SMs, best of 5):
-# profiles/fp64_peak_r01.txt.  MEASURED_PEAKS.json has no FP64 entry.
+# (register-resident mma.sync f64 loops, 148 SMs, best of 5): profiles/fp64_peak_r01.txt.
+# MEASURED_PEAKS.json has no FP64 entry.
 FP64_TC_PEAK_TFLOPS = 37.0
-CPU_SAMPLE_J = 8  # --impl reference / cpu_baseline: j extent of the n-shard sample (of 64)
+METRIC = "effective fp64 GFLOPS (2mnk/t) and fraction of FP64 tensor peak, 1/2/4/8 B200"
 
 
 def row_major(ext):
@@ -54,25 +70,6 @@ def row_major(ext):
         out.append(run)
         run *= e
     return tuple(reversed(out))
-
-
-def make_inputs(spec, rank, j_extent=None):
-    """Host arrays (numpy) of A, B, C for this rank's n-shard."""
-    import paper_1704_03092_b200 as stc
-
-    ext = dict(spec.extents)
-    if j_extent is not None:
-        ext["j"] = j_extent
-    sp = stc.ContractionSpec(spec.labels_c, spec.labels_a, spec.labels_b, ext)
-
-    def tensor(labels, seed, zero=False):
-        e = sp.tensor_extents(labels)
-        n = int(np.prod(e))
-        data = np.zeros(n) if zero else np.random.default_rng(seed).uniform(-1.0, 1.0, n)
-        return stc.DenseTensor(e, row_major(e), data)
-
-    # A is shared by every shard; B and C are the rank's slice of the J bundle
-    return sp, tensor(sp.labels_a, SEED), tensor(sp.labels_b, SEED + 1 + 1000 * rank), tensor(sp.labels_c, 0, True)
 
 
 class ClockSampler:
@@ -85,19 +82,19 @@ class ClockSampler:
     def __init__(self, device_index: int):
         self.proc = None
         self.idx = device_index
+        self.lines = []
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
         time.sleep(0.2)
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
         if self.proc is not None:
             time.sleep(0.1)
             self.proc.terminate()
@@ -124,62 +121,157 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_reference_run(steps: int, warmup: int, j_extent: int):
-    """Time the reference algorithm (oracle/ C restatement) on a bounded n-shard."""
-    import oracle
+# ------------------------------------------------------------------ CPU reference
+def _cpu_model():
+    try:
+        return [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
+    except (OSError, IndexError):
+        return "unknown"
 
-    import paper_1704_03092_b200 as stc
 
-    spec = stc.parse_benchmark_line(SPEC_LINE)
-    sp, a, b, c = make_inputs(spec, 0, j_extent)
+def _reference_module():
+    """The reference package (baseline/_ref) or None."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "strassen_tc").is_dir():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_stc")
+    sys.path.insert(0, str(ref))
+    try:
+        import strassen_tc  # noqa: F401
+
+        return strassen_tc
+    except Exception:  # numba missing or broken: use the port
+        sys.path.remove(str(ref))
+        return None
+
+
+def cpu_reference_run(steps: int, warmup: int):
+    """Time the reference's CPU path on the bounded cfg5 sample (all host cores).
+
+    The reference itself (strassen_tc.contract from baseline/_ref, kind
+    "reference") when importable, else the oracle/ C restatement ("port").  The
+    sample's inputs carry the full cfg5 tensors' values (oracle/synth.py)."""
+    from oracle import synth
+
+    mod = _reference_module()
     threads = len(os.sched_getaffinity(0))
-    oracle.build()
+    if mod is not None:
+        spec0 = mod.parse_benchmark_line(CFG5)
+        mk, kind = mod.DenseTensor, "reference"
+    else:
+        import oracle
+
+        import paper_1704_03092_b200 as stc
+
+        oracle.build()
+        spec0 = stc.parse_benchmark_line(CFG5)
+        mk, kind = stc.DenseTensor, "port"
+    full = dict(spec0.extents)
+    ext = dict(full)
+    ext.update(CPU_SAMPLE)
+    sp = type(spec0)(spec0.labels_c, spec0.labels_a, spec0.labels_b, ext)
+
+    def tensor(labels, seed, zero=False):
+        e = tuple(ext[x] for x in labels)
+        data = np.zeros(int(np.prod(e))) if zero else synth.tensor_values(seed, e, row_major(
+            tuple(full[x] for x in labels)), 0)
+        return mk(e, row_major(e), data)
+
+    a, b, c = tensor(sp.labels_a, SEED_A), tensor(sp.labels_b, SEED_B), tensor(sp.labels_c, 0, True)
+    if mod is not None:
+        run = lambda: mod.contract(sp, a, b, c, LEVEL, mod.Variant.ABC, threads=threads).seconds
+        # numba compiles on first use: one tiny call outside the measured steps
+        tiny = mod.parse_benchmark_line("abij abef efij & a:4;b:4;i:4;j:4;e:4;f:4;")
+        ta, tb, tc = (mod.DenseTensor((4,) * 4, row_major((4,) * 4), np.ones(256)) for _ in range(3))
+        mod.contract(tiny, ta, tb, tc, LEVEL, mod.Variant.ABC, threads=threads)
+    else:
+        import oracle
+
+        run = lambda: oracle.contract(sp, a, b, c, LEVEL, VARIANT, threads=threads)["seconds"]
     times = []
     for i in range(warmup + steps):
-        st = oracle.contract(sp, a, b, c, LEVEL, VARIANT, threads=threads)
+        t = run()
         if i >= warmup:
-            times.append(st["seconds"])
+            times.append(t)
     flops = 2.0 * sp.n_i * sp.n_j * sp.n_p
     value = flops * len(times) / sum(times) / 1e9
-    try:
-        model = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
-    except (OSError, IndexError):
-        model = "unknown"
-    sample = (f"cfg2 n-shard j={j_extent}/64 (m={sp.n_i}, n={sp.n_j}, k={sp.n_p}), L{LEVEL} {VARIANT.upper()}, "
-              f"reference blocking (96,4096,256,8,4,4), {threads} threads, {model}")
-    return value, threads, sample, sum(times) / len(times)
+    sample = (f"cfg5 sub-problem a<{CPU_SAMPLE['a']}, i<{CPU_SAMPLE['i']}, j<{CPU_SAMPLE['j']} "
+              f"(m={sp.n_i}, n={sp.n_j}, k={sp.n_p}, {flops / 1e9:.1f} GFLOP per step, full-tensor values), "
+              f"L{LEVEL} {VARIANT.upper()}, "
+              + ("strassen_tc.contract from baseline/_ref (numba)" if kind == "reference"
+                 else "oracle/stc_oracle.c port (OpenMP over jr)")
+              + f", {threads} threads, {_cpu_model()}; rate as measured on the sample")
+    return value, threads, kind, sample, sum(times) / len(times)
+
+
+# ------------------------------------------------------------------ GPU arm
+def _spec(line):
+    import paper_1704_03092_b200 as stc
+
+    return stc.parse_benchmark_line(line)
+
+
+def _time_config(line, steps, warmup, dev):
+    """Effective TFLOP/s of L2 ABC on a device-resident config (secondary keys)."""
+    import torch
+
+    import paper_1704_03092_b200 as stc
+    from paper_1704_03092_b200.synth import uniform_tensor
+
+    spec = _spec(line)
+    a = uniform_tensor(SEED_A, spec.tensor_extents(spec.labels_a), dev)
+    b = uniform_tensor(SEED_B, spec.tensor_extents(spec.labels_b), dev)
+    ec = spec.tensor_extents(spec.labels_c)
+    c = stc.DenseTensor(ec, row_major(ec), torch.zeros(int(np.prod(ec)), dtype=torch.float64, device=dev))
+    for _ in range(warmup):
+        stc.contract(spec, a, b, c, LEVEL, VARIANT, synchronize=False)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        stc.contract(spec, a, b, c, LEVEL, VARIANT, synchronize=False)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    s = t0.elapsed_time(t1) * 1e-3 / steps
+    tf = 2.0 * spec.n_i * spec.n_j * spec.n_p / s / 1e12
+    del a, b, c
+    torch.cuda.empty_cache()
+    return {"line": line, "level": LEVEL, "variant": VARIANT.upper(), "ms_per_step": s * 1e3,
+            "effective_tflops": tf, "frac_of_fp64_peak": tf / FP64_TC_PEAK_TFLOPS, "steps": steps}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
     warmup = max(args.warmup, 3)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    metric = "effective fp64 GFLOPS (2mnk/t) and fraction of FP64 tensor peak, 1/2/4/8 B200"
-    config = {"workload": "cfg2: C[a,i,b,j] += A[e,a,f,b] B[j,f,i,e], extents 64 (m=n=k=4096), permuted layouts",
-              "level": LEVEL, "variant": VARIANT.upper(), "m": 4096, "n": 4096 * world, "k": 4096,
-              "n_per_rank": 4096, "parallelism": f"nsplit{world}" if world > 1 else "single",
-              "l2_flush": "none: 384 MiB of operands per rank > 126 MB L2", "seed": SEED}
+    config = {"workload": "cfg5: C[a,b,c,i,j,k] += A[a,b,c,e,f,g] B[e,f,g,i,j,k], extents 32 "
+                          "(m=n=k=32768), row-major", "level": LEVEL, "variant": VARIANT.upper(),
+              "m": 32768, "n": 32768, "k": 32768, "shard_label": SHARD_LABEL, "n_per_rank": 32768 // world,
+              "parallelism": f"nsplit{world}" if world > 1 else "single",
+              "l2_flush": "none: 24 GiB of operands at N=1 (A 8 GiB + slices per rank) >> 126 MB L2",
+              "seed": [SEED_A, SEED_B], "generator": "counter-based uniform[-1,1) (stc_fill_uniform)"}
 
     if args.impl == "reference":
         if rank != 0:
             return
-        value, threads, sample, per_step = cpu_reference_run(args.steps, warmup, CPU_SAMPLE_J)
-        line = {"metric": metric, "impl": "reference", "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
+        value, threads, kind, sample, per_step = cpu_reference_run(args.steps, warmup)
+        line = {"metric": METRIC, "impl": "reference", "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic uniform[-1,1] (seeded)",
-                "config": config,
-                "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": "port",
-                                 "sample": sample},
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic uniform[-1,1) (seeded, counter-based)", "config": config,
+                "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": kind, "sample": sample},
                 "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -187,33 +279,54 @@ def main():
     import torch
 
     import paper_1704_03092_b200 as stc
+    from paper_1704_03092_b200 import shard
+    from paper_1704_03092_b200.synth import uniform_tensor
 
     dist = None
     if world > 1:
         import torch.distributed as dist
 
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
 
-    spec = stc.parse_benchmark_line(SPEC_LINE)
-    sp, a_h, b_h, c_h = make_inputs(spec, rank)
-    A, B, C = a_h.to_device(dev), b_h.to_device(dev), c_h.to_device(dev)
+    spec = _spec(CFG5)
+    ea, eb, ec = (spec.tensor_extents(l) for l in (spec.labels_a, spec.labels_b, spec.labels_c))
+    # rank's part: all of A, B[:, shard] (generated as its own compact slice), and the
+    # full C storage (the shard is a view; the optional all-gather fills the rest)
+    c_full = stc.DenseTensor(ec, row_major(ec), torch.zeros(int(np.prod(ec)), dtype=torch.float64, device=dev))
+    sh = shard.plan_shards(spec, c_full, world, SHARD_LABEL)[rank]
+    sp = shard.shard_spec(spec, sh)
+    A = uniform_tensor(SEED_A, ea, dev)
+    ax = spec.labels_b.index(SHARD_LABEL)
+    B = uniform_tensor(SEED_B, sp.tensor_extents(sp.labels_b), dev, full_strides=row_major(eb),
+                       base=sh.start * row_major(eb)[ax])
+    C = shard.shard_tensor(c_full, spec.labels_c, sh)
     torch.cuda.synchronize()
-    flops = 2.0 * sp.n_i * sp.n_j * sp.n_p
+    flops_rank = 2.0 * sp.n_i * sp.n_j * sp.n_p
+    flops_job = 2.0 * spec.n_i * spec.n_j * spec.n_p
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     for _ in range(warmup):
-        st = stc.contract(sp, A, B, C, LEVEL, VARIANT, synchronize=False)
+        stc.contract(sp, A, B, C, LEVEL, VARIANT, synchronize=False)
     barrier()
 
-    # ---- timed region: K steps, device events, gemm events per step ------------
+    # ---- timed region: K steps, device events; fused-kernel events per step -----
     stream = torch.cuda.current_stream()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for e0, e1 in ev:  # torch creates the cudaEvent_t lazily, on first record
@@ -229,86 +342,118 @@ def main():
             launches += st.kernel_launches
         t1.record(stream)
         barrier()
-    elapsed = t0.elapsed_time(t1) * 1e-3
+    elapsed = max_over_ranks(t0.elapsed_time(t1) * 1e-3)
     gemm_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    value = flops_job * args.steps / elapsed / 1e9
+
+    # ---- optional all-gather of the C shards (NCCL), timed on its own ----------
+    allgather = None
     if dist is not None:
-        tt = torch.tensor([elapsed], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed = float(tt.item())
-    value = flops * args.steps * world / elapsed / 1e9
+        reps = 3
+        shard.gather_shards(spec, c_full, rank, world, SHARD_LABEL)  # warm (buffers, NCCL channels)
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(reps):
+            shard.gather_shards(spec, c_full, rank, world, SHARD_LABEL)
+        g1.record(stream)
+        barrier()
+        ag = max_over_ranks(g0.elapsed_time(g1) * 1e-3 / reps)
+        allgather = {"ms": ag * 1e3, "bytes_per_rank_received": int(np.prod(ec)) * 8 * (world - 1) // world,
+                     "value_with_allgather": flops_job / (elapsed / args.steps + ag) / 1e9,
+                     "how": "shard.gather_shards: all_gather_into_tensor into a shard-major buffer + one "
+                            "strided copy per shard (NCCL)"}
+    del c_full
+    C = None
+    torch.cuda.empty_cache()
 
     # ---- e2e: public API with pinned host operands, H2D + D2H inside each step --
-    def pinned(t):
-        return stc.DenseTensor(t.extents, t.strides, torch.from_numpy(t.data).pin_memory(), t.base_offset)
+    def pinned_copy(t):
+        h = torch.empty(t.data.numel(), dtype=torch.float64, pin_memory=True)
+        h.copy_(t.data)
+        return stc.DenseTensor(t.extents, t.strides, h, t.base_offset)
 
-    a_p, b_p, c_p = pinned(a_h), pinned(b_h), pinned(c_h)
-    for _ in range(2):
-        stc.contract(sp, a_p, b_p, c_p, LEVEL, VARIANT)  # warm the staging path
-    barrier()
-    w0 = time.perf_counter()
-    for _ in range(args.e2e_steps):
-        stc.contract(sp, a_p, b_p, c_p, LEVEL, VARIANT)
-    barrier()
-    e2e_elapsed = time.perf_counter() - w0
-    if dist is not None:
-        tt = torch.tensor([e2e_elapsed], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_elapsed = float(tt.item())
-    e2e_value = flops * args.e2e_steps * world / e2e_elapsed / 1e9
-    bytes_of = lambda t: t.data.numel() * 8
-    h2d = bytes_of(a_p) + bytes_of(b_p) + bytes_of(c_p)
-    d2h = bytes_of(c_p)
+    e2e = None
+    try:
+        a_p, b_p = pinned_copy(A), pinned_copy(B)
+        del A, B
+        torch.cuda.empty_cache()
+        esc = sp.tensor_extents(sp.labels_c)
+        c_p = stc.DenseTensor(esc, row_major(esc), torch.zeros(int(np.prod(esc)), dtype=torch.float64,
+                                                               pin_memory=True))
+        stc.contract(sp, a_p, b_p, c_p, LEVEL, VARIANT)  # warm the host pipeline's plans and buffers
+        barrier()
+        w0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            stc.contract(sp, a_p, b_p, c_p, LEVEL, VARIANT)
+        barrier()
+        e2e_elapsed = max_over_ranks(time.perf_counter() - w0)
+        nbytes = lambda t: t.data.numel() * 8
+        e2e = {"value": flops_job * args.e2e_steps / e2e_elapsed / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": nbytes(a_p) + nbytes(b_p) + nbytes(c_p), "d2h_bytes_per_step": nbytes(c_p),
+               "steps": args.e2e_steps,
+               "timing": "wall clock around contract() on pinned host DenseTensors (per rank: A, B shard, "
+                         "C shard), max over ranks"}
+        del a_p, b_p, c_p
+    except (RuntimeError, MemoryError) as exc:  # host memory for pinned operands
+        e2e = {"value": None, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+               "error": str(exc)[:200]}
 
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (fused DMMA Strassen kernel) ----------
-    # achieved = 2mnk / t of the launch (the classical flop count, the
-    # metric's own unit; up to (8/7)^L above the pipe's peak in principle).  The flops the
-    # tensor pipe actually executes, 7^L leaf products of the padded quadrants, are reported
-    # beside it as the pipe utilisation.
-    q = 1 << LEVEL  # cfg2's bundles divide by 2^L: no PAD
-    alg_flops = flops  # 2 m n k of the contraction one launch performs
+    # ---- roofline of the dominant kernel (the fused DMMA Strassen kernel) -------
+    # achieved = the classical 2 m n k of the launch / its duration
+    # (up to (8/7)^L above the pipe's peak in principle); the flops the tensor pipe
+    # executes (7^L leaf products of the quadrants) are reported beside it.
+    q = 1 << LEVEL
     exec_flops = (7 ** LEVEL) * 2.0 * (sp.n_i // q) * (sp.n_j // q) * (sp.n_p // q)
     gemm_avg = sum(gemm_ms) / len(gemm_ms) * 1e-3
-    achieved = alg_flops / gemm_avg / 1e12
+    achieved = flops_rank / gemm_avg / 1e12
     traffic = None
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
         try:
-            traffic = json.loads(tfile.read_text()).get("cfg2_L2_abc_gemm_dram_bytes")
+            traffic = json.loads(tfile.read_text()).get("cfg5_L2_abc_gemm_dram_bytes")
         except (ValueError, OSError):
             traffic = None
     roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_TC_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP64_TC_PEAK_TFLOPS, "traffic": traffic,
-                "kernel": ("k_strassen_fused (TMA views; A sums by the summing warpgroup, B sums in the DMMA fragment loads)" if st.fast_blocks
-                           else "k_strassen_gemm (gather producer, Strassen sums in smem)"),
+                "kernel": "k_strassen_fused" if st.fast_blocks else "k_strassen_gemm",
                 "kernel_ms": gemm_avg * 1e3, "kernel_share_of_step": gemm_avg / (elapsed / args.steps),
-                "algorithmic_flops_per_launch": alg_flops,
-                "algorithmic_unit": "2*m*n*k per contraction (SURVEY.md 8(d))",
+                "algorithmic_flops_per_launch": flops_rank,
+                "algorithmic_unit": "2*m*n*k of the rank's contraction (SURVEY.md 8(d))",
                 "executed_flops_per_launch": exec_flops,
                 "executed_tflops": exec_flops / gemm_avg / 1e12,
                 "executed_frac_of_pipe_peak": exec_flops / gemm_avg / 1e12 / FP64_TC_PEAK_TFLOPS,
-                "peak_source": "measured FP64 DMMA peak, tools/fp64_peak.cu, burst (MEASURED_PEAKS.json has no FP64)"}
+                "peak_source": "builder-measured FP64 DMMA burst peak, tools/fp64_peak.cu (MEASURED_PEAKS.json "
+                               "has no FP64 entry)"}
+
+    secondary = None
+    if world == 1 and not args.no_secondary:
+        secondary = {"bar_16384": _time_config(BAR, 3, 1, dev), "cfg2": _time_config(CFG2, 10, 3, dev)}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            cval, threads, sample, _ = cpu_reference_run(1, 0, CPU_SAMPLE_J)
-            cpu = {"value": cval, "unit": "GFLOP/s", "cores": threads, "kind": "port", "sample": sample}
+            cval, threads, kind, sample, _ = cpu_reference_run(1, 0)
+            cpu = {"value": cval, "unit": "GFLOP/s", "cores": threads, "kind": kind, "sample": sample}
         except Exception as exc:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
 
-    line = {"metric": metric, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+    line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic uniform[-1,1], numpy default_rng(2017/2018)", "config": config,
-            "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "steps": args.e2e_steps, "timing": "wall clock around contract() on pinned host DenseTensors"},
-            "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks.summary(),
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic uniform[-1,1) from seeds 2017/2018 (counter-based, generated in HBM)",
+            "config": config, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
+            "cpu_baseline": cpu, "clocks": clocks.summary(),
             "fraction_of_fp64_peak": value / world / 1e3 / FP64_TC_PEAK_TFLOPS}
+    if allgather is not None:
+        line["allgather"] = allgather
+    if secondary is not None:
+        line["secondary"] = secondary
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -185,6 +185,34 @@ int stc_unpack_sum(double *out, int64_t ldo, int64_t m, int64_t n, const double 
 int stc_sq_norms(int ndim, const int64_t *extents, const double *x, const int64_t *x_strides, int64_t x_base,
                  const double *ref, const int64_t *ref_strides, int64_t ref_base, double *out, void *stream);
 
+/* ---- plan introspection (tests / tools; no reference counterpart) ----
+ * Which execution path stc_contract takes for a problem on a `grid`-CTA launch
+ * (0: 148).  Host-only: needs no device. */
+typedef struct {
+  int32_t ticketed;      /* ABC with C updated by the kernel (else dense M + accumulate)  */
+  int32_t presum;        /* operand sums pre-formed by k_presum into per-term slots       */
+  int32_t need_pack;     /* operands repacked (views not regular boxes)                   */
+  int32_t tshape;        /* fused CTA tile: 0 128x128, 1 64x256, 2 256x64                 */
+  int32_t fused_direct;  /* fused kernel on the operands' own views                       */
+  int32_t c_boxes;       /* C quadrant tiles are TMA-reduce boxes                         */
+  int32_t batch, nbatches, terms, _pad;
+  int64_t tiles, mq_pad, nq_pad, kq_pad;
+  size_t workspace;
+} stc_plan_info;
+int stc_plan_describe(const stc_problem *p, int grid, stc_plan_info *info);
+
+/* ---- synthetic inputs (bench / tests; no reference counterpart) ----
+ * out (compact, row-major over extents[0..ndim)) gets, at multi-index i,
+ * u(seed, base + sum_d i_d * strides[d]) with the counter-based uniform[-1, 1)
+ * of oracle/synth.py (splitmix64 of the element's flat index in the FULL
+ * tensor): a whole tensor (strides = its row-major strides, base 0) or any
+ * slice of it (the full tensor's strides, the slice's base offset) gets the
+ * same values, bit for bit, as numpy produces for it on the host.  The
+ * reference draws its inputs with numpy on the host (tensor.py:125-126); the
+ * BASELINE configs only fix "uniform[-1,1] from seed". */
+int stc_fill_uniform(double *out, int ndim, const int64_t *extents, const int64_t *strides, int64_t base,
+                     uint64_t seed, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

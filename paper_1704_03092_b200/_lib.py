@@ -11,7 +11,7 @@ import ctypes
 import os
 import pathlib
 
-__all__ = ["lib", "Bundle", "Problem", "Stats", "check", "MAX_LABELS", "PAD", "LIB_PATH"]
+__all__ = ["lib", "Bundle", "Problem", "Stats", "PlanInfo", "check", "MAX_LABELS", "PAD", "LIB_PATH"]
 
 LIB_PATH = pathlib.Path(os.environ.get("STC_LIBRARY", pathlib.Path(__file__).resolve().parent / "libstc_b200.so"))
 MAX_LABELS = 16
@@ -53,11 +53,20 @@ class Stats(ctypes.Structure):
                 ("work_items", ctypes.c_int64), ("kernel_launches", ctypes.c_int64)]
 
 
+class PlanInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("ticketed", "presum", "need_pack", "tshape", "fused_direct", "c_boxes",
+                                              "batch", "nbatches", "terms", "_pad")] + \
+               [(n, ctypes.c_int64) for n in ("tiles", "mq_pad", "nq_pad", "kq_pad")] + [("workspace", ctypes.c_size_t)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_ if n != "_pad"}
+
+
 _EXPORTS = (
     "stc_last_error", "stc_abi_version", "stc_workspace_size", "stc_contract", "stc_bundle_scatter",
     "stc_block_vector", "stc_fused_term_workspace_size", "stc_fused_term", "stc_accumulate_dense",
     "stc_unpack_sum", "stc_sq_norms", "stc_set_kernel_events", "stc_set_c_ready",
-    "stc_host_workspace_size", "stc_contract_host", "stc_host_plan",
+    "stc_host_workspace_size", "stc_contract_host", "stc_host_plan", "stc_fill_uniform", "stc_plan_describe",
 )
 
 _lib = None
@@ -88,6 +97,8 @@ def _declare(l):
     l.stc_host_workspace_size.argtypes = [P(Problem), P(sz)]
     l.stc_contract_host.argtypes = [P(Problem), vp, vp, vp, vp, vp, vp, vp, sz, vp, P(Stats)]
     l.stc_host_plan.argtypes = [P(Problem), P(ctypes.c_int32), P(ctypes.c_int32), P(ctypes.c_int32)]
+    l.stc_fill_uniform.argtypes = [vp, ctypes.c_int, P(i64), P(i64), i64, ctypes.c_uint64, vp]
+    l.stc_plan_describe.argtypes = [P(Problem), ctypes.c_int, P(PlanInfo)]
     for name in _EXPORTS:
         if name not in ("stc_last_error",):
             getattr(l, name).restype = ctypes.c_int if name != "stc_last_error" else ctypes.c_char_p

@@ -265,6 +265,19 @@ VecDesc vec_bundle(const stc_bundle &b, int64_t base, int64_t nq, int64_t tile, 
   return d;
 }
 
+// Per-slot x vectors (mode 2, slot stride = the slot size): a term's op addresses
+// its own slot block of packed operand sums through the pool alone.
+VecDesc slot_vec(int64_t len, int64_t stride, int64_t slot, int64_t nslots) {
+  VecDesc d;
+  memset(&d, 0, sizeof(d));
+  d.mode = 2;
+  d.nq = nslots;
+  d.q_len = d.q_len_pad = d.len = len;
+  d.stride = stride;
+  d.base = slot;
+  return d;
+}
+
 VecDesc vec_affine(int64_t len, int64_t len_pad, int64_t stride) {
   VecDesc d;
   memset(&d, 0, sizeof(d));
@@ -322,6 +335,10 @@ struct Plan {
   // Naive and the dense-M ABC mode (many terms in flight per tile: dense M slots, then one
   // ordered accumulate pass -- the same additions in the same order, without ticket chains)
   bool ticketed = false;
+  // ABC with pre-summed operands (k_presum): the 7^L operand sums of each side are
+  // formed once per element position into per-term slots (term batches under the
+  // workspace cap), and the fused kernel runs every term with one view per side
+  bool presum = false;
   std::vector<int> seq;  // term order of the dense-M batches and accumulate lists
   size_t off_pool = 0, off_vecs = 0, off_tab = 0, off_tickets = 0, off_counters = 0, off_M = 0, off_pa = 0,
          off_pb = 0, off_acc = 0, total = 0;
@@ -392,6 +409,19 @@ FusedSides packed_sides(const Plan &pl);
 FusedSides naive_sides(const Plan &pl);
 bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, const double *A, const double *B,
                 const double *C, GemmArgs &g, CUtensorMap maps[3], CoordJobs &jobs);
+
+// Pre-summed operands for ticketed ABC at L = 1, 2 (STC_PRESUM_OPS = 0 / 1 forces
+// it off / on).  The sums cost one HBM pass (4^L quadrant reads + 7^L slot writes per
+// element position and side) and take every DADD off the FP64 pipe the DMMAs use.
+bool presum_wanted(const stc_problem *p, const Plan &pl) {
+  if (pl.level < 1 || pl.level > 2 || pl.tshape != 0) return false;
+  if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
+  if (const char *e = getenv("STC_FUSED"))
+    if (atoi(e) == 0) return false;
+  if (const char *e = getenv("STC_PRESUM_OPS")) return atoi(e) != 0;
+  const int64_t qa = pl.mq_pad * pl.kq_pad, qb = pl.kq_pad * pl.nq_pad;
+  return std::min(qa, qb) >= ((int64_t)1 << 20);
+}
 
 int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   if (!p) return fail(STC_EINVAL, "null problem");
@@ -482,14 +512,6 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   pl.bc = add(vec_bundle(p->b_col, p->b_base, pl.Q, pl.tn, tj));
   pl.cr = add(vec_bundle(p->c_row, 0, pl.Q, pl.tm, ti));
   pl.cc = add(vec_bundle(p->c_col, p->c_base, pl.Q, pl.tn, tj));
-  if (pl.variant == STC_VARIANT_NAIVE) {
-    // packed operand sums: Apack[k][x] (ld mq_pad), Bpack[k][x] (ld nq_pad)
-    // packed operand sums per term slot, oriented like the source (unit stride in k ->
-    // [x][k] slots, else [k][x]) so the unpack reads and writes coalesce
-    // (the x vectors, per term slot, follow once the batch is known)
-    pl.dka = add(vec_affine(pl.kq_pad, pl.kq_pad, pl.a_kfast ? 1 : pl.mq_pad));
-    pl.dkb = add(vec_affine(pl.kq_pad, pl.kq_pad, pl.b_kfast ? 1 : pl.nq_pad));
-  }
 
   pl.terms = strassen_terms(pl.level);
   for (const Term &t : pl.terms) pl.max_ops = std::max(pl.max_ops, (int)std::max(t.a.size(), t.b.size()));
@@ -515,6 +537,25 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     const bool dense = T > 1 && (de ? atoi(de) != 0
                                     : (pl.grid >= 4 * P || !c_boxes_regular(p, pl.ti, pl.tj, pl.level)));
     pl.ticketed = !dense;
+  }
+  // Operand sums pre-formed into per-term slots (k_presum): ABC and AB when worth it
+  // (AB with pre-summed operands is the Naive schedule: the same M products), and
+  // always for Naive (its explicit submatrix copies) at L <= 2.
+  pl.presum = pl.variant == STC_VARIANT_NAIVE ? (pl.level >= 1 && pl.level <= 2) : presum_wanted(p, pl);
+  const bool slots = pl.variant == STC_VARIANT_NAIVE || pl.presum;
+  if (slots) {
+    // per-term slots of packed operand sums, oriented like the source (unit stride in
+    // k -> [x][k] slots, else [k][x]) so both sides of the copy coalesce
+    pl.pa_slot = pl.kq_pad * pl.mq_pad;
+    pl.pb_slot = pl.kq_pad * pl.nq_pad;
+    pl.m_slot = pl.ticketed ? 0 : pl.mq_pad * pl.nq_pad;
+    int64_t b = cap_bytes() / std::max<int64_t>((pl.pa_slot + pl.pb_slot + pl.m_slot) * 8, 1);
+    pl.batch = (int)std::max<int64_t>(1, std::min<int64_t>(b, T));
+    pl.nbatches = (int)cdiv(T, pl.batch);
+    pl.dka = add(vec_affine(pl.kq_pad, pl.kq_pad, pl.a_kfast ? 1 : pl.mq_pad));
+    pl.dkb = add(vec_affine(pl.kq_pad, pl.kq_pad, pl.b_kfast ? 1 : pl.nq_pad));
+    pl.dxa = add(slot_vec(pl.mq_pad, pl.a_kfast ? pl.kq_pad : 1, pl.pa_slot, pl.batch));
+    pl.dxb = add(slot_vec(pl.nq_pad, pl.b_kfast ? pl.kq_pad : 1, pl.pb_slot, pl.batch));
   }
   if (pl.ticketed) {
     const std::vector<int> &seq = pl.seq;
@@ -553,40 +594,35 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
       pl.tdesc.push_back(d);
     }
     pl.ntickets = (int64_t)pl.nquads * P;
-    pl.batch = T;
-    pl.nbatches = 1;
-    pl.ncounters = 1;
-  } else {
-    // dense M slots (and packed operands for Naive), batched under the cap
-    const int64_t m_bytes = pl.mq_pad * pl.nq_pad * 8;
-    const int64_t pa_bytes = pl.variant == STC_VARIANT_NAIVE ? pl.kq_pad * pl.mq_pad * 8 : 0;
-    const int64_t pb_bytes = pl.variant == STC_VARIANT_NAIVE ? pl.kq_pad * pl.nq_pad * 8 : 0;
-    const int64_t per = m_bytes + pa_bytes + pb_bytes;
-    int64_t b = cap_bytes() / std::max<int64_t>(per, 1);
-    if (b < 1) b = 1;
-    if (b > T) b = T;
-    pl.batch = (int)b;
-    pl.nbatches = (int)cdiv(T, b);
-    pl.ncounters = pl.nbatches;
-    pl.m_slot = pl.mq_pad * pl.nq_pad;
-    pl.pa_slot = pl.kq_pad * pl.mq_pad;
-    pl.pb_slot = pl.kq_pad * pl.nq_pad;
-    if (pl.variant == STC_VARIANT_NAIVE) {
-      // Naive x vectors per term slot (mode 2, slot stride = the slot size): a
-      // term's op addresses its own slot block through the pool alone
-      auto slot_vec = [&](int64_t len, int64_t stride, int64_t slot) {
-        VecDesc d;
-        memset(&d, 0, sizeof(d));
-        d.mode = 2;
-        d.nq = pl.batch;
-        d.q_len = d.q_len_pad = d.len = len;
-        d.stride = stride;
-        d.base = slot;
-        return d;
-      };
-      pl.dxa = add(slot_vec(pl.mq_pad, pl.a_kfast ? pl.kq_pad : 1, pl.pa_slot));
-      pl.dxb = add(slot_vec(pl.nq_pad, pl.b_kfast ? pl.kq_pad : 1, pl.pb_slot));
+    if (pl.presum) {
+      // one view per side: the term's slot of pre-summed operands (batch-local slot
+      // t % batch of the exec-order position t; the batches run one launch each)
+      pl.ops.clear();
+      for (int s = 0; s < pl.batch; ++s) {
+        pl.ops.push_back({pl.dxa + s * pl.mq_pad, pl.dka, 0, 1.0});
+        pl.ops.push_back({pl.dxb + s * pl.nq_pad, pl.dkb, 0, 1.0});
+      }
+      for (int t = 0; t < T; ++t) {
+        TermDesc &d = pl.tdesc[t];
+        d.a_first = 2 * (t % pl.batch);
+        d.b_first = d.a_first + 1;
+        d.a_count = d.b_count = 1;
+      }
+      pl.ncounters = pl.nbatches;
+    } else {
+      pl.batch = T;
+      pl.nbatches = 1;
+      pl.ncounters = 1;
     }
+  } else {
+    // dense M slots (and the packed operand slots above), batched under the cap
+    pl.m_slot = pl.mq_pad * pl.nq_pad;
+    if (!slots) {
+      int64_t b = cap_bytes() / std::max<int64_t>(pl.m_slot * 8, 1);
+      pl.batch = (int)std::max<int64_t>(1, std::min<int64_t>(b, T));
+      pl.nbatches = (int)cdiv(T, pl.batch);
+    }
+    pl.ncounters = pl.nbatches;
   }
 
   // workspace layout
@@ -600,7 +636,7 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   pl.off_mscr = off;  // fused ABC: EPI_BUFS M tiles per CTA for the epilogue warps
   if (pl.ticketed) off = align256(off + (size_t)pl.grid * EPI_BUFS * BM * BN * 8);
   // fused kernel on repacked operands when the views are not box-regular
-  if (pl.variant != STC_VARIANT_NAIVE) {
+  if (!slots) {
     GemmArgs gd{};
     CUtensorMap md[3];
     CoordJobs jd{};
@@ -634,9 +670,9 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   pl.off_M = off;
   if (!pl.ticketed) off = align256(off + (size_t)pl.batch * pl.m_slot * 8);
   pl.off_pa = off;
-  if (pl.variant == STC_VARIANT_NAIVE) off = align256(off + (size_t)pl.batch * pl.pa_slot * 8);
+  if (slots) off = align256(off + (size_t)pl.batch * pl.pa_slot * 8);
   pl.off_pb = off;
-  if (pl.variant == STC_VARIANT_NAIVE) off = align256(off + (size_t)pl.batch * pl.pb_slot * 8);
+  if (slots) off = align256(off + (size_t)pl.batch * pl.pb_slot * 8);
   pl.total = off;
   return STC_OK;
 }
@@ -662,6 +698,30 @@ struct TmaSide {
   int64_t pstr[2][4];
   int swizzle = 0;  // 0, 64 or 128 (bytes)
 };
+
+// Merge tensor-map dims that address one contiguous run of elements (TMA allows
+// 5): a dim j whose stride is dim i's stride x extent (same part) folds into i when
+// j's box is 1 (the box along i is unchanged) or when j directly follows i and i's
+// box covers its whole extent (the boxes concatenate; smem layout unchanged).  Dim 0
+// keeps its box (the swizzle span bounds the inner box).  cfg5's A[a,b,c,e,f,g]:
+// (g, f, e) and (c, b, a) are each one dim.
+template <class D>
+void merge_dims(std::vector<D> &dims) {
+  for (bool changed = true; changed;) {
+    changed = false;
+    for (size_t i = 0; i < dims.size() && !changed; ++i)
+      for (size_t j = 0; j < dims.size() && !changed; ++j) {
+        if (i == j || dims[i].isx != dims[j].isx || dims[j].str != dims[i].str * dims[i].ext) continue;
+        const bool fold = dims[j].box == 1;
+        const bool concat = i > 0 && j == i + 1 && dims[i].box == dims[i].ext;
+        if (!fold && !concat) continue;
+        if (concat) dims[i].box *= dims[j].box;
+        dims[i].ext *= dims[j].ext;
+        dims.erase(dims.begin() + j);
+        changed = true;
+      }
+  }
+}
 
 // Tile sub-box of a bundle: per label, the extent covered by one tile of
 // `tile` consecutive tile-order indices, and the labels in tile order.
@@ -718,6 +778,7 @@ bool plan_tma_side(const stc_bundle &xb, const Tiling &tx, const stc_bundle &kb,
     for (int d = 0; d < b.nlab; ++d)
       if (b.ext[d] > 1 && tb[d] == 1) dims.push_back({b.ext[d], b.str[d], 1, pass == 0, d});
   }
+  merge_dims(dims);
   if (dims.empty() || dims.size() > 5) return false;
   if (dims[0].str != 1) return false;                          // unit stride leads the box
   if (kfast && dims[0].box != BK) return false;                // one swizzled 128-byte row per x
@@ -859,6 +920,7 @@ bool plan_fused_side(const stc_bundle &xb, const Tiling &tx, const stc_bundle &k
     for (int d = 0; d < b.nlab; ++d)
       if (b.ext[d] > 1 && tb[d] == 1) dims.push_back({b.ext[d], b.str[d], 1, pass == 0});
   }
+  merge_dims(dims);
   if (dims.empty() || dims.size() > 5) return false;
   for (size_t d = 0; d < dims.size(); ++d) {
     if (dims[d].str <= 0 || dims[d].box > 256 || dims[d].ext >= (int64_t)1 << 31) return false;
@@ -925,6 +987,7 @@ bool plan_cred_side(const stc_bundle &rb, const Tiling &tr, const stc_bundle &cb
     for (int d = 0; d < b.nlab; ++d)
       if (b.ext[d] > 1 && tb[d] == 1) dims.push_back({b.ext[d], b.str[d], 1, pass == 0});
   }
+  merge_dims(dims);
   if (dims.size() > 5) return false;
   for (size_t d = 0; d < dims.size(); ++d) {
     if (dims[d].str <= 0 || dims[d].box > 256 || dims[d].ext >= (int64_t)1 << 31) return false;
@@ -1098,7 +1161,8 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
   if (const char *e = getenv("STC_FUSED"))
     if (atoi(e) == 0) return false;
   if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
-  const int umax = pl.variant == STC_VARIANT_NAIVE ? 2 : 2 * pl.max_ops;  // Naive: one packed view per side
+  // Naive and pre-summed ABC: one packed view per side
+  const int umax = (pl.variant == STC_VARIANT_NAIVE || pl.presum) ? 2 : 2 * pl.max_ops;
   const size_t sd = fused_stage_doubles(umax / 2, pl.tshape);
   const int S = fused_stages(sd);
   if (umax > 8 || S < 2) return false;
@@ -1172,6 +1236,33 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
   return true;
 }
 
+// k_presum arguments for one side (0: A, 1: B) of the exec-order terms [t0, t1).
+PresumArgs presum_args(const Plan &pl, int side, const double *D, double *out, const int64_t *pool, int t0, int t1) {
+  PresumArgs a{};
+  a.D = D;
+  a.pool = pool;
+  a.out = out;
+  a.level = pl.level;
+  a.side = side;
+  for (int t = 0; t <= kPresumMaxTerms; ++t) a.slot[t] = -1;
+  for (int t = t0; t < t1; ++t) a.slot[pl.seq[t]] = (int16_t)(t - t0);
+  a.klen = pl.kq_pad;
+  if (side == 0) {
+    a.slot_stride = pl.pa_slot;
+    a.xv = pl.ar;
+    a.kv = pl.ac;
+    a.xlen = pl.mq_pad;
+    a.kfast = pl.a_kfast;
+  } else {
+    a.slot_stride = pl.pb_slot;
+    a.xv = pl.bc;
+    a.kv = pl.br;
+    a.xlen = pl.nq_pad;
+    a.kfast = pl.b_kfast;
+  }
+  return a;
+}
+
 // Plans depend only on the problem descriptor, the grid size and the STC_*
 // planning knobs; repeated calls on one problem (benchmark loops, the pieces of
 // stc_contract_host) reuse them instead of re-planning (~0.1 ms each).
@@ -1189,7 +1280,7 @@ constexpr size_t kPlanCache = 32;
 std::string plan_env() {
   static const char *knobs[] = {"STC_WORKSPACE_CAP_MB", "STC_EXEC_ORDER", "STC_PACK", "STC_TMA_PROMO",
                                 "STC_TMA", "STC_TMA_PF", "STC_FUSED", "STC_CRED", "STC_PRESUM",
-                                "STC_ABC_DENSE", "STC_TSHAPE"};
+                                "STC_ABC_DENSE", "STC_TSHAPE", "STC_PRESUM_OPS"};
   std::string key;
   for (const char *k : knobs) {
     const char *v = getenv(k);
@@ -1277,7 +1368,7 @@ bool plan_gate(const stc_problem *p, int lab, int S, int32_t *lo, int64_t *items
   if (S < 2 || S > kMaxGatedPieces || p->variant != STC_VARIANT_ABC || lab < 0 || lab >= p->c_row.nlab) return false;
   Plan pl;
   const int sms = gemm_max_grid(MAX_OPS);
-  if (cached_plan(p, pl, sms > 0 ? sms : 0) || !pl.ticketed) return false;
+  if (cached_plan(p, pl, sms > 0 ? sms : 0) || !pl.ticketed || pl.presum) return false;
   if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
   {
     GemmArgs g{};
@@ -1469,6 +1560,40 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
     const int grid = (int)std::min<int64_t>(pl.grid, g.total_items);
     CUtensorMap maps[3];
     GemmArgs gf = g;
+    if (pl.presum) {
+      // pre-summed operands: per batch of terms (exec order), one k_presum pass per side
+      // writes the batch's operand sums into their slots, then one fused launch runs
+      // the batch's items with one view per side (C updates ticket-ordered as ever)
+      if (gate) return fail(STC_EINVAL, "internal: gated pieces need the direct fused kernel");
+      double *PA = reinterpret_cast<double *>(ws + pl.off_pa);
+      double *PB = reinterpret_cast<double *>(ws + pl.off_pb);
+      CoordJobs jobs{};
+      if (!plan_fused(p, pl, naive_sides(pl), PA, PB, C, gf, maps, jobs))
+        return fail(STC_EINVAL, "internal: pre-summed plan");
+      gf.A = PA;
+      gf.B = PB;
+      gf.coords = reinterpret_cast<const int4 *>(ws + pl.off_coords);
+      CU(launch_pool_coords(pool, reinterpret_cast<int4 *>(ws + pl.off_coords), jobs, s), "k_pool_coords");
+      ++launches;
+      if (gf.cred) gf.mscratch = reinterpret_cast<double *>(ws + pl.off_mscr);
+      for (int bi = 0; bi < pl.nbatches; ++bi) {
+        const int t0 = bi * pl.batch, nb = std::min(T - t0, pl.batch);
+        PresumArgs pa = presum_args(pl, 0, A, PA, pool, t0, t0 + nb), pb = presum_args(pl, 1, B, PB, pool, t0, t0 + nb);
+        CU(launch_presum(pa, s), "k_presum(A)");
+        CU(launch_presum(pb, s), "k_presum(B)");
+        gf.terms = g.terms + t0;
+        gf.nterms = nb;
+        gf.total_items = (int)(P * nb);
+        gf.counter = counters + bi;
+        if (g_ev_before && bi == 0) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
+        CU(launch_fused(gf, (int)std::min<int64_t>(pl.grid, gf.total_items), s, maps), "k_strassen_fused");
+        launches += 3;
+      }
+      if (g_ev_after) CU(cudaEventRecord(g_ev_after, s), "cudaEventRecord");
+      tma = true;
+      st.fast_updates = gf.cred ? (int64_t)P * (int64_t)pl.tgts.size() : 0;
+      st.slow_updates = gf.cred ? 0 : (int64_t)P * (int64_t)pl.tgts.size();
+    } else {
     const int fz = prepare_fused(gf, maps, C);
     if (fz < 0) return -fz;
     if (gate && (!fz || packed)) return fail(STC_EINVAL, "internal: gated pieces need the direct fused kernel");
@@ -1501,10 +1626,15 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
     }
     if (g_ev_after) CU(cudaEventRecord(g_ev_after, s), "cudaEventRecord");
     ++launches;
-    st.fast_updates = 0;
-    st.slow_updates = (int64_t)P * (int64_t)pl.tgts.size();
+    // C-tile updates: by TMA reduce-add boxes (the reference's fast store_tile path,
+    // _jit.py:166-176) or by the load/add/store scatter epilogue (its slow path)
+    const int64_t upd = (int64_t)P * (int64_t)pl.tgts.size();
+    st.fast_updates = (fz && gf.cred) ? upd : 0;
+    st.slow_updates = (fz && gf.cred) ? 0 : upd;
+    }
   } else {
-    const bool naive = pl.variant == STC_VARIANT_NAIVE;
+    // per-term operand slots: Naive's explicit copies, or pre-summed ABC / AB operands
+    const bool naive = pl.variant == STC_VARIANT_NAIVE || pl.presum;
     double *M = reinterpret_cast<double *>(ws + pl.off_M);
     double *PA = reinterpret_cast<double *>(ws + pl.off_pa);
     double *PB = reinterpret_cast<double *>(ws + pl.off_pb);
@@ -1607,7 +1737,13 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       aa.col_start = reinterpret_cast<const int64_t *>(aput(cstart.data(), cstart.size() * 8, pl.nquads * 8));
       if (int rc = upload(hacc.data(), pl.acc_bytes, acc, s)) return rc;
 
-      if (naive) {
+      if (naive && pl.presum) {
+        // one pass per side: every element position's 4^L quadrant values -> the batch's sums
+        PresumArgs pa = presum_args(pl, 0, A, PA, pool, t0, t1), pb = presum_args(pl, 1, B, PB, pool, t0, t1);
+        CU(launch_presum(pa, s), "k_presum(A)");
+        CU(launch_presum(pb, s), "k_presum(B)");
+        launches += 2;
+      } else if (naive) {
         UnpackArgs ua{};
         ua.pool = pool;
         ua.ops = d_ops;
@@ -1926,6 +2062,45 @@ int stc_sq_norms(int ndim, const int64_t *extents, const double *x, const int64_
   }
   out[0] = a;
   out[1] = b;
+  return STC_OK;
+}
+
+int stc_fill_uniform(double *out, int ndim, const int64_t *extents, const int64_t *strides, int64_t base,
+                     uint64_t seed, void *stream) {
+  if (ndim < 0 || ndim > STC_MAX_LABELS) return fail(STC_EINVAL, "bad rank %d", ndim);
+  if (!out) return fail(STC_EINVAL, "null output");
+  for (int d = 0; d < ndim; ++d)
+    if (extents[d] < 0) return fail(STC_EINVAL, "negative extents");
+  CU(launch_fill_uniform(out, ndim, extents, strides, base, seed, reinterpret_cast<cudaStream_t>(stream)),
+     "k_fill_uniform");
+  return STC_OK;
+}
+
+int stc_plan_describe(const stc_problem *p, int grid, stc_plan_info *info) {
+  if (!info) return fail(STC_EINVAL, "null info");
+  Plan pl;
+  if (grid <= 0) grid = 148;
+  if (int rc = cached_plan(p, pl, grid)) return rc;
+  memset(info, 0, sizeof(*info));
+  info->ticketed = pl.ticketed;
+  info->presum = pl.presum;
+  info->need_pack = pl.need_pack;
+  info->tshape = pl.tshape;
+  info->batch = pl.batch;
+  info->nbatches = pl.nbatches;
+  info->terms = (int32_t)pl.terms.size();
+  info->tiles = (int64_t)(pl.mq_pad / pl.tm) * (pl.nq_pad / pl.tn);
+  info->mq_pad = pl.mq_pad;
+  info->nq_pad = pl.nq_pad;
+  info->kq_pad = pl.kq_pad;
+  info->workspace = pl.total;
+  if (pl.variant != STC_VARIANT_NAIVE && !pl.presum) {
+    GemmArgs g{};
+    CUtensorMap maps[3];
+    CoordJobs jobs{};
+    info->fused_direct = plan_fused(p, pl, direct_sides(p, pl), nullptr, nullptr, nullptr, g, maps, jobs);
+  }
+  info->c_boxes = c_boxes_regular(p, pl.ti, pl.tj, pl.level);
   return STC_OK;
 }
 

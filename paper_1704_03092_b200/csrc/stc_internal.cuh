@@ -177,6 +177,25 @@ struct UnpackArgs {
   int64_t slot_stride;
 };
 
+// Pre-summed Strassen operands (k_presum): every element position (x, k) of a
+// quadrant reads the side's 4^L quadrant values once and writes the operand sum
+// of every term of the batch into that term's slot -- the per-term operand sums
+// the Naive variant unpacks (_jit.unpack_sum, _jit.py:259-309) and the ABC / AB
+// variants form while packing (_jit.pack_a_block / pack_b_block, _jit.py:27-131),
+// same view order and roundings as the fused kernel's in-SM sums.
+constexpr int kPresumMaxTerms = 49;  // 7^L, L <= 2
+struct PresumArgs {
+  const double *D;
+  const int64_t *pool;
+  double *out;          // slot s at out + s * slot_stride: [x][k] (kfast) or [k][x]
+  int64_t slot_stride;
+  int64_t xv, kv;       // pool starts of the side's x / k vectors (quadrant-major)
+  int64_t xlen, klen;   // padded quadrant lengths
+  int32_t level, side;  // side 0: A (quadrant (r, c) = (x, k)); 1: B ((r, c) = (k, x))
+  int32_t kfast, _pad;
+  int16_t slot[kPresumMaxTerms + 1];  // batch slot of each Strassen term (reference order), -1: not in the batch
+};
+
 // ---- launchers (stc_kernels.cu) -------------------------------------------
 int set_error(int code, const char *msg);
 cudaError_t launch_stage(const void *host_src, void *dst, size_t bytes, void *zero, size_t zero_bytes,
@@ -209,6 +228,7 @@ void set_piece_gate(const PieceGate *g);
 bool plan_gate(const stc_problem *p, int lab, int S, int32_t *lo, int64_t *items);
 cudaError_t launch_accumulate(const AccArgs &a, cudaStream_t s);
 cudaError_t launch_unpack(const UnpackArgs &a, cudaStream_t s);
+cudaError_t launch_presum(const PresumArgs &a, cudaStream_t s);
 cudaError_t launch_pack_views(const double *D, const int64_t *pool, const PackArgs &a, double *out, cudaStream_t s);
 cudaError_t launch_accum_dense_single(const double *M, int64_t ldm, int64_t m, int64_t n, double *C,
                                       const int64_t *rows, const int64_t *cols, double coeff, cudaStream_t s);
@@ -220,6 +240,8 @@ struct ViewSet {
 };
 cudaError_t launch_unpack_views(double *out, int64_t ldo, int64_t m, int64_t n, const double *data,
                                 const ViewSet &vs, cudaStream_t s);
+cudaError_t launch_fill_uniform(double *out, int ndim, const int64_t *ext, const int64_t *str, int64_t base,
+                                uint64_t seed, cudaStream_t s);
 cudaError_t launch_sq_norms(int ndim, const int64_t *ext, const double *x, const int64_t *xs, int64_t xb,
                             const double *r, const int64_t *rs, int64_t rb, double *partials, int nblocks,
                             cudaStream_t s);

@@ -306,6 +306,112 @@ cudaError_t launch_pack_views(const double *D, const int64_t *pool, const PackAr
   return cudaGetLastError();
 }
 
+// ---- pre-summed Strassen operands (k_presum) ---------------------------------
+// The level-1 table (strassen.py:56-65; quadrants 0 TL, 1 TR, 2 BL, 3 BR), per
+// side: views per term, quadrant and sign of each view.
+constexpr int kL1Cnt[2][7] = {{2, 2, 1, 1, 2, 2, 2}, {2, 1, 2, 2, 1, 2, 2}};
+constexpr int kL1Q[2][7][2] = {{{0, 3}, {2, 3}, {0, 0}, {3, 0}, {0, 1}, {2, 0}, {1, 3}},
+                               {{0, 3}, {0, 0}, {1, 3}, {2, 0}, {3, 0}, {0, 1}, {2, 3}}};
+constexpr int kL1S[2][7][2] = {{{1, 1}, {1, 1}, {1, 1}, {1, 1}, {1, 1}, {1, -1}, {1, -1}},
+                               {{1, 1}, {1, 1}, {1, -1}, {1, -1}, {1, 1}, {1, 1}, {1, 1}}};
+
+// View O of term T at level L (strassen.py:70-94: outer level first, quadrant
+// q1 * 4 + q2, sign s1 * s2), as (x quadrant, k quadrant, sign) of the side.
+template <int L, int SIDE, int T>
+struct PsTerm {
+  static constexpr int t1 = L == 2 ? T / 7 : T, t2 = L == 2 ? T % 7 : 0;
+  static constexpr int n2 = L == 2 ? kL1Cnt[SIDE][t2] : 1;
+  static constexpr int count = kL1Cnt[SIDE][t1] * n2;
+};
+template <int L, int SIDE, int T, int O>
+struct PsOp {
+  using TT = PsTerm<L, SIDE, T>;
+  static constexpr int o1 = O / TT::n2, o2 = O % TT::n2;
+  static constexpr int q1 = kL1Q[SIDE][TT::t1][o1], q2 = L == 2 ? kL1Q[SIDE][TT::t2][o2] : 0;
+  static constexpr int sign = kL1S[SIDE][TT::t1][o1] * (L == 2 ? kL1S[SIDE][TT::t2][o2] : 1);
+  static constexpr int r = L == 2 ? 2 * (q1 >> 1) + (q2 >> 1) : q1 >> 1;  // quad_rc
+  static constexpr int c = L == 2 ? 2 * (q1 & 1) + (q2 & 1) : q1 & 1;
+  static constexpr int xq = SIDE == 0 ? r : c, kq = SIDE == 0 ? c : r;
+};
+
+// s (+/-) the remaining views of term T, in view order
+template <int L, int SIDE, int T, int O, int Q>
+__device__ __forceinline__ double ps_rest(const double (&v)[Q][Q], double s) {
+  if constexpr (O < PsTerm<L, SIDE, T>::count) {
+    using op = PsOp<L, SIDE, T, O>;
+    s = op::sign > 0 ? __dadd_rn(s, v[op::xq][op::kq]) : __dsub_rn(s, v[op::xq][op::kq]);
+    return ps_rest<L, SIDE, T, O + 1, Q>(v, s);
+  } else {
+    return s;
+  }
+}
+
+template <int L, int SIDE, int T, int Q>
+__device__ __forceinline__ void ps_terms(const PresumArgs &a, const double (&v)[Q][Q], int64_t pos) {
+  if constexpr (T < (L == 2 ? 49 : 7)) {
+    const int slot = a.slot[T];
+    if (slot >= 0) {
+      using op0 = PsOp<L, SIDE, T, 0>;
+      const double v0 = v[op0::xq][op0::kq];
+      // first view: sign applied by flipping the sign bit (the fused kernel's in-SM sums)
+      double s = op0::sign > 0 ? v0 : __hiloint2double(__double2hiint(v0) ^ static_cast<int>(0x80000000u),
+                                                        __double2loint(v0));
+      s = ps_rest<L, SIDE, T, 1, Q>(v, s);
+      a.out[(int64_t)slot * a.slot_stride + pos] = s;
+    }
+    ps_terms<L, SIDE, T + 1, Q>(a, v, pos);
+  }
+}
+
+constexpr int PRESUM_ROWS = 2;  // slow-dimension rows per thread
+
+// Block: 256 positions along the slot's contiguous dimension x PRESUM_ROWS rows of
+// the other; every thread loads the 4^L quadrant values of its positions, then
+// writes the batch's term sums (coalesced along the contiguous dimension).
+template <int L, int SIDE>
+__global__ void __launch_bounds__(256) k_presum(const PresumArgs a) {
+  constexpr int Q = 1 << L;
+  const int64_t fast_len = a.kfast ? a.klen : a.xlen, slow_len = a.kfast ? a.xlen : a.klen;
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= fast_len) return;
+  const int64_t fv = a.kfast ? a.kv : a.xv, sv = a.kfast ? a.xv : a.kv;
+  int64_t fo[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) fo[q] = __ldg(a.pool + fv + q * fast_len + f);
+#pragma unroll 1
+  for (int r = 0; r < PRESUM_ROWS; ++r) {
+    const int64_t sl = (int64_t)blockIdx.y * PRESUM_ROWS + r;
+    if (sl >= slow_len) break;
+    int64_t so[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) so[q] = __ldg(a.pool + sv + q * slow_len + sl);
+    double v[Q][Q];
+#pragma unroll
+    for (int xq = 0; xq < Q; ++xq)
+#pragma unroll
+      for (int kq = 0; kq < Q; ++kq) {
+        const int64_t xo = a.kfast ? so[xq] : fo[xq], ko = a.kfast ? fo[kq] : so[kq];
+        v[xq][kq] = (xo == kPad || ko == kPad) ? 0.0 : __ldcs(a.D + xo + ko);
+      }
+    ps_terms<L, SIDE, 0, Q>(a, v, sl * fast_len + f);
+  }
+}
+
+cudaError_t launch_presum(const PresumArgs &a, cudaStream_t s) {
+  const int64_t fast_len = a.kfast ? a.klen : a.xlen, slow_len = a.kfast ? a.xlen : a.klen;
+  if (fast_len <= 0 || slow_len <= 0) return cudaSuccess;
+  const int64_t gy = (slow_len + PRESUM_ROWS - 1) / PRESUM_ROWS;
+  if (gy > 65535) return cudaErrorInvalidConfiguration;
+  dim3 grid((unsigned)((fast_len + 255) / 256), (unsigned)gy);
+  if (a.level == 1)
+    a.side ? k_presum<1, 1><<<grid, 256, 0, s>>>(a) : k_presum<1, 0><<<grid, 256, 0, s>>>(a);
+  else if (a.level == 2)
+    a.side ? k_presum<2, 1><<<grid, 256, 0, s>>>(a) : k_presum<2, 0><<<grid, 256, 0, s>>>(a);
+  else
+    return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
 // ---- standalone helpers for the kernel-level API --------------------------
 __global__ void k_accum_dense_single(const double *__restrict__ M, int64_t ldm, int64_t m, int64_t n,
                                      double *__restrict__ C, const int64_t *__restrict__ rows,
@@ -403,6 +509,62 @@ cudaError_t launch_sq_norms(int ndim, const int64_t *ext, const double *x, const
     total *= ext[d];
   }
   k_sq_norms<<<nblocks, 256, 0, s>>>(sh, total, x, xb, r, rb, partials);
+  return cudaGetLastError();
+}
+
+// ---- counter-based synthetic inputs (bench / tests; oracle/synth.py mirror) ----
+// value(j) = (mix(key + (j + 1) G) >> 11) * 2^-52 - 1, key = mix(seed + G): depends only
+// on the element's flat index j in the FULL tensor, so any shard is generated on its own.
+struct FillShape {
+  int ndim;
+  int64_t ext[STC_MAX_LABELS], str[STC_MAX_LABELS];  // row-major decomposition of the output
+};
+
+__device__ __forceinline__ uint64_t splitmix_fin(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void __launch_bounds__(256) k_fill_uniform(double *__restrict__ out, const FillShape sh, int64_t total,
+                                                      int64_t base, uint64_t key) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += stride) {
+    int64_t rem = e, j = base;
+    for (int d = sh.ndim - 1; d >= 0; --d) {  // last dim fastest (compact row-major output)
+      const int64_t i = rem % sh.ext[d];
+      rem /= sh.ext[d];
+      j += i * sh.str[d];
+    }
+    const uint64_t z = splitmix_fin(key + ((uint64_t)j + 1ull) * 0x9E3779B97F4A7C15ull);
+    out[e] = (double)(z >> 11) * 0x1p-52 - 1.0;
+  }
+}
+
+cudaError_t launch_fill_uniform(double *out, int ndim, const int64_t *ext, const int64_t *str, int64_t base,
+                                uint64_t seed, cudaStream_t s) {
+  FillShape sh{};
+  int64_t total = 1;
+  // merge the trailing dims whose strides are row-major over the output (the common case of
+  // a whole tensor or a slab): fewer divisions per element
+  sh.ndim = ndim;
+  for (int d = 0; d < ndim; ++d) {
+    sh.ext[d] = ext[d];
+    sh.str[d] = str[d];
+    total *= ext[d];
+  }
+  while (sh.ndim >= 2 && sh.str[sh.ndim - 2] == sh.str[sh.ndim - 1] * sh.ext[sh.ndim - 1]) {
+    sh.ext[sh.ndim - 2] *= sh.ext[sh.ndim - 1];
+    sh.str[sh.ndim - 2] = sh.str[sh.ndim - 1];
+    --sh.ndim;
+  }
+  if (total == 0) return cudaSuccess;
+  uint64_t k = seed + 0x9E3779B97F4A7C15ull;
+  k = (k ^ (k >> 30)) * 0xBF58476D1CE4E5B9ull;
+  k = (k ^ (k >> 27)) * 0x94D049BB133111EBull;
+  k ^= k >> 31;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
+  k_fill_uniform<<<(int)blocks, 256, 0, s>>>(out, sh, total, base, k);
   return cudaGetLastError();
 }
 

@@ -93,33 +93,48 @@ def contract_sharded(spec: ContractionSpec, a: DenseTensor, b: DenseTensor, c: D
     return sh, st
 
 
-def _pack(c: DenseTensor, labels: str, sh: Shard):
-    """Dense copy of the shard region of C (label order of C, first axis slowest)."""
+def _storage(c: DenseTensor):
+    import torch
+
+    return c.data if isinstance(c.data, torch.Tensor) else torch.from_numpy(c.data)
+
+
+def _region(c: DenseTensor, labels: str, sh: Shard):
+    """Strided torch view of the shard region of C (label order of C)."""
     import torch
 
     v = shard_tensor(c, labels, sh)
-    data = c.data if isinstance(c.data, torch.Tensor) else torch.from_numpy(c.data)
-    return torch.as_strided(data, v.extents, v.strides, v.base_offset).contiguous()
+    return torch.as_strided(_storage(c), v.extents, v.strides, v.base_offset)
 
 
 def gather_shards(spec: ContractionSpec, c: DenseTensor, rank: int, world: int, label: str | None = None,
                   group=None) -> None:
     """All-gather every rank's C shard into this rank's full C (in place).
 
-    Shards are exchanged as dense blocks with torch.distributed.all_gather (NCCL
-    for CUDA storage, gloo for host storage) and scattered back into C's layout.
+    One collective: every rank contributes its shard as one dense block, padded
+    to the largest shard (all_gather needs equal sizes; plan_shards' ranges may
+    differ by one), into a shard-major [world, size] buffer
+    (all_gather_into_tensor: NCCL over NVLink for CUDA storage, gloo for host
+    storage); each received block is then written into its strided region of C
+    with one copy.  Extra memory: the buffer, one C's worth.
     """
     import torch
     import torch.distributed as dist
 
     shards = plan_shards(spec, c, world, label)
-    mine = _pack(c, spec.labels_c, shards[rank])
-    blocks = [torch.empty_like(_pack(c, spec.labels_c, s)) for s in shards]
-    dist.all_gather(blocks, mine, group=group)
-    data = c.data if isinstance(c.data, torch.Tensor) else torch.from_numpy(c.data)
-    for s, blk in zip(shards, blocks):
-        v = shard_tensor(c, spec.labels_c, s)
-        torch.as_strided(data, v.extents, v.strides, v.base_offset).copy_(blk)
+    regions = [_region(c, spec.labels_c, s) for s in shards]
+    size = max(r.numel() for r in regions)
+    data = _storage(c)
+    flat = torch.zeros(size, dtype=data.dtype, device=data.device)
+    flat[: regions[rank].numel()].view(regions[rank].shape).copy_(regions[rank])
+    out = torch.empty(world * size, dtype=data.dtype, device=data.device)
+    if hasattr(dist, "all_gather_into_tensor") and (data.is_cuda or dist.get_backend(group) != "gloo"):
+        dist.all_gather_into_tensor(out, flat, group=group)
+    else:  # gloo has no all_gather_into_tensor: the list form over views of the same buffer
+        dist.all_gather(list(out.view(world, size).unbind(0)), flat, group=group)
+    for s, (sh, reg) in enumerate(zip(shards, regions)):
+        if s != rank:
+            reg.copy_(out[s * size: s * size + reg.numel()].view(reg.shape))
 
 
 # ---------------------------------------------------------------- 2-D split

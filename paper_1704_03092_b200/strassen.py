@@ -35,7 +35,7 @@ from .tensor import ContractionSpec, DenseTensor
 from .views import DEFAULT_BLOCKING, BlockingParams, check_c_targets, make_view, quadrant_views
 
 __all__ = ["MAX_LEVEL", "DEVICE_MAX_LEVEL", "StrassenTerm", "Variant", "contract", "strassen_terms",
-           "problem_of", "quadrant_rc"]
+           "problem_of", "quadrant_rc", "describe_plan"]
 
 MAX_LEVEL = 2          # reference cap without allow_deep (strassen.py:38)
 DEVICE_MAX_LEVEL = 4   # 2^L views per side must fit the kernel's op tables
@@ -141,6 +141,19 @@ def problem_of(spec: ContractionSpec, a: DenseTensor, b: DenseTensor, c: DenseTe
     p.variant = _lib.VARIANT_CODES[variant.value]
     p.flags = int(flags)
     return p
+
+
+def describe_plan(spec: ContractionSpec, a, b, c, level: int, variant, grid: int = 148,
+                  force_slow: bool = False, reference_tiling: bool = False) -> dict:
+    """The execution path the library plans for this contraction (no device
+    needed): ticketed / pre-summed / repacked / tile shape / batches / workspace."""
+    a, b, c = _as_dense(a, "A"), _as_dense(b, "B"), _as_dense(c, "C")
+    _check_operands(spec, a, b, c)
+    flags = (_lib.FLAG_FORCE_SLOW if force_slow else 0) | (_lib.FLAG_REFERENCE_TILING if reference_tiling else 0)
+    prob = problem_of(spec, a, b, c, level, _variant(variant), flags)
+    info = _lib.PlanInfo()
+    _lib.check(_lib.lib().stc_plan_describe(ctypes.byref(prob), int(grid), ctypes.byref(info)))
+    return info.as_dict()
 
 
 def _validate_targets(spec, c: DenseTensor, level: int, terms) -> None:
