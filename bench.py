@@ -28,9 +28,11 @@ its shard of C -- no data-path collective (strong scaling of one problem).
 
 --impl reference times the reference's own CPU implementation (strassen_tc,
 installed under baseline/_ref; the oracle/ C port when it cannot be imported),
-all host cores, on a bounded sample of cfg5: the sub-problem a < 2, i < 1,
-j < 8 (m = 2048, n = 256, k = 32768, 34.4 GFLOP, the full k), with the full
-tensors' values.  Its rate is reported as measured on that sample.
+all host cores, on a bounded sample of cfg5: the sub-problem a < 2, i < 2,
+e < 4 (m = n = 2048, k = 4096, 34.4 GFLOP: L2 leaves of 512 x 512 x 1024), with
+the full tensors' values.  Its rate is reported as measured on that sample (the
+reference's own cfg5 n-shard run, tests/golden/big.json, ran at a similar rate:
+5.9 GFLOP/s on 8 cores).
 """
 
 from __future__ import annotations
@@ -55,8 +57,8 @@ CFG2 = "aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;"
 SHARD_LABEL = "i"
 LEVEL, VARIANT = 2, "abc"
 SEED_A, SEED_B = 2017, 2018
-# CPU sample of cfg5: the leading ranges of a, i and j (full k): m = 2048, n = 256
-CPU_SAMPLE = {"a": 2, "i": 1, "j": 8}
+# CPU sample of cfg5: the leading ranges of a, i and e: m = n = 2048, k = 4096
+CPU_SAMPLE = {"a": 2, "i": 2, "e": 4}
 # FP64 tensor-core (DMMA) peak of this pool's B200, measured with tools/fp64_peak.cu
 # (register-resident mma.sync f64 loops, 148 SMs, best of 5): profiles/fp64_peak_r01.txt.
 # MEASURED_PEAKS.json has no FP64 entry.
@@ -195,7 +197,7 @@ def cpu_reference_run(steps: int, warmup: int):
             times.append(t)
     flops = 2.0 * sp.n_i * sp.n_j * sp.n_p
     value = flops * len(times) / sum(times) / 1e9
-    sample = (f"cfg5 sub-problem a<{CPU_SAMPLE['a']}, i<{CPU_SAMPLE['i']}, j<{CPU_SAMPLE['j']} "
+    sample = (f"cfg5 sub-problem " + ", ".join(f"{k}<{v}" for k, v in CPU_SAMPLE.items()) + " "
               f"(m={sp.n_i}, n={sp.n_j}, k={sp.n_p}, {flops / 1e9:.1f} GFLOP per step, full-tensor values), "
               f"L{LEVEL} {VARIANT.upper()}, "
               + ("strassen_tc.contract from baseline/_ref (numba)" if kind == "reference"
@@ -306,6 +308,7 @@ def main():
     B = uniform_tensor(SEED_B, sp.tensor_extents(sp.labels_b), dev, full_strides=row_major(eb),
                        base=sh.start * row_major(eb)[ax])
     C = shard.shard_tensor(c_full, spec.labels_c, sh)
+    A_desc, B_desc, C_desc = A, B, C  # layouts for the plan description (no storage use)
     torch.cuda.synchronize()
     flops_rank = 2.0 * sp.n_i * sp.n_j * sp.n_p
     flops_job = 2.0 * spec.n_i * spec.n_j * spec.n_p
@@ -408,6 +411,10 @@ def main():
     # achieved = the classical 2 m n k of the launch / its duration
     # (up to (8/7)^L above the pipe's peak in principle); the flops the tensor pipe
     # executes (7^L leaf products of the quadrants) are reported beside it.
+    info = stc.describe_plan(sp, A_desc, B_desc, C_desc, LEVEL, VARIANT)
+    kernel_name = ("k_strassen_fused on pre-summed operand slots (k_presum), "
+                   + ("TMA reduce-add C epilogue" if info["ticketed"] else "dense M + k_accumulate")
+                   if info["presum"] else "k_strassen_fused (in-kernel operand sums)")
     q = 1 << LEVEL
     exec_flops = (7 ** LEVEL) * 2.0 * (sp.n_i // q) * (sp.n_j // q) * (sp.n_p // q)
     gemm_avg = sum(gemm_ms) / len(gemm_ms) * 1e-3
@@ -421,7 +428,7 @@ def main():
             traffic = None
     roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_TC_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP64_TC_PEAK_TFLOPS, "traffic": traffic,
-                "kernel": "k_strassen_fused" if st.fast_blocks else "k_strassen_gemm",
+                "kernel": kernel_name,
                 "kernel_ms": gemm_avg * 1e3, "kernel_share_of_step": gemm_avg / (elapsed / args.steps),
                 "algorithmic_flops_per_launch": flops_rank,
                 "algorithmic_unit": "2*m*n*k of the rank's contraction (SURVEY.md 8(d))",

@@ -1825,7 +1825,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       }
       if (g_ev_before && bi == 0) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
       if (fused) {
-        tma = !packed && !naive;
+        tma = !packed;  // TMA boxes of the operands or of their packed slots (the reference's Naive GEMM: dense, fast blocks)
         CU(launch_fused(gf, grid, s, maps_ab), "k_strassen_fused(dense)");
       } else {
         if (pl.tshape != 0) return fail(STC_EINVAL, "internal: tile shape %d needs the fused kernel", pl.tshape);
