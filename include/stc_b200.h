@@ -76,7 +76,12 @@ typedef struct {
 } stc_problem;
 
 /* Mirrors RunStats counters (oracle.py:22-43); GPU tiles replace mr x nr
- * register blocks, so block/update counts are per GPU tile. */
+ * register blocks, so block/update counts are per GPU tile.  fast / slow
+ * blocks: operand tiles staged by TMA boxes of a regular view or packed slot
+ * (the reference's constant-stride fast path, _jit.py:54-65) vs per-element
+ * gathers; fast / slow updates: C-tile updates by TMA reduce-add boxes (its
+ * fast store_tile path, _jit.py:166-176) vs the load/add/store scatter or the
+ * dense-M accumulate pass. */
 typedef struct {
   double total_flops;      /* executed MMA flops incl. tile padding          */
   int64_t fast_blocks;     /* operand tiles staged on the vectorised path    */
@@ -86,6 +91,11 @@ typedef struct {
   int64_t leaf_multiplies; /* 7^L                                            */
   int64_t work_items;      /* (term, tile) items executed                    */
   int64_t kernel_launches; /* kernels this call enqueued                      */
+  int64_t pieces;          /* independent L-level contractions the call ran:
+                              1, or stc_contract_host's piece count (each piece
+                              an L-level Strassen over its own quadrants: pieces
+                              x 7^L leaf products ran; leaf_multiplies stays 7^L,
+                              the reference's per-call count)                 */
 } stc_stats;
 
 /* ---- library ---- */

@@ -50,7 +50,7 @@ class Stats(ctypes.Structure):
     _fields_ = [("total_flops", ctypes.c_double), ("fast_blocks", ctypes.c_int64),
                 ("slow_blocks", ctypes.c_int64), ("fast_updates", ctypes.c_int64),
                 ("slow_updates", ctypes.c_int64), ("leaf_multiplies", ctypes.c_int64),
-                ("work_items", ctypes.c_int64), ("kernel_launches", ctypes.c_int64)]
+                ("work_items", ctypes.c_int64), ("kernel_launches", ctypes.c_int64), ("pieces", ctypes.c_int64)]
 
 
 class PlanInfo(ctypes.Structure):

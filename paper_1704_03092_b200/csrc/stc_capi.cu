@@ -30,7 +30,6 @@ namespace {
 thread_local std::string g_err;
 thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;  // stc_set_kernel_events
 thread_local const int32_t *g_c_ready = nullptr;                        // stc_set_c_ready
-thread_local const stc::PieceGate *g_gate = nullptr;                     // stc::set_piece_gate
 
 int fail(int code, const char *fmt, ...) {
   char buf[512];
@@ -347,10 +346,18 @@ struct Plan {
   int64_t m_slot = 0, pa_slot = 0, pb_slot = 0;
 };
 
+// Workspace cap for the term batches of dense M / operand slots: STC_WORKSPACE_CAP_MB,
+// else half the free device memory at planning time (at least 24 GiB).  The batch
+// count changes no result: each batch's C pass continues the previous one's sums.
 int64_t cap_bytes() {
-  const char *e = getenv("STC_WORKSPACE_CAP_MB");
-  int64_t mb = e ? atoll(e) : 24 * 1024;
-  return mb * (int64_t)1024 * 1024;
+  if (const char *e = getenv("STC_WORKSPACE_CAP_MB")) return atoll(e) * (int64_t)1024 * 1024;
+  const int64_t floor_bytes = (int64_t)24 << 30;
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+    cudaGetLastError();  // no device (planning on a CPU host): clear the sticky-free error
+    return floor_bytes;
+  }
+  return std::max<int64_t>(floor_bytes, (int64_t)(fr / 2));
 }
 
 // Reorder terms so that terms running concurrently (within `window`
@@ -410,17 +417,30 @@ FusedSides naive_sides(const Plan &pl);
 bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, const double *A, const double *B,
                 const double *C, GemmArgs &g, CUtensorMap maps[3], CoordJobs &jobs);
 
-// Pre-summed operands for ticketed ABC at L = 1, 2 (STC_PRESUM_OPS = 0 / 1 forces
-// it off / on).  The sums cost one HBM pass (4^L quadrant reads + 7^L slot writes per
-// element position and side) and take every DADD off the FP64 pipe the DMMAs use.
+// Pre-summed operands for ABC / AB at L = 1, 2 (STC_PRESUM_OPS = 0 / 1 forces it off /
+// on).  The sums cost one HBM pass per side (4^L quadrant reads + 7^L slot writes per
+// element position) and take every DADD off the FP64 pipe the DMMAs use: the fused
+// kernel's in-SM sums cost it about 5 % (L1) / 18 % (L2) of its DMMA time (cfg2, 16384^3,
+// cfg5; tools/presum_sweep.py).  Operands whose views are not TMA boxes are repacked
+// anyway (one read + one write of every quadrant), which the presum pass replaces.
+// Cost model at 5 TB/s and 33 TF/s executed.
 bool presum_wanted(const stc_problem *p, const Plan &pl) {
   if (pl.level < 1 || pl.level > 2 || pl.tshape != 0) return false;
   if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
   if (const char *e = getenv("STC_FUSED"))
     if (atoi(e) == 0) return false;
   if (const char *e = getenv("STC_PRESUM_OPS")) return atoi(e) != 0;
-  const int64_t qa = pl.mq_pad * pl.kq_pad, qb = pl.kq_pad * pl.nq_pad;
-  return std::min(qa, qb) >= ((int64_t)1 << 20);
+  const double qa = (double)pl.mq_pad * pl.kq_pad, qb = (double)pl.kq_pad * pl.nq_pad;
+  const double quads = (double)pl.nquads, T = (double)pl.terms.size();
+  const double t_presum = 8.0 * (quads + T) * (qa + qb) / 5e12;
+  GemmArgs g{};
+  CUtensorMap maps[3];
+  CoordJobs jobs{};
+  const bool direct = plan_fused(p, pl, direct_sides(p, pl), nullptr, nullptr, nullptr, g, maps, jobs);
+  const double t_repack = direct ? 0.0 : 8.0 * 2.0 * quads * (qa + qb) / 3e12;  // gathers: ~50 % of HBM
+  const double t_gemm = T * 2.0 * (double)pl.mq_pad * pl.nq_pad * pl.kq_pad / 33e12;
+  const double penalty = pl.level == 1 ? 0.05 : 0.18;
+  return t_presum < penalty * t_gemm + t_repack;
 }
 
 int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
@@ -1221,6 +1241,7 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
   }
   g.tma = 0;
   g.umax = umax;
+  g.one_view = umax == 2;  // L0, Naive slots, pre-summed slots: one view per side, sign +1
   g.stages = g.cred ? fused_stages_red(sd) : S;
   g.stage_dbl = (int32_t)sd;
   g.tshape = pl.tshape;
@@ -1330,86 +1351,6 @@ bool plan_ticketed(const stc_problem *p) {
   return pl.ticketed;
 }
 
-void set_piece_gate(const PieceGate *g) { g_gate = g; }
-
-// Label `lab` index of entry o of an I/J pool vector (mode 0, as k_build_pool
-// decodes it: tile order -> quadrant-local reference index -> labels), -1 for PAD.
-static int64_t vec_label_index(const VecDesc &d, int64_t o, int lab) {
-  const int64_t q = o / d.q_len_pad, ip = o - q * d.q_len_pad;
-  if (ip >= d.q_len) return -1;
-  int64_t i = ip;
-  if (d.nbox > 0) {
-    int64_t digit[STC_MAX_LABELS], rem = ip;
-    for (int j = 0; j < d.nbox; ++j) {
-      const int dim = d.order[j];
-      digit[dim] = rem % d.box_ext[dim];
-      rem /= d.box_ext[dim];
-    }
-    i = 0;
-    int64_t mult = 1;
-    for (int dim = 0; dim < d.nbox; ++dim) {
-      i += digit[dim] * mult;
-      mult *= d.box_ext[dim];
-    }
-  }
-  const int64_t l = q * d.q_len + i;
-  if (l >= d.len) return -1;
-  int64_t rem = l;
-  for (int j = 0; j < lab; ++j) rem /= d.ext[j];
-  return rem % d.ext[lab];
-}
-
-// Gated host pieces (stc_host.cu): can the I-bundle split of label `lab` into S
-// equal ranges run as ONE ticketed fused launch whose items are ordered by piece?
-// Needs the direct (non-repacked) fused kernel and every tile row of every
-// quadrant inside one piece, the pieces in tile-row order.  Fills lo[0..S] (tile
-// rows) and items[s] (work items of piece s).
-bool plan_gate(const stc_problem *p, int lab, int S, int32_t *lo, int64_t *items) {
-  if (S < 2 || S > kMaxGatedPieces || p->variant != STC_VARIANT_ABC || lab < 0 || lab >= p->c_row.nlab) return false;
-  Plan pl;
-  const int sms = gemm_max_grid(MAX_OPS);
-  if (cached_plan(p, pl, sms > 0 ? sms : 0) || !pl.ticketed || pl.presum) return false;
-  if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
-  {
-    GemmArgs g{};
-    CUtensorMap maps[3];
-    CoordJobs jobs{};
-    if (!plan_fused(p, pl, direct_sides(p, pl), nullptr, nullptr, nullptr, g, maps, jobs)) return false;
-  }
-  const int64_t ext = p->c_row.ext[lab];
-  if (ext % S) return false;
-  const int64_t plen = ext / S;
-  const VecDesc d = vec_bundle(p->c_row, 0, pl.Q, BM, pl.ti);
-  const int tiles_m = (int)(pl.mq_pad / BM), tiles_n = (int)(pl.nq_pad / BN);
-  std::vector<int> piece(tiles_m, -1);
-  for (int64_t q = 0; q < pl.Q; ++q)
-    for (int ti = 0; ti < tiles_m; ++ti)
-      for (int r = 0; r < BM; ++r) {
-        const int64_t idx = vec_label_index(d, q * d.q_len_pad + (int64_t)ti * BM + r, lab);
-        if (idx < 0) continue;
-        const int sp = (int)(idx / plen);
-        if (piece[ti] < 0) piece[ti] = sp;
-        else if (piece[ti] != sp) return false;  // a tile row straddles two pieces
-      }
-  int prev = 0;
-  for (int ti = 0; ti < tiles_m; ++ti) {
-    if (piece[ti] < 0) piece[ti] = prev;  // all-padding rows ride with the previous piece
-    if (piece[ti] < prev) return false;    // pieces out of tile-row order
-    prev = piece[ti];
-  }
-  const int T = (int)pl.terms.size();
-  for (int sp = 0; sp <= S; ++sp) lo[sp] = tiles_m;
-  for (int ti = tiles_m - 1; ti >= 0; --ti) lo[piece[ti]] = ti;
-  for (int sp = S - 1; sp >= 0; --sp) {
-    if (lo[sp] > lo[sp + 1]) lo[sp] = lo[sp + 1];
-    items[sp] = 0;
-  }
-  for (int sp = 0; sp < S; ++sp) {
-    if (lo[sp + 1] <= lo[sp]) return false;  // every piece owns tile rows
-    items[sp] = (int64_t)T * (lo[sp + 1] - lo[sp]) * tiles_n;
-  }
-  return lo[0] == 0;
-}
 }  // namespace stc
 
 // ======================================================================== ABI
@@ -1512,10 +1453,6 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
 
   const int32_t *c_ready = g_c_ready;  // consumed by this call
   g_c_ready = nullptr;
-  const PieceGate *gate = g_gate;
-  g_gate = nullptr;
-  if (gate && (!pl.ticketed || gate->n > kMaxGatedPieces))
-    return fail(STC_EINVAL, "internal: gated pieces need the ticketed ABC plan");
   GemmArgs g{};
   g.pool = pool;
   g.c_ready = c_ready;
@@ -1564,7 +1501,6 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       // pre-summed operands: per batch of terms (exec order), one k_presum pass per side
       // writes the batch's operand sums into their slots, then one fused launch runs
       // the batch's items with one view per side (C updates ticket-ordered as ever)
-      if (gate) return fail(STC_EINVAL, "internal: gated pieces need the direct fused kernel");
       double *PA = reinterpret_cast<double *>(ws + pl.off_pa);
       double *PB = reinterpret_cast<double *>(ws + pl.off_pb);
       CoordJobs jobs{};
@@ -1596,14 +1532,6 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
     } else {
     const int fz = prepare_fused(gf, maps, C);
     if (fz < 0) return -fz;
-    if (gate && (!fz || packed)) return fail(STC_EINVAL, "internal: gated pieces need the direct fused kernel");
-    if (gate) {
-      gf.npieces = gate->n;
-      for (int i = 0; i <= gate->n; ++i) gf.piece_lo[i] = gate->lo[i];
-      gf.piece_ready = gate->ready;
-      gf.piece_done = gate->done;
-      gf.c_ready = nullptr;
-    }
     if (fz) {
       // fused kernel: TMA boxes of 128 x 8, sums in the consumers' fragment loads
       tma = !packed;
@@ -1808,6 +1736,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         gf.b_kfast = base.b_kfast;
         gf.coords = base.coords;
         gf.umax = base.umax;
+        gf.one_view = base.one_view;
         gf.stages = base.stages;
         gf.stage_dbl = base.stage_dbl;
         gf.tshape = base.tshape;
@@ -1852,6 +1781,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
   st.leaf_multiplies = T;
   st.work_items = P * T;
   st.kernel_launches = launches + g_stage_launches;
+  st.pieces = 1;
   if (stats) *stats = st;
   g_ev_before = g_ev_after = nullptr;
   return STC_OK;

@@ -5,30 +5,13 @@
 #include "stc_internal.cuh"
 #include "stc_ptx.cuh"
 
-#ifdef STC_EXPERIMENT_NOTICKET
-#define STC_NOTICKET 1  // timing experiment only (C-tile updates race)
-#else
-#define STC_NOTICKET 0
-#endif
 
 namespace stc {
 
 // Work item -> (term slot, tile row ti, tile column tj, tile id pos).  pos numbers
 // the quadrant's tiles the same way for every term (per-tile tickets).
-__device__ __forceinline__ void tile_of(const GemmArgs &p, int item, int &slot, int &ti, int &tj, int &pos,
-                                        int &piece) {
-  int r0 = 0, rows = p.tiles_m;
-  piece = 0;
-  if (p.npieces > 1) {  // piece-major: every piece is (terms) x (its tile rows) x (all tile columns)
-    for (;;) {
-      rows = p.piece_lo[piece + 1] - p.piece_lo[piece];
-      const int n = p.nterms * rows * p.tiles_n;
-      if (item < n || piece + 1 == p.npieces) break;
-      item -= n;
-      ++piece;
-    }
-    r0 = p.piece_lo[piece];
-  }
+__device__ __forceinline__ void tile_of(const GemmArgs &p, int item, int &slot, int &ti, int &tj, int &pos) {
+  const int rows = p.tiles_m;
   const int P = rows * p.tiles_n;
   slot = item / P;
   const int local = item - slot * P;
@@ -39,27 +22,13 @@ __device__ __forceinline__ void tile_of(const GemmArgs &p, int item, int &slot, 
   const int first = g * gm;
   const int gsz = min(rows - first, gm);
   const int r = local - g * per_group;
-  ti = r0 + first + r % gsz;
+  ti = first + r % gsz;
   tj = r / gsz;
   pos = ti * p.tiles_n + tj;
 }
 __device__ __forceinline__ void tile_of(const GemmArgs &p, int item, int &slot, int &ti, int &tj) {
-  int pos, piece;
-  tile_of(p, item, slot, ti, tj, pos, piece);
-}
-
-// Gated pieces: wait until piece s's operands and C rows are in HBM (thread 0 of
-// the caller polls), then order the TMA (async proxy) accesses after it.
-__device__ __forceinline__ void wait_piece(const GemmArgs &p, int piece) {
-  if (!p.piece_ready) return;
-  while (ld_acquire_gpu(p.piece_ready + piece) == 0) __nanosleep(256);
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-// Gated pieces: one more finished item of piece s (after all its C updates).
-__device__ __forceinline__ void piece_item_done(const GemmArgs &p, int piece) {
-  if (!p.piece_done) return;
-  __threadfence();
-  atomicAdd(p.piece_done + piece, 1);
+  int pos;
+  tile_of(p, item, slot, ti, tj, pos);
 }
 
 // stc_set_c_ready: block until C has arrived (thread 0 polls, the consumer
@@ -98,8 +67,8 @@ __device__ __forceinline__ int epi_col(int nt, int tig) {  // first of the pair 
 template <int PA = 0, int PB = 0, int RB = 1, int TBM = BM, int TBN = BN>
 __device__ __forceinline__ void epilogue_store(const GemmArgs &p, const double (&acc)[4][4][4], int item, int tid,
                                                int wm, int wn, int g, int tig) {
-  int slot, ti, tj, pos, piece;
-  tile_of(p, item, slot, ti, tj, pos, piece);
+  int slot, ti, tj, pos;
+  tile_of(p, item, slot, ti, tj, pos);
   const TermDesc td = p.terms[slot];
   const int row0 = ti * TBM + wm * 64;
   const int col0 = tj * TBN + wn * 32;
@@ -117,14 +86,10 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs &p, const double (
         }
     return;
   }
-  if (p.piece_ready) {  // gated pieces: C rows of this piece uploaded
-    if (tid == 0) wait_piece(p, piece);
-    named_bar(2, 32 * CONSUMER_WARPS);
-  }
   for (int j = 0; j < td.c_count; ++j) {
     const TgtDesc tg = p.tgts[td.c_first + j];
     int32_t *ticket = p.tickets + tg.ticket_base + pos;
-    if (p.use_tickets && !STC_NOTICKET) {
+    if (p.use_tickets) {
       if (tid == 0) {
         while (ld_acquire_gpu(ticket) < tg.order) __nanosleep(128);
       }
@@ -159,16 +124,11 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs &p, const double (
             __stcg(p.C + ro[i] + co[c], old[i][c] + tg.sign * acc[mt][c >> 1][2 * h + (c & 1)]);
       }
     }
-    if (p.use_tickets && !STC_NOTICKET) {
+    if (p.use_tickets) {
       __threadfence();
       named_bar(2, 32 * CONSUMER_WARPS);
       if (tid == 0) st_release_gpu(ticket, tg.order + 1);
     }
-  }
-  if (p.piece_done) {
-    __threadfence();
-    named_bar(2, 32 * CONSUMER_WARPS);
-    if (tid == 0) piece_item_done(p, piece);
   }
 }
 

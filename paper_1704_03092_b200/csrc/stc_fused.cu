@@ -399,17 +399,13 @@ __device__ __forceinline__ void tma_reduce_add(const CUtensorMap *map, int rank,
 template <int PA, int PB>
 __device__ __forceinline__ void epilogue_red(const GemmArgs &p, const double (&acc)[4][4][4], int item, int tid, int wm,
                                              int wn, int g, int tig, double *buf, const CUtensorMap *tmC) {
-  int slot, ti, tj, pos, piece;
-  tile_of(p, item, slot, ti, tj, pos, piece);
+  int slot, ti, tj, pos;
+  tile_of(p, item, slot, ti, tj, pos);
   const TermDesc td = p.terms[slot];
-  if (p.piece_ready) {  // gated pieces: C rows of this piece uploaded
-    if (tid == 0) wait_piece(p, piece);
-    named_bar(2, 32 * CONSUMER_WARPS);
-  }
   int nb = 0;  // piece buffer
   for (int j = 0; j < td.c_count; ++j) {
     const TgtDesc tg = p.tgts[td.c_first + j];
-    if (p.use_tickets && !STC_NOTICKET) {
+    if (p.use_tickets) {
       if (tid == 0)
         while (ld_acquire_gpu(p.tickets + tg.ticket_base + pos) < tg.order) __nanosleep(64);
     }
@@ -449,16 +445,12 @@ __device__ __forceinline__ void epilogue_red(const GemmArgs &p, const double (&a
     }
     if (tid == 0) {  // this target's adds performed: hand the tile to the next term at once
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-      if (p.use_tickets && !STC_NOTICKET) {
+      if (p.use_tickets) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
         __threadfence();
         st_release_gpu(p.tickets + tg.ticket_base + pos, tg.order + 1);
       }
     }
-  }
-  if (tid == 0 && p.piece_done) {
-    asm volatile("cp.async.bulk.wait_group 0;\nfence.proxy.async.global;" ::: "memory");
-    piece_item_done(p, piece);
   }
 }
 
@@ -483,13 +475,9 @@ __device__ __forceinline__ void epilogue_warps(const GemmArgs &p, uint64_t *epi_
       named_bar(3, EPI_THREADS);
       c_seen = true;
     }
-    int slot, ti, tj, pos, piece;
-    tile_of(p, item, slot, ti, tj, pos, piece);
+    int slot, ti, tj, pos;
+    tile_of(p, item, slot, ti, tj, pos);
     const TermDesc td = p.terms[slot];
-    if (p.piece_ready) {  // gated pieces: C rows of this piece uploaded
-      if (t == 0) wait_piece(p, piece);
-      named_bar(3, EPI_THREADS);
-    }
     const double *Mt = p.mscratch + ((size_t)blockIdx.x * EPI_BUFS + eb) * TILE_DOUBLES;
     for (int j = 0; j < td.c_count; ++j) {
       const TgtDesc tg = p.tgts[td.c_first + j];
@@ -498,7 +486,7 @@ __device__ __forceinline__ void epilogue_warps(const GemmArgs &p, uint64_t *epi_
         cols[i] = __ldcg(p.pool + tg.col_start + tj * BN + i);
       }
       int32_t *ticket = p.tickets + tg.ticket_base + pos;
-      if (p.use_tickets && !STC_NOTICKET) {
+      if (p.use_tickets) {
         if (t == 0)
           while (ld_acquire_gpu(ticket) < tg.order) __nanosleep(64);
       }
@@ -527,14 +515,13 @@ __device__ __forceinline__ void epilogue_warps(const GemmArgs &p, uint64_t *epi_
           for (int q = 0; q < 4; ++q)
             if (ro[rr] != kPad && co[q] != kPad) __stcg(p.C + ro[rr] + co[q], c[rr][q] + tg.sign * m[rr][q]);
       }
-      if (p.use_tickets && !STC_NOTICKET) {
+      if (p.use_tickets) {
         __threadfence();
         named_bar(3, EPI_THREADS);
         if (t == 0) st_release_gpu(ticket, tg.order + 1);
       }
       named_bar(3, EPI_THREADS);  // offset tables reused by the next target
     }
-    if (t == 0) piece_item_done(p, piece);
     __syncwarp();
     if (lane == 0) mbar_arrive(&epi_empty[eb]);
     if (++eb == EPI_BUFS) {
@@ -565,16 +552,15 @@ __device__ __forceinline__ void epilogue_warps_red(const GemmArgs &p, uint64_t *
         while (ld_acquire_gpu(p.c_ready) == 0) __nanosleep(256);
       c_seen = true;
     }
-    int slot, ti, tj, pos, piece;
-    tile_of(p, item, slot, ti, tj, pos, piece);
+    int slot, ti, tj, pos;
+    tile_of(p, item, slot, ti, tj, pos);
     const TermDesc td = p.terms[slot];
-    if (t == 0 && p.piece_ready) wait_piece(p, piece);  // gated pieces: C rows uploaded
     const double *Mt = p.mscratch + ((size_t)blockIdx.x * EPI_BUFS + eb) * TILE_DOUBLES;
     int nb = 0;
     for (int j = 0; j < td.c_count; ++j) {
       const TgtDesc tg = p.tgts[td.c_first + j];
       const uint32_t flip = __double_as_longlong(tg.sign) < 0 ? 0x80000000u : 0u;
-      if (t == 0 && p.use_tickets && !STC_NOTICKET)
+      if (t == 0 && p.use_tickets)
         while (ld_acquire_gpu(p.tickets + tg.ticket_base + pos) < tg.order) __nanosleep(64);
       int4 cc = make_int4(0, 0, 0, 0);
       if (t == 0) cc = p.coords[(tg.col_start + (int64_t)tj * BN) >> 3];
@@ -606,16 +592,12 @@ __device__ __forceinline__ void epilogue_warps_red(const GemmArgs &p, uint64_t *
       }
       if (t == 0) {  // this target's adds performed: hand the tile to the next term
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        if (p.use_tickets && !STC_NOTICKET) {
+        if (p.use_tickets) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
           __threadfence();
           st_release_gpu(p.tickets + tg.ticket_base + pos, tg.order + 1);
         }
       }
-    }
-    if (t == 0 && p.piece_done) {
-      asm volatile("cp.async.bulk.wait_group 0;\nfence.proxy.async.global;" ::: "memory");
-      piece_item_done(p, piece);
     }
     named_bar(3, EPI_THREADS);  // every warp is done with this M buffer
     if (lane == 0) mbar_arrive(&epi_empty[eb]);
@@ -705,18 +687,13 @@ __device__ __forceinline__ void summer_warps(const GemmArgs &p, double *stages, 
         negmask = __ballot_sync(0xffffffffu, neg);
         do_a = na > 1 || (negmask & 1u);
         do_b = sum_b && (nb > 1 || ((negmask >> na) & 1u));
-#ifdef STC_EXPERIMENT_NOSUM
-        do_a = do_b = false;  // timing experiment only: no sums formed
-#endif
       }
       double *st = stages + (size_t)rs * sstride;
       if (do_a) sum_side<SH::AV>(reinterpret_cast<double2 *>(st), 0, na, negmask, t);
       if constexpr (TS == 0)  // shapes 1, 2 run with psum = 1
         if (do_b) sum_side<SH::BV>(reinterpret_cast<double2 *>(st + na * SH::AV), 0, nb, negmask >> na, t);
       // generic writes before the async proxy (TMA) refills this stage
-#ifndef STC_EXPERIMENT_NOPROXYFENCE
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#endif
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&summed[rs]);
@@ -749,7 +726,10 @@ __device__ __forceinline__ void skip_item(int S, uint64_t *full, uint64_t *empty
 // PS: a summing warpgroup forms (some of) the operand sums in place (p.psum);
 // otherwise the consumers form them all in their fragment loads.
 // TS: CTA tile shape (Shape<TS>; 1 and 2 only with PS and dense M output).
-template <int AKF, int BKF, bool PS, int TS>
+// ONE: every term has one view per side with sign +1 (pre-summed operand slots,
+// Naive's packed sums): the consumers only run consume_item<1, 1> -- without the
+// other view-count specialisations in the kernel, the consumers need no spills.
+template <int AKF, int BKF, bool PS, int TS, bool ONE = false>
 __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
     k_strassen_fused(const GemmArgs p, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC) {
@@ -772,10 +752,6 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
   const bool offload = p.mscratch != nullptr;  // ABC: epilogue warps update C from the M tiles
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-#ifdef STC_EXPERIMENT_ALIGNCHECK
-  if (tid == 0 && (smem_u32(stages) & 1023) != 0)
-    printf("[align] block %d smem base %u stages %u\n", blockIdx.x, smem_u32(smem), smem_u32(stages));
-#endif
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -807,7 +783,6 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
     }
     int stage = 0;
     uint32_t phase = 0;
-    int ready_piece = -1;
     for (;;) {
       int item = 0;
       if (lane == 0) item = atomicAdd(p.counter, 1);
@@ -820,13 +795,8 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
         }
         break;
       }
-      int slot, ti, tj, pos, piece;
-      tile_of(p, item, slot, ti, tj, pos, piece);
-      if (p.piece_ready && piece != ready_piece) {  // gated pieces: operands of this piece in HBM
-        if (lane == 0) wait_piece(p, piece);
-        __syncwarp();
-        ready_piece = piece;
-      }
+      int slot, ti, tj;
+      tile_of(p, item, slot, ti, tj);
       const TermDesc td = p.terms[slot];
       const int na = td.a_count, U = td.a_count + td.b_count;
       // lane u < U stages view u (A views first, then B views) of every chunk
@@ -844,11 +814,7 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
       int src[5];
 #pragma unroll
       for (int d = 0; d < 5; ++d) src[d] = p.tm_src[sd][d];
-#ifdef STC_EXPERIMENT_TWOVIEWS
-      const uint32_t bytes = (uint32_t)(SH::AV + SH::BV) * 8;
-#else
       const uint32_t bytes = (uint32_t)(na * SH::AV + (U - na) * SH::BV) * 8;
-#endif
       // stage layout: A view u at u * AV, B view w at na * AV + w * BV
       const size_t vofs = lane < na ? (size_t)lane * SH::AV : (size_t)na * SH::AV + (size_t)(lane - na) * SH::BV;
       for (int c = 0; c < kchunks; ++c) {
@@ -860,12 +826,7 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
           mbar_expect_tx_f(&full[stage], bytes);
         }
         __syncwarp();
-#ifdef STC_EXPERIMENT_TWOVIEWS
-        // timing experiment only: the first view of each side is loaded, the other slots are stale
-        if (lane == 0 || lane == na) {
-#else
         if (lane < U) {
-#endif
           int32_t cc[5];
 #pragma unroll
           for (int d = 0; d < 5; ++d) cc[d] = src[d] < 4 ? coord_of(xc, src[d]) : coord_of(kc, src[d] - 4);
@@ -944,16 +905,14 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
           bool neg = false;
           if (lane < nb) neg = __double_as_longlong(p.ops[td.b_first + lane].sign) < 0;
           const uint32_t negmask = __ballot_sync(0xffffffffu, neg) << 1;
-#ifdef STC_EXPERIMENT_NOBSUM
-          switch (1) {  // timing experiment only: the consumers read one B view
-#else
           switch (nb) {
-#endif
             case 1: consume_item<1, 1, true, SH::AV, SH::BV>(acc, stages, sstride, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bbase); break;
             case 2: consume_item<1, 2, true, SH::AV, SH::BV>(acc, stages, sstride, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bbase); break;
             default: consume_item<1, 4, true, SH::AV, SH::BV>(acc, stages, sstride, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bbase); break;
           }
         }
+      } else if constexpr (ONE) {
+        consume_item<1, 1, false>(acc, stages, sstride, S, full, empty, stage, phase, kchunks, 0u, offA, offB, lane);
       } else {
       // coefficient signs of the item's views: one load per lane, one ballot
       bool neg = false;
@@ -1029,18 +988,6 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
         }
         continue;
       }
-#ifdef STC_EXPERIMENT_NOEPI
-      {  // timing experiment only: keep every accumulator live, skip the C updates
-        double z = 0.0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) z += acc[i][j][r];
-        if (z == 1.2345e300) p.C[0] = z;
-      }
-#else
       if constexpr (TS != 0) {  // shapes 1, 2: dense M output only
         epilogue_store<AKF + 1, BKF + 1, 2, SH::BMT, SH::BNT>(p, acc, item, tid, wm, wn, g, tig);
       } else {
@@ -1050,30 +997,31 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
         else
           epilogue_store<AKF + 1, BKF + 1, 2>(p, acc, item, tid, wm, wn, g, tig);
       }
-#endif
     }
   }
 }
 
 using FusedKernel = void (*)(const GemmArgs, const CUtensorMap, const CUtensorMap, const CUtensorMap);
 
-template <bool PS, int TS>
+template <bool PS, int TS, bool ONE = false>
 static FusedKernel fused_for_ts(int akf, int bkf) {
-  if (akf) return bkf ? k_strassen_fused<1, 1, PS, TS> : k_strassen_fused<1, 0, PS, TS>;
-  return bkf ? k_strassen_fused<0, 1, PS, TS> : k_strassen_fused<0, 0, PS, TS>;
+  if (akf) return bkf ? k_strassen_fused<1, 1, PS, TS, ONE> : k_strassen_fused<1, 0, PS, TS, ONE>;
+  return bkf ? k_strassen_fused<0, 1, PS, TS, ONE> : k_strassen_fused<0, 0, PS, TS, ONE>;
 }
 
-static FusedKernel fused_for(int akf, int bkf, bool ps, int ts) {
+static FusedKernel fused_for(int akf, int bkf, bool ps, int ts, bool one) {
   if (ps) return ts == 1 ? fused_for_ts<true, 1>(akf, bkf) : ts == 2 ? fused_for_ts<true, 2>(akf, bkf)
                                                              : fused_for_ts<true, 0>(akf, bkf);
-  return fused_for_ts<false, 0>(akf, bkf);
+  return one ? fused_for_ts<false, 0, true>(akf, bkf) : fused_for_ts<false, 0>(akf, bkf);
 }
 
 cudaError_t launch_fused(const GemmArgs &a, int grid, cudaStream_t s, const void *maps) {
   const bool ps = a.psum != 0;
   if (a.tshape != 0 && (!ps || !a.dense_out || (a.psum & 2))) return cudaErrorInvalidValue;
   const size_t sm = FusedLayout::bytes((size_t)a.stage_dbl, a.stages, a.cred != 0);
-  FusedKernel k = fused_for(a.a_kfast, a.b_kfast, ps, a.tshape);
+  // one unsigned view per side (umax 2 with sign-free slots): the spill-free specialisation
+  const bool one = !ps && a.tshape == 0 && a.umax == 2 && a.one_view;
+  FusedKernel k = fused_for(a.a_kfast, a.b_kfast, ps, a.tshape, one);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   CUtensorMap m[3];

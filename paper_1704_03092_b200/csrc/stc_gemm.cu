@@ -721,11 +721,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
             for (int nt = 0; nt < 4; ++nt) {
-#ifdef STC_EXPERIMENT_NOMMA
-              acc[mt][nt][0] += af[mt][0] * bf[nt] * 1e-300;  // timing experiment only
-#else
               dmma_16x8x4(acc[mt][nt], af[mt][0], af[mt][1], bf[nt]);
-#endif
             }
         }
         __syncwarp();

@@ -99,11 +99,19 @@ struct TensorLabels {
     for (int d = 0; d < n; ++d) e *= ext[d];
     return e;
   }
-  // [base, hi): the storage the tensor's elements occupy (non-negative strides)
+  // [lo, hi): the storage the tensor's elements occupy (strides of either sign; the
+  // reference's DenseTensor allows negative strides, tensor.py:43-97)
+  int64_t lo() const {
+    int64_t l = base;
+    for (int d = 0; d < n; ++d)
+      if (str[d] < 0) l += (ext[d] - 1) * str[d];
+    return l;
+  }
   int64_t hi() const {
     int64_t h = base;
-    for (int d = 0; d < n; ++d) h += (ext[d] - 1) * str[d];
-    return elems() ? h + 1 : base;
+    for (int d = 0; d < n; ++d)
+      if (str[d] > 0) h += (ext[d] - 1) * str[d];
+    return elems() ? h + 1 : lo();
   }
   // strides a permutation of a dense row-major layout: the elements fill [base, base + elems)
   bool compact() const {
@@ -201,9 +209,9 @@ cudaError_t copy_piece(double *dst, const double *src, const TensorLabels &t, in
 }
 
 cudaError_t copy_span(double *dst, const double *src, const TensorLabels &t, cudaMemcpyKind kind, cudaStream_t s) {
-  const int64_t n = t.hi() - t.base;
+  const int64_t lo = t.lo(), n = t.hi() - lo;
   if (n <= 0) return cudaSuccess;
-  return cudaMemcpyAsync(dst + t.base, src + t.base, n * 8, kind, s);
+  return cudaMemcpyAsync(dst + lo, src + lo, n * 8, kind, s);
 }
 
 struct HostStreams {
@@ -228,6 +236,20 @@ int host_streams(HostStreams *&hs) {
 }
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// An error after the first enqueue returns while copies and kernels may still be
+// queued on the library's streams, reading and writing the caller's buffers: wait
+// for them before handing control (and the buffers) back.
+struct DrainOnError {
+  HostStreams *hs = nullptr;
+  bool armed = true;
+  ~DrainOnError() {
+    if (!armed || !hs) return;
+    for (cudaStream_t s : {hs->h2d, hs->d2h, hs->comp[0], hs->comp[1]})
+      if (s) cudaStreamSynchronize(s);
+    cudaGetLastError();
+  }
+};
 
 int piece_workspace(const stc_problem &p, const Split &sp, size_t &per_slot) {
   const stc_bundle &cb = sp.side == 0 ? p.c_row : p.c_col;
@@ -255,137 +277,6 @@ struct Events {
 
 // cuStreamWaitValue32 (driver API stream memory operation): the download stream
 // waits on the device-side item counter of a piece (gated mode).
-using WaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-WaitValue32Fn wait_value_fn() {
-  static WaitValue32Fn fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<WaitValue32Fn>(p);
-  });
-  return fn;
-}
-
-bool page_locked(const void *p) {
-  cudaPointerAttributes pa{};
-  const bool ok = cudaPointerGetAttributes(&pa, p) == cudaSuccess && pa.type == cudaMemoryTypeHost;
-  cudaGetLastError();  // a failed query leaves an error code behind
-  return ok;
-}
-
-// Gated mode: the I-bundle pieces run as ONE ticketed fused launch over the whole
-// problem, items ordered by piece, each piece's items waiting on the device for
-// its copy-engine-written flag (operand rows + C rows in HBM) and counting
-// themselves done; the download stream waits on those counters
-// (cuStreamWaitValue32).  One launch: no per-piece last wave, no piece-sized
-// Strassen -- and C bitwise equal to stc_contract on the same data.  Opt-in
-// (STC_HOST_GATED=1): measured slower at cfg2 (S = 4: 10.6 vs 9.5 ms per call),
-// because a piece holds only 2 of the 8 tile rows, so ~9 terms per C tile are in
-// flight and the C-tile tickets serialise them (the dense-M mode that avoids this
-// for the per-piece contractions needs an accumulate launch per piece, and the
-// persistent gated launch holds every SM).
-bool gate_for(const stc_problem &p, const Split &sp, int32_t *lo, int64_t *items) {
-  const char *e = getenv("STC_HOST_GATED");
-  if (!e || atoi(e) == 0) return false;
-  if (sp.pieces < 2 || sp.side != 0 || !wait_value_fn()) return false;
-  return plan_gate(&p, sp.lab, sp.pieces, lo, items);
-}
-
-int contract_gated(const stc_problem *p, const Split &sp, const int32_t *lo, const int64_t *items,
-                   const double *hA, const double *hB, double *hC, double *dA, double *dB, double *dC,
-                   void *workspace, size_t per, cudaStream_t us, stc_stats *stats) {
-  HostStreams *hs = nullptr;
-  if (int rc = host_streams(hs)) return rc;
-  stc_set_c_ready(nullptr);
-  stc_set_kernel_events(nullptr, nullptr);
-  const TensorLabels A = labels_of(p->a_row, p->a_col, p->a_base), B = labels_of(p->b_row, p->b_col, p->b_base),
-                     C = labels_of(p->c_row, p->c_col, p->c_base);
-  const int32_t *pf = pinned_flag_values();
-  if (!pf) return herr(STC_ECUDA, "cudaHostAlloc failed for the piece flags");
-  int32_t *flags = reinterpret_cast<int32_t *>(reinterpret_cast<char *>(workspace) + per);
-  int32_t *done = flags + kMaxPieces;
-  const int S = sp.pieces;
-  const int64_t lext = p->c_row.ext[sp.lab];
-  Events E;
-  cudaEvent_t start, zeroed, end;
-  HCU(E.make(start), "cudaEventCreate");
-  HCU(E.make(zeroed), "cudaEventCreate");
-  HCU(E.make(end), "cudaEventCreate");
-  HCU(cudaEventRecord(start, us), "cudaEventRecord");
-  for (cudaStream_t s : {hs->h2d, hs->d2h, hs->comp[0]}) HCU(cudaStreamWaitEvent(s, start, 0), "cudaStreamWaitEvent");
-  // STC_HOST_TRACE=1: per piece the flag (inputs in) and the download (C out), kernel end
-  const bool trace = getenv("STC_HOST_TRACE") != nullptr;
-  std::vector<cudaEvent_t> tr(trace ? 2 + 2 * S : 0);
-  for (auto &e : tr) HCU(cudaEventCreate(&e), "cudaEventCreate");
-  if (trace) HCU(cudaEventRecord(tr[0], us), "cudaEventRecord");
-  // flags and counters zeroed (copy engine) before the launch can read them
-  HCU(cudaMemcpyAsync(flags, pf, S * sizeof(int32_t), cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(flags)");
-  HCU(cudaMemcpyAsync(done, pf, S * sizeof(int32_t), cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(counters)");
-  HCU(cudaEventRecord(zeroed, hs->h2d), "cudaEventRecord");
-  HCU(cudaStreamWaitEvent(hs->comp[0], zeroed, 0), "cudaStreamWaitEvent");
-  // the launch first: its CTAs wait on the device while the pieces stream in
-  PieceGate gate{};
-  gate.n = S;
-  for (int i = 0; i <= S; ++i) gate.lo[i] = lo[i];
-  gate.ready = flags;
-  gate.done = done;
-  set_piece_gate(&gate);
-  stc_stats st{};
-  const int rc = stc_contract(p, dA, dB, dC, workspace, per, hs->comp[0], &st);
-  set_piece_gate(nullptr);
-  if (rc) {
-    cudaStreamSynchronize(hs->h2d);
-    return rc;
-  }
-  if (trace) HCU(cudaEventRecord(tr[1], hs->comp[0]), "cudaEventRecord");
-  // uploads: B (every piece reads all of it), then per piece its A rows, C rows, flag
-  HCU(copy_span(dB, hB, B, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(B)");
-  for (int s = 0; s < S; ++s) {
-    const int64_t r0 = lext * s / S, len = lext * (s + 1) / S - r0;
-    HCU(copy_piece(dA, hA, A, p->a_row.str[sp.lab], lext, r0, len, cudaMemcpyHostToDevice, hs->h2d),
-        "cudaMemcpy2DAsync(A piece)");
-    HCU(copy_piece(dC, hC, C, p->c_row.str[sp.lab], lext, r0, len, cudaMemcpyHostToDevice, hs->h2d),
-        "cudaMemcpy2DAsync(C piece)");
-    HCU(cudaMemcpyAsync(flags + s, pf + kMaxPieces, sizeof(int32_t), cudaMemcpyHostToDevice, hs->h2d),
-        "cudaMemcpyAsync(flag)");
-    if (trace) HCU(cudaEventRecord(tr[2 + 2 * s], hs->h2d), "cudaEventRecord");
-  }
-  // downloads: C rows of piece s once its items are done
-  WaitValue32Fn wait = wait_value_fn();
-  for (int s = 0; s < S; ++s) {
-    const int64_t r0 = lext * s / S, len = lext * (s + 1) / S - r0;
-    if (wait(reinterpret_cast<CUstream>(hs->d2h), reinterpret_cast<CUdeviceptr>(done + s), (cuuint32_t)items[s],
-             CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-      return herr(STC_ECUDA, "cuStreamWaitValue32 failed");
-    HCU(copy_piece(hC, dC, C, p->c_row.str[sp.lab], lext, r0, len, cudaMemcpyDeviceToHost, hs->d2h),
-        "cudaMemcpy2DAsync(C piece)");
-    if (trace) HCU(cudaEventRecord(tr[3 + 2 * s], hs->d2h), "cudaEventRecord");
-  }
-  HCU(cudaEventRecord(end, hs->d2h), "cudaEventRecord");
-  if (trace) {
-    cudaEventSynchronize(end);
-    float t = 0;
-    cudaEventElapsedTime(&t, tr[0], tr[1]);
-    fprintf(stderr, "[stc host gated] pieces=%d kernel end %.2f ms:", S, t);
-    for (int s = 0; s < S; ++s) {
-      fprintf(stderr, " |%d", s);
-      for (int k = 0; k < 2; ++k) {
-        cudaEventElapsedTime(&t, tr[0], tr[2 + 2 * s + k]);
-        fprintf(stderr, " %.2f", t);
-      }
-    }
-    fprintf(stderr, "  (in, out ms)\n");
-    for (cudaEvent_t e : tr) cudaEventDestroy(e);
-  }
-  HCU(cudaStreamWaitEvent(hs->comp[0], end, 0), "cudaStreamWaitEvent");  // the next call's launch
-  HCU(cudaStreamWaitEvent(us, end, 0), "cudaStreamWaitEvent");
-  if (stats) *stats = st;
-  return STC_OK;
-}
-
 }  // namespace
 
 extern "C" {
@@ -405,13 +296,6 @@ int stc_host_workspace_size(const stc_problem *p, size_t *bytes) {
   size_t per = 0;
   if (int rc = piece_workspace(*p, sp, per)) return rc;
   size_t need = per * (sp.pieces > 1 ? 2 : 1) + kFlagBytes;
-  int32_t lo[kMaxGatedPieces + 1];
-  int64_t items[kMaxGatedPieces];
-  if (gate_for(*p, sp, lo, items)) {  // gated mode: one whole-problem workspace + flags and counters
-    size_t b = 0;                     // (the per-piece path stays possible: pageable host buffers)
-    if (int rc = stc_workspace_size(p, &b)) return rc;
-    need = std::max(need, align256(std::max<size_t>(b, 256)) + kFlagBytes);
-  }
   if (bytes) *bytes = need;
   return STC_OK;
 }
@@ -421,21 +305,6 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
   if (!p) return herr(STC_EINVAL, "null problem");
   if (!hA || !hB || !hC || !dA || !dB || !dC) return herr(STC_EINVAL, "null operand pointer");
   const Split sp = choose_split(*p);
-  {
-    int32_t lo[kMaxGatedPieces + 1];
-    int64_t items[kMaxGatedPieces];
-    if (gate_for(*p, sp, lo, items) && page_locked(hA) && page_locked(hB) && page_locked(hC)) {
-      size_t b = 0;
-      if (int rc = stc_workspace_size(p, &b)) return rc;
-      const size_t per = align256(std::max<size_t>(b, 256));
-      if (!workspace || workspace_bytes < per + kFlagBytes)
-        return herr(STC_EWORKSPACE, "workspace too small: need %zu bytes, got %zu", per + kFlagBytes,
-                    workspace_bytes);
-      if (reinterpret_cast<uintptr_t>(workspace) & 255) return herr(STC_EINVAL, "workspace must be 256-byte aligned");
-      return contract_gated(p, sp, lo, items, hA, hB, hC, dA, dB, dC, workspace, per,
-                            reinterpret_cast<cudaStream_t>(stream), stats);
-    }
-  }
   size_t per = 0;
   if (int rc = piece_workspace(*p, sp, per)) return rc;
   const int slots = sp.pieces > 1 ? 2 : 1;
@@ -457,6 +326,8 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
   }
   HostStreams *hs = nullptr;
   if (int rc = host_streams(hs)) return rc;
+  DrainOnError drain;
+  drain.hs = hs;
   // the per-call hooks belong to device-operand calls
   stc_set_c_ready(nullptr);
   stc_set_kernel_events(nullptr, nullptr);
@@ -593,6 +464,8 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
     for (cudaEvent_t e : tr) cudaEventDestroy(e);
   }
   HCU(cudaStreamWaitEvent(us, end, 0), "cudaStreamWaitEvent");
+  drain.armed = false;
+  total.pieces = sp.pieces;
   if (stats) *stats = total;
   return STC_OK;
 }

@@ -25,7 +25,6 @@ constexpr int THREADS = 32 * (CONSUMER_WARPS + PRODUCER_WARPS);
 constexpr int CONSUMER_REGS = 192;
 constexpr int PRODUCER_REGS = 64;
 constexpr int MAX_OPS = 16;
-constexpr int kMaxGatedPieces = 16;  // host pipeline pieces in one launch
 #ifndef STC_EPI_BUFS
 #define STC_EPI_BUFS 2
 #endif
@@ -97,6 +96,7 @@ struct GemmArgs {
   // fused kernel (stc_fused.cu)
   const int4 *coords;        // coords[i]: map coordinates (one part) of pool entry 8 i
   int32_t umax, stages;      // views per chunk stage (2 * max_ops), ring depth
+  int32_t one_view;          // every term: one view per side, sign +1 (packed / pre-summed slots)
   int32_t stage_dbl;         // doubles per stage (max_ops x (A view + B view))
   int32_t tshape;            // CTA tile shape: 0 128 x 128, 1 64 x 256, 2 256 x 64 (stc_fused.cu Shape)
   int32_t psum;              // summing warpgroup (stc_fused.cu): bit 0 sums the A side, bit 1 the B
@@ -104,14 +104,6 @@ struct GemmArgs {
   double *mscratch;          // ABC: [grid][2][BM * BN] M tiles handed to the epilogue warps
   int32_t cred;              // ABC: C updates by TMA reduce-add of M pieces (C views regular)
   const int32_t *c_ready;    // stc_set_c_ready: wait until *c_ready != 0 before touching C
-  // Host-operand pieces in one launch (stc_host.cu, gated mode): items ordered piece-major,
-  // piece s = tile rows [piece_lo[s], piece_lo[s + 1]); its operand rows and C rows are in
-  // HBM once piece_ready[s] != 0 (copy-engine-written), and piece_done[s] counts its
-  // finished items (a stream waits on it before downloading the piece's C rows).
-  int32_t npieces;           // 0: one piece, no gating
-  int32_t piece_lo[kMaxGatedPieces + 1];
-  const int32_t *piece_ready;
-  int32_t *piece_done;
 };
 
 // Jobs of k_pool_coords: one per operand pool vector (x or k part of A or B).
@@ -217,15 +209,6 @@ cudaError_t launch_fused(const GemmArgs &a, int grid, cudaStream_t s, const void
 cudaError_t launch_pool_coords(const int64_t *pool, int4 *coords, const CoordJobs &jobs, cudaStream_t s);
 int gemm_max_grid(int max_ops);
 bool plan_ticketed(const stc_problem *p);  // stc_capi.cu
-// Gated host pieces (stc_host.cu -> the next stc_contract call on this thread)
-struct PieceGate {
-  int n;
-  int32_t lo[kMaxGatedPieces + 1];
-  const int32_t *ready;
-  int32_t *done;
-};
-void set_piece_gate(const PieceGate *g);
-bool plan_gate(const stc_problem *p, int lab, int S, int32_t *lo, int64_t *items);
 cudaError_t launch_accumulate(const AccArgs &a, cudaStream_t s);
 cudaError_t launch_unpack(const UnpackArgs &a, cudaStream_t s);
 cudaError_t launch_presum(const PresumArgs &a, cudaStream_t s);

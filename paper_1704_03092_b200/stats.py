@@ -11,12 +11,22 @@ __all__ = ["RunStats", "effective_gflops"]
 class RunStats:
     """Timing and counters of one ``contract`` call.
 
-    ``seconds`` is the device time of the call (CUDA events on its stream).
+    ``seconds`` is the wall clock of the whole call, as the reference times it
+    (perf_counter around the call body, strassen.py:154,205): planning, host
+    staging and transfers for host operands, and the device work, synchronised
+    before return.  ``device_seconds`` is the device time of the work the call
+    enqueued (CUDA events on its stream).  ``synchronize=False`` calls return
+    without either (the caller times its stream).
     ``total_flops`` counts executed MMA flops including tile padding;
-    ``effective_gflops`` always uses the classical 2*N_I*N_J*N_P, so Strassen's
-    saving shows as a higher effective rate (same definition as the reference,
-    oracle.py:46-50).  Block/update counters are per GPU tile (the reference
-    counts per mr x nr register block).
+    ``effective_gflops`` always uses the classical 2*N_I*N_J*N_P over
+    ``seconds``, so Strassen's saving shows as a higher effective rate (same
+    definition as the reference, oracle.py:46-50).  Block/update counters are
+    per GPU tile (the reference counts per mr x nr register block): fast blocks
+    are operand tiles staged by TMA boxes, slow blocks by per-element gathers;
+    fast updates are C-tile updates by TMA reduce-add boxes, slow updates by the
+    scatter epilogue or the dense-M accumulate pass.  ``leaf_multiplies`` is 7^L
+    per contraction as in the reference; ``pieces`` > 1 when host operands were
+    contracted in independent pieces (pieces x 7^L leaf products ran).
     """
 
     seconds: float = 0.0
@@ -30,6 +40,8 @@ class RunStats:
     leaf_multiplies: int = 0
     work_items: int = 0
     kernel_launches: int = 0
+    pieces: int = 1
+    device_seconds: float = 0.0
 
     def total_gflops(self) -> float:
         return self.total_flops / self.seconds / 1e9 if self.seconds > 0 else 0.0
@@ -44,6 +56,7 @@ class RunStats:
         self.leaf_multiplies += st.leaf_multiplies
         self.work_items += st.work_items
         self.kernel_launches += st.kernel_launches
+        self.pieces = max(1, int(st.pieces))
 
 
 def effective_gflops(n_i: int, n_j: int, n_p: int, seconds: float) -> float:

@@ -16,14 +16,16 @@ Operands may be reference-style ``DenseTensor`` objects with host (numpy)
 storage -- staged through HBM, C copied back -- or HBM-resident: strided
 float64 CUDA ``torch.Tensor`` or ``DenseTensor`` with CUDA storage.  The work
 itself always runs in ``libstc_b200.so`` (C ABI, include/stc_b200.h); there is
-no CPU path.  ``params`` (CPU blocking) and ``threads`` are accepted and
-ignored: the GPU tiling is fixed (views.TILE).
+no CPU path.  ``params`` (the reference's CPU cache blocking, validated on
+construction like the reference's) is accepted and has no GPU counterpart --
+the GPU tiling is fixed, described by views.TILE -- and ``threads`` is ignored.
 """
 
 from __future__ import annotations
 
 import ctypes
 import os
+import time
 from dataclasses import dataclass
 from enum import Enum
 
@@ -179,10 +181,10 @@ def _flat_host(t: DenseTensor):
     return d.ctypes.data, d.size
 
 
-def _contract_host(spec, a, b, c, level, variant, force_slow, reference_tiling, validate, terms, dev) -> RunStats:
+def _contract_host(spec, a, b, c, level, variant, force_slow, reference_tiling, validate, terms, dev,
+                   t_start) -> RunStats:
     """Host operands: stc_contract_host pipelines the uploads, the piecewise
-    contraction and the download of C (stc_host.cu).  ``seconds`` covers the
-    whole call (transfers included)."""
+    contraction and the download of C (stc_host.cu)."""
     import torch
 
     (pa, na), (pb, nb), (pc, nc) = _flat_host(a), _flat_host(b), _flat_host(c)
@@ -211,7 +213,8 @@ def _contract_host(spec, a, b, c, level, variant, force_slow, reference_tiling, 
         e1.record(stream)
         e1.synchronize()  # C is host memory: complete before returning
         stats.absorb(st)
-        stats.seconds = max(e0.elapsed_time(e1) * 1e-3, 1e-12)
+        stats.device_seconds = max(e0.elapsed_time(e1) * 1e-3, 1e-12)
+    stats.seconds = max(time.perf_counter() - t_start, 1e-12)
     stats.effective_gflops = effective_gflops(spec.n_i, spec.n_j, spec.n_p, stats.seconds)
     return stats
 
@@ -246,9 +249,16 @@ def contract(spec: ContractionSpec, a, b, c, level: int, variant, params: Blocki
 
     Level 0 is the plain block-scatter GEMM.  All variants compute the same
     result up to floating-point reordering and execute exactly 7^level leaf
-    products.  ``RunStats.seconds`` is the device time of the call (CUDA
-    events on the current stream; host staging excluded).
+    products.  ``RunStats.seconds`` is the wall clock of the whole call (the
+    reference's timer, strassen.py:154,205); ``device_seconds`` the CUDA-event
+    time of the work it enqueued on the current stream.  ``params`` (the
+    reference's CPU cache blocking) has no GPU counterpart: it is validated like
+    the reference does and otherwise ignored -- the GPU tiles are fixed
+    (views.TILE describes them).  ``threads`` is ignored.
     """
+    t_start = time.perf_counter()
+    if not all(hasattr(params, f) for f in ("mc", "nc", "kc", "mr", "nr", "kr")):
+        raise TypeError("params must be a BlockingParams (the reference's blocking; the GPU tiling is views.TILE)")
     a, b, c = _as_dense(a, "A"), _as_dense(b, "B"), _as_dense(c, "C")
     _check_operands(spec, a, b, c)
     terms = strassen_terms(level, allow_deep)
@@ -268,7 +278,8 @@ def contract(spec: ContractionSpec, a, b, c, level: int, variant, params: Blocki
     # flag before their first C update (stc_set_c_ready).
     if not (a.on_device or b.on_device or c.on_device) and kernel_events is None \
             and os.environ.get("STC_HOST_PIPELINE", "1") != "0" and all(_flat_host(t) is not None for t in (a, b, c)):
-        return _contract_host(spec, a, b, c, level, variant, force_slow, reference_tiling, validate, terms, dev)
+        return _contract_host(spec, a, b, c, level, variant, force_slow, reference_tiling, validate, terms, dev,
+                              t_start)
     c_ready = None
     main = torch.cuda.current_stream(dev)
     A = a if a.on_device else a.to_device(dev)
@@ -324,6 +335,7 @@ def contract(spec: ContractionSpec, a, b, c, level: int, variant, params: Blocki
             # stream-ordered only: the caller times the stream itself; no per-call seconds
             return stats
         e1.synchronize()
-        stats.seconds = max(e0.elapsed_time(e1) * 1e-3, 1e-12)
+        stats.device_seconds = max(e0.elapsed_time(e1) * 1e-3, 1e-12)
+    stats.seconds = max(time.perf_counter() - t_start, 1e-12)
     stats.effective_gflops = effective_gflops(spec.n_i, spec.n_j, spec.n_p, stats.seconds)
     return stats

@@ -54,9 +54,18 @@ __all__ = [
 
 PAD = _lib.PAD
 
-# GPU tile configuration of the DMMA kernel (csrc/stc_internal.cuh).
-TILE = {"BM": 128, "BN": 128, "BK": 16, "stages": 4, "consumer_warps": 8, "producer_warps": 4,
-        "mma": "mma.sync.m16n8k4.f64 (DMMA)"}
+# GPU tiling of the fused DMMA kernel (csrc/stc_fused.cu), the counterpart of the
+# reference's BlockingParams: fixed, not configurable per call.
+TILE = {
+    "cta_tile": (128, 128),              # 64 x 256 / 256 x 64 for 64-wide quadrants (dense-M launches)
+    "warp_tile": (64, 32),               # 8 consumer warps, mma.sync.m16n8k4.f64 (DMMA) fragments
+    "k_chunk": 8,                        # one TMA box per view per stage: 128 x 8 doubles
+    "stages": "8 with one view per side (L0, pre-summed or Naive slots); 6 / 3 with 2 / 4 views per side",
+    "producer_warps": 4,                 # warp 0 issues the TMA loads, warps 1-3 run the C epilogue
+    "summing_warps": 4,                  # in-kernel operand sums (L >= 1 without pre-summed slots)
+    "mma": "mma.sync.m16n8k4.row.col.f64 (SASS DMMA.8x8x4)",
+    "gather_kernel": {"cta_tile": (128, 128), "k_chunk": 16, "stages": 3},  # k_strassen_gemm (force_slow, L >= 3)
+}
 
 
 @dataclass(frozen=True)

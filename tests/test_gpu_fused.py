@@ -42,17 +42,8 @@ def _operands(spec, seed):
 
 
 def _run(spec, a, b, c0, level, variant, fused):
-    old = os.environ.get("STC_FUSED")
-    os.environ["STC_FUSED"] = "1" if fused else "0"
-    try:
-        c = c0.to_device()
-        st = stc.contract(spec, a, b, c, level, variant)
-        return c.to_host(), st
-    finally:
-        if old is None:
-            del os.environ["STC_FUSED"]
-        else:
-            os.environ["STC_FUSED"] = old
+    # the in-kernel operand sums (pre-summed slots are compared in test_presum_*)
+    return _run_env(spec, a, b, c0, level, variant, {"STC_FUSED": "1" if fused else "0", "STC_PRESUM_OPS": "0"})
 
 
 @pytest.mark.parametrize("name", sorted(LAYOUTS))
@@ -72,6 +63,7 @@ def test_fused_matches_gather_bitwise_and_classical(name):
 
 
 def _run_env(spec, a, b, c0, level, variant, env):
+    env = {"STC_PRESUM_OPS": "0", **env}  # in-kernel sums unless a test asks for the slots
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
@@ -298,3 +290,53 @@ def test_random_contractions_fuzz():
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
     assert mod.main(24, 7) == 0
+
+
+@pytest.mark.parametrize("name", sorted(LAYOUTS))
+def test_presummed_operands_match_in_kernel_sums_bitwise(name):
+    # k_presum forms every term's operand sums once per element position (same view order
+    # and roundings as the in-SM sums), the fused kernel then reads one slot per side:
+    # C must be bitwise equal to the in-kernel sums, for every C-update path
+    spec = stc.parse_benchmark_line(LAYOUTS[name])
+    a, b, c0 = _operands(spec, 67)
+    for level in (1, 2):
+        for variant in ("abc", "ab"):
+            for epi in ({}, {"STC_ABC_DENSE": "1"}, {"STC_CRED": "0"}):
+                ck, _ = _run_env(spec, a, b, c0, level, variant, {"STC_PRESUM_OPS": "0", **epi})
+                cp, st = _run_env(spec, a, b, c0, level, variant, {"STC_PRESUM_OPS": "1", **epi})
+                assert np.array_equal(cp.data, ck.data), (name, level, variant, epi)
+                assert st.fast_blocks > 0 and st.leaf_multiplies == 7 ** level
+
+
+@pytest.mark.parametrize("line", [
+    "abcij eafbc ifje & a:10;b:7;c:13;i:14;j:9;e:18;f:11;",  # irregular, PAD quadrants
+    "abcijk abcefg efgijk & a:4;b:8;c:8;i:4;j:8;k:8;e:4;f:8;g:8;",  # cfg5 pattern: 8-wide C runs at L2
+])
+def test_presummed_irregular_layouts_match_oracle(line):
+    spec = stc.parse_benchmark_line(line)
+    a, b, c0 = _operands(spec, 73)
+    classical = c0.copy()
+    oracle.contract_reference(spec, a.to_host(), b.to_host(), classical)
+    for level in (1, 2):
+        for variant in ("abc", "ab", "naive"):
+            cp, _ = _run_env(spec, a, b, c0, level, variant, {"STC_PRESUM_OPS": "1"})
+            ck, _ = _run_env(spec, a, b, c0, level, variant, {"STC_PRESUM_OPS": "0"})
+            assert np.array_equal(cp.data, ck.data), (line, level, variant)
+            assert stc.relative_error(cp, classical) <= TOL, (line, level, variant)
+
+
+@pytest.mark.parametrize("line,level", [
+    ("abcij eafbc ifje & a:50;b:7;c:13;i:70;j:45;e:90;f:33;", 0),  # cfg4 L0: the consumers' scatter epilogue
+    ("aibj eafb jfie & a:32;b:64;i:32;j:64;e:32;f:32;", 2),         # L2 ABC, TMA reduce-add epilogue
+])
+def test_repeated_runs_bitwise_stable(line, level):
+    # regression guard for the TMA-refill race (a stage refilled while
+    # fragment loads were in flight gave wrong 64-row blocks about 1 run in 4): the same
+    # contraction repeated must give the same bits every time, on both C-update paths
+    spec = stc.parse_benchmark_line(line)
+    a, b, c0 = _operands(spec, 79)
+    for ps in ("0", "1"):
+        first, _ = _run_env(spec, a, b, c0, level, "abc", {"STC_PRESUM_OPS": ps})
+        for _ in range(12):
+            again, _ = _run_env(spec, a, b, c0, level, "abc", {"STC_PRESUM_OPS": ps})
+            assert np.array_equal(again.data, first.data), (line, level, ps)

@@ -186,29 +186,46 @@ def _pinned(t):
 
 
 @pytest.mark.parametrize("pieces", ["2", "4"])
-def test_host_pipeline_gated_single_launch_bitwise_equals_device_path(pieces):
-    # STC_HOST_GATED=1, page-locked operands, I split: the pieces run as ONE ticketed launch over the whole
-    # problem (items gated per piece on copy-engine-written flags, downloads behind
-    # device-side item counters), so C equals the device-operand path bitwise
+def test_host_pipeline_pieces_against_device_path(pieces):
+    # host operands: the problem is cut into pieces, each its own L-level Strassen over
+    # its own quadrants (a different pairing than the whole problem: rounding-level
+    # differences only); RunStats reports the piece count beside leaf_multiplies = 7^L
     import torch
 
     spec = stc.parse_benchmark_line("aibj eafb jfie & a:32;b:64;i:32;j:64;e:32;f:32;")
     a, b, c0 = (_tensor(spec, l, s, False) for l, s in ((spec.labels_a, 7), (spec.labels_b, 8), (spec.labels_c, 9)))
     dev = stc.DenseTensor(c0.extents, c0.strides, torch.from_numpy(c0.data.copy()).cuda(), 0)
-    stc.contract(spec, a.to_device(), b.to_device(), dev, 2, "abc")
+    sd = stc.contract(spec, a.to_device(), b.to_device(), dev, 2, "abc")
+    assert sd.pieces == 1
     want = dev.data.cpu().numpy()
     ha, hb, hc = _pinned(a), _pinned(b), _pinned(c0.copy())
-    env = {"STC_HOST_PIECES": pieces, "STC_ABC_DENSE": "0", "STC_HOST_GATED": "1"}  # the gate needs the ticketed plan
-    st = _with_env(env, lambda: stc.contract(spec, ha, hb, hc, 2, "abc"))
-    assert st.kernel_launches < 10, st  # one contraction, not one per piece
-    assert np.array_equal(hc.data.numpy(), want), pieces
-    # the per-piece contractions (STC_HOST_GATED=0) agree in norm
-    hc2 = _pinned(c0.copy())
-    _with_env({**env, "STC_HOST_GATED": "0"}, lambda: stc.contract(spec, ha, hb, hc2, 2, "abc"))  # per piece
-    assert np.linalg.norm(hc2.data.numpy() - want) / np.linalg.norm(want) <= TOL
-    # repeated calls reuse the flags and counters (zeroed per call)
-    hc3 = _pinned(c0.copy())
-    for _ in range(2):
-        hc3 = _pinned(c0.copy())
-        _with_env(env, lambda: stc.contract(spec, ha, hb, hc3, 2, "abc"))
-    assert np.array_equal(hc3.data.numpy(), want)
+    st = _with_env({"STC_HOST_PIECES": pieces}, lambda: stc.contract(spec, ha, hb, hc, 2, "abc"))
+    assert st.pieces == int(pieces) and st.leaf_multiplies == 49, st
+    assert np.linalg.norm(hc.data.numpy() - want) / np.linalg.norm(want) <= TOL
+    ref = c0.copy()
+    oracle.contract_reference(spec, a, b, ref, threads=oracle.max_threads())
+    got = stc.DenseTensor(c0.extents, c0.strides, hc.data.numpy())
+    assert oracle.relative_error(got, ref) <= TOL
+
+
+@pytest.mark.parametrize("level,variant", [(1, "abc"), (2, "naive")])
+def test_host_operands_with_negative_strides(level, variant):
+    # the reference's DenseTensor allows negative strides (tensor.py:43-97): a reversed
+    # numpy view as A and as C, host storage, through the host pipeline
+    spec = stc.parse_benchmark_line("abij abef efij & a:7;b:6;i:5;j:9;e:4;f:8;")
+    a, b, c0 = (_tensor(spec, l, s, False) for l, s in ((spec.labels_a, 3), (spec.labels_b, 4), (spec.labels_c, 5)))
+
+    def reversed_first_axis(t):
+        st = list(t.strides)
+        base = t.base_offset + (t.extents[0] - 1) * st[0]
+        st[0] = -st[0]
+        # the same elements addressed from the other end: value at index i is the old (n-1-i)
+        return stc.DenseTensor(t.extents, tuple(st), t.data.copy(), base)
+
+    ra, rc = reversed_first_axis(a), reversed_first_axis(c0)
+    ref = rc.copy()
+    oracle.contract_reference(spec, ra, b, ref)
+    got = rc.copy()
+    st = stc.contract(spec, ra, b, got, level, variant)
+    assert st.leaf_multiplies == 7 ** level
+    assert oracle.relative_error(got, ref) <= TOL

@@ -50,10 +50,12 @@ def _worker(rank, world, port, line, ret):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("line", ["abcijk abcefg efgijk & a:3;b:2;c:4;i:4;j:3;k:2;e:2;f:3;g:2;",
-                                  "aibj eafb jfie & a:5;b:3;i:6;j:4;e:3;f:2;"])
-def test_two_rank_nsplit_gloo(line):
-    world = 2
+@pytest.mark.parametrize("line,world", [("abcijk abcefg efgijk & a:3;b:2;c:4;i:4;j:3;k:2;e:2;f:3;g:2;", 2),
+                                        ("aibj eafb jfie & a:5;b:3;i:6;j:4;e:3;f:2;", 2),
+                                        # odd J extents: shards of unequal size (the all-gather pads)
+                                        ("aibj eafb jfie & a:4;b:3;i:5;j:3;e:3;f:2;", 2),
+                                        ("abcijk abcefg efgijk & a:2;b:3;c:2;i:5;j:7;k:3;e:2;f:3;g:2;", 3)])
+def test_nsplit_gloo(line, world):
     mgr = mp.Manager()
     ret = mgr.dict()
     mp.spawn(_worker, args=(world, _free_port(), line, ret), nprocs=world, join=True)

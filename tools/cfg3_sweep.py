@@ -31,7 +31,7 @@ def main(levels):
             flops = 2.0 * spec.n_i * spec.n_j * spec.n_p
             for level in levels:
                 stc.contract(spec, a, b, c, level, "abc")
-                best = min(stc.contract(spec, a, b, c, level, "abc").seconds for _ in range(3))
+                best = min(stc.contract(spec, a, b, c, level, "abc").device_seconds for _ in range(3))
                 print(f"cfg3 {reading:7s} N_a={na:3d} N_i={ni:4d} m={spec.n_i:6d} n={spec.n_j:8d} k={spec.n_p} "
                       f"L{level} ABC {best * 1e3:9.3f} ms  eff {flops / best / 1e12:6.2f} TF/s "
                       f"({100 * flops / best / 1e12 / 37.0:5.1f}% of 37.0)", flush=True)

@@ -15,4 +15,4 @@ c = dev_tensor(spec.tensor_extents(spec.labels_c), 3, zero=True)
 for _ in range(reps):
     st = stc.contract(spec, a, b, c, level, variant)
 torch.cuda.synchronize()
-print(f"{name} L{level} {variant}: {st.seconds*1e3:.3f} ms eff {2.0*spec.n_i*spec.n_j*spec.n_p/st.seconds/1e12:.2f} TF/s")
+print(f"{name} L{level} {variant}: {st.device_seconds*1e3:.3f} ms eff {2.0*spec.n_i*spec.n_j*spec.n_p/st.device_seconds/1e12:.2f} TF/s")
