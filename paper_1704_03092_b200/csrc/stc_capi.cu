@@ -996,9 +996,17 @@ bool plan_cred_side(const stc_bundle &rb, const Tiling &tr, const stc_bundle &cb
   std::vector<Dim> dims;
   if (noc == 0 || cb.str[oc[0]] != 1) return false;
   const int64_t e0 = cb.ext[oc[0]], b0 = tbc[oc[0]];
-  if (b0 < 16 || b0 % 16 != 0 || (b0 > 16 && e0 % 16 != 0)) return false;
-  dims.push_back({b0 > 16 ? 16 : e0, 1, 16, false});
-  if (b0 > 16) dims.push_back({e0 / 16, 16, b0 / 16, false});
+  // the unit-stride label's tile extent: 16+ doubles -> 128-byte rows (128B swizzle);
+  // exactly 8 (a quadrant split of that label, e.g. cfg5's k at L2) -> 64-byte rows
+  // (64B swizzle; GemmArgs::cred8)
+  const bool w8 = b0 == 8;
+  if (w8) {
+    dims.push_back({e0, 1, 8, false});
+  } else {
+    if (b0 < 16 || b0 % 16 != 0 || (b0 > 16 && e0 % 16 != 0)) return false;
+    dims.push_back({b0 > 16 ? 16 : e0, 1, 16, false});
+    if (b0 > 16) dims.push_back({e0 / 16, 16, b0 / 16, false});
+  }
   for (int j = 1; j < noc; ++j) dims.push_back({cb.ext[oc[j]], cb.str[oc[j]], tbc[oc[j]], false});
   for (int j = 0; j < nor; ++j) dims.push_back({rb.ext[orr[j]], rb.str[orr[j]], tbr[orr[j]], true});
   for (int pass = 0; pass < 2; ++pass) {
@@ -1036,7 +1044,7 @@ bool plan_cred_side(const stc_bundle &rb, const Tiling &tr, const stc_bundle &cb
     if (d > 0) ts.strides[d - 1] = (cuuint64_t)(dims[d].str * 8);
   }
   for (int d = ts.rank; d < 5; ++d) ts.src[d] = 0;
-  ts.swizzle = 128;
+  ts.swizzle = w8 ? 64 : 128;
   return true;
 }
 
@@ -1221,6 +1229,7 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
       plan_cred_side(p->c_row, pl.ti, p->c_col, pl.tj, pl.level, C, p->c_base, sc) &&
       encode_side(sc, C, p->c_base, maps[2])) {
     g.cred = 1;
+    g.cred8 = sc.swizzle == 64;
     g.tm_rank[2] = sc.rank;
     for (int d = 0; d < 5; ++d) g.tm_src[2][d] = sc.src[d];
     for (int part = 0; part < 2; ++part) {

@@ -365,6 +365,13 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
 __device__ __forceinline__ int red_index(int r, int c) {
   return r * BN + (c >> 4) * 16 + ((((c & 15) >> 1) ^ (c >> 4)) << 1) + (c & 1);
 }
+// The 8-wide variant (GemmArgs::cred8): box [r][c / 8][c % 8], 64-byte lines, 64B
+// swizzle (16-byte granule index XOR bits 7-8 of the byte offset).
+__device__ __forceinline__ int red_index8(int r, int c) {
+  const int line = r * (BN / 8) + (c >> 3);
+  return line * 8 + ((((c & 7) >> 1) ^ ((line >> 1) & 3)) << 1) + (c & 1);
+}
+__device__ __forceinline__ int red_idx(bool w8, int r, int c) { return w8 ? red_index8(r, c) : red_index(r, c); }
 
 __device__ __forceinline__ void tma_reduce_add(const CUtensorMap *map, int rank, const int32_t (&c)[5], const void *src) {
   const uint32_t sa = smem_u32(src);
@@ -421,7 +428,7 @@ __device__ __forceinline__ void epilogue_red(const GemmArgs &p, const double (&a
 #pragma unroll
           for (int nt = 0; nt < 4; ++nt) {
             const int c = wn * 32 + epi_col<PB>(nt, tig);
-            *reinterpret_cast<double2 *>(pb + red_index(r, c)) =
+            *reinterpret_cast<double2 *>(pb + red_idx(p.cred8, r, c)) =
                 make_double2(tg.sign * acc[mt][nt][2 * h], tg.sign * acc[mt][nt][2 * h + 1]);
           }
         }
@@ -574,7 +581,7 @@ __device__ __forceinline__ void epilogue_warps_red(const GemmArgs &p, uint64_t *
           double2 v = *reinterpret_cast<const double2 *>(Mt + (size_t)(RED_ROWS * pc + r) * BN + c);
           v.x = __hiloint2double(__double2hiint(v.x) ^ (int)flip, __double2loint(v.x));
           v.y = __hiloint2double(__double2hiint(v.y) ^ (int)flip, __double2loint(v.y));
-          *reinterpret_cast<double2 *>(pb + red_index(r, c)) = v;
+          *reinterpret_cast<double2 *>(pb + red_idx(p.cred8, r, c)) = v;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         named_bar(3, EPI_THREADS);

@@ -103,6 +103,7 @@ struct GemmArgs {
                              // side in place; 0: the consumers form every sum in their fragment loads
   double *mscratch;          // ABC: [grid][2][BM * BN] M tiles handed to the epilogue warps
   int32_t cred;              // ABC: C updates by TMA reduce-add of M pieces (C views regular)
+  int32_t cred8;             // the C box's unit-stride rows are 8 doubles (64B swizzle) instead of 16
   const int32_t *c_ready;    // stc_set_c_ready: wait until *c_ready != 0 before touching C
 };
 

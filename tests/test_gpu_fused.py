@@ -110,6 +110,13 @@ def test_abc_dense_m_matches_ticketed_bitwise(line):
         ct, _ = _run_env(spec, a, b, c0, level, "abc", {"STC_ABC_DENSE": "0"})
         cd, _ = _run_env(spec, a, b, c0, level, "abc", {"STC_ABC_DENSE": "1"})
         assert np.array_equal(ct.data, cd.data), (line, level)
+        for ps in ("1",):  # pre-summed slots, ticketed (TMA reduce-add where C boxes allow)
+            cp, _ = _run_env(spec, a, b, c0, level, "abc", {"STC_ABC_DENSE": "0", "STC_PRESUM_OPS": ps})
+            assert np.array_equal(cp.data, cd.data), (line, level, ps)
+            for epi in ({"STC_EPI_OFFLOAD": "0"}, {"STC_CRED": "0"}):
+                ce, _ = _run_env(spec, a, b, c0, level, "abc", {"STC_ABC_DENSE": "0", "STC_PRESUM_OPS": ps, **epi})
+                assert np.array_equal(ce.data, cd.data), (line, level, ps, epi)
+
         for fused in ("0",):  # the gather kernel takes the same two paths
             cg, _ = _run_env(spec, a, b, c0, level, "abc", {"STC_ABC_DENSE": "1", "STC_FUSED": fused})
             assert np.array_equal(cg.data, cd.data), (line, level)
@@ -340,3 +347,29 @@ def test_repeated_runs_bitwise_stable(line, level):
         for _ in range(12):
             again, _ = _run_env(spec, a, b, c0, level, "abc", {"STC_PRESUM_OPS": ps})
             assert np.array_equal(again.data, first.data), (line, level, ps)
+
+
+def test_eight_wide_c_boxes_match_dense_m_bitwise():
+    # cfg5 pattern, row-major: at L2 the C quadrants hold 8-wide runs of the unit-stride
+    # label k (a quadrant split of it), so the TMA reduce-add boxes have 64-byte rows
+    # (GemmArgs::cred8, 64B swizzle): bitwise equal to the dense-M accumulate path
+    spec = stc.parse_benchmark_line("abcijk abcefg efgijk & a:4;b:8;c:32;i:4;j:8;k:32;e:4;f:8;g:32;")
+
+    def rm_tensor(labels, seed):
+        e = spec.tensor_extents(labels)
+        st = tuple(int(np.prod(e[i + 1:])) for i in range(len(e)))
+        return stc.DenseTensor(e, st, np.random.default_rng(seed).uniform(-1, 1, int(np.prod(e))))
+
+    a, b, c0 = rm_tensor(spec.labels_a, 81), rm_tensor(spec.labels_b, 82), rm_tensor(spec.labels_c, 83)
+    info = stc.describe_plan(spec, a, b, c0, 2, "abc")
+    assert info["c_boxes"] == 1 and info["presum"] == 1, info
+    classical = c0.copy()
+    oracle.contract_reference(spec, a, b, classical)
+    cd, _ = _run_env(spec, a, b, c0, 2, "abc", {"STC_ABC_DENSE": "1", "STC_PRESUM_OPS": "1"})
+    assert stc.relative_error(cd, classical) <= TOL
+    for env in ({"STC_ABC_DENSE": "0", "STC_PRESUM_OPS": "1"},
+                {"STC_ABC_DENSE": "0", "STC_PRESUM_OPS": "1", "STC_EPI_OFFLOAD": "0"},
+                {"STC_ABC_DENSE": "0", "STC_PRESUM_OPS": "0"},
+                {"STC_ABC_DENSE": "0", "STC_PRESUM_OPS": "0", "STC_CRED": "0"}):
+        ct, _ = _run_env(spec, a, b, c0, 2, "abc", env)
+        assert np.array_equal(ct.data, cd.data), env
