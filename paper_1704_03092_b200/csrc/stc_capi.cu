@@ -347,17 +347,19 @@ struct Plan {
 };
 
 // Workspace cap for the term batches of dense M / operand slots: STC_WORKSPACE_CAP_MB,
-// else half the free device memory at planning time (at least 24 GiB).  The batch
-// count changes no result: each batch's C pass continues the previous one's sums.
+// else 40 % of the device's memory (at least 24 GiB; 72 GB on a B200).  A function of
+// the device, not of its current free memory, so a re-planned problem gets the same
+// workspace size.  The batch count changes no result: each batch's C pass continues
+// the previous one's sums in the same order.
 int64_t cap_bytes() {
   if (const char *e = getenv("STC_WORKSPACE_CAP_MB")) return atoll(e) * (int64_t)1024 * 1024;
   const int64_t floor_bytes = (int64_t)24 << 30;
   size_t fr = 0, tot = 0;
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
-    cudaGetLastError();  // no device (planning on a CPU host): clear the sticky-free error
+    cudaGetLastError();  // no device (planning on a CPU host): clear the error
     return floor_bytes;
   }
-  return std::max<int64_t>(floor_bytes, (int64_t)(fr / 2));
+  return std::max<int64_t>(floor_bytes, (int64_t)(tot / 10 * 4));
 }
 
 // Reorder terms so that terms running concurrently (within `window`
@@ -425,13 +427,13 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
 // anyway (one read + one write of every quadrant), which the presum pass replaces.
 // Cost model at 5 TB/s and 33 TF/s executed.
 bool presum_wanted(const stc_problem *p, const Plan &pl) {
-  if (pl.level < 1 || pl.level > 2 || pl.tshape != 0) return false;
+  if (pl.level < 1 || pl.level > 2 || pl.variant == STC_VARIANT_NAIVE) return false;
   if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
   if (const char *e = getenv("STC_FUSED"))
     if (atoi(e) == 0) return false;
   if (const char *e = getenv("STC_PRESUM_OPS")) return atoi(e) != 0;
   const double qa = (double)pl.mq_pad * pl.kq_pad, qb = (double)pl.kq_pad * pl.nq_pad;
-  const double quads = (double)pl.nquads, T = (double)pl.terms.size();
+  const double quads = (double)pl.nquads, T = pl.level == 1 ? 7.0 : 49.0;
   const double t_presum = 8.0 * (quads + T) * (qa + qb) / 5e12;
   GemmArgs g{};
   CUtensorMap maps[3];
@@ -506,11 +508,11 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   pl.tp = tp;
   pl.a_kfast = a_min == 1;
   pl.b_kfast = b_min == 0;
-  if (pl.tshape != 0) {  // the direct fused layout must cut the new tiles as boxes
-    GemmArgs gd{};
+  if (pl.tshape != 0) {  // the direct fused layout must cut the new tiles as boxes -- or the
+    GemmArgs gd{};      // operands come from pre-summed slots, box-regular by construction
     CUtensorMap md[3];
     CoordJobs jd{};
-    if (!plan_fused(p, pl, direct_sides(p, pl), nullptr, nullptr, nullptr, gd, md, jd)) {
+    if (!plan_fused(p, pl, direct_sides(p, pl), nullptr, nullptr, nullptr, gd, md, jd) && !presum_wanted(p, pl)) {
       pl.tshape = 0;
       pl.tm = BM;
       pl.tn = BN;
@@ -545,7 +547,10 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   if (pl.variant == STC_VARIANT_ABC) {
     // C-tile update order (tickets, or the dense-M accumulate order): terms
     // that run concurrently should write disjoint quadrants
-    const int window = (int)std::min<int64_t>(T, cdiv(pl.grid, P) + 1);
+    // (window from the 128 x 128 tile count: every tile shape and operand path of a
+    // problem gets the same C-update order, so their results stay bitwise equal)
+    const int64_t P128 = cdiv(pl.mq, BM) * cdiv(pl.nq, BN);
+    const int window = (int)std::min<int64_t>(T, cdiv(pl.grid, P128) + 1);
     pl.seq = exec_order(pl.terms, window);
     // dense-M mode when many terms per C tile would be in flight at once: the
     // ticket chains then serialise (cfg2 pieces of m = 1024: 9 terms in flight,
@@ -1552,7 +1557,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       // TMA reduce (C not box-regular: only L0 reaches here) the consumers' own
       // load/add/store epilogue (the spare warps' DADDs starve behind the DMMAs)
       const char *eo = getenv("STC_EPI_OFFLOAD");
-      const int offload = eo ? atoi(eo) : (gf.cred ? 1 : 0);
+      const int offload = (eo ? atoi(eo) : (gf.cred ? 1 : 0)) || (gf.cred && gf.cred8);  // 8-wide boxes: offloaded
       if (offload) gf.mscratch = reinterpret_cast<double *>(ws + pl.off_mscr);
       if (g_ev_before) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
       CU(launch_fused(gf, grid, s, maps), "k_strassen_fused");

@@ -371,7 +371,8 @@ __device__ __forceinline__ int red_index8(int r, int c) {
   const int line = r * (BN / 8) + (c >> 3);
   return line * 8 + ((((c & 7) >> 1) ^ ((line >> 1) & 3)) << 1) + (c & 1);
 }
-__device__ __forceinline__ int red_idx(bool w8, int r, int c) { return w8 ? red_index8(r, c) : red_index(r, c); }
+template <bool W8>
+__device__ __forceinline__ int red_idx(int r, int c) { return W8 ? red_index8(r, c) : red_index(r, c); }
 
 __device__ __forceinline__ void tma_reduce_add(const CUtensorMap *map, int rank, const int32_t (&c)[5], const void *src) {
   const uint32_t sa = smem_u32(src);
@@ -403,7 +404,7 @@ __device__ __forceinline__ void tma_reduce_add(const CUtensorMap *map, int rank,
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
-template <int PA, int PB>
+template <int PA, int PB, bool W8>
 __device__ __forceinline__ void epilogue_red(const GemmArgs &p, const double (&acc)[4][4][4], int item, int tid, int wm,
                                              int wn, int g, int tig, double *buf, const CUtensorMap *tmC) {
   int slot, ti, tj, pos;
@@ -428,7 +429,7 @@ __device__ __forceinline__ void epilogue_red(const GemmArgs &p, const double (&a
 #pragma unroll
           for (int nt = 0; nt < 4; ++nt) {
             const int c = wn * 32 + epi_col<PB>(nt, tig);
-            *reinterpret_cast<double2 *>(pb + red_idx(p.cred8, r, c)) =
+            *reinterpret_cast<double2 *>(pb + red_idx<W8>(r, c)) =
                 make_double2(tg.sign * acc[mt][nt][2 * h], tg.sign * acc[mt][nt][2 * h + 1]);
           }
         }
@@ -544,6 +545,7 @@ __device__ __forceinline__ void epilogue_warps(const GemmArgs &p, uint64_t *epi_
 // sign-bit flip -- no FP64 work competing with the consumers' DMMAs) and added
 // into each C target in L2 by cp.reduce.async.bulk.tensor, in ticket order.
 // The consumers only write M and go on with the next item.
+template <bool W8>
 __device__ __forceinline__ void epilogue_warps_red(const GemmArgs &p, uint64_t *epi_full, uint64_t *epi_empty,
                                                    const int *epi_item, double *buf, const CUtensorMap *tmC, int t) {
   int eb = 0;
@@ -581,7 +583,7 @@ __device__ __forceinline__ void epilogue_warps_red(const GemmArgs &p, uint64_t *
           double2 v = *reinterpret_cast<const double2 *>(Mt + (size_t)(RED_ROWS * pc + r) * BN + c);
           v.x = __hiloint2double(__double2hiint(v.x) ^ (int)flip, __double2loint(v.x));
           v.y = __hiloint2double(__double2hiint(v.y) ^ (int)flip, __double2loint(v.y));
-          *reinterpret_cast<double2 *>(pb + red_idx(p.cred8, r, c)) = v;
+          *reinterpret_cast<double2 *>(pb + red_idx<W8>(r, c)) = v;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         named_bar(3, EPI_THREADS);
@@ -783,7 +785,8 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(FUSED_PRODUCER_REGS));
     if (warp != CONSUMER_WARPS) {
       if (offload && red)
-        epilogue_warps_red(p, epi_full, epi_empty, epi_item, redbuf, &tmC, tid - 32 * (CONSUMER_WARPS + 1));
+        p.cred8 ? epilogue_warps_red<true>(p, epi_full, epi_empty, epi_item, redbuf, &tmC, tid - 32 * (CONSUMER_WARPS + 1))
+                : epilogue_warps_red<false>(p, epi_full, epi_empty, epi_item, redbuf, &tmC, tid - 32 * (CONSUMER_WARPS + 1));
       else if (offload)
         epilogue_warps(p, epi_full, epi_empty, epi_item, epi_rows, epi_cols, tid - 32 * (CONSUMER_WARPS + 1));
       return;
@@ -919,7 +922,8 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
           }
         }
       } else if constexpr (ONE) {
-        consume_item<1, 1, false>(acc, stages, sstride, S, full, empty, stage, phase, kchunks, 0u, offA, offB, lane);
+        consume_item<1, 1, false, SH::AV, SH::BV>(acc, stages, sstride, S, full, empty, stage, phase, kchunks, 0u,
+                                                  offA, offB, lane, SH::AV);
       } else {
       // coefficient signs of the item's views: one load per lane, one ballot
       bool neg = false;
@@ -1000,7 +1004,8 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
       } else {
         if (!p.dense_out) wait_c_ready(p, tid, c_seen);
         if (red)
-          epilogue_red<AKF + 1, BKF + 1>(p, acc, item, tid, wm, wn, g, tig, redbuf, &tmC);
+          // (8-wide C boxes always go through the epilogue warps: launch_fused)
+          epilogue_red<AKF + 1, BKF + 1, false>(p, acc, item, tid, wm, wn, g, tig, redbuf, &tmC);
         else
           epilogue_store<AKF + 1, BKF + 1, 2>(p, acc, item, tid, wm, wn, g, tig);
       }
@@ -1019,15 +1024,21 @@ static FusedKernel fused_for_ts(int akf, int bkf) {
 static FusedKernel fused_for(int akf, int bkf, bool ps, int ts, bool one) {
   if (ps) return ts == 1 ? fused_for_ts<true, 1>(akf, bkf) : ts == 2 ? fused_for_ts<true, 2>(akf, bkf)
                                                              : fused_for_ts<true, 0>(akf, bkf);
-  return one ? fused_for_ts<false, 0, true>(akf, bkf) : fused_for_ts<false, 0>(akf, bkf);
+  if (one)
+    return ts == 1 ? fused_for_ts<false, 1, true>(akf, bkf) : ts == 2 ? fused_for_ts<false, 2, true>(akf, bkf)
+                                                                : fused_for_ts<false, 0, true>(akf, bkf);
+  return fused_for_ts<false, 0>(akf, bkf);
 }
 
 cudaError_t launch_fused(const GemmArgs &a, int grid, cudaStream_t s, const void *maps) {
   const bool ps = a.psum != 0;
-  if (a.tshape != 0 && (!ps || !a.dense_out || (a.psum & 2))) return cudaErrorInvalidValue;
-  const size_t sm = FusedLayout::bytes((size_t)a.stage_dbl, a.stages, a.cred != 0);
   // one unsigned view per side (umax 2 with sign-free slots): the spill-free specialisation
-  const bool one = !ps && a.tshape == 0 && a.umax == 2 && a.one_view;
+  const bool one = !ps && a.umax == 2 && a.one_view;
+  // shapes 1 / 2: dense M output, A sums by the summing warpgroup or one view per side
+  if (a.tshape != 0 && (!(ps || one) || !a.dense_out || (a.psum & 2))) return cudaErrorInvalidValue;
+  if (a.cred && a.cred8 && !a.mscratch) return cudaErrorInvalidValue;  // the consumers' inline TMA-reduce
+                                                                      // epilogue has 16-wide boxes only
+  const size_t sm = FusedLayout::bytes((size_t)a.stage_dbl, a.stages, a.cred != 0);
   FusedKernel k = fused_for(a.a_kfast, a.b_kfast, ps, a.tshape, one);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;

@@ -251,13 +251,21 @@ struct DrainOnError {
   }
 };
 
+// Workspace of one piece slot: the largest over the pieces (their plans differ in the
+// base offsets, which can change the path -- e.g. whether a view is a TMA box -- and
+// with it the workspace).
 int piece_workspace(const stc_problem &p, const Split &sp, size_t &per_slot) {
   const stc_bundle &cb = sp.side == 0 ? p.c_row : p.c_col;
-  const int64_t len = (cb.ext[sp.lab] + sp.pieces - 1) / sp.pieces;
-  stc_problem q = sp.pieces > 1 ? piece_problem(p, sp, 0, len) : p;
-  size_t b = 0;
-  if (int rc = stc_workspace_size(&q, &b)) return rc;
-  per_slot = align256(std::max<size_t>(b, 256));
+  const int64_t lext = sp.pieces > 1 ? cb.ext[sp.lab] : 1;
+  size_t most = 256;
+  for (int s = 0; s < sp.pieces; ++s) {
+    const int64_t r0 = lext * s / sp.pieces, r1 = lext * (s + 1) / sp.pieces;
+    stc_problem q = sp.pieces > 1 ? piece_problem(p, sp, r0, r1 - r0) : p;
+    size_t b = 0;
+    if (int rc = stc_workspace_size(&q, &b)) return rc;
+    most = std::max(most, b);
+  }
+  per_slot = align256(most);
   return STC_OK;
 }
 

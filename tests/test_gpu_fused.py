@@ -142,6 +142,11 @@ def test_tile_shapes_match_square_tiles_bitwise(line, shape):
         assert stc.relative_error(cs, classical) <= TOL
         if level == 2:  # the shaped launch has half the padded work items
             assert ss.work_items < sq.work_items, (ss.work_items, sq.work_items)
+        # the same shapes on pre-summed slots (one view per side): bitwise the same again
+        cp, sp_ = _run_env(spec, a, b, c0, level, variant, {"STC_PRESUM_OPS": "1"})
+        assert np.array_equal(cp.data, cq.data), (line, level, variant)
+        if level == 2:
+            assert sp_.work_items == ss.work_items, (sp_.work_items, ss.work_items)
 
 
 def test_fused_matches_oracle_strassen():
