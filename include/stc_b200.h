@@ -195,6 +195,20 @@ int stc_unpack_sum(double *out, int64_t ldo, int64_t m, int64_t n, const double 
 int stc_sq_norms(int ndim, const int64_t *extents, const double *x, const int64_t *x_strides, int64_t x_base,
                  const double *ref, const int64_t *ref_strides, int64_t ref_base, double *out, void *stream);
 
+/* ---- multi-GPU n-split (north-star subsystem 5) ----
+ * The sub-problem rank `rank` of `world` contracts when J label `label` (index
+ * in the J bundle; < 0: the label with extent >= world that divides evenly,
+ * then the largest C stride, as shard.plan_shards) is cut into `world`
+ * contiguous ranges (sizes within 1): that label's extent in B and C reduced,
+ * B's and C's base offsets moved.  Every rank calls stc_contract on it with all
+ * of A and the same B / C storage (or storage holding only its slice, offsets
+ * rebased); no reduction.  The optional all-gather of C is the caller's
+ * collective (shard.gather_shards: NCCL all_gather_into_tensor over
+ * torch.distributed).  The reference has no distributed path.
+ * Returns the range [start, stop) and the label chosen.  Host-only. */
+int stc_shard_problem(const stc_problem *p, int world, int rank, int label, stc_problem *out, int64_t *start,
+                      int64_t *stop, int32_t *label_out);
+
 /* ---- plan introspection (tests / tools; no reference counterpart) ----
  * Which execution path stc_contract takes for a problem on a `grid`-CTA launch
  * (0: 148).  Host-only: needs no device. */

@@ -2048,4 +2048,43 @@ int stc_plan_describe(const stc_problem *p, int grid, stc_plan_info *info) {
   return STC_OK;
 }
 
+int stc_shard_problem(const stc_problem *p, int world, int rank, int label, stc_problem *out, int64_t *start,
+                      int64_t *stop, int32_t *label_out) {
+  if (!p || !out) return fail(STC_EINVAL, "null argument");
+  if (world < 1) return fail(STC_EINVAL, "world size must be positive");
+  if (rank < 0 || rank >= world) return fail(STC_EINVAL, "rank %d outside [0, %d)", rank, world);
+  const stc_bundle &cj = p->c_col;
+  if (cj.nlab == 0) return fail(STC_EINVAL, "the J bundle is empty: nothing to split");
+  if (label < 0) {  // shard.plan_shards' default: divisible extents first, then the largest C stride
+    int best = -1;
+    for (int d = 0; d < cj.nlab; ++d) {
+      if (cj.ext[d] < world) continue;
+      const bool div = cj.ext[d] % world == 0;
+      if (best < 0) {
+        best = d;
+        continue;
+      }
+      const bool bdiv = cj.ext[best] % world == 0;
+      const int64_t s = cj.str[d] < 0 ? -cj.str[d] : cj.str[d], bs = cj.str[best] < 0 ? -cj.str[best] : cj.str[best];
+      if (div > bdiv || (div == bdiv && s > bs)) best = d;
+    }
+    if (best < 0) return fail(STC_EINVAL, "no J label has extent >= %d", world);
+    label = best;
+  }
+  if (label >= cj.nlab) return fail(STC_EINVAL, "label %d is not in the J bundle", label);
+  const int64_t ext = cj.ext[label], base = ext / world, extra = ext % world;
+  const int64_t s0 = rank * base + std::min<int64_t>(rank, extra);
+  const int64_t n = base + (rank < extra ? 1 : 0);
+  if (n < 1) return fail(STC_EINVAL, "rank %d gets an empty range of label %d", rank, label);
+  *out = *p;
+  out->b_col.ext[label] = n;
+  out->c_col.ext[label] = n;
+  out->b_base += s0 * p->b_col.str[label];
+  out->c_base += s0 * p->c_col.str[label];
+  if (start) *start = s0;
+  if (stop) *stop = s0 + n;
+  if (label_out) *label_out = label;
+  return STC_OK;
+}
+
 }  // extern "C"

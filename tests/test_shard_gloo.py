@@ -148,3 +148,33 @@ def test_plan_grid_tiles_c_exactly():
         shard.plan_grid(spec, c, 2, 1, row_label="i")
     with pytest.raises(ValueError, match="extent"):
         shard.plan_grid(spec, c, 7, 1)
+
+
+@pytest.mark.parametrize("line", ["abcijk abcefg efgijk & a:2;b:2;c:2;i:5;j:3;k:8;e:2;f:2;g:2;",
+                                  "aibj eafb jfie & a:4;b:3;i:5;j:3;e:3;f:2;",
+                                  "abcij eafbc ifje & a:5;b:7;c:3;i:7;j:9;e:4;f:3;"])
+def test_c_abi_shard_planner_matches_plan_shards(line):
+    # stc_shard_problem (the C-ABI n-split) and shard.plan_shards / shard_tensor pick the
+    # same label, ranges and moved base offsets (host-only: no device needed)
+    import ctypes
+
+    from paper_1704_03092_b200 import _lib
+    from paper_1704_03092_b200.strassen import Variant, problem_of
+
+    spec = stc.parse_benchmark_line(line)
+    a, b, c = _operands(spec)
+    prob = problem_of(spec, a, b, c, 2, Variant.ABC)
+    for world in (1, 2, 3, 4):
+        if max(spec.extents[l] for l in spec.bundle_j) < world:
+            continue
+        shards = shard.plan_shards(spec, c, world)
+        for rank in range(world):
+            out = _lib.Problem()
+            s0, s1, lab = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+            _lib.check(_lib.lib().stc_shard_problem(ctypes.byref(prob), world, rank, -1, ctypes.byref(out),
+                                                    ctypes.byref(s0), ctypes.byref(s1), ctypes.byref(lab)))
+            sh = shards[rank]
+            assert spec.bundle_j[lab.value] == sh.label and (s0.value, s1.value) == (sh.start, sh.stop)
+            want = problem_of(shard.shard_spec(spec, sh), a, shard.shard_tensor(b, spec.labels_b, sh),
+                              shard.shard_tensor(c, spec.labels_c, sh), 2, Variant.ABC)
+            assert bytes(out) == bytes(want), (world, rank)
