@@ -1783,6 +1783,8 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       aa.mq = pl.mq;
       aa.nq = pl.nq;
       aa.nquads = pl.nquads;
+      aa.max_list = 0;
+      for (int q = 0; q < pl.nquads; ++q) aa.max_list = std::max(aa.max_list, lstart[q + 1] - lstart[q]);
       CU(launch_accumulate(aa, s), "k_accumulate");
       launches += 2;
       st.slow_updates += (int64_t)lslot.size();

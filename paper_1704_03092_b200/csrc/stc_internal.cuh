@@ -149,7 +149,7 @@ struct AccArgs {
   double *C;
   const int64_t *pool;
   int64_t mq, nq;              // valid (unpadded) quadrant extents
-  int32_t nquads, _pad;
+  int32_t nquads, max_list;    // quadrants; longest (slot, sign) list of a quadrant
   const int32_t *list_start;   // [nquads + 1]
   const int32_t *list_slot;    // M slots in term order
   const double *list_sign;
