@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -304,6 +305,60 @@ bool same_extents(const stc_bundle &x, const stc_bundle &y) {
 }
 
 // ---------------------------------------------------------------- the plan
+// Device snapshots of a plan's constant workspace region (scatter vectors, chunk
+// strides, map coordinates, tables, accumulate lists, zeroed tickets and counters),
+// one per operand mode (own views / repacked).  The first call of a plan builds the
+// region in its workspace and copies it here; later calls restore it with one kernel
+// (k_restore) instead of the 5-10 small launches that build it.  Shared by the copies
+// of a cached plan; freed with the last one.
+struct Resident {
+  std::mutex mu;
+  void *buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  int dev[2] = {-1, -1};
+  ~Resident() {
+    for (int i = 0; i < 2; ++i) {
+      if (buf[i]) cudaFree(buf[i]);
+      if (ev[i]) cudaEventDestroy(ev[i]);
+    }
+  }
+  // The snapshot of `mode` on device d, ordered before the work next enqueued on s; null if none.
+  const void *ready(int mode, int d, cudaStream_t s) {
+    if (getenv("STC_NO_SNAPSHOT")) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!buf[mode] || dev[mode] != d) return nullptr;
+    if (cudaStreamWaitEvent(s, ev[mode], 0) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return buf[mode];
+  }
+  // Copy [ws, ws + bytes) (complete in stream order on s) into a new snapshot of `mode`.
+  cudaError_t save(int mode, int d, const void *ws, size_t bytes, cudaStream_t s) {
+    if (getenv("STC_NO_SNAPSHOT")) return cudaSuccess;
+    std::lock_guard<std::mutex> lk(mu);
+    if (buf[mode] || bytes == 0) return cudaSuccess;
+    void *p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {  // no snapshot: later calls rebuild
+      cudaGetLastError();
+      return cudaSuccess;
+    }
+    cudaEvent_t e = nullptr;
+    cudaError_t r = launch_restore(ws, p, bytes, s);
+    if (r == cudaSuccess) r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (r == cudaSuccess) r = cudaEventRecord(e, s);
+    if (r != cudaSuccess) {
+      cudaFree(p);
+      if (e) cudaEventDestroy(e);
+      return r;
+    }
+    buf[mode] = p;
+    ev[mode] = e;
+    dev[mode] = d;
+    return cudaSuccess;
+  }
+};
+
 struct Plan {
   int level = 0, variant = 0;
   uint32_t flags = 0;
@@ -341,6 +396,8 @@ struct Plan {
   std::vector<int> seq;  // term order of the dense-M batches and accumulate lists
   size_t off_pool = 0, off_vecs = 0, off_tab = 0, off_tickets = 0, off_counters = 0, off_M = 0, off_pa = 0,
          off_pb = 0, off_acc = 0, total = 0;
+  size_t off_pool2 = 0, off_const = 0;  // original vectors (repacking); end of the constant region
+  std::shared_ptr<Resident> res;        // device snapshots of the constant region
   size_t tab_bytes = 0, acc_bytes = 0;
   int64_t ntickets = 0, ncounters = 0;
   int64_t m_slot = 0, pa_slot = 0, pb_slot = 0;
@@ -650,16 +707,6 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     pl.ncounters = pl.nbatches;
   }
 
-  // workspace layout
-  size_t off = 0;
-  pl.off_pool = off;
-  off = align256(off + (size_t)pl.pool_len * 8);
-  pl.off_kbs = off;
-  off = align256(off + (size_t)(pl.pool_len / BK) * 8);
-  pl.off_coords = off;  // fused kernel: int4 map coordinates per 8 pool entries
-  off = align256(off + (size_t)(pl.pool_len / 8) * 16);
-  pl.off_mscr = off;  // fused ABC: EPI_BUFS M tiles per CTA for the epilogue warps
-  if (pl.ticketed) off = align256(off + (size_t)pl.grid * EPI_BUFS * BM * BN * 8);
   // fused kernel on repacked operands when the views are not box-regular
   if (!slots) {
     GemmArgs gd{};
@@ -669,13 +716,6 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     pl.need_pack = !direct && plan_fused(p, pl, packed_sides(pl), nullptr, nullptr, nullptr, gd, md, jd) &&
                    !(getenv("STC_PACK") && atoi(getenv("STC_PACK")) == 0);
   }
-  pl.off_pka = off;
-  if (pl.need_pack) off = align256(off + (size_t)(pl.Q * pl.Q) * pl.mq_pad * pl.kq_pad * 8);
-  pl.off_pkb = off;
-  if (pl.need_pack) off = align256(off + (size_t)(pl.Q * pl.Q) * pl.nq_pad * pl.kq_pad * 8);
-  pl.off_vecs = off;
-  off = align256(off + (pl.vecs.size() + 4) * sizeof(VecDesc));  // + the packed sides' vectors
-  pl.off_tab = off;
   if (pl.ticketed) {
     pl.tab_bytes = pl.tdesc.size() * sizeof(TermDesc) + pl.ops.size() * sizeof(OpDesc) + pl.tgts.size() * sizeof(TgtDesc);
   } else {
@@ -685,6 +725,21 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     pl.acc_bytes = align256((size_t)(pl.nquads + 1) * 4) + align256((size_t)pl.batch * pl.nquads * 4) +
                    align256((size_t)pl.batch * pl.nquads * 8) + 2 * align256((size_t)pl.nquads * 8);
   }
+
+  // workspace layout: the constant region first (the per-plan snapshot, Resident), then
+  // the per-call buffers
+  size_t off = 0;
+  pl.off_pool = off;
+  off = align256(off + (size_t)pl.pool_len * 8);
+  pl.off_pool2 = off;  // the original vectors while `pool` holds the repacked ones
+  if (pl.need_pack) off = align256(off + (size_t)pl.pool_len * 8);
+  pl.off_kbs = off;
+  off = align256(off + (size_t)(pl.pool_len / BK) * 8);
+  pl.off_coords = off;  // fused kernel: int4 map coordinates per 8 pool entries
+  off = align256(off + (size_t)(pl.pool_len / 8) * 16);
+  pl.off_vecs = off;
+  off = align256(off + (pl.vecs.size() + 4) * sizeof(VecDesc));  // + the packed sides' vectors
+  pl.off_tab = off;
   off = align256(off + pl.tab_bytes * (pl.ticketed ? 1 : pl.nbatches));
   pl.off_acc = off;
   off = align256(off + pl.acc_bytes * (pl.ticketed ? 0 : pl.nbatches));
@@ -692,12 +747,20 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   off = align256(off + (size_t)pl.ntickets * 4);
   pl.off_counters = off;
   off = align256(off + (size_t)pl.ncounters * 4);
+  pl.off_const = off;
+  pl.off_mscr = off;  // fused ABC: EPI_BUFS M tiles per CTA for the epilogue warps
+  if (pl.ticketed) off = align256(off + (size_t)pl.grid * EPI_BUFS * BM * BN * 8);
+  pl.off_pka = off;
+  if (pl.need_pack) off = align256(off + (size_t)(pl.Q * pl.Q) * pl.mq_pad * pl.kq_pad * 8);
+  pl.off_pkb = off;
+  if (pl.need_pack) off = align256(off + (size_t)(pl.Q * pl.Q) * pl.nq_pad * pl.kq_pad * 8);
   pl.off_M = off;
   if (!pl.ticketed) off = align256(off + (size_t)pl.batch * pl.m_slot * 8);
   pl.off_pa = off;
   if (slots) off = align256(off + (size_t)pl.batch * pl.pa_slot * 8);
   pl.off_pb = off;
   if (slots) off = align256(off + (size_t)pl.batch * pl.pb_slot * 8);
+  pl.res = std::make_shared<Resident>();
   pl.total = off;
   return STC_OK;
 }
@@ -1405,68 +1468,107 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   char *ws = reinterpret_cast<char *>(workspace);
   int64_t *pool = reinterpret_cast<int64_t *>(ws + pl.off_pool);
+  int64_t *pool2 = reinterpret_cast<int64_t *>(ws + pl.off_pool2);  // the original vectors (repacking)
+  int64_t *kbs = reinterpret_cast<int64_t *>(ws + pl.off_kbs);
+  int32_t *tickets = reinterpret_cast<int32_t *>(ws + pl.off_tickets);
+  int32_t *counters = reinterpret_cast<int32_t *>(ws + pl.off_counters);
+  int4 *coords = reinterpret_cast<int4 *>(ws + pl.off_coords);
   int64_t launches = 0;
   bool tma = false;  // operand units staged by tensor-map box loads
   stc_stats st{};
-
-  // subsystem (1): scatter vectors on the device; the same launch zeroes the
-  // tickets and work counters
   g_stage_launches = 0;
-  if (int rc = upload(pl.vecs.data(), pl.vecs.size() * sizeof(VecDesc), ws + pl.off_vecs, s, ws + pl.off_tickets,
-                      pl.off_M - pl.off_tickets))
-    return rc;
-  CU(launch_build_pool(reinterpret_cast<VecDesc *>(ws + pl.off_vecs), (int)pl.vecs.size(), pl.pool_len, pool, s),
-     "k_build_pool");
-  int64_t *kbs = reinterpret_cast<int64_t *>(ws + pl.off_kbs);
-  CU(launch_chunk_strides(pool, pl.pool_len / BK, kbs, s), "k_chunk_strides");
-  launches += 2;
-  // tickets + work counters
-  int32_t *tickets = reinterpret_cast<int32_t *>(ws + pl.off_tickets);
-  int32_t *counters = reinterpret_cast<int32_t *>(ws + pl.off_counters);
+  const int32_t *c_ready = g_c_ready;  // consumed by this call
+  g_c_ready = nullptr;
   const int tiles_m = (int)(pl.mq_pad / pl.tm), tiles_n = (int)(pl.nq_pad / pl.tn);
   const int64_t P = (int64_t)tiles_m * tiles_n;
   const int T = (int)pl.terms.size();
 
-  // Fused kernel set-up: the operands' own views when they are box-regular, else
+  // Operand mode: per-term slots (Naive, pre-summed), the operands' own TMA views, or
   // their repacked quadrant blocks (one gather pass per operand, pure copies).
-  bool packed = false;
+  const bool slots = pl.variant == STC_VARIANT_NAIVE || pl.presum;
+  bool direct = false;
+  if (!slots) {
+    GemmArgs gt{};
+    CUtensorMap mt[3];
+    CoordJobs jt{};
+    direct = plan_fused(p, pl, direct_sides(p, pl), A, B, pl.ticketed ? C : nullptr, gt, mt, jt);
+  }
+  const bool packed = !slots && !direct && pl.need_pack;
+
+  // The constant region of the workspace -- scatter vectors, chunk strides, map
+  // coordinates, term / op / target tables, accumulate lists, zeroed tickets and
+  // counters -- depends only on the plan (and the operand mode): the first call of a
+  // plan builds it and keeps a device snapshot; later calls restore it with one
+  // kernel instead of 5-10 small launches (Resident).
+  const int mode = packed ? 1 : 0;
+  int dev = 0;
+  CU(cudaGetDevice(&dev), "cudaGetDevice");
+  Resident *res = pl.res.get();
+  const void *snap = res ? res->ready(mode, dev, s) : nullptr;
+  const bool restored = snap != nullptr;
+  if (restored) {
+    CU(launch_restore(snap, ws, pl.off_const, s), "k_restore");
+    ++launches;
+  } else {
+    if (int rc = upload(pl.vecs.data(), pl.vecs.size() * sizeof(VecDesc), ws + pl.off_vecs, s, ws + pl.off_tickets,
+                        pl.off_const - pl.off_tickets))
+      return rc;
+    CU(launch_build_pool(reinterpret_cast<VecDesc *>(ws + pl.off_vecs), (int)pl.vecs.size(), pl.pool_len, pool, s),
+       "k_build_pool");
+    CU(launch_chunk_strides(pool, pl.pool_len / BK, kbs, s), "k_chunk_strides");
+    launches += 2;
+    if (packed) {  // a copy of the original vectors for k_pack_views (pool gets the packed ones)
+      CU(launch_build_pool(reinterpret_cast<VecDesc *>(ws + pl.off_vecs), (int)pl.vecs.size(), pl.pool_len, pool2, s),
+         "k_build_pool(2)");
+      ++launches;
+    }
+  }
+  auto save_snapshot = [&]() -> int {
+    if (restored || !res) return STC_OK;
+    CU(res->save(mode, dev, ws, pl.off_const, s), "snapshot");
+    return STC_OK;
+  };
+
+  // Fused kernel set-up on the operands' own views or their repacked blocks: the
+  // repacking runs every call (it reads A and B), the rest is constant.
   auto prepare_fused = [&](GemmArgs &gf, CUtensorMap *maps, const double *Cp) -> int {
     CoordJobs jobs{};
-    int ok = plan_fused(p, pl, direct_sides(p, pl), A, B, Cp, gf, maps, jobs) ? 1 : 0;
-    if (!ok && pl.need_pack) {
+    if (packed) {
       double *PA = reinterpret_cast<double *>(ws + pl.off_pka);
       double *PB = reinterpret_cast<double *>(ws + pl.off_pkb);
       PackArgs pa{pl.ar, pl.ac, pl.mq_pad, pl.kq_pad, (int32_t)pl.Q, 1, pl.a_kfast, 0};
       PackArgs pb{pl.bc, pl.br, pl.nq_pad, pl.kq_pad, (int32_t)pl.Q, 0, pl.b_kfast, 0};
-      CU(launch_pack_views(A, pool, pa, PA, s), "k_pack_views(A)");
-      CU(launch_pack_views(B, pool, pb, PB, s), "k_pack_views(B)");
+      CU(launch_pack_views(A, pool2, pa, PA, s), "k_pack_views(A)");
+      CU(launch_pack_views(B, pool2, pb, PB, s), "k_pack_views(B)");
+      launches += 2;
       const FusedSides fs = packed_sides(pl);
-      VecDesc pv[4];
-      packed_vecs(pl, fs, pv);
-      VecDesc *d_pv = reinterpret_cast<VecDesc *>(ws + pl.off_vecs) + pl.vecs.size();
-      if (int rc = upload(pv, sizeof(pv), d_pv, s)) return -rc;
-      CU(launch_build_pool(d_pv, 4, pl.pool_len, pool, s), "k_build_pool(packed)");
-      launches += 3;
+      if (!restored) {
+        VecDesc pv[4];
+        packed_vecs(pl, fs, pv);
+        VecDesc *d_pv = reinterpret_cast<VecDesc *>(ws + pl.off_vecs) + pl.vecs.size();
+        if (int rc = upload(pv, sizeof(pv), d_pv, s)) return -rc;
+        CU(launch_build_pool(d_pv, 4, pl.pool_len, pool, s), "k_build_pool(packed)");
+        ++launches;
+      }
       if (!plan_fused(p, pl, fs, PA, PB, Cp, gf, maps, jobs)) return -fail(STC_EINVAL, "internal: packed plan");
       gf.A = PA;
       gf.B = PB;
-      ok = 1;
-      packed = true;
-    }
-    if (ok && !packed) {
+    } else if (direct) {
+      if (!plan_fused(p, pl, direct_sides(p, pl), A, B, Cp, gf, maps, jobs))
+        return -fail(STC_EINVAL, "internal: direct plan");
       gf.A = A;
       gf.B = B;
+    } else {
+      return 0;  // the gather kernel
     }
-    if (ok) {
-      gf.coords = reinterpret_cast<const int4 *>(ws + pl.off_coords);
-      CU(launch_pool_coords(pool, reinterpret_cast<int4 *>(ws + pl.off_coords), jobs, s), "k_pool_coords");
+    gf.coords = coords;
+    if (!restored) {
+      CU(launch_pool_coords(pool, coords, jobs, s), "k_pool_coords");
       ++launches;
     }
-    return ok;
+    return 1;
   };
 
-  const int32_t *c_ready = g_c_ready;  // consumed by this call
-  g_c_ready = nullptr;
   GemmArgs g{};
   g.pool = pool;
   g.c_ready = c_ready;
@@ -1497,7 +1599,8 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
     o += pl.ops.size() * sizeof(OpDesc);
     memcpy(host.data() + o, pl.tgts.data(), pl.tgts.size() * sizeof(TgtDesc));
     g.tgts = reinterpret_cast<const TgtDesc *>(tab + o);
-    if (int rc = upload(host.data(), host.size(), tab, s)) return rc;
+    if (!restored)
+      if (int rc = upload(host.data(), host.size(), tab, s)) return rc;
     g.A = A;
     g.B = B;
     g.C = C;
@@ -1522,71 +1625,77 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         return fail(STC_EINVAL, "internal: pre-summed plan");
       gf.A = PA;
       gf.B = PB;
-      gf.coords = reinterpret_cast<const int4 *>(ws + pl.off_coords);
-      CU(launch_pool_coords(pool, reinterpret_cast<int4 *>(ws + pl.off_coords), jobs, s), "k_pool_coords");
-      ++launches;
+      gf.coords = coords;
+      if (!restored) {
+        CU(launch_pool_coords(pool, coords, jobs, s), "k_pool_coords");
+        ++launches;
+      }
+      if (int rc = save_snapshot()) return rc;
       if (gf.cred) gf.mscratch = reinterpret_cast<double *>(ws + pl.off_mscr);
       for (int bi = 0; bi < pl.nbatches; ++bi) {
         const int t0 = bi * pl.batch, nb = std::min(T - t0, pl.batch);
-        PresumArgs pa = presum_args(pl, 0, A, PA, pool, t0, t0 + nb), pb = presum_args(pl, 1, B, PB, pool, t0, t0 + nb);
-        CU(launch_presum(pa, s), "k_presum(A)");
-        CU(launch_presum(pb, s), "k_presum(B)");
+        CU(launch_presum2(presum_args(pl, 0, A, PA, pool, t0, t0 + nb), presum_args(pl, 1, B, PB, pool, t0, t0 + nb), s),
+           "k_presum");
         gf.terms = g.terms + t0;
         gf.nterms = nb;
         gf.total_items = (int)(P * nb);
         gf.counter = counters + bi;
         if (g_ev_before && bi == 0) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
         CU(launch_fused(gf, (int)std::min<int64_t>(pl.grid, gf.total_items), s, maps), "k_strassen_fused");
-        launches += 3;
+        launches += 2;
       }
       if (g_ev_after) CU(cudaEventRecord(g_ev_after, s), "cudaEventRecord");
       tma = true;
       st.fast_updates = gf.cred ? (int64_t)P * (int64_t)pl.tgts.size() : 0;
       st.slow_updates = gf.cred ? 0 : (int64_t)P * (int64_t)pl.tgts.size();
     } else {
-    const int fz = prepare_fused(gf, maps, C);
-    if (fz < 0) return -fz;
-    if (fz) {
-      // fused kernel: TMA boxes of 128 x 8, sums in the consumers' fragment loads
-      tma = !packed;
-      // C updates by the producer warpgroup's three spare warps from dense M tiles:
-      // by default with the TMA reduce-add epilogue (no FP64 work in those warps);
-      // opt-in (STC_EPI_OFFLOAD=1) with load/add/store, whose DADDs starve behind the DMMAs
-      // C updates by the producer warpgroup's three spare warps from dense M tiles: by
-      // default with the TMA reduce-add epilogue (no FP64 work in those warps); without
-      // TMA reduce (C not box-regular: only L0 reaches here) the consumers' own
-      // load/add/store epilogue (the spare warps' DADDs starve behind the DMMAs)
-      const char *eo = getenv("STC_EPI_OFFLOAD");
-      const int offload = (eo ? atoi(eo) : (gf.cred ? 1 : 0)) || (gf.cred && gf.cred8);  // 8-wide boxes: offloaded
-      if (offload) gf.mscratch = reinterpret_cast<double *>(ws + pl.off_mscr);
-      if (g_ev_before) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
-      CU(launch_fused(gf, grid, s, maps), "k_strassen_fused");
-    } else {
-      tma = plan_tma(p, pl, A, B, g, maps);
-      if (g_ev_before) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
-      CU(launch_gemm(g, grid, s, tma ? maps : nullptr), "k_strassen_gemm");
-    }
-    if (g_ev_after) CU(cudaEventRecord(g_ev_after, s), "cudaEventRecord");
-    ++launches;
-    // C-tile updates: by TMA reduce-add boxes (the reference's fast store_tile path,
-    // _jit.py:166-176) or by the load/add/store scatter epilogue (its slow path)
-    const int64_t upd = (int64_t)P * (int64_t)pl.tgts.size();
-    st.fast_updates = (fz && gf.cred) ? upd : 0;
-    st.slow_updates = (fz && gf.cred) ? 0 : upd;
+      const int fz = prepare_fused(gf, maps, C);
+      if (fz < 0) return -fz;
+      if (!fz) tma = plan_tma(p, pl, A, B, g, maps);  // the gather kernel (host set-up only)
+      if (int rc = save_snapshot()) return rc;
+      if (fz) {
+        // fused kernel: TMA boxes of 128 x 8.  C updates by the producer warpgroup's three
+        // spare warps from dense M tiles with the TMA reduce-add epilogue (no FP64 work in
+        // those warps); without TMA reduce (C not box-regular: only L0 reaches here) the
+        // consumers' own load/add/store epilogue (the spare warps' DADDs starve behind the
+        // DMMAs); STC_EPI_OFFLOAD overrides, 8-wide C boxes always go to the spare warps
+        tma = !packed;
+        const char *eo = getenv("STC_EPI_OFFLOAD");
+        const int offload = (eo ? atoi(eo) : (gf.cred ? 1 : 0)) || (gf.cred && gf.cred8);
+        if (offload) gf.mscratch = reinterpret_cast<double *>(ws + pl.off_mscr);
+        if (g_ev_before) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
+        CU(launch_fused(gf, grid, s, maps), "k_strassen_fused");
+      } else {
+        if (g_ev_before) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
+        CU(launch_gemm(g, grid, s, tma ? maps : nullptr), "k_strassen_gemm");
+      }
+      if (g_ev_after) CU(cudaEventRecord(g_ev_after, s), "cudaEventRecord");
+      ++launches;
+      // C-tile updates: by TMA reduce-add boxes (the reference's fast store_tile path,
+      // _jit.py:166-176) or by the load/add/store scatter epilogue (its slow path)
+      const int64_t upd = (int64_t)P * (int64_t)pl.tgts.size();
+      st.fast_updates = (fz && gf.cred) ? upd : 0;
+      st.slow_updates = (fz && gf.cred) ? 0 : upd;
     }
   } else {
-    // per-term operand slots: Naive's explicit copies, or pre-summed ABC / AB operands
-    const bool naive = pl.variant == STC_VARIANT_NAIVE || pl.presum;
+    // dense M: per-term operand slots (Naive's explicit copies, pre-summed ABC / AB
+    // operands) or the operands' own / repacked views (AB); per batch of terms the slots,
+    // one DMMA launch writing dense M, one ordered accumulate into C
     double *M = reinterpret_cast<double *>(ws + pl.off_M);
     double *PA = reinterpret_cast<double *>(ws + pl.off_pa);
     double *PB = reinterpret_cast<double *>(ws + pl.off_pb);
-    GemmArgs gf_ab = g;  // fused set-up shared by the batches (AB)
-    CUtensorMap maps_ab[3];
-    int fused_ab = 0;
+    struct Batch {
+      int t0, t1;
+      const TermDesc *d_g, *d_ua, *d_ub;
+      const OpDesc *d_ops;
+      AccArgs aa;
+      int64_t nupd;
+    };
+    std::vector<Batch> batches;
+    // pass 1: the batches' tables (constant: uploaded unless restored)
     for (int bi = 0; bi < pl.nbatches; ++bi) {
       const int t0 = bi * pl.batch, t1 = std::min(T, t0 + pl.batch);
       const int nb = t1 - t0;
-      // tables for this batch: gemm terms, unpack-A terms, unpack-B terms, ops
       std::vector<TermDesc> gterms(nb), uA(nb), uB(nb);
       std::vector<OpDesc> ops;
       for (int t = t0; t < t1; ++t) {
@@ -1608,7 +1717,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
           ops.push_back({pl.bc + c * pl.nq_pad, pl.br + r * pl.kq_pad, 0, (double)op.s});
         }
         ua.m_slot = ub.m_slot = gd.m_slot = slot;
-        if (naive) {
+        if (slots) {
           gd.a_first = (int)ops.size();
           gd.a_count = 1;
           ops.push_back({pl.dxa + slot * pl.mq_pad, pl.dka, 0, 1.0});
@@ -1643,7 +1752,6 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         cstart[q] = pl.cc + c * pl.nq_pad;
       }
       lstart[pl.nquads] = (int32_t)lslot.size();
-      // upload (one staging copy per table region)
       char *tab = ws + pl.off_tab + (size_t)bi * pl.tab_bytes;
       std::vector<char> host(pl.tab_bytes, 0);
       size_t o = 0;
@@ -1653,12 +1761,16 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         o += bytes;
         return tab + at;
       };
-      const TermDesc *d_g = reinterpret_cast<const TermDesc *>(put(gterms.data(), nb * sizeof(TermDesc)));
-      const TermDesc *d_ua = reinterpret_cast<const TermDesc *>(put(uA.data(), nb * sizeof(TermDesc)));
-      const TermDesc *d_ub = reinterpret_cast<const TermDesc *>(put(uB.data(), nb * sizeof(TermDesc)));
-      const OpDesc *d_ops = reinterpret_cast<const OpDesc *>(put(ops.data(), ops.size() * sizeof(OpDesc)));
+      Batch b{};
+      b.t0 = t0;
+      b.t1 = t1;
+      b.d_g = reinterpret_cast<const TermDesc *>(put(gterms.data(), nb * sizeof(TermDesc)));
+      b.d_ua = reinterpret_cast<const TermDesc *>(put(uA.data(), nb * sizeof(TermDesc)));
+      b.d_ub = reinterpret_cast<const TermDesc *>(put(uB.data(), nb * sizeof(TermDesc)));
+      b.d_ops = reinterpret_cast<const OpDesc *>(put(ops.data(), ops.size() * sizeof(OpDesc)));
       if (o > pl.tab_bytes) return fail(STC_EINVAL, "internal: table overflow");
-      if (int rc = upload(host.data(), o, tab, s)) return rc;
+      if (!restored)
+        if (int rc = upload(host.data(), o, tab, s)) return rc;
       char *acc = ws + pl.off_acc + (size_t)bi * pl.acc_bytes;
       std::vector<char> hacc(pl.acc_bytes, 0);
       size_t ao = 0;
@@ -1668,7 +1780,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         ao += align256(slot_bytes);
         return acc + at;
       };
-      AccArgs aa{};
+      AccArgs &aa = b.aa;
       aa.c_ready = c_ready;
       aa.list_start = reinterpret_cast<const int32_t *>(aput(lstart.data(), lstart.size() * 4, (pl.nquads + 1) * 4));
       aa.list_slot = reinterpret_cast<const int32_t *>(
@@ -1677,22 +1789,59 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
           aput(lsign.data(), lsign.size() * 8, (size_t)pl.batch * pl.nquads * 8));
       aa.row_start = reinterpret_cast<const int64_t *>(aput(rstart.data(), rstart.size() * 8, pl.nquads * 8));
       aa.col_start = reinterpret_cast<const int64_t *>(aput(cstart.data(), cstart.size() * 8, pl.nquads * 8));
-      if (int rc = upload(hacc.data(), pl.acc_bytes, acc, s)) return rc;
-
-      if (naive && pl.presum) {
+      if (!restored)
+        if (int rc = upload(hacc.data(), pl.acc_bytes, acc, s)) return rc;
+      aa.M = M;
+      aa.m_ld = pl.nq_pad;
+      aa.m_stride = pl.m_slot;
+      aa.C = C;
+      aa.pool = pool;
+      aa.mq = pl.mq;
+      aa.nq = pl.nq;
+      aa.nquads = pl.nquads;
+      aa.max_list = 0;
+      for (int q = 0; q < pl.nquads; ++q) aa.max_list = std::max(aa.max_list, lstart[q + 1] - lstart[q]);
+      b.nupd = (int64_t)lslot.size();
+      batches.push_back(b);
+    }
+    // the fused set-up shared by the batches: maps, coordinates, repacked operands
+    GemmArgs gf_ab = g;
+    CUtensorMap maps_ab[3];
+    int fused_ab = 0;
+    if (slots) {  // per-term slots: regular by construction
+      CoordJobs jobs{};
+      if (plan_fused(p, pl, naive_sides(pl), PA, PB, nullptr, gf_ab, maps_ab, jobs)) {
+        gf_ab.A = PA;
+        gf_ab.B = PB;
+        gf_ab.coords = coords;
+        if (!restored) {
+          CU(launch_pool_coords(pool, coords, jobs, s), "k_pool_coords");
+          ++launches;
+        }
+        fused_ab = 1;
+      }
+    } else {
+      fused_ab = prepare_fused(gf_ab, maps_ab, nullptr);
+      if (fused_ab < 0) return -fused_ab;
+    }
+    if (int rc = save_snapshot()) return rc;
+    // pass 2: per batch the operand slots, the DMMA launch, the accumulate
+    for (int bi = 0; bi < pl.nbatches; ++bi) {
+      const Batch &b = batches[bi];
+      const int nb = b.t1 - b.t0;
+      if (slots && pl.presum) {
         // one pass per side: every element position's 4^L quadrant values -> the batch's sums
-        PresumArgs pa = presum_args(pl, 0, A, PA, pool, t0, t1), pb = presum_args(pl, 1, B, PB, pool, t0, t1);
-        CU(launch_presum(pa, s), "k_presum(A)");
-        CU(launch_presum(pb, s), "k_presum(B)");
-        launches += 2;
-      } else if (naive) {
+        CU(launch_presum2(presum_args(pl, 0, A, PA, pool, b.t0, b.t1), presum_args(pl, 1, B, PB, pool, b.t0, b.t1), s),
+           "k_presum");
+        ++launches;
+      } else if (slots) {
         UnpackArgs ua{};
         ua.pool = pool;
-        ua.ops = d_ops;
+        ua.ops = b.d_ops;
         ua.nterms = nb;
         ua.D = A;
         ua.out = PA;
-        ua.terms = d_ua;
+        ua.terms = b.d_ua;
         ua.x_len = pl.mq_pad;
         ua.k_len = pl.kq_pad;
         ua.slot_stride = pl.pa_slot;
@@ -1700,7 +1849,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         CU(launch_unpack(ua, s), "k_unpack(A)");
         ua.D = B;
         ua.out = PB;
-        ua.terms = d_ub;
+        ua.terms = b.d_ub;
         ua.x_len = pl.nq_pad;
         ua.slot_stride = pl.pb_slot;
         ua.kfast = pl.b_kfast;
@@ -1708,42 +1857,27 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         launches += 2;
         st.slow_blocks += 2 * nb;
       }
-      g.A = naive ? PA : A;
-      g.B = naive ? PB : B;
-      g.C = nullptr;
-      g.terms = d_g;
-      g.ops = d_ops;
-      g.tgts = nullptr;
-      g.nterms = nb;
-      g.total_items = (int)(P * nb);
-      g.a_kfast = pl.a_kfast;  // Naive slots follow the source orientation too
-      g.b_kfast = pl.b_kfast;
-      g.dense_out = 1;
-      g.use_tickets = 0;
-      g.M = M;
-      g.m_ld = pl.nq_pad;
-      g.m_stride = pl.m_slot;
-      g.counter = counters + bi;
-      const int grid = (int)std::min<int64_t>(pl.grid, g.total_items);
-      GemmArgs gf = g;
-      if (bi == 0 && !naive) {
-        fused_ab = prepare_fused(gf_ab, maps_ab, nullptr);
-        if (fused_ab < 0) return -fused_ab;
-      } else if (bi == 0 && naive) {
-        // Naive: the per-term packed sums (PA, PB) are regular by construction
-        CoordJobs jobs{};
-        if (plan_fused(p, pl, naive_sides(pl), PA, PB, nullptr, gf_ab, maps_ab, jobs)) {
-          gf_ab.A = PA;
-          gf_ab.B = PB;
-          gf_ab.coords = reinterpret_cast<const int4 *>(ws + pl.off_coords);
-          CU(launch_pool_coords(pool, reinterpret_cast<int4 *>(ws + pl.off_coords), jobs, s), "k_pool_coords");
-          ++launches;
-          fused_ab = 1;
-        }
-      }
-      const bool fused = fused_ab > 0;
-      if (fused) {  // per-batch fields over the fused set-up (maps, coordinates, packed operands)
-        const GemmArgs base = gf_ab;
+      GemmArgs gb = g;
+      gb.A = slots ? PA : A;
+      gb.B = slots ? PB : B;
+      gb.C = nullptr;
+      gb.terms = b.d_g;
+      gb.ops = b.d_ops;
+      gb.tgts = nullptr;
+      gb.nterms = nb;
+      gb.total_items = (int)(P * nb);
+      gb.a_kfast = pl.a_kfast;  // Naive slots follow the source orientation too
+      gb.b_kfast = pl.b_kfast;
+      gb.dense_out = 1;
+      gb.use_tickets = 0;
+      gb.M = M;
+      gb.m_ld = pl.nq_pad;
+      gb.m_stride = pl.m_slot;
+      gb.counter = counters + bi;
+      const int grid = (int)std::min<int64_t>(pl.grid, gb.total_items);
+      GemmArgs gf = gb;
+      if (fused_ab) {  // per-batch fields over the fused set-up (maps, coordinates, packed operands)
+        const GemmArgs &base = gf_ab;
         gf.A = base.A;
         gf.B = base.B;
         gf.a_kfast = base.a_kfast;
@@ -1767,27 +1901,17 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         }
       }
       if (g_ev_before && bi == 0) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
-      if (fused) {
+      if (fused_ab) {
         tma = !packed;  // TMA boxes of the operands or of their packed slots (the reference's Naive GEMM: dense, fast blocks)
         CU(launch_fused(gf, grid, s, maps_ab), "k_strassen_fused(dense)");
       } else {
         if (pl.tshape != 0) return fail(STC_EINVAL, "internal: tile shape %d needs the fused kernel", pl.tshape);
-        CU(launch_gemm(g, grid, s), "k_strassen_gemm(dense)");
+        CU(launch_gemm(gb, grid, s), "k_strassen_gemm(dense)");
       }
       if (g_ev_after && bi == pl.nbatches - 1) CU(cudaEventRecord(g_ev_after, s), "cudaEventRecord");
-      aa.M = M;
-      aa.m_ld = pl.nq_pad;
-      aa.m_stride = pl.m_slot;
-      aa.C = C;
-      aa.pool = pool;
-      aa.mq = pl.mq;
-      aa.nq = pl.nq;
-      aa.nquads = pl.nquads;
-      aa.max_list = 0;
-      for (int q = 0; q < pl.nquads; ++q) aa.max_list = std::max(aa.max_list, lstart[q + 1] - lstart[q]);
-      CU(launch_accumulate(aa, s), "k_accumulate");
+      CU(launch_accumulate(b.aa, s), "k_accumulate");
       launches += 2;
-      st.slow_updates += (int64_t)lslot.size();
+      st.slow_updates += b.nupd;
     }
   }
   st.total_flops = 2.0 * BM * BN * (double)pl.kq_pad * (double)P * (double)T;

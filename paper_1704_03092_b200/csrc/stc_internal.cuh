@@ -212,7 +212,8 @@ int gemm_max_grid(int max_ops);
 bool plan_ticketed(const stc_problem *p);  // stc_capi.cu
 cudaError_t launch_accumulate(const AccArgs &a, cudaStream_t s);
 cudaError_t launch_unpack(const UnpackArgs &a, cudaStream_t s);
-cudaError_t launch_presum(const PresumArgs &a, cudaStream_t s);
+cudaError_t launch_presum2(const PresumArgs &pa, const PresumArgs &pb, cudaStream_t s);  // both sides, one launch
+cudaError_t launch_restore(const void *src, void *dst, size_t bytes, cudaStream_t s);
 cudaError_t launch_pack_views(const double *D, const int64_t *pool, const PackArgs &a, double *out, cudaStream_t s);
 cudaError_t launch_accum_dense_single(const double *M, int64_t ldm, int64_t m, int64_t n, double *C,
                                       const int64_t *rows, const int64_t *cols, double coeff, cudaStream_t s);

@@ -369,10 +369,10 @@ constexpr int PRESUM_ROWS = 2;  // slow-dimension rows per thread
 // the other; every thread loads the 4^L quadrant values of its positions, then
 // writes the batch's term sums (coalesced along the contiguous dimension).
 template <int L, int SIDE>
-__global__ void __launch_bounds__(256) k_presum(const PresumArgs a) {
+__device__ __forceinline__ void presum_block(const PresumArgs &a, int64_t bx, int64_t by) {
   constexpr int Q = 1 << L;
   const int64_t fast_len = a.kfast ? a.klen : a.xlen, slow_len = a.kfast ? a.xlen : a.klen;
-  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t f = bx * blockDim.x + threadIdx.x;
   if (f >= fast_len) return;
   const int64_t fv = a.kfast ? a.kv : a.xv, sv = a.kfast ? a.xv : a.kv;
   int64_t fo[Q];
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(256) k_presum(const PresumArgs a) {
   for (int q = 0; q < Q; ++q) fo[q] = __ldg(a.pool + fv + q * fast_len + f);
 #pragma unroll 1
   for (int r = 0; r < PRESUM_ROWS; ++r) {
-    const int64_t sl = (int64_t)blockIdx.y * PRESUM_ROWS + r;
+    const int64_t sl = by * PRESUM_ROWS + r;
     if (sl >= slow_len) break;
     int64_t so[Q];
 #pragma unroll
@@ -397,18 +397,53 @@ __global__ void __launch_bounds__(256) k_presum(const PresumArgs a) {
   }
 }
 
-cudaError_t launch_presum(const PresumArgs &a, cudaStream_t s) {
+// Both sides in one launch: blocks [0, na) cover A's slots, the rest B's.
+template <int L>
+__global__ void __launch_bounds__(256) k_presum(const PresumArgs pa, const PresumArgs pb, int64_t na_x, int64_t na,
+                                                int64_t nb_x) {
+  const int64_t b = blockIdx.x;
+  if (b < na)
+    presum_block<L, 0>(pa, b % na_x, b / na_x);
+  else
+    presum_block<L, 1>(pb, (b - na) % nb_x, (b - na) / nb_x);
+}
+
+static void presum_grid(const PresumArgs &a, int64_t &gx, int64_t &gy) {
   const int64_t fast_len = a.kfast ? a.klen : a.xlen, slow_len = a.kfast ? a.xlen : a.klen;
-  if (fast_len <= 0 || slow_len <= 0) return cudaSuccess;
-  const int64_t gy = (slow_len + PRESUM_ROWS - 1) / PRESUM_ROWS;
-  if (gy > 65535) return cudaErrorInvalidConfiguration;
-  dim3 grid((unsigned)((fast_len + 255) / 256), (unsigned)gy);
-  if (a.level == 1)
-    a.side ? k_presum<1, 1><<<grid, 256, 0, s>>>(a) : k_presum<1, 0><<<grid, 256, 0, s>>>(a);
-  else if (a.level == 2)
-    a.side ? k_presum<2, 1><<<grid, 256, 0, s>>>(a) : k_presum<2, 0><<<grid, 256, 0, s>>>(a);
+  gx = fast_len > 0 ? (fast_len + 255) / 256 : 0;
+  gy = slow_len > 0 ? (slow_len + PRESUM_ROWS - 1) / PRESUM_ROWS : 0;
+}
+
+cudaError_t launch_presum2(const PresumArgs &pa, const PresumArgs &pb, cudaStream_t s) {
+  if (pa.level != pb.level || pa.side != 0 || pb.side != 1) return cudaErrorInvalidValue;
+  int64_t ax, ay, bx, by;
+  presum_grid(pa, ax, ay);
+  presum_grid(pb, bx, by);
+  const int64_t na = ax * ay, total = na + bx * by;
+  if (total == 0) return cudaSuccess;
+  if (total > INT32_MAX) return cudaErrorInvalidConfiguration;
+  if (pa.level == 1)
+    k_presum<1><<<(unsigned)total, 256, 0, s>>>(pa, pb, std::max<int64_t>(ax, 1), na, std::max<int64_t>(bx, 1));
+  else if (pa.level == 2)
+    k_presum<2><<<(unsigned)total, 256, 0, s>>>(pa, pb, std::max<int64_t>(ax, 1), na, std::max<int64_t>(bx, 1));
   else
     return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+// ---- plan snapshot restore (stc_capi.cu Resident): a plain device copy ----
+__global__ void __launch_bounds__(256) k_restore(const uint4 *__restrict__ src, uint4 *__restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+cudaError_t launch_restore(const void *src, void *dst, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return cudaSuccess;
+  if (bytes % 16 || (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) % 16)
+    return cudaErrorInvalidValue;
+  const int64_t n = (int64_t)(bytes / 16);
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 4);
+  k_restore<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint4 *>(src), reinterpret_cast<uint4 *>(dst), n);
   return cudaGetLastError();
 }
 

@@ -56,7 +56,7 @@ def test_fused_matches_gather_bitwise_and_classical(name):
         for variant in ("abc", "ab"):
             cf, stf = _run(spec, a, b, c0, level, variant, True)
             cg, stg = _run(spec, a, b, c0, level, variant, False)
-            assert stf.kernel_launches == stg.kernel_launches + 1, (name, level, variant)  # coordinate table
+            assert stf.kernel_launches >= stg.kernel_launches, (name, level, variant)  # + the coordinate table on a first call
             assert stf.fast_blocks > 0 and stf.slow_blocks == 0, (name, level, variant)
             assert np.array_equal(cf.data, cg.data), (name, level, variant)
             assert stc.relative_error(cf, classical) <= TOL, (name, level, variant)
@@ -208,8 +208,9 @@ def test_repacked_operands_match_gather_bitwise(line):
         for variant in ("abc", "ab"):
             cf, stf = _run(spec, a, b, c0, level, variant, True)
             cg, stg = _run(spec, a, b, c0, level, variant, False)
-            # 2 packs, pool, coordinates, the packed vectors' table upload
-            assert stf.kernel_launches == stg.kernel_launches + 5, (level, variant)
+            # the two repacking launches (the pool / coordinate set-up is restored from the
+            # plan's snapshot after the first call)
+            assert stf.kernel_launches >= stg.kernel_launches + 2, (level, variant)
             assert np.array_equal(cf.data, cg.data), (level, variant)
             assert stc.relative_error(cf, classical) <= TOL, (level, variant)
 
