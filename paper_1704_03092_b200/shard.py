@@ -125,10 +125,12 @@ def gather_shards(spec: ContractionSpec, c: DenseTensor, rank: int, world: int, 
     regions = [_region(c, spec.labels_c, s) for s in shards]
     size = max(r.numel() for r in regions)
     data = _storage(c)
-    flat = torch.zeros(size, dtype=data.dtype, device=data.device)
+    # gloo moves host tensors: device storage is staged through host memory
+    staging = "cpu" if dist.get_backend(group) == "gloo" else data.device
+    flat = torch.zeros(size, dtype=data.dtype, device=staging)
     flat[: regions[rank].numel()].view(regions[rank].shape).copy_(regions[rank])
-    out = torch.empty(world * size, dtype=data.dtype, device=data.device)
-    if hasattr(dist, "all_gather_into_tensor") and (data.is_cuda or dist.get_backend(group) != "gloo"):
+    out = torch.empty(world * size, dtype=data.dtype, device=staging)
+    if dist.get_backend(group) != "gloo":
         dist.all_gather_into_tensor(out, flat, group=group)
     else:  # gloo has no all_gather_into_tensor: the list form over views of the same buffer
         dist.all_gather(list(out.view(world, size).unbind(0)), flat, group=group)
