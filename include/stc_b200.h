@@ -120,18 +120,26 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
  * the DMMA work, pageable memory works but serialises) and dA, dB, dC are
  * DEVICE mirrors with the same element offsets (at least max offset + 1
  * elements each; contents ignored, dC ends equal to the result).  The problem
- * is cut along one label of the I or J bundle into pieces whose uploads,
- * contractions (stc_contract) and downloads are pipelined on library streams
- * (stc_host.cu); STC_HOST_PIECES=n overrides the piece count (1: no split).
- * Stream-ordered after prior work on `stream`; hC holds the result once
- * `stream` has completed.  Stats are summed over the pieces (leaf_multiplies
- * stays 7^L: every piece is an L-level Strassen contraction). */
+ * is cut along one label of the I or J bundle (or one of each: an I x J grid,
+ * stc_host_grid) into pieces whose uploads, contractions (stc_contract) and
+ * downloads are pipelined on library streams (stc_host.cu); STC_HOST_PIECES=n
+ * overrides the piece count (1: no split).  Stream-ordered after prior work on
+ * `stream`; hC holds the result once `stream` has completed.  Stats are summed
+ * over the pieces (leaf_multiplies stays 7^L: every piece is an L-level
+ * Strassen contraction; stats->pieces says how many ran). */
 int stc_host_workspace_size(const stc_problem *p, size_t *bytes);
 int stc_contract_host(const stc_problem *p, const double *A, const double *B, double *C, double *dA, double *dB,
                       double *dC, void *workspace, size_t workspace_bytes, void *stream, stc_stats *stats);
 /* The split stc_contract_host would use: side 0 = I bundle (A and C), 1 = J
- * bundle (B and C); label = index in that bundle; pieces = 1 for no split. */
+ * bundle (B and C); label = index in that bundle; pieces = 1 for no split
+ * (for an I x J grid: side 0, the I label, pieces = the grid's size). */
 int stc_host_plan(const stc_problem *p, int32_t *side, int32_t *label, int32_t *pieces);
+/* The full grid: I label `i_label` cut into `i_pieces` ranges (A rows, C rows) and J
+ * label `j_label` into `j_pieces` (B columns, C columns); piece (r, c) is an
+ * independent L-level contraction.  Problems of 16 GB and more get a 4 x 4 grid, so
+ * the first piece starts after a quarter of each operand arrived (STC_HOST_GRID=SAxSB
+ * forces a grid; STC_HOST_GRID=1 or STC_HOST_PIECES=n keep the 1-D cut).  Host-only. */
+int stc_host_grid(const stc_problem *p, int32_t *i_label, int32_t *i_pieces, int32_t *j_label, int32_t *j_pieces);
 
 /* Overlap hook (no reference counterpart): the next stc_contract call on this
  * thread makes its kernels wait on the device until *c_ready != 0 (a device

@@ -67,7 +67,7 @@ _EXPORTS = (
     "stc_block_vector", "stc_fused_term_workspace_size", "stc_fused_term", "stc_accumulate_dense",
     "stc_unpack_sum", "stc_sq_norms", "stc_set_kernel_events", "stc_set_c_ready",
     "stc_host_workspace_size", "stc_contract_host", "stc_host_plan", "stc_fill_uniform", "stc_plan_describe",
-    "stc_shard_problem",
+    "stc_shard_problem", "stc_host_grid",
 )
 
 _lib = None
@@ -98,6 +98,7 @@ def _declare(l):
     l.stc_host_workspace_size.argtypes = [P(Problem), P(sz)]
     l.stc_contract_host.argtypes = [P(Problem), vp, vp, vp, vp, vp, vp, vp, sz, vp, P(Stats)]
     l.stc_host_plan.argtypes = [P(Problem), P(ctypes.c_int32), P(ctypes.c_int32), P(ctypes.c_int32)]
+    l.stc_host_grid.argtypes = [P(Problem)] + [P(ctypes.c_int32)] * 4
     l.stc_fill_uniform.argtypes = [vp, ctypes.c_int, P(i64), P(i64), i64, ctypes.c_uint64, vp]
     l.stc_plan_describe.argtypes = [P(Problem), ctypes.c_int, P(PlanInfo)]
     l.stc_shard_problem.argtypes = [P(Problem), ctypes.c_int, ctypes.c_int, ctypes.c_int, P(Problem), P(i64), P(i64),

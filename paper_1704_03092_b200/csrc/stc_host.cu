@@ -136,11 +136,14 @@ TensorLabels labels_of(const stc_bundle &r, const stc_bundle &c, int64_t base) {
   return t;
 }
 
-// A split of the I (side 0: A and C) or J (side 1: B and C) bundle on label
-// `lab` of that bundle into `pieces` equal ranges.
+// A grid of pieces: label `la` of the I bundle (A rows and C rows) cut into `sa`
+// equal ranges and label `lb` of the J bundle (B columns and C columns) into `sb`;
+// piece s = r * sb + c holds I range r and J range c.  sa = 1 or sb = 1 is the 1-D
+// split of round 1 (side / lab / pieces describe it for stc_host_plan).
 struct Split {
-  int side = 0, lab = 0, pieces = 1;
-  int64_t run = 0;  // shortest copy run, bytes
+  int la = 0, sa = 1, lb = 0, sb = 1;
+  int side = 0, lab = 0, pieces = 1;  // 1-D view: the cut side (0: I, 1: J), its label, sa * sb
+  int64_t run = 0;                    // shortest copy run, bytes
 };
 
 int64_t bundle_elems(const stc_bundle &b) {
@@ -149,55 +152,131 @@ int64_t bundle_elems(const stc_bundle &b) {
   return n;
 }
 
+Split one_d(int side, int lab, int S, int64_t run) {
+  Split sp;
+  sp.side = side;
+  sp.lab = lab;
+  sp.pieces = S;
+  sp.run = run;
+  if (side == 0) {
+    sp.la = lab;
+    sp.sa = S;
+  } else {
+    sp.lb = lab;
+    sp.sb = S;
+  }
+  return sp;
+}
+
+// The best cut of one side into `want` (or fewer, halving) pieces: the label with the
+// longest copy runs in both tensors it touches; false if none qualifies.
+bool best_cut(const stc_problem &p, int side, int want, bool forced, int &lab, int &S, int64_t &run) {
+  const stc_bundle &ob = side == 0 ? p.a_row : p.b_col;  // the operand's split bundle
+  const stc_bundle &cb = side == 0 ? p.c_row : p.c_col;
+  const int64_t quad = int64_t(1) << p.level;
+  const int64_t blen = bundle_elems(cb);
+  bool found = false;
+  for (int l = 0; l < cb.nlab; ++l) {
+    for (int n = want; n >= 2; n /= 2) {
+      if (cb.ext[l] % n) continue;
+      // each piece keeps at least two 128-wide tiles per quadrant, and copy runs
+      // are long enough for full PCIe rate (forced counts: only divisibility)
+      if (!forced && blen / n < quad * 256) continue;
+      const int64_t r = 8 * (cb.ext[l] / n) * std::min(ob.str[l], cb.str[l]);
+      if (!forced && r < kMinRunBytes) continue;
+      if (!found || n > S || (n == S && r > run)) {
+        lab = l;
+        S = n;
+        run = r;
+        found = true;
+      }
+      break;
+    }
+  }
+  return found;
+}
+
 Split choose_split(const stc_problem &p) {
   Split best;
   const TensorLabels A = labels_of(p.a_row, p.a_col, p.a_base), B = labels_of(p.b_row, p.b_col, p.b_base),
                      C = labels_of(p.c_row, p.c_col, p.c_base);
   const int64_t bytes = 8 * (A.elems() + B.elems() + 2 * C.elems());
+  if (!C.compact()) return best;
+  // I x J grid (STC_HOST_GRID=SAxSB forces it, "1" disables): for problems of 16 GB and
+  // more a 1-D cut must upload a whole operand before the first piece can start (cfg5:
+  // 8.6 GB, 0.17 s); a 4 x 4 grid starts after a quarter of each (0.08 s)
+  const char *genv = getenv("STC_HOST_GRID");
+  int ga = 0, gb = 0;
+  if (genv && sscanf(genv, "%dx%d", &ga, &gb) != 2) ga = gb = 0;
   const char *env = getenv("STC_HOST_PIECES");
-  // 4 pieces; 8 for problems of 16 GB and more, whose last C piece's download (the
-  // call's tail) would otherwise take tens of ms (cfg5: 4 pieces 1.82 s, 8 pieces 1.79 s)
-  const int want = env ? std::max(1, std::min(kMaxPieces, atoi(env))) : (bytes >= (16ll << 30) ? 8 : 4);
-  if (want <= 1 || (!env && bytes < kMinSplitBytes) || !C.compact()) return best;
-  const int64_t quad = int64_t(1) << p.level;
-  for (int side = 0; side < 2; ++side) {
-    const stc_bundle &ob = side == 0 ? p.a_row : p.b_col;  // the operand's split bundle
-    const stc_bundle &cb = side == 0 ? p.c_row : p.c_col;
-    if (!(side == 0 ? A : B).compact()) continue;
-    const int64_t blen = bundle_elems(cb);
-    for (int l = 0; l < cb.nlab; ++l) {
-      for (int S = want; S >= 2; S /= 2) {
-        if (cb.ext[l] % S) continue;
-        // each piece keeps at least two 128-wide tiles per quadrant, and copy runs
-        // are long enough for full PCIe rate (STC_HOST_PIECES set: only divisibility)
-        if (!env && blen / S < quad * 256) continue;
-        const int64_t run = 8 * (cb.ext[l] / S) * std::min(ob.str[l], cb.str[l]);
-        if (!env && run < kMinRunBytes) continue;
-        const bool better = S > best.pieces || (S == best.pieces && run > best.run);
-        if (better) best = Split{side, l, S, run};
-        break;
-      }
+  if (!env && (ga > 0 || (!genv && bytes >= (16ll << 30))) && A.compact() && B.compact()) {
+    const bool forced = ga > 0;
+    int la = 0, lb = 0, sa = 0, sb = 0;
+    int64_t ra = 0, rb = 0;
+    if (best_cut(p, 0, forced ? ga : 4, forced, la, sa, ra) && best_cut(p, 1, forced ? gb : 4, forced, lb, sb, rb) &&
+        sa * sb <= kMaxPieces && (forced || (sa >= 2 && sb >= 2))) {
+      best.la = la;
+      best.sa = sa;
+      best.lb = lb;
+      best.sb = sb;
+      best.side = 0;
+      best.lab = la;
+      best.pieces = sa * sb;
+      best.run = std::min(ra, rb);
+      return best;
     }
+  }
+  // 1-D: 4 pieces; 8 for problems of 16 GB and more (a shorter tail: the last C piece's download)
+  const int want = env ? std::max(1, std::min(kMaxPieces, atoi(env))) : (bytes >= (16ll << 30) ? 8 : 4);
+  if (want <= 1 || (!env && bytes < kMinSplitBytes)) return best;
+  for (int side = 0; side < 2; ++side) {
+    if (!(side == 0 ? A : B).compact()) continue;
+    int l = 0, S = 0;
+    int64_t run = 0;
+    if (!best_cut(p, side, want, env != nullptr, l, S, run)) continue;
+    const bool better = S > best.pieces || (S == best.pieces && run > best.run);
+    if (better) best = one_d(side, l, S, run);
   }
   return best;
 }
 
-// The sub-problem of piece s: label `lab` of the split bundle restricted to
-// [r0, r0 + len); bases move by r0 * stride in the two tensors it touches.
-stc_problem piece_problem(const stc_problem &p, const Split &sp, int64_t r0, int64_t len) {
+// The piece's I range [i0, i0 + ni) of label la and J range [j0, j0 + nj) of label lb:
+// those labels' extents in the tensors they index reduced, the bases moved.
+stc_problem piece_problem(const stc_problem &p, const Split &sp, int64_t i0, int64_t ni, int64_t j0, int64_t nj) {
   stc_problem q = p;
-  if (sp.side == 0) {
-    q.a_row.ext[sp.lab] = len;
-    q.c_row.ext[sp.lab] = len;
-    q.a_base += r0 * p.a_row.str[sp.lab];
-    q.c_base += r0 * p.c_row.str[sp.lab];
-  } else {
-    q.b_col.ext[sp.lab] = len;
-    q.c_col.ext[sp.lab] = len;
-    q.b_base += r0 * p.b_col.str[sp.lab];
-    q.c_base += r0 * p.c_col.str[sp.lab];
+  if (sp.sa > 1) {
+    q.a_row.ext[sp.la] = ni;
+    q.c_row.ext[sp.la] = ni;
+    q.a_base += i0 * p.a_row.str[sp.la];
+    q.c_base += i0 * p.c_row.str[sp.la];
+  }
+  if (sp.sb > 1) {
+    q.b_col.ext[sp.lb] = nj;
+    q.c_col.ext[sp.lb] = nj;
+    q.b_base += j0 * p.b_col.str[sp.lb];
+    q.c_base += j0 * p.c_col.str[sp.lb];
   }
   return q;
+}
+
+// Ranges of piece s: I range r = s / sb of label la, J range c = s % sb of label lb.
+struct PieceRange {
+  int64_t i0 = 0, ni = 1, j0 = 0, nj = 1;
+};
+PieceRange piece_range(const stc_problem &p, const Split &sp, int s) {
+  PieceRange pr;
+  const int r = s / sp.sb, c = s % sp.sb;
+  if (sp.sa > 1) {
+    const int64_t e = p.c_row.ext[sp.la];
+    pr.i0 = e * r / sp.sa;
+    pr.ni = e * (r + 1) / sp.sa - pr.i0;
+  }
+  if (sp.sb > 1) {
+    const int64_t e = p.c_col.ext[sp.lb];
+    pr.j0 = e * c / sp.sb;
+    pr.nj = e * (c + 1) / sp.sb - pr.j0;
+  }
+  return pr;
 }
 
 // Copy of the elements of compact tensor t with one label (stride lstr,
@@ -208,6 +287,28 @@ cudaError_t copy_piece(double *dst, const double *src, const TensorLabels &t, in
   const int64_t pitch = lext * lstr, rows = t.elems() / pitch;
   const int64_t off = t.base + r0 * lstr;
   return cudaMemcpy2DAsync(dst + off, pitch * 8, src + off, pitch * 8, len * lstr * 8, rows, kind, s);
+}
+
+// The elements of compact tensor t with label X (stride xs, extent xe) restricted to
+// [x0, x0 + xn) and label Y (stride ys, extent ye) to [y0, y0 + yn): for every index of
+// the outer of the two (the larger stride) one 2-D copy of the inner one's restriction.
+cudaError_t copy_block(double *dst, const double *src, const TensorLabels &t, int64_t xs, int64_t xe, int64_t x0,
+                       int64_t xn, int64_t ys, int64_t ye, int64_t y0, int64_t yn, cudaMemcpyKind kind,
+                       cudaStream_t s) {
+  if (xs < ys) {
+    std::swap(xs, ys);
+    std::swap(xe, ye);
+    std::swap(x0, y0);
+    std::swap(xn, yn);
+  }
+  // outer label x (stride xs), inner y: within one x index, rows of ye * ys elements
+  const int64_t pitch = ye * ys, rows = xs / pitch;
+  for (int64_t v = x0; v < x0 + xn; ++v) {
+    const int64_t off = t.base + v * xs + y0 * ys;
+    cudaError_t e = cudaMemcpy2DAsync(dst + off, pitch * 8, src + off, pitch * 8, yn * ys * 8, rows, kind, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t copy_span(double *dst, const double *src, const TensorLabels &t, cudaMemcpyKind kind, cudaStream_t s) {
@@ -257,12 +358,10 @@ struct DrainOnError {
 // base offsets, which can change the path -- e.g. whether a view is a TMA box -- and
 // with it the workspace).
 int piece_workspace(const stc_problem &p, const Split &sp, size_t &per_slot) {
-  const stc_bundle &cb = sp.side == 0 ? p.c_row : p.c_col;
-  const int64_t lext = sp.pieces > 1 ? cb.ext[sp.lab] : 1;
   size_t most = 256;
   for (int s = 0; s < sp.pieces; ++s) {
-    const int64_t r0 = lext * s / sp.pieces, r1 = lext * (s + 1) / sp.pieces;
-    stc_problem q = sp.pieces > 1 ? piece_problem(p, sp, r0, r1 - r0) : p;
+    const PieceRange pr = piece_range(p, sp, s);
+    stc_problem q = sp.pieces > 1 ? piece_problem(p, sp, pr.i0, pr.ni, pr.j0, pr.nj) : p;
     size_t b = 0;
     if (int rc = stc_workspace_size(&q, &b)) return rc;
     most = std::max(most, b);
@@ -290,6 +389,16 @@ struct Events {
 }  // namespace
 
 extern "C" {
+
+int stc_host_grid(const stc_problem *p, int32_t *i_label, int32_t *i_pieces, int32_t *j_label, int32_t *j_pieces) {
+  if (!p) return herr(STC_EINVAL, "null problem");
+  const Split sp = choose_split(*p);
+  if (i_label) *i_label = sp.la;
+  if (i_pieces) *i_pieces = sp.sa;
+  if (j_label) *j_label = sp.lb;
+  if (j_pieces) *j_pieces = sp.sb;
+  return STC_OK;
+}
 
 int stc_host_plan(const stc_problem *p, int32_t *side, int32_t *label, int32_t *pieces) {
   if (!p) return herr(STC_EINVAL, "null problem");
@@ -322,17 +431,13 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
     return herr(STC_EWORKSPACE, "workspace too small: need %zu bytes, got %zu", per * slots + kFlagBytes,
                 workspace_bytes);
   if (reinterpret_cast<uintptr_t>(workspace) & 255) return herr(STC_EINVAL, "workspace must be 256-byte aligned");
-  // the pieces: label `lab` of the split bundle cut into equal ranges
-  const stc_bundle &cb = sp.side == 0 ? p->c_row : p->c_col;
-  const stc_bundle &ob = sp.side == 0 ? p->a_row : p->b_col;
-  const int64_t lext = sp.pieces > 1 ? cb.ext[sp.lab] : 1;
+  // the pieces: an I range x a J range each (the grid of choose_split)
   std::vector<stc_problem> parts;
-  std::vector<int64_t> r0s, lens;
+  std::vector<PieceRange> ranges;
   for (int s = 0; s < sp.pieces; ++s) {
-    const int64_t r0 = lext * s / sp.pieces, r1 = lext * (s + 1) / sp.pieces;
-    parts.push_back(sp.pieces > 1 ? piece_problem(*p, sp, r0, r1 - r0) : *p);
-    r0s.push_back(r0);
-    lens.push_back(r1 - r0);
+    const PieceRange pr = piece_range(*p, sp, s);
+    parts.push_back(sp.pieces > 1 ? piece_problem(*p, sp, pr.i0, pr.ni, pr.j0, pr.nj) : *p);
+    ranges.push_back(pr);
   }
   HostStreams *hs = nullptr;
   if (int rc = host_streams(hs)) return rc;
@@ -344,9 +449,6 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
 
   const TensorLabels A = labels_of(p->a_row, p->a_col, p->a_base), B = labels_of(p->b_row, p->b_col, p->b_base),
                      C = labels_of(p->c_row, p->c_col, p->c_base);
-  const TensorLabels &O = sp.side == 0 ? A : B;  // split operand
-  const double *hO = sp.side == 0 ? hA : hB;
-  double *dO = sp.side == 0 ? dA : dB;
   cudaStream_t us = reinterpret_cast<cudaStream_t>(stream);
   Events E;
   cudaEvent_t start, end;
@@ -377,25 +479,38 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
     if (trace) HCU(cudaEventRecord(tr[1 + 4 * s], hs->h2d), "cudaEventRecord");
     return STC_OK;
   };
-  if (sp.pieces == 1) {
-    HCU(copy_span(dA, hA, A, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(A)");
-    HCU(copy_span(dB, hB, B, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(B)");
-    HCU(E.make(opin[0]), "cudaEventCreate");
-    HCU(cudaEventRecord(opin[0], hs->h2d), "cudaEventRecord");
-    HCU(copy_span(dC, hC, C, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(C)");
-    if (int rc = c_arrived(0)) return rc;
-  } else {
-    if (sp.side == 0)
-      HCU(copy_span(dB, hB, B, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(B)");
-    else
-      HCU(copy_span(dA, hA, A, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(A)");
-    for (int s = 0; s < sp.pieces; ++s) {
-      HCU(copy_piece(dO, hO, O, ob.str[sp.lab], lext, r0s[s], lens[s], cudaMemcpyHostToDevice, hs->h2d),
-          "cudaMemcpy2DAsync(operand piece)");
+  // A's I range r (all of A when the I bundle is not cut), B's J range c, C's block
+  auto copy_a = [&](int r) -> cudaError_t {
+    if (sp.sa == 1) return copy_span(dA, hA, A, cudaMemcpyHostToDevice, hs->h2d);
+    const PieceRange &pr = ranges[r * sp.sb];
+    return copy_piece(dA, hA, A, p->a_row.str[sp.la], p->a_row.ext[sp.la], pr.i0, pr.ni, cudaMemcpyHostToDevice,
+                      hs->h2d);
+  };
+  auto copy_b = [&](int c) -> cudaError_t {
+    if (sp.sb == 1) return copy_span(dB, hB, B, cudaMemcpyHostToDevice, hs->h2d);
+    const PieceRange &pr = ranges[c];
+    return copy_piece(dB, hB, B, p->b_col.str[sp.lb], p->b_col.ext[sp.lb], pr.j0, pr.nj, cudaMemcpyHostToDevice,
+                      hs->h2d);
+  };
+  auto copy_c = [&](double *dst, const double *src, int s, cudaMemcpyKind kind, cudaStream_t st) -> cudaError_t {
+    const PieceRange &pr = ranges[s];
+    if (sp.sa > 1 && sp.sb > 1)
+      return copy_block(dst, src, C, p->c_row.str[sp.la], p->c_row.ext[sp.la], pr.i0, pr.ni, p->c_col.str[sp.lb],
+                        p->c_col.ext[sp.lb], pr.j0, pr.nj, kind, st);
+    if (sp.sa > 1) return copy_piece(dst, src, C, p->c_row.str[sp.la], p->c_row.ext[sp.la], pr.i0, pr.ni, kind, st);
+    if (sp.sb > 1) return copy_piece(dst, src, C, p->c_col.str[sp.lb], p->c_col.ext[sp.lb], pr.j0, pr.nj, kind, st);
+    return copy_span(dst, src, C, kind, st);
+  };
+  // uploads in piece order: A's range r, B's range c (first row of the grid only), then
+  // the piece's C block and its arrival flag
+  for (int r = 0; r < sp.sa; ++r) {
+    HCU(copy_a(r), "cudaMemcpyAsync(A piece)");
+    for (int c = 0; c < sp.sb; ++c) {
+      const int s = r * sp.sb + c;
+      if (r == 0) HCU(copy_b(c), "cudaMemcpyAsync(B piece)");
       HCU(E.make(opin[s]), "cudaEventCreate");
       HCU(cudaEventRecord(opin[s], hs->h2d), "cudaEventRecord");
-      HCU(copy_piece(dC, hC, C, cb.str[sp.lab], lext, r0s[s], lens[s], cudaMemcpyHostToDevice, hs->h2d),
-          "cudaMemcpy2DAsync(C piece)");
+      HCU(copy_c(dC, hC, s, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(C piece)");
       if (int rc = c_arrived(s)) return rc;
     }
   }
@@ -411,11 +526,7 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
   // download of piece s's C once the piece finished
   auto download = [&](int s) -> int {
     HCU(cudaStreamWaitEvent(hs->d2h, done[s], 0), "cudaStreamWaitEvent");
-    if (sp.pieces == 1)
-      HCU(copy_span(hC, dC, C, cudaMemcpyDeviceToHost, hs->d2h), "cudaMemcpyAsync(C)");
-    else
-      HCU(copy_piece(hC, dC, C, cb.str[sp.lab], lext, r0s[s], lens[s], cudaMemcpyDeviceToHost, hs->d2h),
-          "cudaMemcpy2DAsync(C piece)");
+    HCU(copy_c(hC, dC, s, cudaMemcpyDeviceToHost, hs->d2h), "cudaMemcpyAsync(C piece)");
     if (trace) HCU(cudaEventRecord(tr[4 + 4 * s], hs->d2h), "cudaEventRecord");
     return STC_OK;
   };
@@ -462,7 +573,7 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
   if (trace) {
     cudaEventSynchronize(end);
     float t = 0;
-    fprintf(stderr, "[stc host] pieces=%d side=%d label=%d:", sp.pieces, sp.side, sp.lab);
+    fprintf(stderr, "[stc host] pieces=%d (I label %d x %d, J label %d x %d):", sp.pieces, sp.la, sp.sa, sp.lb, sp.sb);
     for (int s = 0; s < sp.pieces; ++s) {
       fprintf(stderr, " |%d", s);
       for (int k = 0; k < 4; ++k) {

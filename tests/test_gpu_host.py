@@ -229,3 +229,19 @@ def test_host_operands_with_negative_strides(level, variant):
     st = stc.contract(spec, ra, b, got, level, variant)
     assert st.leaf_multiplies == 7 ** level
     assert oracle.relative_error(got, ref) <= TOL
+
+
+@pytest.mark.parametrize("grid", ["2x2", "2x4", "4x2"])
+def test_host_grid_pieces_integer_exact(grid):
+    # the I x J grid of host pieces (large problems' default, forced here): each piece an
+    # independent contraction of its (I range, J range) block; integer data -> exact
+    spec = stc.parse_benchmark_line("abcijk abcefg efgijk & a:8;b:6;c:4;i:8;j:6;k:4;e:4;f:6;g:8;")
+    a, b, c0 = (_tensor(spec, l, s, True) for l, s in ((spec.labels_a, 21), (spec.labels_b, 22), (spec.labels_c, 23)))
+    ref = c0.copy()
+    oracle.contract_reference(spec, a, b, ref, threads=8)
+    for level, variant in ((1, "abc"), (2, "abc"), (2, "ab"), (2, "naive")):
+        c = _pinned(c0.copy())
+        st = _with_env({"STC_HOST_GRID": grid}, lambda: stc.contract(spec, _pinned(a), _pinned(b), c, level, variant))
+        sa, sb = (int(x) for x in grid.split("x"))
+        assert st.pieces == sa * sb and st.leaf_multiplies == 7 ** level, st
+        assert np.array_equal(c.data.numpy(), ref.data), (grid, level, variant)

@@ -98,3 +98,49 @@ def test_host_workspace_covers_two_piece_slots():
     _lib.check(L.stc_host_workspace_size(ctypes.byref(p), ctypes.byref(host)))
     assert piece.value > 49 * 256 * 1024 * 8  # the dense M slots of 49 terms
     assert 2 * piece.value <= host.value <= 2 * piece.value + 4096  # two piece slots + flags
+
+
+class _Stub:
+    """extents / strides / base of a tensor too large to allocate (problem_of reads no data)."""
+
+    def __init__(self, e):
+        self.extents, self.strides, self.base_offset, self.data = tuple(e), _row_major(e), 0, None
+
+
+def _grid(line, env=None):
+    spec = stc.parse_benchmark_line(line)
+
+    def t(labels):
+        # planning reads only extents and strides: a small stand-in for the storage
+        e = spec.tensor_extents(labels)
+        return stc.DenseTensor(e, _row_major(e), np.zeros(int(np.prod(e)) if np.prod(e) < 1 << 22 else 1)) \
+            if np.prod(e) < 1 << 22 else _Stub(e)
+
+    p = problem_of(spec, t(spec.labels_a), t(spec.labels_b), t(spec.labels_c), 2, Variant.ABC)
+    out = [ctypes.c_int32() for _ in range(4)]
+    old = {k: os.environ.get(k) for k in (env or {})}
+    os.environ.update(env or {})
+    try:
+        _lib.check(_lib.lib().stc_host_grid(ctypes.byref(p), *[ctypes.byref(x) for x in out]))
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    return spec, tuple(x.value for x in out)
+
+
+def test_large_problems_get_an_i_by_j_grid():
+    # cfg5 (24 GiB of operands): 4 x 4 pieces, the outermost label of each bundle
+    spec, (la, sa, lb, sb) = _grid("abcijk abcefg efgijk & a:32;b:32;c:32;i:32;j:32;k:32;e:32;f:32;g:32;")
+    assert (sa, sb) == (4, 4)
+    assert spec.bundle_i[la] == "a" and spec.bundle_j[lb] == "i"
+    # STC_HOST_GRID=1 keeps the 1-D cut; a forced 2 x 8 grid
+    assert _grid("abcijk abcefg efgijk & a:32;b:32;c:32;i:32;j:32;k:32;e:32;f:32;g:32;",
+                 {"STC_HOST_GRID": "1"})[1][1] * _grid(
+        "abcijk abcefg efgijk & a:32;b:32;c:32;i:32;j:32;k:32;e:32;f:32;g:32;", {"STC_HOST_GRID": "1"})[1][3] == 8
+    assert _grid("aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;", {"STC_HOST_GRID": "2x8"})[1][1::2] == (2, 8)
+    # small problems stay 1-D
+    _, (la, sa, lb, sb) = _grid("aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;")
+    assert sa * sb == 4 and min(sa, sb) == 1
