@@ -540,8 +540,12 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
                          !(getenv("STC_FUSED") && atoi(getenv("STC_FUSED")) == 0) &&
                          !(getenv("STC_PRESUM") && atoi(getenv("STC_PRESUM")) != 1) &&
                          !(pl.variant == STC_VARIANT_ABC && getenv("STC_ABC_DENSE") && atoi(getenv("STC_ABC_DENSE")) == 0);
-    if (allowed && pl.mq % BM != 0 && pl.mq % BM <= 64 && pl.nq >= 256) pl.tshape = 1;
-    else if (allowed && pl.nq % BN != 0 && pl.nq % BN <= 64 && pl.mq >= 256) pl.tshape = 2;
+    // the shape with the least padded area (128 x 128 on ties): cfg4 L2 (1138 x 788
+    // quadrants) keeps 128 x 128 (87 % useful) over 256 x 64 (84 %)
+    const int64_t a0 = rup(pl.mq, BM) * rup(pl.nq, BN), a1 = rup(pl.mq, 64) * rup(pl.nq, 256),
+                  a2 = rup(pl.mq, 256) * rup(pl.nq, 64);
+    if (allowed && pl.mq % BM != 0 && pl.mq % BM <= 64 && pl.nq >= 256 && a1 < a0) pl.tshape = 1;
+    else if (allowed && pl.nq % BN != 0 && pl.nq % BN <= 64 && pl.mq >= 256 && a2 < a0) pl.tshape = 2;
   }
   pl.tm = pl.tshape == 1 ? 64 : pl.tshape == 2 ? 256 : BM;
   pl.tn = pl.tshape == 1 ? 256 : pl.tshape == 2 ? 64 : BN;
