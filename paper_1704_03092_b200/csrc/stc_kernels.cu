@@ -203,17 +203,21 @@ __global__ void k_accumulate(const AccArgs a) {
     }
     __syncthreads();
   }
-  const int q = blockIdx.y;
+  // blockIdx.x = quadrant (fastest): the blocks of one element chunk of every quadrant
+  // run together, so an M slot's chunk -- read by each quadrant the term targets (1-4) --
+  // comes from DRAM once and from L2 after (cfg2 AB L2: 144 slot reads for 49 slots)
+  const int q = blockIdx.x;
   const int64_t total = a.mq * a.nq;
   const int64_t rs = a.row_start[q], cs = a.col_start[q];
   const int l0 = a.list_start[q], l1 = a.list_start[q + 1];
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t e = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.y * blockDim.x) {
     const int64_t i = e / a.nq, j = e - i * a.nq;
     const int64_t ro = a.pool[rs + i], co = a.pool[cs + j];
     if (ro == kPad || co == kPad) continue;
     double v = a.C[ro + co];
     const double *m = a.M + i * a.m_ld + j;
-    for (int l = l0; l < l1; ++l) v += a.list_sign[l] * __ldcs(m + (int64_t)a.list_slot[l] * a.m_stride);
+#pragma unroll 4
+    for (int l = l0; l < l1; ++l) v += a.list_sign[l] * __ldg(m + (int64_t)a.list_slot[l] * a.m_stride);
     a.C[ro + co] = v;
   }
 }
@@ -221,8 +225,8 @@ __global__ void k_accumulate(const AccArgs a) {
 cudaError_t launch_accumulate(const AccArgs &a, cudaStream_t s) {
   const int64_t total = a.mq * a.nq;
   if (total <= 0 || a.nquads <= 0) return cudaSuccess;
-  int bx = (int)std::min<int64_t>((total + 255) / 256, 4096);
-  dim3 grid(bx, a.nquads);
+  const int by = (int)std::min<int64_t>((total + 255) / 256, 65535);
+  dim3 grid(a.nquads, by);
   k_accumulate<<<grid, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
