@@ -7,6 +7,7 @@ multiples of 16) and many hit the repacked / gather paths.  Prints failures and 
 Usage: python tools/fuzz_gpu.py [cases] [seed]
 """
 
+import os
 import pathlib
 import random
 import sys
@@ -66,8 +67,11 @@ def main(cases, seed):
                    tensor(spec, spec.labels_c, gen, 0))
         ref = c + torch.einsum(f"{spec.labels_a},{spec.labels_b}->{spec.labels_c}", a, b)
         nref = torch.linalg.vector_norm(ref).item()
-        for level in (0, 1, 2):
-            for variant in ("abc", "ab", "naive"):
+        for level, variant, env in [(lv, var, env) for lv in (0, 1, 2) for var in ("abc", "ab", "naive")
+                                    for env in ({}, {"STC_PRESUM_OPS": "1"}, {"STC_PRESUM_OPS": "0"})
+                                    if not (env and (lv == 0 or var == "naive"))]:
+                os.environ.pop("STC_PRESUM_OPS", None)
+                os.environ.update(env)
                 cc = c.clone()
                 st = stc.contract(spec, a, b, cc, level, variant)
                 paths["fast" if st.fast_blocks else "slow"] += 1
@@ -75,8 +79,9 @@ def main(cases, seed):
                 worst = max(worst, err)
                 if not err <= 1e-12:
                     fails += 1
-                    print("FAIL", stc.to_benchmark_line(spec), "offset", off, "L", level, variant, err, flush=True)
-    print(f"{cases} cases x 9 runs: {fails} failures, worst rel err {worst:.3e}, staging {paths}", flush=True)
+                    print("FAIL", stc.to_benchmark_line(spec), "offset", off, "L", level, variant, env, err, flush=True)
+    os.environ.pop("STC_PRESUM_OPS", None)
+    print(f"{cases} cases x 13 runs: {fails} failures, worst rel err {worst:.3e}, staging {paths}", flush=True)
     return fails
 
 
