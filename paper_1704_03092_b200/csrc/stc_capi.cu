@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -383,7 +384,7 @@ struct Plan {
   int max_ops = 1;  // most views on one side of any term (2^L)
   size_t off_kbs = 0, off_coords = 0, off_mscr = 0, off_pka = 0, off_pkb = 0;
   bool need_pack = false;  // fused kernel on repacked operands (layout not box-regular)
-  int tshape = 0;          // fused kernel CTA tile shape (stc_fused.cu Shape): 0 128 x 128, 1 64 x 256, 2 256 x 64
+  int tshape = 0;          // fused kernel CTA tile shape (stc_fused.cu Shape): 0 128 x 128, 1 64 x 256, 2 256 x 64, 3 64 x 128
   int64_t tm = BM, tn = BN;  // its tile rows / columns (quadrants padded to them)
   // ABC with C updated straight from the kernel, ticket-ordered per C tile; false for AB,
   // Naive and the dense-M ABC mode (many terms in flight per tile: dense M slots, then one
@@ -546,9 +547,16 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
                   a2 = rup(pl.mq, 256) * rup(pl.nq, 64);
     if (allowed && pl.mq % BM != 0 && pl.mq % BM <= 64 && pl.nq >= 256 && a1 < a0) pl.tshape = 1;
     else if (allowed && pl.nq % BN != 0 && pl.nq % BN <= 64 && pl.mq >= 256 && a2 < a0) pl.tshape = 2;
+    // shape 3 (64 x 128 with 4 consumer warps): when the items of the chosen shape do not
+    // fill the grid and shape 3's, of half the work each, still do (one wave): the call
+    // takes about one item's time either way (cfg1 L1: 105 items instead of 70)
+    const int64_t T = (int64_t)std::pow(7.0, pl.level), grid = grid_hint > 0 ? grid_hint : 148;
+    const int64_t tm0 = pl.tshape == 1 ? 64 : pl.tshape == 2 ? 256 : BM, tn0 = pl.tshape == 1 ? 256 : pl.tshape == 2 ? 64 : BN;
+    const int64_t p_cur = cdiv(pl.mq, tm0) * cdiv(pl.nq, tn0), p3 = cdiv(pl.mq, 64) * cdiv(pl.nq, 128);
+    if (allowed && T > 1 && T * p_cur < grid && T * p3 <= grid && grid >= 4 * p3) pl.tshape = 3;
   }
-  pl.tm = pl.tshape == 1 ? 64 : pl.tshape == 2 ? 256 : BM;
-  pl.tn = pl.tshape == 1 ? 256 : pl.tshape == 2 ? 64 : BN;
+  pl.tm = pl.tshape == 1 || pl.tshape == 3 ? 64 : pl.tshape == 2 ? 256 : BM;
+  pl.tn = pl.tshape == 1 ? 256 : pl.tshape == 2 ? 64 : pl.tshape == 3 ? 128 : BN;
   pl.mq_pad = rup(pl.mq, pl.tm);
   pl.nq_pad = rup(pl.nq, pl.tn);
   pl.kq_pad = rup(pl.kq, BK);
@@ -576,7 +584,7 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     if (!plan_fused(p, pl, direct_sides(p, pl), nullptr, nullptr, nullptr, gd, md, jd) && !presum_wanted(p, pl)) {
       pl.tshape = 0;
       pl.tm = BM;
-      pl.tn = BN;
+      pl.tn = BN;  // (the dense / ticketed choice below sees the 128 x 128 tiles)
       pl.mq_pad = rup(pl.mq, BM);
       pl.nq_pad = rup(pl.nq, BN);
     }

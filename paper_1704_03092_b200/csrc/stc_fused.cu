@@ -39,10 +39,14 @@ constexpr int VIEW_DOUBLES = BM * FK;        // one raw view of one chunk (BM ==
 // 256 x 64 for quadrants that are 64 wide in I or J (cfg3 at m or n = 256, L2), whose
 // 128-wide tiles would be half padding.  Shapes 1 and 2 run with dense M output and
 // the summing warpgroup only.  A views hold BMT x 8, B views BNT x 8 doubles.
+// 3: 64 x 128 with 4 of the 8 consumer warps (the others idle) -- for problems whose
+// items do not fill the 148 SMs (cfg1 L1: 105 items of half the work instead of 70),
+// dense M output.
 template <int TS>
 struct Shape {
-  static constexpr int WM = TS == 1 ? 1 : TS == 2 ? 4 : 2;
-  static constexpr int WN = CONSUMER_WARPS / WM;
+  static constexpr int WM = TS == 1 || TS == 3 ? 1 : TS == 2 ? 4 : 2;
+  static constexpr int WN = TS == 3 ? 4 : CONSUMER_WARPS / WM;
+  static constexpr int ACTIVE = WM * WN;  // consumer warps with a warp tile
   static constexpr int BMT = 64 * WM, BNT = 32 * WN;
   static constexpr int AV = BMT * FK, BV = BNT * FK;
 };
@@ -134,8 +138,8 @@ int fused_stages_red(size_t sd) {
 
 // Doubles per stage for terms of at most max_ops views per side, tile shape ts.
 size_t fused_stage_doubles(int max_ops, int ts) {
-  const int av = ts == 1 ? Shape<1>::AV : ts == 2 ? Shape<2>::AV : Shape<0>::AV;
-  const int bv = ts == 1 ? Shape<1>::BV : ts == 2 ? Shape<2>::BV : Shape<0>::BV;
+  const int av = ts == 1 ? Shape<1>::AV : ts == 2 ? Shape<2>::AV : ts == 3 ? Shape<3>::AV : Shape<0>::AV;
+  const int bv = ts == 1 ? Shape<1>::BV : ts == 2 ? Shape<2>::BV : ts == 3 ? Shape<3>::BV : Shape<0>::BV;
   return (size_t)max_ops * (av + bv);
 }
 
@@ -856,8 +860,10 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
     // default; with warp_map = 1 in wm, so the warps left when the wm = 1 row half of
     // a tile is padding (skip_item) still cover all four sub-partitions
     // shapes 1 / 2: warp = wn (WM = 1) or wm + 4 wn (WM = 4): all sub-partitions busy either way
-    const int wm = TS == 1 ? 0 : TS == 2 ? warp & 3 : p.warp_map ? warp >> 2 : warp & 1;
-    const int wn = TS == 1 ? warp : TS == 2 ? warp >> 2 : p.warp_map ? warp & 3 : warp >> 1;
+    // shape 3: warps 0-3 = wn, one per sub-partition; warps 4-7 idle (idle_warp)
+    const int wm = TS == 1 || TS == 3 ? 0 : TS == 2 ? warp & 3 : p.warp_map ? warp >> 2 : warp & 1;
+    const int wn = TS == 1 || TS == 3 ? (warp & 7) : TS == 2 ? warp >> 2 : p.warp_map ? warp & 3 : warp >> 1;
+    const bool idle_warp = warp >= SH::ACTIVE;
     // Fragment offsets inside a view: A (kk, h) + 128 * mt; B (kk, nt & 1) + 128 * (nt >> 1).
     // MMA row (column) g + 8 h of each 16-row block (16-column pair) reads tile row
     // (column) frag_perm(kind, g, h) (stc_common.cuh): with it every half-warp of a
@@ -901,7 +907,7 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
         for (int j = 0; j < 4; ++j)
 #pragma unroll
           for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
-      const bool pad_tile = (p.rows_valid > 0 && ti * SH::BMT + wm * 64 >= p.rows_valid) ||
+      const bool pad_tile = idle_warp || (p.rows_valid > 0 && ti * SH::BMT + wm * 64 >= p.rows_valid) ||
                             (p.cols_valid > 0 && tj * SH::BNT + wn * 32 >= p.cols_valid);
       if (pad_tile) {
         skip_item(S, cfull, empty, stage, phase, kchunks, lane);
@@ -999,8 +1005,8 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
         }
         continue;
       }
-      if constexpr (TS != 0) {  // shapes 1, 2: dense M output only
-        epilogue_store<AKF + 1, BKF + 1, 2, SH::BMT, SH::BNT>(p, acc, item, tid, wm, wn, g, tig);
+      if constexpr (TS != 0) {  // shapes 1-3: dense M output only
+        if (!idle_warp) epilogue_store<AKF + 1, BKF + 1, 2, SH::BMT, SH::BNT>(p, acc, item, tid, wm, wn, g, tig);
       } else {
         if (!p.dense_out) wait_c_ready(p, tid, c_seen);
         if (red)
@@ -1022,11 +1028,12 @@ static FusedKernel fused_for_ts(int akf, int bkf) {
 }
 
 static FusedKernel fused_for(int akf, int bkf, bool ps, int ts, bool one) {
-  if (ps) return ts == 1 ? fused_for_ts<true, 1>(akf, bkf) : ts == 2 ? fused_for_ts<true, 2>(akf, bkf)
-                                                             : fused_for_ts<true, 0>(akf, bkf);
+  if (ps)
+    return ts == 1 ? fused_for_ts<true, 1>(akf, bkf) : ts == 2 ? fused_for_ts<true, 2>(akf, bkf)
+           : ts == 3 ? fused_for_ts<true, 3>(akf, bkf) : fused_for_ts<true, 0>(akf, bkf);
   if (one)
     return ts == 1 ? fused_for_ts<false, 1, true>(akf, bkf) : ts == 2 ? fused_for_ts<false, 2, true>(akf, bkf)
-                                                                : fused_for_ts<false, 0, true>(akf, bkf);
+           : ts == 3 ? fused_for_ts<false, 3, true>(akf, bkf) : fused_for_ts<false, 0, true>(akf, bkf);
   return fused_for_ts<false, 0>(akf, bkf);
 }
 
