@@ -26,8 +26,9 @@ for r in rows[2:]:
                 f = float(v.replace(",", ""))
                 if u in ("byte", "Kbyte", "Mbyte", "Gbyte"):
                     f *= {"byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0}[u]
-                elif u in ("nsecond", "usecond", "msecond", "second"):
-                    f *= {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}[u]
+                elif u in ("nsecond", "usecond", "msecond", "second", "ns", "us", "ms", "s"):
+                    f *= {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3, "ns": 1e-6, "us": 1e-3,
+                          "ms": 1.0, "s": 1e3}[u]
                 cells.append(f"{f:.3f}")
             except ValueError:
                 cells.append(v)
