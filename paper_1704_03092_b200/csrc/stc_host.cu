@@ -61,7 +61,7 @@ int herr(int code, const char *fmt, ...) {
 
 constexpr int64_t kMinRunBytes = 4096;          // shortest copy run worth splitting for
 constexpr int64_t kMinSplitBytes = 32ll << 20;  // smaller problems: one piece
-constexpr int kMaxPieces = 16;
+constexpr int kMaxPieces = 32;
 constexpr size_t kFlagBytes = 256;  // per-piece "C piece arrived" flags, after the piece workspaces
 
 // Page-locked constants the flags are copied from: kMaxPieces zeros, then kMaxPieces ones.
