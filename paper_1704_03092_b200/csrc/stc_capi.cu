@@ -480,7 +480,7 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
 // Pre-summed operands for ABC / AB at L = 1, 2 (STC_PRESUM_OPS = 0 / 1 forces it off /
 // on).  The sums cost one HBM pass per side (4^L quadrant reads + 7^L slot writes per
 // element position) and take every DADD off the FP64 pipe the DMMAs use: the fused
-// kernel's in-SM sums cost it about 5 % (L1) / 18 % (L2) of its DMMA time (cfg2, 16384^3,
+// kernel's in-SM sums cost it 4-10 % (L1; 10 % with A k-contiguous) / 18 % (L2) of its DMMA time (cfg2, 16384^3,
 // cfg5; tools/presum_sweep.py).  Operands whose views are not TMA boxes are repacked
 // anyway (one read + one write of every quadrant), which the presum pass replaces.
 // Cost model at 5 TB/s and 33 TF/s executed.
@@ -499,7 +499,7 @@ bool presum_wanted(const stc_problem *p, const Plan &pl) {
   const bool direct = plan_fused(p, pl, direct_sides(p, pl), nullptr, nullptr, nullptr, g, maps, jobs);
   const double t_repack = direct ? 0.0 : 8.0 * 2.0 * quads * (qa + qb) / 3e12;  // gathers: ~50 % of HBM
   const double t_gemm = T * 2.0 * (double)pl.mq_pad * pl.nq_pad * pl.kq_pad / 33e12;
-  const double penalty = pl.level == 1 ? 0.05 : 0.18;
+  const double penalty = pl.level == 1 ? 0.10 : 0.18;
   return t_presum < penalty * t_gemm + t_repack;
 }
 
