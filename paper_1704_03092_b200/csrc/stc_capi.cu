@@ -312,16 +312,62 @@ bool same_extents(const stc_bundle &x, const stc_bundle &y) {
 // region in its workspace and copies it here; later calls restore it with one kernel
 // (k_restore) instead of the 5-10 small launches that build it.  Shared by the copies
 // of a cached plan; freed with the last one.
+//
+// Small problems also keep executable CUDA graphs of their launch sequence (restore,
+// operand sums, DMMA kernel, accumulate), keyed by the operand / workspace pointers:
+// a repeated call replays one graph instead of re-deriving and issuing 4+ launches
+// (the host work would otherwise exceed the device time of a 576^3 contraction).
+struct GraphKey {
+  const void *a, *b, *c, *ws;
+  int dev;
+  int mode;  // the operand mode the pointers imply (its snapshot orders the replays)
+  bool operator==(const GraphKey &o) const {
+    return a == o.a && b == o.b && c == o.c && ws == o.ws && dev == o.dev;
+  }
+};
 struct Resident {
   std::mutex mu;
   void *buf[2] = {nullptr, nullptr};
   cudaEvent_t ev[2] = {nullptr, nullptr};
   int dev[2] = {-1, -1};
+  static constexpr size_t kGraphs = 8;
+  struct Graph {
+    GraphKey key;
+    cudaGraphExec_t exec;
+    stc_stats st;
+  };
+  std::vector<Graph> graphs;
+  size_t graph_next = 0;
   ~Resident() {
+    for (Graph &g : graphs) cudaGraphExecDestroy(g.exec);
     for (int i = 0; i < 2; ++i) {
       if (buf[i]) cudaFree(buf[i]);
       if (ev[i]) cudaEventDestroy(ev[i]);
     }
+  }
+  // Launch the graph of `key` on s; false if there is none (or the launch failed).
+  bool replay(const GraphKey &key, cudaStream_t s, stc_stats &st) {
+    std::lock_guard<std::mutex> lk(mu);
+    for (const Graph &g : graphs)
+      if (g.key == key) {
+        if (cudaStreamWaitEvent(s, ev[g.key.mode], 0) != cudaSuccess || cudaGraphLaunch(g.exec, s) != cudaSuccess) {
+          cudaGetLastError();
+          return false;
+        }
+        st = g.st;
+        return true;
+      }
+    return false;
+  }
+  void keep(const GraphKey &key, cudaGraphExec_t exec, const stc_stats &st) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (graphs.size() < kGraphs) {
+      graphs.push_back({key, exec, st});
+      return;
+    }
+    cudaGraphExecDestroy(graphs[graph_next].exec);  // freed once its pending launches ran
+    graphs[graph_next] = {key, exec, st};
+    graph_next = (graph_next + 1) % kGraphs;
   }
   // The snapshot of `mode` on device d, ordered before the work next enqueued on s; null if none.
   const void *ready(int mode, int d, cudaStream_t s) {
@@ -547,13 +593,17 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
                   a2 = rup(pl.mq, 256) * rup(pl.nq, 64);
     if (allowed && pl.mq % BM != 0 && pl.mq % BM <= 64 && pl.nq >= 256 && a1 < a0) pl.tshape = 1;
     else if (allowed && pl.nq % BN != 0 && pl.nq % BN <= 64 && pl.mq >= 256 && a2 < a0) pl.tshape = 2;
-    // shape 3 (64 x 128 with 4 consumer warps): when the items of the chosen shape do not
-    // fill the grid and shape 3's, of half the work each, still do (one wave): the call
-    // takes about one item's time either way (cfg1 L1: 105 items instead of 70)
+    // shape 3 (64 x 128, 32 x 32 warp tiles): for problems of a few waves, when its
+    // waves x tile area -- the per-SM work in sequence -- is clearly below the chosen
+    // shape's (cfg1 L1: 105 items in one wave instead of 70; L2: 294 items in two waves
+    // instead of 196 in two of twice the work).  Dense M output (grid >= 4 tiles per term).
     const int64_t T = (int64_t)std::pow(7.0, pl.level), grid = grid_hint > 0 ? grid_hint : 148;
     const int64_t tm0 = pl.tshape == 1 ? 64 : pl.tshape == 2 ? 256 : BM, tn0 = pl.tshape == 1 ? 256 : pl.tshape == 2 ? 64 : BN;
     const int64_t p_cur = cdiv(pl.mq, tm0) * cdiv(pl.nq, tn0), p3 = cdiv(pl.mq, 64) * cdiv(pl.nq, 128);
-    if (allowed && T > 1 && T * p_cur < grid && T * p3 <= grid && grid >= 4 * p3) pl.tshape = 3;
+    const int64_t waves_cur = cdiv(T * p_cur, grid), waves3 = cdiv(T * p3, grid);
+    if (allowed && T > 1 && grid >= 4 * p3 && waves_cur <= 4 &&
+        (double)waves3 * 64 * 128 < 0.85 * (double)waves_cur * tm0 * tn0)
+      pl.tshape = 3;
   }
   pl.tm = pl.tshape == 1 || pl.tshape == 3 ? 64 : pl.tshape == 2 ? 256 : BM;
   pl.tn = pl.tshape == 1 ? 256 : pl.tshape == 2 ? 64 : pl.tshape == 3 ? 128 : BN;
@@ -1380,7 +1430,7 @@ struct PlanEntry {
   stc_problem prob;
   int grid;
   std::string env;
-  Plan plan;
+  std::shared_ptr<const Plan> plan;  // shared with the calls using it (no per-call copy)
 };
 std::mutex g_plan_mu;
 std::vector<PlanEntry> g_plans;
@@ -1400,20 +1450,22 @@ std::string plan_env() {
   return key;
 }
 
-int cached_plan(const stc_problem *p, Plan &pl, int grid_hint) {
+int cached_plan(const stc_problem *p, std::shared_ptr<const Plan> &out, int grid_hint) {
   if (!p) return fail(STC_EINVAL, "null problem");
   const std::string env = plan_env();
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     for (const PlanEntry &e : g_plans)
       if (e.grid == grid_hint && e.env == env && memcmp(&e.prob, p, sizeof(stc_problem)) == 0) {
-        pl = e.plan;
+        out = e.plan;
         return STC_OK;
       }
   }
-  if (int rc = build_plan(p, pl, grid_hint)) return rc;
+  auto pl = std::make_shared<Plan>();
+  if (int rc = build_plan(p, *pl, grid_hint)) return rc;
+  out = pl;
   std::lock_guard<std::mutex> lk(g_plan_mu);
-  PlanEntry e{*p, grid_hint, env, pl};
+  PlanEntry e{*p, grid_hint, env, out};
   if (g_plans.size() < kPlanCache) {
     g_plans.push_back(std::move(e));
   } else {
@@ -1434,10 +1486,10 @@ int set_error(int code, const char *msg) {
 // Whether stc_contract runs the problem ticketed (ABC, C updated by the kernel)
 // rather than through dense M slots and an accumulate kernel (stc_host.cu).
 bool plan_ticketed(const stc_problem *p) {
-  Plan pl;
+  std::shared_ptr<const Plan> pl;
   const int sms = gemm_max_grid(MAX_OPS);
   if (cached_plan(p, pl, sms > 0 ? sms : 0)) return false;
-  return pl.ticketed;
+  return pl->ticketed;
 }
 
 }  // namespace stc
@@ -1460,68 +1512,45 @@ int stc_set_c_ready(const int32_t *c_ready) {
 }
 
 int stc_workspace_size(const stc_problem *p, size_t *bytes) {
-  Plan pl;
+  std::shared_ptr<const Plan> pl;
   const int sms = gemm_max_grid(MAX_OPS);  // per-CTA scratch is sized by the launch grid (0 without a device)
   if (int rc = cached_plan(p, pl, sms > 0 ? sms : 0)) return rc;
-  if (bytes) *bytes = pl.total;
+  if (bytes) *bytes = pl->total;
   return STC_OK;
 }
 
-int stc_contract(const stc_problem *p, const double *A, const double *B, double *C, void *workspace,
-                 size_t workspace_bytes, void *stream, stc_stats *stats) {
-  Plan pl;
-  const int grid_hint = gemm_max_grid(MAX_OPS);
-  if (grid_hint <= 0) return fail(STC_ECUDA, "could not size the DMMA grid");
-  if (int rc = cached_plan(p, pl, grid_hint)) return rc;
-  if (!A || !B || !C) return fail(STC_EINVAL, "null operand pointer");
-  if (!workspace || workspace_bytes < pl.total)
-    return fail(STC_EWORKSPACE, "workspace too small: need %zu bytes, got %zu", pl.total, workspace_bytes);
-  if (reinterpret_cast<uintptr_t>(workspace) & 255) return fail(STC_EINVAL, "workspace must be 256-byte aligned");
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  char *ws = reinterpret_cast<char *>(workspace);
-  int64_t *pool = reinterpret_cast<int64_t *>(ws + pl.off_pool);
-  int64_t *pool2 = reinterpret_cast<int64_t *>(ws + pl.off_pool2);  // the original vectors (repacking)
-  int64_t *kbs = reinterpret_cast<int64_t *>(ws + pl.off_kbs);
+// The launch sequence of one contraction on stream s (stc_contract: checks, operand
+// mode, snapshot and graph handling).  `snap`: the plan's snapshot of the constant
+// workspace region for this operand mode, already ordered before s (null: build it).
+static int contract_run(const stc_problem *p, const Plan &pl, const double *A, const double *B, double *C, char *ws,
+                 cudaStream_t s, const int32_t *c_ready, cudaEvent_t ev_before, cudaEvent_t ev_after, bool direct,
+                 bool packed, int mode, int dev, const void *snap, stc_stats *stats) {
+  // The constant region is read where it lives: in the plan's snapshot once there is
+  // one (nothing to restore), else in the workspace, where this call builds it.  Only
+  // the tickets and work counters at its end are per call (zeroed in the workspace).
+  char *cw = snap ? const_cast<char *>(static_cast<const char *>(snap)) : ws;
+  int64_t *pool = reinterpret_cast<int64_t *>(cw + pl.off_pool);
+  int64_t *pool2 = reinterpret_cast<int64_t *>(cw + pl.off_pool2);  // the original vectors (repacking)
+  int64_t *kbs = reinterpret_cast<int64_t *>(cw + pl.off_kbs);
   int32_t *tickets = reinterpret_cast<int32_t *>(ws + pl.off_tickets);
   int32_t *counters = reinterpret_cast<int32_t *>(ws + pl.off_counters);
-  int4 *coords = reinterpret_cast<int4 *>(ws + pl.off_coords);
+  int4 *coords = reinterpret_cast<int4 *>(cw + pl.off_coords);
   int64_t launches = 0;
   bool tma = false;  // operand units staged by tensor-map box loads
   stc_stats st{};
   g_stage_launches = 0;
-  const int32_t *c_ready = g_c_ready;  // consumed by this call
-  g_c_ready = nullptr;
   const int tiles_m = (int)(pl.mq_pad / pl.tm), tiles_n = (int)(pl.nq_pad / pl.tn);
   const int64_t P = (int64_t)tiles_m * tiles_n;
   const int T = (int)pl.terms.size();
-
-  // Operand mode: per-term slots (Naive, pre-summed), the operands' own TMA views, or
-  // their repacked quadrant blocks (one gather pass per operand, pure copies).
   const bool slots = pl.variant == STC_VARIANT_NAIVE || pl.presum;
-  bool direct = false;
-  if (!slots) {
-    GemmArgs gt{};
-    CUtensorMap mt[3];
-    CoordJobs jt{};
-    direct = plan_fused(p, pl, direct_sides(p, pl), A, B, pl.ticketed ? C : nullptr, gt, mt, jt);
-  }
-  const bool packed = !slots && !direct && pl.need_pack;
-
-  // The constant region of the workspace -- scatter vectors, chunk strides, map
-  // coordinates, term / op / target tables, accumulate lists, zeroed tickets and
-  // counters -- depends only on the plan (and the operand mode): the first call of a
-  // plan builds it and keeps a device snapshot; later calls restore it with one
-  // kernel instead of 5-10 small launches (Resident).
-  const int mode = packed ? 1 : 0;
-  int dev = 0;
-  CU(cudaGetDevice(&dev), "cudaGetDevice");
   Resident *res = pl.res.get();
-  const void *snap = res ? res->ready(mode, dev, s) : nullptr;
   const bool restored = snap != nullptr;
-  if (restored) {
-    CU(launch_restore(snap, ws, pl.off_const, s), "k_restore");
-    ++launches;
-  } else {
+  // per call: zero the tickets and counters (by the first k_presum launch when there is one)
+  int32_t *const zero = restored ? tickets : nullptr;
+  const int64_t zero_words = (int64_t)((pl.off_const - pl.off_tickets) / 4);
+  if (restored && !pl.presum) {
+    CU(cudaMemsetAsync(ws + pl.off_tickets, 0, pl.off_const - pl.off_tickets, s), "zero tickets");
+  } else if (!restored) {
     if (int rc = upload(pl.vecs.data(), pl.vecs.size() * sizeof(VecDesc), ws + pl.off_vecs, s, ws + pl.off_tickets,
                         pl.off_const - pl.off_tickets))
       return rc;
@@ -1600,7 +1629,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
   g.tickets = tickets;
 
   if (pl.ticketed) {
-    char *tab = ws + pl.off_tab;
+    char *tab = cw + pl.off_tab;
     std::vector<char> host(pl.tab_bytes);
     size_t o = 0;
     memcpy(host.data() + o, pl.tdesc.data(), pl.tdesc.size() * sizeof(TermDesc));
@@ -1646,17 +1675,21 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       if (gf.cred) gf.mscratch = reinterpret_cast<double *>(ws + pl.off_mscr);
       for (int bi = 0; bi < pl.nbatches; ++bi) {
         const int t0 = bi * pl.batch, nb = std::min(T - t0, pl.batch);
-        CU(launch_presum2(presum_args(pl, 0, A, PA, pool, t0, t0 + nb), presum_args(pl, 1, B, PB, pool, t0, t0 + nb), s),
-           "k_presum");
+        PresumArgs pa = presum_args(pl, 0, A, PA, pool, t0, t0 + nb);
+        if (bi == 0 && zero) {
+          pa.zero = zero;
+          pa.zero_words = zero_words;
+        }
+        CU(launch_presum2(pa, presum_args(pl, 1, B, PB, pool, t0, t0 + nb), s), "k_presum");
         gf.terms = g.terms + t0;
         gf.nterms = nb;
         gf.total_items = (int)(P * nb);
         gf.counter = counters + bi;
-        if (g_ev_before && bi == 0) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
+        if (ev_before && bi == 0) CU(cudaEventRecord(ev_before, s), "cudaEventRecord");
         CU(launch_fused(gf, (int)std::min<int64_t>(pl.grid, gf.total_items), s, maps), "k_strassen_fused");
         launches += 2;
       }
-      if (g_ev_after) CU(cudaEventRecord(g_ev_after, s), "cudaEventRecord");
+      if (ev_after) CU(cudaEventRecord(ev_after, s), "cudaEventRecord");
       tma = true;
       st.fast_updates = gf.cred ? (int64_t)P * (int64_t)pl.tgts.size() : 0;
       st.slow_updates = gf.cred ? 0 : (int64_t)P * (int64_t)pl.tgts.size();
@@ -1675,13 +1708,13 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         const char *eo = getenv("STC_EPI_OFFLOAD");
         const int offload = (eo ? atoi(eo) : (gf.cred ? 1 : 0)) || (gf.cred && gf.cred8);
         if (offload) gf.mscratch = reinterpret_cast<double *>(ws + pl.off_mscr);
-        if (g_ev_before) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
+        if (ev_before) CU(cudaEventRecord(ev_before, s), "cudaEventRecord");
         CU(launch_fused(gf, grid, s, maps), "k_strassen_fused");
       } else {
-        if (g_ev_before) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
+        if (ev_before) CU(cudaEventRecord(ev_before, s), "cudaEventRecord");
         CU(launch_gemm(g, grid, s, tma ? maps : nullptr), "k_strassen_gemm");
       }
-      if (g_ev_after) CU(cudaEventRecord(g_ev_after, s), "cudaEventRecord");
+      if (ev_after) CU(cudaEventRecord(ev_after, s), "cudaEventRecord");
       ++launches;
       // C-tile updates: by TMA reduce-add boxes (the reference's fast store_tile path,
       // _jit.py:166-176) or by the load/add/store scatter epilogue (its slow path)
@@ -1764,7 +1797,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         cstart[q] = pl.cc + c * pl.nq_pad;
       }
       lstart[pl.nquads] = (int32_t)lslot.size();
-      char *tab = ws + pl.off_tab + (size_t)bi * pl.tab_bytes;
+      char *tab = cw + pl.off_tab + (size_t)bi * pl.tab_bytes;
       std::vector<char> host(pl.tab_bytes, 0);
       size_t o = 0;
       auto put = [&](const void *src, size_t bytes) {
@@ -1783,7 +1816,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       if (o > pl.tab_bytes) return fail(STC_EINVAL, "internal: table overflow");
       if (!restored)
         if (int rc = upload(host.data(), o, tab, s)) return rc;
-      char *acc = ws + pl.off_acc + (size_t)bi * pl.acc_bytes;
+      char *acc = cw + pl.off_acc + (size_t)bi * pl.acc_bytes;
       std::vector<char> hacc(pl.acc_bytes, 0);
       size_t ao = 0;
       auto aput = [&](const void *src, size_t bytes, size_t slot_bytes) {
@@ -1843,8 +1876,12 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
       const int nb = b.t1 - b.t0;
       if (slots && pl.presum) {
         // one pass per side: every element position's 4^L quadrant values -> the batch's sums
-        CU(launch_presum2(presum_args(pl, 0, A, PA, pool, b.t0, b.t1), presum_args(pl, 1, B, PB, pool, b.t0, b.t1), s),
-           "k_presum");
+        PresumArgs pa = presum_args(pl, 0, A, PA, pool, b.t0, b.t1);
+        if (bi == 0 && zero) {
+          pa.zero = zero;
+          pa.zero_words = zero_words;
+        }
+        CU(launch_presum2(pa, presum_args(pl, 1, B, PB, pool, b.t0, b.t1), s), "k_presum");
         ++launches;
       } else if (slots) {
         UnpackArgs ua{};
@@ -1912,7 +1949,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
           }
         }
       }
-      if (g_ev_before && bi == 0) CU(cudaEventRecord(g_ev_before, s), "cudaEventRecord");
+      if (ev_before && bi == 0) CU(cudaEventRecord(ev_before, s), "cudaEventRecord");
       if (fused_ab) {
         tma = !packed;  // TMA boxes of the operands or of their packed slots (the reference's Naive GEMM: dense, fast blocks)
         CU(launch_fused(gf, grid, s, maps_ab), "k_strassen_fused(dense)");
@@ -1920,7 +1957,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
         if (pl.tshape != 0) return fail(STC_EINVAL, "internal: tile shape %d needs the fused kernel", pl.tshape);
         CU(launch_gemm(gb, grid, s), "k_strassen_gemm(dense)");
       }
-      if (g_ev_after && bi == pl.nbatches - 1) CU(cudaEventRecord(g_ev_after, s), "cudaEventRecord");
+      if (ev_after && bi == pl.nbatches - 1) CU(cudaEventRecord(ev_after, s), "cudaEventRecord");
       CU(launch_accumulate(b.aa, s), "k_accumulate");
       launches += 2;
       st.slow_updates += b.nupd;
@@ -1935,8 +1972,109 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
   st.kernel_launches = launches + g_stage_launches;
   st.pieces = 1;
   if (stats) *stats = st;
-  g_ev_before = g_ev_after = nullptr;
   return STC_OK;
+}
+
+// Problems up to this many executed flops replay a CUDA graph of their launch
+// sequence (~0.1 ms of DMMA work: the host's per-call work is then comparable).
+constexpr double kGraphFlops = 4e9;
+
+// Per thread and device: the non-blocking stream graphs are captured on.
+static cudaStream_t capture_stream(int dev) {
+  thread_local std::vector<cudaStream_t> streams;
+  if (dev < 0) return nullptr;
+  if ((int)streams.size() <= dev) streams.resize(dev + 1, nullptr);
+  if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    streams[dev] = nullptr;
+  }
+  return streams[dev];
+}
+
+int stc_contract(const stc_problem *p, const double *A, const double *B, double *C, void *workspace,
+                 size_t workspace_bytes, void *stream, stc_stats *stats) {
+  std::shared_ptr<const Plan> plan;
+  const int grid_hint = gemm_max_grid(MAX_OPS);
+  if (grid_hint <= 0) return fail(STC_ECUDA, "could not size the DMMA grid");
+  if (int rc = cached_plan(p, plan, grid_hint)) return rc;
+  const Plan &pl = *plan;
+  if (!A || !B || !C) return fail(STC_EINVAL, "null operand pointer");
+  if (!workspace || workspace_bytes < pl.total)
+    return fail(STC_EWORKSPACE, "workspace too small: need %zu bytes, got %zu", pl.total, workspace_bytes);
+  if (reinterpret_cast<uintptr_t>(workspace) & 255) return fail(STC_EINVAL, "workspace must be 256-byte aligned");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char *ws = reinterpret_cast<char *>(workspace);
+  const int32_t *c_ready = g_c_ready;  // consumed by this call, like the kernel events
+  g_c_ready = nullptr;
+  cudaEvent_t ev_before = g_ev_before, ev_after = g_ev_after;
+  g_ev_before = g_ev_after = nullptr;
+  int dev = 0;
+  CU(cudaGetDevice(&dev), "cudaGetDevice");
+  Resident *res = pl.res.get();
+
+  // Small problems: replay the graph captured for these pointers (the operand mode
+  // below is a function of the plan and the pointers, so the key implies it).
+  const double flops = 2.0 * (double)pl.tm * (double)pl.tn * (double)pl.kq_pad *
+                       (double)((pl.mq_pad / pl.tm) * (pl.nq_pad / pl.tn)) * (double)pl.terms.size();
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  const bool graphs = res && !ev_before && !ev_after && !c_ready && flops <= kGraphFlops && !getenv("STC_NO_GRAPH") &&
+                      !getenv("STC_NO_SNAPSHOT") && cudaStreamIsCapturing(s, &cap) == cudaSuccess &&
+                      cap == cudaStreamCaptureStatusNone;
+  const GraphKey key{A, B, C, ws, dev, 0};
+  if (graphs) {
+    stc_stats gst{};
+    if (res->replay(key, s, gst)) {
+      if (stats) *stats = gst;
+      return STC_OK;
+    }
+  }
+
+  // Operand mode: per-term slots (Naive, pre-summed), the operands' own TMA views, or
+  // their repacked quadrant blocks (one gather pass per operand, pure copies).
+  const bool slots = pl.variant == STC_VARIANT_NAIVE || pl.presum;
+  bool direct = false;
+  if (!slots) {
+    GemmArgs gt{};
+    CUtensorMap mt[3];
+    CoordJobs jt{};
+    direct = plan_fused(p, pl, direct_sides(p, pl), A, B, pl.ticketed ? C : nullptr, gt, mt, jt);
+  }
+  const bool packed = !slots && !direct && pl.need_pack;
+
+  // The constant region of the workspace -- scatter vectors, chunk strides, map
+  // coordinates, term / op / target tables, accumulate lists, zeroed tickets and
+  // counters -- depends only on the plan (and the operand mode): the first call of a
+  // plan builds it and keeps a device snapshot; later calls restore it with one
+  // kernel instead of 5-10 small launches (Resident).
+  const int mode = packed ? 1 : 0;
+  const void *snap = res ? res->ready(mode, dev, s) : nullptr;
+  // the graph is captured on a private stream (the caller's may be the legacy default
+  // stream, which cannot capture) and launched on the caller's
+  cudaStream_t cs = capture_stream(dev);
+  if (graphs && snap && cs && cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+    stc_stats st{};
+    const int rc = contract_run(p, pl, A, B, C, ws, cs, nullptr, nullptr, nullptr, direct, packed, mode, dev, snap, &st);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
+    cudaGraphExec_t exec = nullptr;
+    const bool ok = rc == STC_OK && ec == cudaSuccess && graph &&
+                    cudaGraphInstantiateWithFlags(&exec, graph, 0) == cudaSuccess;
+    if (graph) cudaGraphDestroy(graph);
+    if (ok) {
+      if (cudaGraphLaunch(exec, s) != cudaSuccess) {
+        cudaGraphExecDestroy(exec);
+        return cuda_fail(cudaGetLastError(), "cudaGraphLaunch");
+      }
+      GraphKey k = key;
+      k.mode = mode;
+      res->keep(k, exec, st);
+      if (stats) *stats = st;
+      return STC_OK;
+    }
+    cudaGetLastError();  // nothing ran: fall through to direct launches
+    if (rc != STC_OK && ec == cudaSuccess) return rc;
+  }
+  return contract_run(p, pl, A, B, C, ws, s, c_ready, ev_before, ev_after, direct, packed, mode, dev, snap, stats);
 }
 
 int stc_bundle_scatter(const stc_bundle *bundle, int64_t base, int64_t out_len, int64_t *out, void *stream) {
@@ -2160,9 +2298,10 @@ int stc_fill_uniform(double *out, int ndim, const int64_t *extents, const int64_
 
 int stc_plan_describe(const stc_problem *p, int grid, stc_plan_info *info) {
   if (!info) return fail(STC_EINVAL, "null info");
-  Plan pl;
+  std::shared_ptr<const Plan> plan;
   if (grid <= 0) grid = 148;
-  if (int rc = cached_plan(p, pl, grid)) return rc;
+  if (int rc = cached_plan(p, plan, grid)) return rc;
+  const Plan &pl = *plan;
   memset(info, 0, sizeof(*info));
   info->ticketed = pl.ticketed;
   info->presum = pl.presum;

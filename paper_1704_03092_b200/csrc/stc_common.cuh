@@ -64,18 +64,19 @@ __device__ __forceinline__ int epi_col(int nt, int tig) {  // first of the pair 
   return 16 * (nt >> 1) + frag_perm(PB, 2 * tig, nt & 1);
 }
 
-template <int PA = 0, int PB = 0, int RB = 1, int TBM = BM, int TBN = BN>
+// MT: m16 blocks per warp tile (4: 64 x 32; 2: 32 x 32, dense M output only)
+template <int PA = 0, int PB = 0, int RB = 1, int TBM = BM, int TBN = BN, int MT = 4>
 __device__ __forceinline__ void epilogue_store(const GemmArgs &p, const double (&acc)[4][4][4], int item, int tid,
                                                int wm, int wn, int g, int tig) {
   int slot, ti, tj, pos;
   tile_of(p, item, slot, ti, tj, pos);
   const TermDesc td = p.terms[slot];
-  const int row0 = ti * TBM + wm * 64;
+  const int row0 = ti * TBM + wm * 16 * MT;
   const int col0 = tj * TBN + wn * 32;
   if (p.dense_out) {
     double *Mt = p.M + (int64_t)td.m_slot * p.m_stride;
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
@@ -86,6 +87,7 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs &p, const double (
         }
     return;
   }
+  if constexpr (MT != 4) return;  // 32-row warp tiles run with dense M output only
   for (int j = 0; j < td.c_count; ++j) {
     const TgtDesc tg = p.tgts[td.c_first + j];
     int32_t *ticket = p.tickets + tg.ticket_base + pos;

@@ -39,15 +39,17 @@ constexpr int VIEW_DOUBLES = BM * FK;        // one raw view of one chunk (BM ==
 // 256 x 64 for quadrants that are 64 wide in I or J (cfg3 at m or n = 256, L2), whose
 // 128-wide tiles would be half padding.  Shapes 1 and 2 run with dense M output and
 // the summing warpgroup only.  A views hold BMT x 8, B views BNT x 8 doubles.
-// 3: 64 x 128 with 4 of the 8 consumer warps (the others idle) -- for problems whose
-// items do not fill the 148 SMs (cfg1 L1: 105 items of half the work instead of 70),
-// dense M output.
+// 3: 64 x 128 on the 8 consumer warps with 32 x 32 warp tiles (MT = 2 m16 blocks) --
+// for problems whose items do not fill the 148 SMs (cfg1 L1: 105 items of half the
+// work instead of 70), dense M output.  Every element still accumulates the same
+// DMMA k-steps in the same order: bitwise the 128 x 128 result.
 template <int TS>
 struct Shape {
-  static constexpr int WM = TS == 1 || TS == 3 ? 1 : TS == 2 ? 4 : 2;
-  static constexpr int WN = TS == 3 ? 4 : CONSUMER_WARPS / WM;
+  static constexpr int MT = TS == 3 ? 2 : 4;  // m16 blocks per warp tile (16 MT rows x 32 columns)
+  static constexpr int WM = TS == 1 ? 1 : TS == 2 ? 4 : 2;
+  static constexpr int WN = CONSUMER_WARPS / WM;
   static constexpr int ACTIVE = WM * WN;  // consumer warps with a warp tile
-  static constexpr int BMT = 64 * WM, BNT = 32 * WN;
+  static constexpr int BMT = 16 * MT * WM, BNT = 32 * WN;
   static constexpr int AV = BMT * FK, BV = BNT * FK;
 };
 constexpr int FUSED_PRODUCER_WARPS = 4;  // one warpgroup (setmaxnreg is warpgroup-wide); warp 0 of it issues
@@ -232,7 +234,8 @@ __device__ __forceinline__ void side_sum(double (&out)[I], const double *st, int
 // DADD of the signed value otherwise -- the reference's view order), then issue
 // MMA group V of the current k-step.  Loads go in groups of four values to keep
 // the register footprint inside the consumers' budget.
-template <int NA, int NB, int V, int KN, bool MMA, bool SGN = true, int AV = VIEW_DOUBLES, int BV = VIEW_DOUBLES>
+template <int NA, int NB, int V, int KN, bool MMA, bool SGN = true, int AV = VIEW_DOUBLES, int BV = VIEW_DOUBLES,
+          int MT = 4>
 __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (&fa)[8], const double (&fb)[4],
                                           double (&xa)[8], double (&xb)[4], const double *nst, bool load,
                                           const int (&offA)[2][2], const int (&offB)[2][2], uint32_t negmask,
@@ -249,7 +252,7 @@ __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (
   if (load) {
     if constexpr (V < NA) {
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {  // mt pairs {0, 1}, {2, 3}
+      for (int hh = 0; hh < MT / 2; ++hh) {  // mt pairs {0, 1}, {2, 3}
         double t[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) t[j] = (j & 1 ? pa1 : pa0)[128 * (2 * hh + (j >> 1))];  // immediate offsets
@@ -299,11 +302,11 @@ __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (
   }
   if constexpr (MMA) {
 #pragma unroll
-    for (int i = 16 * V / G; i < 16 * (V + 1) / G; ++i)
+    for (int i = 4 * MT * V / G; i < 4 * MT * (V + 1) / G; ++i)
       dmma_16x8x4(acc[i >> 2][i & 3], fa[2 * (i >> 2)], fa[2 * (i >> 2) + 1], fb[i & 3]);
   }
   if constexpr (V + 1 < G)
-    pipe_view<NA, NB, V + 1, KN, MMA, SGN, AV, BV>(acc, fa, fb, xa, xb, nst, load, offA, offB, negmask, bbase);
+    pipe_view<NA, NB, V + 1, KN, MMA, SGN, AV, BV, MT>(acc, fa, fb, xa, xb, nst, load, offA, offB, negmask, bbase);
 }
 
 // One work item's main loop for terms with NA A-views and NB B-views
@@ -313,7 +316,7 @@ __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (
 // k-step are built one view per group, so no DADD waits on a result it needs
 // right away behind the DMMAs queued on the shared FP64 pipe.  A chunk stage
 // is released as soon as both of its k-steps are in registers.
-template <int NA, int NB, bool SGN = true, int AV = VIEW_DOUBLES, int BV = VIEW_DOUBLES>
+template <int NA, int NB, bool SGN = true, int AV = VIEW_DOUBLES, int BV = VIEW_DOUBLES, int MT = 4>
 __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const double *stages, int sstride, int S,
                                              uint64_t *full, uint64_t *empty, int &stage, uint32_t &phase, int kchunks,
                                              uint32_t negmask, const int (&offA_)[2][2], const int (&offB_)[2][2],
@@ -333,11 +336,11 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
   const int (&offA)[2][2] = oA;
   const int (&offB)[2][2] = oB;
   double fa[8], fb[4], xa[8], xb[4];
-  pipe_view<NA, NB, 0, 0, false, SGN, AV, BV>(acc, fa, fb, fa, fb, stages + stage * sstride, true, offA, offB, negmask,
+  pipe_view<NA, NB, 0, 0, false, SGN, AV, BV, MT>(acc, fa, fb, fa, fb, stages + stage * sstride, true, offA, offB, negmask,
                                               bbase);
   for (int c = 0; c < kchunks; ++c) {
     // k-step 0 of chunk c (fa, fb) -> build k-step 1 of chunk c (xa, xb)
-    pipe_view<NA, NB, 0, 1, true, SGN, AV, BV>(acc, fa, fb, xa, xb, stages + stage * sstride, true, offA, offB, negmask,
+    pipe_view<NA, NB, 0, 1, true, SGN, AV, BV, MT>(acc, fa, fb, xa, xb, stages + stage * sstride, true, offA, offB, negmask,
                                                bbase);
     // The stage's smem was read through the generic proxy and the producer refills it
     // with TMA (async proxy) once every consumer warp arrived: the proxy fence orders the
@@ -355,7 +358,7 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
     // k-step 1 of chunk c (xa, xb) -> build k-step 0 of chunk c + 1 (fa, fb)
     const bool more = c + 1 < kchunks;
     if (more) mbar_wait(&full[stage], phase);
-    pipe_view<NA, NB, 0, 0, true, SGN, AV, BV>(acc, xa, xb, fa, fb, stages + stage * sstride, more, offA, offB, negmask,
+    pipe_view<NA, NB, 0, 0, true, SGN, AV, BV, MT>(acc, xa, xb, fa, fb, stages + stage * sstride, more, offA, offB, negmask,
                                                bbase);
   }
 }
@@ -778,6 +781,8 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();  // the previous kernel's slots / tables / C complete (PDL launch)
+  pdl_launch_dependents();
   const int kchunks = p.kchunks;  // 8-deep chunks
 
   if (PS && warp >= CONSUMER_WARPS + FUSED_PRODUCER_WARPS) {
@@ -860,9 +865,9 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
     // default; with warp_map = 1 in wm, so the warps left when the wm = 1 row half of
     // a tile is padding (skip_item) still cover all four sub-partitions
     // shapes 1 / 2: warp = wn (WM = 1) or wm + 4 wn (WM = 4): all sub-partitions busy either way
-    // shape 3: warps 0-3 = wn, one per sub-partition; warps 4-7 idle (idle_warp)
-    const int wm = TS == 1 || TS == 3 ? 0 : TS == 2 ? warp & 3 : p.warp_map ? warp >> 2 : warp & 1;
-    const int wn = TS == 1 || TS == 3 ? (warp & 7) : TS == 2 ? warp >> 2 : p.warp_map ? warp & 3 : warp >> 1;
+    // shape 3: wm = warp / 4, wn = warp % 4: both row halves on every sub-partition
+    const int wm = TS == 1 ? 0 : TS == 2 ? warp & 3 : TS == 3 || p.warp_map ? warp >> 2 : warp & 1;
+    const int wn = TS == 1 ? (warp & 7) : TS == 2 ? warp >> 2 : TS == 3 || p.warp_map ? warp & 3 : warp >> 1;
     const bool idle_warp = warp >= SH::ACTIVE;
     // Fragment offsets inside a view: A (kk, h) + 128 * mt; B (kk, nt & 1) + 128 * (nt >> 1).
     // MMA row (column) g + 8 h of each 16-row block (16-column pair) reads tile row
@@ -874,7 +879,7 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
     for (int kk = 0; kk < 2; ++kk)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        offA[kk][h] = view_index(AKF, wm * 64 + frag_perm(AKF + 1, g, h), kk * 4 + tig);
+        offA[kk][h] = view_index(AKF, wm * 16 * SH::MT + frag_perm(AKF + 1, g, h), kk * 4 + tig);
         offB[kk][h] = view_index(BKF, wn * 32 + frag_perm(BKF + 1, g, h), kk * 4 + tig);
       }
     int stage = 0;
@@ -907,7 +912,7 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
         for (int j = 0; j < 4; ++j)
 #pragma unroll
           for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
-      const bool pad_tile = idle_warp || (p.rows_valid > 0 && ti * SH::BMT + wm * 64 >= p.rows_valid) ||
+      const bool pad_tile = idle_warp || (p.rows_valid > 0 && ti * SH::BMT + wm * 16 * SH::MT >= p.rows_valid) ||
                             (p.cols_valid > 0 && tj * SH::BNT + wn * 32 >= p.cols_valid);
       if (pad_tile) {
         skip_item(S, cfull, empty, stage, phase, kchunks, lane);
@@ -922,13 +927,13 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
           if (lane < nb) neg = __double_as_longlong(p.ops[td.b_first + lane].sign) < 0;
           const uint32_t negmask = __ballot_sync(0xffffffffu, neg) << 1;
           switch (nb) {
-            case 1: consume_item<1, 1, true, SH::AV, SH::BV>(acc, stages, sstride, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bbase); break;
-            case 2: consume_item<1, 2, true, SH::AV, SH::BV>(acc, stages, sstride, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bbase); break;
-            default: consume_item<1, 4, true, SH::AV, SH::BV>(acc, stages, sstride, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bbase); break;
+            case 1: consume_item<1, 1, true, SH::AV, SH::BV, SH::MT>(acc, stages, sstride, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bbase); break;
+            case 2: consume_item<1, 2, true, SH::AV, SH::BV, SH::MT>(acc, stages, sstride, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bbase); break;
+            default: consume_item<1, 4, true, SH::AV, SH::BV, SH::MT>(acc, stages, sstride, S, cfull, empty, stage, phase, kchunks, negmask, offA, offB, lane, bbase); break;
           }
         }
       } else if constexpr (ONE) {
-        consume_item<1, 1, false, SH::AV, SH::BV>(acc, stages, sstride, S, full, empty, stage, phase, kchunks, 0u,
+        consume_item<1, 1, false, SH::AV, SH::BV, SH::MT>(acc, stages, sstride, S, full, empty, stage, phase, kchunks, 0u,
                                                   offA, offB, lane, SH::AV);
       } else {
       // coefficient signs of the item's views: one load per lane, one ballot
@@ -1006,7 +1011,7 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
         continue;
       }
       if constexpr (TS != 0) {  // shapes 1-3: dense M output only
-        if (!idle_warp) epilogue_store<AKF + 1, BKF + 1, 2, SH::BMT, SH::BNT>(p, acc, item, tid, wm, wn, g, tig);
+        if (!idle_warp) epilogue_store<AKF + 1, BKF + 1, 2, SH::BMT, SH::BNT, SH::MT>(p, acc, item, tid, wm, wn, g, tig);
       } else {
         if (!p.dense_out) wait_c_ready(p, tid, c_seen);
         if (red)
@@ -1052,8 +1057,7 @@ cudaError_t launch_fused(const GemmArgs &a, int grid, cudaStream_t s, const void
   CUtensorMap m[3];
   memcpy(m, maps, (a.cred ? 3 : 2) * sizeof(CUtensorMap));
   if (!a.cred) memset(&m[2], 0, sizeof(CUtensorMap));
-  k<<<grid, ps ? FUSED_THREADS_PS : FUSED_THREADS, sm, s>>>(a, m[0], m[1], m[2]);
-  return cudaGetLastError();
+  return launch_pdl(k, dim3(grid), dim3(ps ? FUSED_THREADS_PS : FUSED_THREADS), sm, s, a, m[0], m[1], m[2]);
 }
 
 // ---- coordinate table --------------------------------------------------------

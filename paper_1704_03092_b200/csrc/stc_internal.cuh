@@ -186,6 +186,8 @@ struct PresumArgs {
   int64_t xlen, klen;   // padded quadrant lengths
   int32_t level, side;  // side 0: A (quadrant (r, c) = (x, k)); 1: B ((r, c) = (k, x))
   int32_t kfast, _pad;
+  int32_t *zero;        // A side of the call's first launch: the tickets / work counters to zero
+  int64_t zero_words;
   int16_t slot[kPresumMaxTerms + 1];  // batch slot of each Strassen term (reference order), -1: not in the batch
 };
 
@@ -230,5 +232,31 @@ cudaError_t launch_fill_uniform(double *out, int ndim, const int64_t *ext, const
 cudaError_t launch_sq_norms(int ndim, const int64_t *ext, const double *x, const int64_t *xs, int64_t xb,
                             const double *r, const int64_t *rs, int64_t rb, double *partials, int nblocks,
                             cudaStream_t s);
+
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// The kernels of a contraction's warm sequence (k_restore, k_presum,
+// k_strassen_fused, k_accumulate) launch with programmatic stream serialization:
+// each lets the next one launch as soon as all its CTAs are running
+// (launch_dependents), and waits for the previous grid's completion and memory
+// (griddepcontrol.wait) before its first global access -- the launch latency and
+// the next kernel's prologue overlap the current kernel.  STC_PDL=0 disables it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();  // stc_kernels.cu
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args &&...args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<Args &&>(args)...);
+}
 
 }  // namespace stc

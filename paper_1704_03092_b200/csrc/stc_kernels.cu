@@ -193,6 +193,8 @@ cudaError_t launch_copy_pad(const int64_t *in, int64_t len, int64_t len_pad, int
 // C_q(i,j) += s_1 M_1(i,j) + s_2 M_2(i,j) + ... in term order, one RMW per
 // element (bitwise the reference's per-term accum_dense sequence).
 __global__ void k_accumulate(const AccArgs a) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (a.c_ready) {  // stc_set_c_ready: C's upload may still be in flight
     if (threadIdx.x == 0) {
       int v;
@@ -227,8 +229,7 @@ cudaError_t launch_accumulate(const AccArgs &a, cudaStream_t s) {
   if (total <= 0 || a.nquads <= 0) return cudaSuccess;
   const int by = (int)std::min<int64_t>((total + 255) / 256, 65535);
   dim3 grid(a.nquads, by);
-  k_accumulate<<<grid, 256, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k_accumulate, grid, dim3(256), 0, s, a);
 }
 
 // out_slot[k*x_len + x] (or [x*k_len + k] when kfast) = sum_op sign * D[x_vec[x] + k_vec[k]]
@@ -405,6 +406,12 @@ __device__ __forceinline__ void presum_block(const PresumArgs &a, int64_t bx, in
 template <int L>
 __global__ void __launch_bounds__(256) k_presum(const PresumArgs pa, const PresumArgs pb, int64_t na_x, int64_t na,
                                                 int64_t nb_x) {
+  pdl_wait();
+  pdl_launch_dependents();
+  // the call's tickets and work counters (read by the next kernel, after this grid completes)
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pa.zero_words;
+       i += (int64_t)gridDim.x * blockDim.x)
+    pa.zero[i] = 0;
   const int64_t b = blockIdx.x;
   if (b < na)
     presum_block<L, 0>(pa, b % na_x, b / na_x);
@@ -426,17 +433,24 @@ cudaError_t launch_presum2(const PresumArgs &pa, const PresumArgs &pb, cudaStrea
   const int64_t na = ax * ay, total = na + bx * by;
   if (total == 0) return cudaSuccess;
   if (total > INT32_MAX) return cudaErrorInvalidConfiguration;
-  if (pa.level == 1)
-    k_presum<1><<<(unsigned)total, 256, 0, s>>>(pa, pb, std::max<int64_t>(ax, 1), na, std::max<int64_t>(bx, 1));
-  else if (pa.level == 2)
-    k_presum<2><<<(unsigned)total, 256, 0, s>>>(pa, pb, std::max<int64_t>(ax, 1), na, std::max<int64_t>(bx, 1));
-  else
-    return cudaErrorInvalidValue;
-  return cudaGetLastError();
+  const int64_t ax1 = std::max<int64_t>(ax, 1), bx1 = std::max<int64_t>(bx, 1);
+  if (pa.level == 1) return launch_pdl(k_presum<1>, dim3((unsigned)total), dim3(256), 0, s, pa, pb, ax1, na, bx1);
+  if (pa.level == 2) return launch_pdl(k_presum<2>, dim3((unsigned)total), dim3(256), 0, s, pa, pb, ax1, na, bx1);
+  return cudaErrorInvalidValue;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("STC_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 // ---- plan snapshot restore (stc_capi.cu Resident): a plain device copy ----
 __global__ void __launch_bounds__(256) k_restore(const uint4 *__restrict__ src, uint4 *__restrict__ dst, int64_t n) {
+  pdl_wait();
+  pdl_launch_dependents();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = src[i];
 }
@@ -447,8 +461,8 @@ cudaError_t launch_restore(const void *src, void *dst, size_t bytes, cudaStream_
     return cudaErrorInvalidValue;
   const int64_t n = (int64_t)(bytes / 16);
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 4);
-  k_restore<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint4 *>(src), reinterpret_cast<uint4 *>(dst), n);
-  return cudaGetLastError();
+  return launch_pdl(k_restore, dim3(blocks), dim3(256), 0, s, reinterpret_cast<const uint4 *>(src),
+                    reinterpret_cast<uint4 *>(dst), n);
 }
 
 // ---- standalone helpers for the kernel-level API --------------------------

