@@ -305,6 +305,31 @@ bool same_extents(const stc_bundle &x, const stc_bundle &y) {
   return true;
 }
 
+// Fast-index step of a gather pass's source (stc_internal.cuh FastMap): for a bundle
+// kept in the reference order (first label fastest) whose unit-stride label u is not
+// its first, the quadrant-local step that advances u by one (the product of the
+// extents before it); 0 otherwise.  `group`: the t values per run, a power of two
+// up to 4 (a 32-byte sector) and up to the extent of u and the runs a quadrant holds.
+int64_t unit_step(const stc_bundle &b, const Tiling &t, int64_t fast_len, int &group) {
+  group = 0;
+  if (t.nbox > 0) return 0;  // tile order: the unit-stride label already leads
+  int64_t mult = 1;
+  for (int d = 0; d < b.nlab; ++d) {
+    const int64_t s = b.str[d] < 0 ? -b.str[d] : b.str[d];
+    if (s == 1 && b.ext[d] > 1) {
+      if (d == 0 || mult < 8) return 0;
+      const int64_t runs = std::min<int64_t>(b.ext[d], cdiv(fast_len, mult));
+      int g = 1;
+      while (g < 4 && 2 * g <= runs) g *= 2;
+      if (g < 2) return 0;
+      group = g;
+      return mult;
+    }
+    mult *= b.ext[d];
+  }
+  return 0;
+}
+
 // ---------------------------------------------------------------- the plan
 // Device snapshots of a plan's constant workspace region (scatter vectors, chunk
 // strides, map coordinates, tables, accumulate lists, zeroed tickets and counters),
@@ -414,6 +439,8 @@ struct Plan {
   int64_t Q = 1;  // quadrants per dimension
   int nquads = 1;
   int a_kfast = 0, b_kfast = 0;
+  int64_t a_ustep = 0, b_ustep = 0;  // gather passes: fast-index step of the unit-stride label (FastMap)
+  int a_ugroup = 0, b_ugroup = 0;
   Tiling ti, tj, tp;  // tile orders of the I, J, P bundles
   std::vector<VecDesc> vecs;
   int64_t pool_len = 0;
@@ -627,6 +654,12 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   pl.tp = tp;
   pl.a_kfast = a_min == 1;
   pl.b_kfast = b_min == 0;
+  if (!getenv("STC_NO_USTEP")) {
+    pl.a_ustep = pl.a_kfast ? unit_step(p->a_col, tp, rup(pl.kq, BK), pl.a_ugroup)
+                            : unit_step(p->a_row, ti, rup(pl.mq, pl.tm), pl.a_ugroup);
+    pl.b_ustep = pl.b_kfast ? unit_step(p->b_row, tp, rup(pl.kq, BK), pl.b_ugroup)
+                            : unit_step(p->b_col, tj, rup(pl.nq, pl.tn), pl.b_ugroup);
+  }
   if (pl.tshape != 0) {  // the direct fused layout must cut the new tiles as boxes -- or the
     GemmArgs gd{};      // operands come from pre-summed slots, box-regular by construction
     CUtensorMap md[3];
@@ -1413,12 +1446,16 @@ PresumArgs presum_args(const Plan &pl, int side, const double *D, double *out, c
     a.kv = pl.ac;
     a.xlen = pl.mq_pad;
     a.kfast = pl.a_kfast;
+    a.ustep = pl.a_ustep;
+    a.ugroup = pl.a_ugroup;
   } else {
     a.slot_stride = pl.pb_slot;
     a.xv = pl.bc;
     a.kv = pl.br;
     a.xlen = pl.nq_pad;
     a.kfast = pl.b_kfast;
+    a.ustep = pl.b_ustep;
+    a.ugroup = pl.b_ugroup;
   }
   return a;
 }
@@ -1440,7 +1477,7 @@ constexpr size_t kPlanCache = 32;
 std::string plan_env() {
   static const char *knobs[] = {"STC_WORKSPACE_CAP_MB", "STC_EXEC_ORDER", "STC_PACK", "STC_TMA_PROMO",
                                 "STC_TMA", "STC_TMA_PF", "STC_FUSED", "STC_CRED", "STC_PRESUM",
-                                "STC_ABC_DENSE", "STC_TSHAPE", "STC_PRESUM_OPS"};
+                                "STC_ABC_DENSE", "STC_TSHAPE", "STC_PRESUM_OPS", "STC_NO_USTEP", "STC_EPI_OFFLOAD"};
   std::string key;
   for (const char *k : knobs) {
     const char *v = getenv(k);
@@ -1577,8 +1614,8 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
     if (packed) {
       double *PA = reinterpret_cast<double *>(ws + pl.off_pka);
       double *PB = reinterpret_cast<double *>(ws + pl.off_pkb);
-      PackArgs pa{pl.ar, pl.ac, pl.mq_pad, pl.kq_pad, (int32_t)pl.Q, 1, pl.a_kfast, 0};
-      PackArgs pb{pl.bc, pl.br, pl.nq_pad, pl.kq_pad, (int32_t)pl.Q, 0, pl.b_kfast, 0};
+      PackArgs pa{pl.ar, pl.ac, pl.mq_pad, pl.kq_pad, (int32_t)pl.Q, 1, pl.a_kfast, 0, pl.a_ustep, pl.a_ugroup, 0};
+      PackArgs pb{pl.bc, pl.br, pl.nq_pad, pl.kq_pad, (int32_t)pl.Q, 0, pl.b_kfast, 0, pl.b_ustep, pl.b_ugroup, 0};
       CU(launch_pack_views(A, pool2, pa, PA, s), "k_pack_views(A)");
       CU(launch_pack_views(B, pool2, pb, PB, s), "k_pack_views(B)");
       launches += 2;

@@ -140,6 +140,8 @@ struct PackArgs {
   int64_t xlen, klen;  // padded quadrant lengths
   int32_t Q, xfirst;   // quadrants per dimension; block y = qa * Q + qb, x quadrant = xfirst ? qa : qb
   int32_t kfast, _pad; // packed block layout: 0 [k][x], 1 [x][k]
+  int64_t ustep;       // > 0: fast-index step of the source's unit-stride label (unit_step)
+  int32_t ugroup, _pad2;
 };
 
 // AB / Naive accumulate: C_q += sum over the quadrant's terms of sign * M_slot.
@@ -188,6 +190,8 @@ struct PresumArgs {
   int32_t kfast, _pad;
   int32_t *zero;        // A side of the call's first launch: the tickets / work counters to zero
   int64_t zero_words;
+  int64_t ustep;        // > 0: fast-index step of the source's unit-stride label (unit_step)
+  int32_t ugroup, _pad2;
   int16_t slot[kPresumMaxTerms + 1];  // batch slot of each Strassen term (reference order), -1: not in the batch
 };
 
@@ -232,6 +236,40 @@ cudaError_t launch_fill_uniform(double *out, int ndim, const int64_t *ext, const
 cudaError_t launch_sq_norms(int ndim, const int64_t *ext, const double *x, const int64_t *xs, int64_t xb,
                             const double *r, const int64_t *rs, int64_t rb, double *partials, int nblocks,
                             cudaStream_t s);
+
+// Fast-index mapping of the gather passes (k_presum, k_pack_views).  Normally a
+// block's threads take consecutive positions f of the fast dimension.  When the
+// source's unit-stride label u is a slow label of that bundle in the reference
+// order (padded quadrants, e.g. cfg4's A: i = a + 50 b + 350 c, c unit stride), f
+// and f + ustep are adjacent in memory: threads then take f = r + ustep * t with
+// the G = ugroup values of t innermost, so G lanes read one run of G doubles (a
+// 32-byte sector for G = 4) instead of G sectors.  Blocks: (r chunk, t group).
+struct FastMap {
+  int64_t ustep, nrb;
+  int g, r_per_block;
+  __host__ __device__ FastMap(int64_t step, int group, int threads) : ustep(step), nrb(0), g(group), r_per_block(0) {
+    if (ustep > 0) {
+      r_per_block = threads / g;
+      nrb = (ustep + r_per_block - 1) / r_per_block;
+    }
+  }
+  __host__ __device__ int64_t blocks(int64_t fast_len, int threads) const {
+    if (ustep <= 0) return (fast_len + threads - 1) / threads;
+    const int64_t nt = (fast_len + ustep - 1) / ustep;
+    return nrb * ((nt + g - 1) / g);
+  }
+  // position of thread `tid` of fast block `bx`; -1 outside [0, fast_len)
+  __host__ __device__ int64_t pos(int64_t bx, int tid, int threads, int64_t fast_len) const {
+    if (ustep <= 0) {
+      const int64_t f = bx * threads + tid;
+      return f < fast_len ? f : -1;
+    }
+    const int64_t rb = bx % nrb, tb = bx / nrb;
+    const int64_t r = rb * r_per_block + tid / g, t = tb * g + tid % g;
+    const int64_t f = r + ustep * t;
+    return (r < ustep && f < fast_len) ? f : -1;
+  }
+};
 
 // ---- programmatic dependent launch (PDL) -----------------------------------
 // The kernels of a contraction's warm sequence (k_restore, k_presum,

@@ -288,8 +288,8 @@ __global__ void __launch_bounds__(256) k_pack_views(const double *__restrict__ D
   double *o = out + (int64_t)blockIdx.z * a.xlen * a.klen;
   const int64_t fast_len = a.kfast ? a.klen : a.xlen, slow_len = a.kfast ? a.xlen : a.klen;
   const int64_t *fv = a.kfast ? kv : xv, *sv = a.kfast ? xv : kv;
-  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= fast_len) return;
+  const int64_t f = FastMap(a.ustep, a.ugroup, blockDim.x).pos(blockIdx.x, threadIdx.x, blockDim.x, fast_len);
+  if (f < 0) return;
   const int64_t fo = __ldg(fv + f);
   const int64_t s0 = (int64_t)blockIdx.y * UNPACK_ROWS;
 #pragma unroll 4
@@ -306,7 +306,7 @@ cudaError_t launch_pack_views(const double *D, const int64_t *pool, const PackAr
   if (fast_len <= 0 || slow_len <= 0) return cudaSuccess;
   const int64_t gy = (slow_len + UNPACK_ROWS - 1) / UNPACK_ROWS;
   if (gy > 65535 || a.Q * a.Q > 65535) return cudaErrorInvalidConfiguration;
-  dim3 grid((unsigned)((fast_len + 255) / 256), (unsigned)gy, (unsigned)(a.Q * a.Q));
+  dim3 grid((unsigned)FastMap(a.ustep, a.ugroup, 256).blocks(fast_len, 256), (unsigned)gy, (unsigned)(a.Q * a.Q));
   k_pack_views<<<grid, 256, 0, s>>>(D, pool, a, out);
   return cudaGetLastError();
 }
@@ -377,8 +377,8 @@ template <int L, int SIDE>
 __device__ __forceinline__ void presum_block(const PresumArgs &a, int64_t bx, int64_t by) {
   constexpr int Q = 1 << L;
   const int64_t fast_len = a.kfast ? a.klen : a.xlen, slow_len = a.kfast ? a.xlen : a.klen;
-  const int64_t f = bx * blockDim.x + threadIdx.x;
-  if (f >= fast_len) return;
+  const int64_t f = FastMap(a.ustep, a.ugroup, blockDim.x).pos(bx, threadIdx.x, blockDim.x, fast_len);
+  if (f < 0) return;
   const int64_t fv = a.kfast ? a.kv : a.xv, sv = a.kfast ? a.xv : a.kv;
   int64_t fo[Q];
 #pragma unroll
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(256) k_presum(const PresumArgs pa, const Presu
 
 static void presum_grid(const PresumArgs &a, int64_t &gx, int64_t &gy) {
   const int64_t fast_len = a.kfast ? a.klen : a.xlen, slow_len = a.kfast ? a.xlen : a.klen;
-  gx = fast_len > 0 ? (fast_len + 255) / 256 : 0;
+  gx = fast_len > 0 ? FastMap(a.ustep, a.ugroup, 256).blocks(fast_len, 256) : 0;
   gy = slow_len > 0 ? (slow_len + PRESUM_ROWS - 1) / PRESUM_ROWS : 0;
 }
 

@@ -254,6 +254,24 @@ def _contract_host(spec, a, b, c, level, variant, force_slow, reference_tiling, 
 
 _SIDE = {}
 _ONE = []
+_WS = {}
+_WS_KEEP = 64 << 20  # workspaces up to this size stay cached per (device, stream)
+
+
+def _workspace(dev, stream, nbytes: int):
+    """The call's workspace.  Small ones are kept per (device, stream) and reused by
+    the next call on that stream (stream order serialises the uses; the pointer then
+    stays stable, which the library's graph replay keys on); large ones come from
+    the caching allocator each call and are released after it."""
+    import torch
+
+    if nbytes > _WS_KEEP:
+        return torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    key = (dev.index, stream.cuda_stream)
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = _WS[key] = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+    return ws
 
 
 def _pinned_one():
@@ -322,12 +340,12 @@ def contract(spec: ContractionSpec, a, b, c, level: int, variant, params: Blocki
         return _contract_host(spec, a, b, c, level, variant, force_slow, reference_tiling, validate, terms, dev,
                               t_start)
     c_ready = None
-    main = torch.cuda.current_stream(dev)
     A = a if a.on_device else a.to_device(dev)
     B = b if b.on_device else b.to_device(dev)
     if not c.on_device and os.environ.get("STC_C_OVERLAP", "0") != "0":
         # C's upload starts after A and B's (it would only slow them down) and runs
         # under the DMMA main loop; buffers come from the main stream's pool
+        main = torch.cuda.current_stream(dev)
         c_ready = torch.zeros(1, dtype=torch.int32, device=dev)
         src = c.data if torch.is_tensor(c.data) else torch.from_numpy(c.data)
         cd = torch.empty(src.shape, dtype=src.dtype, device=dev)
@@ -345,26 +363,29 @@ def contract(spec: ContractionSpec, a, b, c, level: int, variant, params: Blocki
         _validate_targets(spec, C, level, terms)
     L = _lib.lib()
     stats = RunStats()
+    timed = not (c.on_device and not synchronize)  # stream-ordered calls: no events
     with torch.cuda.device(dev):
         need = ctypes.c_size_t()
         _lib.check(L.stc_workspace_size(ctypes.byref(prob), ctypes.byref(need)))
-        ws = torch.empty(max(int(need.value), 256), dtype=torch.uint8, device=dev)
+        stream = torch.cuda.current_stream()
+        ws = _workspace(dev, stream, max(int(need.value), 256))
         if os.environ.get("STC_DEBUG_POISON"):  # debugging aid: the library must not read stale workspace
             ws.fill_(int(os.environ["STC_DEBUG_POISON"]) & 255)
-        stream = torch.cuda.current_stream()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, e1 = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) if timed else (None, None)
         st = _lib.Stats()
         if kernel_events is not None:  # profiling hook: events around the DMMA launch(es)
             L.stc_set_kernel_events(ctypes.c_void_p(kernel_events[0].cuda_event),
                                     ctypes.c_void_p(kernel_events[1].cuda_event))
         if c_ready is not None:
             L.stc_set_c_ready(ctypes.c_void_p(c_ready.data_ptr()))
-        e0.record(stream)
+        if timed:
+            e0.record(stream)
         _lib.check(L.stc_contract(ctypes.byref(prob), ctypes.c_void_p(A.data.data_ptr()),
                                   ctypes.c_void_p(B.data.data_ptr()), ctypes.c_void_p(C.data.data_ptr()),
                                   ctypes.c_void_p(ws.data_ptr()), ws.numel(), ctypes.c_void_p(stream.cuda_stream),
                                   ctypes.byref(st)))
-        e1.record(stream)
+        if timed:
+            e1.record(stream)
         stats.absorb(st)
         if not c.on_device:
             if c_ready is not None:
