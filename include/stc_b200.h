@@ -224,10 +224,11 @@ typedef struct {
   int32_t ticketed;      /* ABC with C updated by the kernel (else dense M + accumulate)  */
   int32_t presum;        /* operand sums pre-formed by k_presum into per-term slots       */
   int32_t need_pack;     /* operands repacked (views not regular boxes)                   */
-  int32_t tshape;        /* fused CTA tile: 0 128x128, 1 64x256, 2 256x64                 */
+  int32_t tshape;        /* fused CTA tile: 0 128x128, 1 64x256, 2 256x64, 3 64x128       */
   int32_t fused_direct;  /* fused kernel on the operands' own views                       */
   int32_t c_boxes;       /* C quadrant tiles are TMA-reduce boxes                         */
-  int32_t batch, nbatches, terms, _pad;
+  int32_t batch, nbatches, terms;
+  int32_t presum_sides;  /* pre-summed sides: bit 0 A, bit 1 B (0: none)                  */
   int64_t tiles, mq_pad, nq_pad, kq_pad;
   size_t workspace;
 } stc_plan_info;

@@ -55,7 +55,7 @@ class Stats(ctypes.Structure):
 
 class PlanInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("ticketed", "presum", "need_pack", "tshape", "fused_direct", "c_boxes",
-                                              "batch", "nbatches", "terms", "_pad")] + \
+                                              "batch", "nbatches", "terms", "presum_sides")] + \
                [(n, ctypes.c_int64) for n in ("tiles", "mq_pad", "nq_pad", "kq_pad")] + [("workspace", ctypes.c_size_t)]
 
     def as_dict(self):

@@ -467,6 +467,15 @@ struct Plan {
   // formed once per element position into per-term slots (term batches under the
   // workspace cap), and the fused kernel runs every term with one view per side
   bool presum = false;
+  // which sides come from slots (bit 0 A, bit 1 B): both, or -- for dense plans one tile
+  // wide in I (J), 64 x 256 (256 x 64) tiles -- only the short side's A (B): its sums cost
+  // nothing, the long side's slots would be 49 x its quadrant (cfg3 at m = 256, L2:
+  // 6.6 GB), and a stage of raw long-side views + one slot view leaves room for 3 stages
+  int presum_sides = 0;
+  // dense-M item order with a tile position's terms consecutive: for problems one
+  // tile wide in I or J (cfg3 at m or n = 256), where term-major order re-reads the
+  // long operand's views from DRAM once per term (19 GB at 2^24, N_a = 16, L2)
+  bool term_inner = false;
   std::vector<int> seq;  // term order of the dense-M batches and accumulate lists
   size_t off_pool = 0, off_vecs = 0, off_tab = 0, off_tickets = 0, off_counters = 0, off_M = 0, off_pa = 0,
          off_pb = 0, off_acc = 0, total = 0;
@@ -547,6 +556,7 @@ bool c_boxes_regular(const stc_problem *p, const Tiling &ti, const Tiling &tj, i
 FusedSides direct_sides(const stc_problem *p, const Plan &pl);
 FusedSides packed_sides(const Plan &pl);
 FusedSides naive_sides(const Plan &pl);
+FusedSides mixed_sides(const stc_problem *p, const Plan &pl);
 bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, const double *A, const double *B,
                 const double *C, GemmArgs &g, CUtensorMap maps[3], CoordJobs &jobs);
 
@@ -631,6 +641,7 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     if (allowed && T > 1 && grid >= 4 * p3 && waves_cur <= 4 &&
         (double)waves3 * 64 * 128 < 0.85 * (double)waves_cur * tm0 * tn0)
       pl.tshape = 3;
+    if (allowed && ts && atoi(ts) > 0 && atoi(ts) <= 3) pl.tshape = atoi(ts);  // forced (diagnostics)
   }
   pl.tm = pl.tshape == 1 || pl.tshape == 3 ? 64 : pl.tshape == 2 ? 256 : BM;
   pl.tn = pl.tshape == 1 ? 256 : pl.tshape == 2 ? 64 : pl.tshape == 3 ? 128 : BN;
@@ -715,16 +726,45 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
                                     : (pl.grid >= 4 * P || !c_boxes_regular(p, pl.ti, pl.tj, pl.level)));
     pl.ticketed = !dense;
   }
+  {
+    const char *ti_env = getenv("STC_TERM_INNER");
+    const bool skinny = pl.mq_pad / pl.tm == 1 || pl.nq_pad / pl.tn == 1;
+    pl.term_inner = !pl.ticketed && T > 1 && (ti_env ? atoi(ti_env) != 0 : skinny);
+  }
   // Operand sums pre-formed into per-term slots (k_presum): ABC and AB when worth it
   // (AB with pre-summed operands is the Naive schedule: the same M products), and
   // always for Naive (its explicit submatrix copies) at L <= 2.
   pl.presum = pl.variant == STC_VARIANT_NAIVE ? (pl.level >= 1 && pl.level <= 2) : presum_wanted(p, pl);
+  pl.presum_sides = pl.presum ? 3 : 0;
+  if (pl.variant != STC_VARIANT_NAIVE && !pl.ticketed && pl.level >= 1 && pl.level <= 2 &&
+      !(pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) &&
+      bundle_len(p->a_col) == pl.Q * pl.kq_pad) {  // (the direct side's k quadrants need no padding)
+    const char *e = getenv("STC_PRESUM_SIDES");  // 1 / 2 / 3 force (diagnostics), 0 disables one-sided
+    const int want = e ? (atoi(e) & 3) : getenv("STC_PRESUM_OPS") ? 0 : pl.tshape == 1 ? 1 : pl.tshape == 2 ? 2 : 0;
+    if (want == 3) {
+      pl.presum = true;
+      pl.presum_sides = 3;
+    } else if (want == 1 || want == 2) {
+      const bool was = pl.presum;
+      const int was_sides = pl.presum_sides;
+      pl.presum = true;
+      pl.presum_sides = want;
+      GemmArgs gx{};
+      CUtensorMap mx[3];
+      CoordJobs jx{};
+      if (!plan_fused(p, pl, mixed_sides(p, pl), nullptr, nullptr, nullptr, gx, mx, jx)) {
+        pl.presum = was;  // the long side's own views are not boxes: keep the default
+        pl.presum_sides = was_sides;
+      }
+    }
+  }
   const bool slots = pl.variant == STC_VARIANT_NAIVE || pl.presum;
   if (slots) {
     // per-term slots of packed operand sums, oriented like the source (unit stride in
     // k -> [x][k] slots, else [k][x]) so both sides of the copy coalesce
-    pl.pa_slot = pl.kq_pad * pl.mq_pad;
-    pl.pb_slot = pl.kq_pad * pl.nq_pad;
+    const bool all = pl.variant == STC_VARIANT_NAIVE || pl.presum_sides == 3;  // (Naive: k_presum or k_unpack)
+    pl.pa_slot = all || (pl.presum_sides & 1) ? pl.kq_pad * pl.mq_pad : 0;
+    pl.pb_slot = all || (pl.presum_sides & 2) ? pl.kq_pad * pl.nq_pad : 0;
     pl.m_slot = pl.ticketed ? 0 : pl.mq_pad * pl.nq_pad;
     int64_t b = cap_bytes() / std::max<int64_t>((pl.pa_slot + pl.pb_slot + pl.m_slot) * 8, 1);
     pl.batch = (int)std::max<int64_t>(1, std::min<int64_t>(b, T));
@@ -1328,6 +1368,42 @@ FusedSides naive_sides(const Plan &pl) {
   return f;
 }
 
+// Pre-summed sides from their slots (naive_sides), the others' own views (direct_sides).
+FusedSides mixed_sides(const stc_problem *p, const Plan &pl) {
+  const FusedSides n = naive_sides(pl);
+  if (pl.presum_sides == 3 || pl.variant == STC_VARIANT_NAIVE) return n;
+  FusedSides f = direct_sides(p, pl);
+  if (pl.presum_sides & 1) {
+    f.ax = n.ax;
+    f.ak = n.ak;
+    f.tax = n.tax;
+    f.tak = n.tak;
+    f.akf = n.akf;
+    f.a_base = n.a_base;
+    f.qxa = n.qxa;
+    for (int i = 0; i < 2; ++i) {
+      f.start[i] = n.start[i];
+      f.len[i] = n.len[i];
+      f.vbase[i] = n.vbase[i];
+    }
+  }
+  if (pl.presum_sides & 2) {
+    f.bx = n.bx;
+    f.bk = n.bk;
+    f.tbx = n.tbx;
+    f.tbk = n.tbk;
+    f.bkf = n.bkf;
+    f.b_base = n.b_base;
+    f.qxb = n.qxb;
+    for (int i = 2; i < 4; ++i) {
+      f.start[i] = n.start[i];
+      f.len[i] = n.len[i];
+      f.vbase[i] = n.vbase[i];
+    }
+  }
+  return f;
+}
+
 // The packed sides' pool vectors (mode 2), written over ar, ac, br, bc once the
 // operands are packed (the ops tables then address the packed blocks unchanged).
 void packed_vecs(const Plan &pl, const FusedSides &f, VecDesc out[4]) {
@@ -1352,9 +1428,12 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
   if (const char *e = getenv("STC_FUSED"))
     if (atoi(e) == 0) return false;
   if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
-  // Naive and pre-summed ABC: one packed view per side
-  const int umax = (pl.variant == STC_VARIANT_NAIVE || pl.presum) ? 2 : 2 * pl.max_ops;
-  const size_t sd = fused_stage_doubles(umax / 2, pl.tshape);
+  // Naive and pre-summed sides: one packed view per side
+  const bool all_slots = pl.variant == STC_VARIANT_NAIVE || (pl.presum && pl.presum_sides == 3);
+  const int va = all_slots || (pl.presum && (pl.presum_sides & 1)) ? 1 : pl.max_ops;
+  const int vb = all_slots || (pl.presum && (pl.presum_sides & 2)) ? 1 : pl.max_ops;
+  const int umax = va + vb;
+  const size_t sd = fused_stage_doubles2(va, vb, pl.tshape);
   const int S = fused_stages(sd);
   if (umax > 8 || S < 2) return false;
   TmaSide sa, sb;
@@ -1477,7 +1556,8 @@ constexpr size_t kPlanCache = 32;
 std::string plan_env() {
   static const char *knobs[] = {"STC_WORKSPACE_CAP_MB", "STC_EXEC_ORDER", "STC_PACK", "STC_TMA_PROMO",
                                 "STC_TMA", "STC_TMA_PF", "STC_FUSED", "STC_CRED", "STC_PRESUM",
-                                "STC_ABC_DENSE", "STC_TSHAPE", "STC_PRESUM_OPS", "STC_NO_USTEP", "STC_EPI_OFFLOAD"};
+                                "STC_ABC_DENSE", "STC_TSHAPE", "STC_PRESUM_OPS", "STC_NO_USTEP", "STC_EPI_OFFLOAD", "STC_TERM_INNER",
+                                "STC_PRESUM_SIDES"};
   std::string key;
   for (const char *k : knobs) {
     const char *v = getenv(k);
@@ -1658,6 +1738,7 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
   g.warp_map = (pl.mq % BM != 0 && pl.mq % BM <= 64) && !(pl.nq % BN != 0 && pl.nq % BN <= 96);
   g.kchunks = (int)(pl.kq_pad / BK);
   g.group_m = 8;
+  g.term_inner = pl.term_inner ? 1 : 0;
   g.max_ops = pl.max_ops;
   g.nraw = gemm_nraw(pl.max_ops);
   g.kwin = gemm_kwin(pl.max_ops);
@@ -1766,6 +1847,8 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
     double *M = reinterpret_cast<double *>(ws + pl.off_M);
     double *PA = reinterpret_cast<double *>(ws + pl.off_pa);
     double *PB = reinterpret_cast<double *>(ws + pl.off_pb);
+    const bool slot_a = slots && (pl.variant == STC_VARIANT_NAIVE || (pl.presum_sides & 1));
+    const bool slot_b = slots && (pl.variant == STC_VARIANT_NAIVE || (pl.presum_sides & 2));
     struct Batch {
       int t0, t1;
       const TermDesc *d_g, *d_ua, *d_ub;
@@ -1799,13 +1882,21 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
           ops.push_back({pl.bc + c * pl.nq_pad, pl.br + r * pl.kq_pad, 0, (double)op.s});
         }
         ua.m_slot = ub.m_slot = gd.m_slot = slot;
-        if (slots) {
-          gd.a_first = (int)ops.size();
-          gd.a_count = 1;
-          ops.push_back({pl.dxa + slot * pl.mq_pad, pl.dka, 0, 1.0});
-          gd.b_first = (int)ops.size();
-          gd.b_count = 1;
-          ops.push_back({pl.dxb + slot * pl.nq_pad, pl.dkb, 0, 1.0});
+        if (slots) {  // a pre-summed side: the term's slot; the other (one-sided): its own views
+          gd.a_first = ua.a_first;
+          gd.a_count = ua.a_count;
+          gd.b_first = ub.a_first;
+          gd.b_count = ub.a_count;
+          if (slot_a) {
+            gd.a_first = (int)ops.size();
+            gd.a_count = 1;
+            ops.push_back({pl.dxa + slot * pl.mq_pad, pl.dka, 0, 1.0});
+          }
+          if (slot_b) {
+            gd.b_first = (int)ops.size();
+            gd.b_count = 1;
+            ops.push_back({pl.dxb + slot * pl.nq_pad, pl.dkb, 0, 1.0});
+          }
         } else {
           gd.a_first = ua.a_first;
           gd.a_count = ua.a_count;
@@ -1890,11 +1981,11 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
     GemmArgs gf_ab = g;
     CUtensorMap maps_ab[3];
     int fused_ab = 0;
-    if (slots) {  // per-term slots: regular by construction
+    if (slots) {  // per-term slots (regular by construction) and, one-sided, the other side's views
       CoordJobs jobs{};
-      if (plan_fused(p, pl, naive_sides(pl), PA, PB, nullptr, gf_ab, maps_ab, jobs)) {
-        gf_ab.A = PA;
-        gf_ab.B = PB;
+      if (plan_fused(p, pl, mixed_sides(p, pl), slot_a ? PA : A, slot_b ? PB : B, nullptr, gf_ab, maps_ab, jobs)) {
+        gf_ab.A = slot_a ? PA : A;
+        gf_ab.B = slot_b ? PB : B;
         gf_ab.coords = coords;
         if (!restored) {
           CU(launch_pool_coords(pool, coords, jobs, s), "k_pool_coords");
@@ -1913,12 +2004,12 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
       const int nb = b.t1 - b.t0;
       if (slots && pl.presum) {
         // one pass per side: every element position's 4^L quadrant values -> the batch's sums
-        PresumArgs pa = presum_args(pl, 0, A, PA, pool, b.t0, b.t1);
+        PresumArgs pa = presum_args(pl, 0, A, slot_a ? PA : nullptr, pool, b.t0, b.t1);
         if (bi == 0 && zero) {
           pa.zero = zero;
           pa.zero_words = zero_words;
         }
-        CU(launch_presum2(pa, presum_args(pl, 1, B, PB, pool, b.t0, b.t1), s), "k_presum");
+        CU(launch_presum2(pa, presum_args(pl, 1, B, slot_b ? PB : nullptr, pool, b.t0, b.t1), s), "k_presum");
         ++launches;
       } else if (slots) {
         UnpackArgs ua{};
@@ -1944,8 +2035,8 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
         st.slow_blocks += 2 * nb;
       }
       GemmArgs gb = g;
-      gb.A = slots ? PA : A;
-      gb.B = slots ? PB : B;
+      gb.A = slot_a ? PA : A;
+      gb.B = slot_b ? PB : B;
       gb.C = nullptr;
       gb.terms = b.d_g;
       gb.ops = b.d_ops;
@@ -2342,6 +2433,7 @@ int stc_plan_describe(const stc_problem *p, int grid, stc_plan_info *info) {
   memset(info, 0, sizeof(*info));
   info->ticketed = pl.ticketed;
   info->presum = pl.presum;
+  info->presum_sides = pl.presum ? pl.presum_sides : 0;
   info->need_pack = pl.need_pack;
   info->tshape = pl.tshape;
   info->batch = pl.batch;

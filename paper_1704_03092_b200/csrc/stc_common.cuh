@@ -13,8 +13,14 @@ namespace stc {
 __device__ __forceinline__ void tile_of(const GemmArgs &p, int item, int &slot, int &ti, int &tj, int &pos) {
   const int rows = p.tiles_m;
   const int P = rows * p.tiles_n;
-  slot = item / P;
-  const int local = item - slot * P;
+  int local;
+  if (p.term_inner) {  // dense M: a tile position's terms run together and share its operand panels in L2
+    local = item / p.nterms;
+    slot = item - local * p.nterms;
+  } else {
+    slot = item / P;
+    local = item - slot * P;
+  }
   // grouped rasterisation: group_m tile-rows share the B panels in L2
   const int gm = min(p.group_m, rows);
   const int per_group = gm * p.tiles_n;

@@ -139,10 +139,13 @@ int fused_stages_red(size_t sd) {
 }
 
 // Doubles per stage for terms of at most max_ops views per side, tile shape ts.
-size_t fused_stage_doubles(int max_ops, int ts) {
+size_t fused_stage_doubles(int max_ops, int ts) { return fused_stage_doubles2(max_ops, max_ops, ts); }
+
+// ... with va A views and vb B views per chunk (one-sided pre-summed slots)
+size_t fused_stage_doubles2(int va, int vb, int ts) {
   const int av = ts == 1 ? Shape<1>::AV : ts == 2 ? Shape<2>::AV : ts == 3 ? Shape<3>::AV : Shape<0>::AV;
   const int bv = ts == 1 ? Shape<1>::BV : ts == 2 ? Shape<2>::BV : ts == 3 ? Shape<3>::BV : Shape<0>::BV;
-  return (size_t)max_ops * (av + bv);
+  return (size_t)va * av + (size_t)vb * bv;
 }
 
 // Element offset of (x, k) inside a raw view.

@@ -70,6 +70,7 @@ struct GemmArgs {
   int32_t dense_out;         // 1: write M_slot densely instead of C targets
   int32_t use_tickets;       // serialise C-tile updates across terms
   int32_t group_m;           // tile rasterisation group
+  int32_t term_inner;        // item order: 0 term-major; 1 the terms of one tile position consecutive
   int32_t max_ops;           // op-table capacity in smem (per side)
   int32_t force_slow;        // reference force_slow: always take the per-element gather
   int32_t nraw;              // raw cp.async slots in smem (units in flight + 1)
@@ -212,6 +213,7 @@ int gemm_tma_config(int max_ops, int &nraw, int &kwin);
 int fused_stages(size_t stage_doubles);
 int fused_stages_red(size_t stage_doubles);
 size_t fused_stage_doubles(int max_ops, int tshape);
+size_t fused_stage_doubles2(int va, int vb, int tshape);
 cudaError_t launch_fused(const GemmArgs &a, int grid, cudaStream_t s, const void *maps);
 cudaError_t launch_pool_coords(const int64_t *pool, int4 *coords, const CoordJobs &jobs, cudaStream_t s);
 int gemm_max_grid(int max_ops);

@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(256) k_presum(const PresumArgs pa, const Presu
 
 static void presum_grid(const PresumArgs &a, int64_t &gx, int64_t &gy) {
   const int64_t fast_len = a.kfast ? a.klen : a.xlen, slow_len = a.kfast ? a.xlen : a.klen;
-  gx = fast_len > 0 ? FastMap(a.ustep, a.ugroup, 256).blocks(fast_len, 256) : 0;
+  gx = fast_len > 0 && a.out ? FastMap(a.ustep, a.ugroup, 256).blocks(fast_len, 256) : 0;  // out null: side not pre-summed
   gy = slow_len > 0 ? (slow_len + PRESUM_ROWS - 1) / PRESUM_ROWS : 0;
 }
 

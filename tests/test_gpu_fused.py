@@ -153,6 +153,37 @@ def test_tile_shapes_match_square_tiles_bitwise(line, shape):
             assert sp_.work_items == ss.work_items, (sp_.work_items, ss.work_items)
 
 
+@pytest.mark.parametrize("line", [
+    "abij abef efij & a:16;b:16;i:32;j:64;e:32;f:16;",   # m = 256: 64 x 256 tiles, A slots only
+    "abij abef efij & a:64;b:32;i:16;j:16;e:32;f:16;",   # n = 256: 256 x 64 tiles, B slots only
+    "aibj eafb jfie & a:16;b:16;i:16;j:128;e:16;f:32;",  # m = 256, permuted layouts
+])
+def test_one_sided_presum_matches_bitwise(line):
+    # one side's sums from k_presum slots, the other's formed in the kernel: every M
+    # element sees the same sums in the same order -> bitwise the in-kernel / both-sided C
+    spec = stc.parse_benchmark_line(line)
+    a, b, c0 = _operands(spec, 85)
+    classical = c0.copy()
+    oracle.contract_reference(spec, a.to_host(), b.to_host(), classical)
+    for level, variant in ((2, "abc"), (2, "ab"), (1, "abc")):
+        ref, _ = _run_env(spec, a, b, c0, level, variant, {"STC_PRESUM_OPS": "0", "STC_PRESUM_SIDES": "0"})
+        assert stc.relative_error(ref, classical) <= TOL
+        for sides in ("1", "2", "3"):
+            env = {"STC_PRESUM_SIDES": sides}
+            old = {k: os.environ.get(k) for k in env}
+            os.environ.update(env)
+            try:
+                info = stc.describe_plan(spec, a, b, c0, level, variant)
+            finally:
+                for k, v in old.items():
+                    os.environ.pop(k) if v is None else os.environ.__setitem__(k, v)
+            cs, st = _run_env(spec, a, b, c0, level, variant, env)
+            assert np.array_equal(cs.data, ref.data), (line, level, variant, sides, info)
+            assert st.leaf_multiplies == 7 ** level
+    # the default plan of the 64-wide case at L2 takes the one-sided slots
+    assert stc.describe_plan(spec, a, b, c0, 2, "abc")["presum_sides"] in (1, 2)
+
+
 def test_fused_matches_oracle_strassen():
     # the oracle's own L2 ABC Strassen on the same inputs (different summation
     # order inside the leaf GEMMs, so compared in norm)
