@@ -20,6 +20,7 @@ CONFIGS = {
                                                                  (2, "naive")]),
     "cfg3a": ("abij abef efij & a:16;b:16;i:16;j:16;e:64;f:64;", [(1, "abc"), (2, "abc")]),
     "cfg3e": ("abij abef efij & a:256;b:256;i:16;j:16;e:64;f:64;", [(1, "abc"), (2, "abc")]),
+    "cfg3m": ("abij abef efij & a:16;b:16;i:256;j:256;e:64;f:64;", [(1, "abc"), (2, "abc")]),
     "cfg4": ("abcij eafbc ifje & a:50;b:7;c:13;i:70;j:45;e:90;f:33;", [(1, "ab"), (1, "naive"), (2, "ab"),
                                                                        (2, "naive"), (2, "abc"), (0, "abc")]),
     "cfg2s": ("aibj eafb jfie & a:32;b:64;i:32;j:64;e:32;f:64;", [(2, "abc"), (1, "abc"), (0, "abc"), (2, "ab"),
