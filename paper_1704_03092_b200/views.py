@@ -57,8 +57,8 @@ PAD = _lib.PAD
 # GPU tiling of the fused DMMA kernel (csrc/stc_fused.cu), the counterpart of the
 # reference's BlockingParams: fixed, not configurable per call.
 TILE = {
-    "cta_tile": (128, 128),              # 64 x 256 / 256 x 64 for 64-wide quadrants (dense-M launches)
-    "warp_tile": (64, 32),               # 8 consumer warps, mma.sync.m16n8k4.f64 (DMMA) fragments
+    "cta_tile": (128, 128),              # 64 x 256 / 256 x 64 for 64-wide quadrants, 64 x 128 for small problems
+    "warp_tile": (64, 32),               # 8 consumer warps (32 x 32 on the 64 x 128 tiles), m16n8k4.f64 (DMMA)
     "k_chunk": 8,                        # one TMA box per view per stage: 128 x 8 doubles
     "stages": "8 with one view per side (L0, pre-summed or Naive slots); 6 / 3 with 2 / 4 views per side",
     "producer_warps": 4,                 # warp 0 issues the TMA loads, warps 1-3 run the C epilogue

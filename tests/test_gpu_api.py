@@ -251,3 +251,38 @@ def test_grid_blocks_on_one_gpu_match_unsharded():
         for rank in range(gm * gn):
             shard.contract_grid(spec, a, b, c, 2, "abc", rank, gm, gn)
         assert stc.relative_error(c, full) < 1e-12, (gm, gn)
+
+
+# ---- small-problem path: CUDA-graph replay of a plan's launch sequence ------------
+def test_graph_replay_follows_inputs_and_pointers():
+    # a small problem replays a graph captured for its (A, B, C, workspace) pointers: new
+    # values in the same buffers, a second C buffer (a second graph) and the graph-free
+    # path must all give the oracle's result, bitwise equal to one another
+    import os
+
+    import torch
+
+    spec = stc.parse_benchmark_line("abij abef efij & a:24;b:24;i:24;j:24;e:24;f:24;")  # cfg1
+    a, b, c = _tensors(spec, 1301, fill="int")
+    da, db = a.to_device(), b.to_device()
+    cs = [c.to_device(), c.to_device()]
+    for level, variant in ((1, "abc"), (2, "abc"), (1, "ab"), (2, "naive")):
+        for it in range(4):
+            # integer values: the result is exact, so every path must equal the oracle
+            vals = np.random.default_rng(it + 10 * level).integers(-64, 65, da.data.numel()).astype(np.float64)
+            da.data.copy_(torch.from_numpy(vals))
+            ha = stc.DenseTensor(a.extents, a.strides, vals)
+            cd = cs[it % 2]
+            cd.data.zero_()
+            st = stc.contract(spec, da, db, cd, level, variant)
+            ref = stc.DenseTensor(c.extents, c.strides, np.zeros(c.data.size))
+            oracle.contract_reference(spec, ha, b, ref)
+            assert np.array_equal(cd.to_host().data, ref.data), (level, variant, it)
+            assert st.leaf_multiplies == 7 ** level
+        os.environ["STC_NO_GRAPH"] = "1"  # the direct launches, same inputs as the last replay
+        try:
+            cs[0].data.zero_()
+            stc.contract(spec, da, db, cs[0], level, variant)
+        finally:
+            del os.environ["STC_NO_GRAPH"]
+        assert np.array_equal(cs[0].to_host().data, ref.data), (level, variant)
