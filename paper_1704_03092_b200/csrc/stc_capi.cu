@@ -32,6 +32,8 @@ namespace {
 thread_local std::string g_err;
 thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;  // stc_set_kernel_events
 thread_local const int32_t *g_c_ready = nullptr;                        // stc_set_c_ready
+thread_local stc::SlotOverride g_slot_ovr;                                // stc::set_slot_override
+thread_local bool g_slot_ovr_set = false;
 
 int fail(int code, const char *fmt, ...) {
   char buf[512];
@@ -1611,6 +1613,22 @@ bool plan_ticketed(const stc_problem *p) {
   return pl->ticketed;
 }
 
+bool plan_slot_bytes(const stc_problem *p, size_t &a_bytes, size_t &b_bytes) {
+  a_bytes = b_bytes = 0;
+  std::shared_ptr<const Plan> pl;
+  const int sms = gemm_max_grid(MAX_OPS);
+  if (cached_plan(p, pl, sms > 0 ? sms : 0)) return false;
+  if (!pl->presum || pl->presum_sides != 3 || pl->nbatches != 1 || pl->variant == STC_VARIANT_NAIVE) return false;
+  a_bytes = (size_t)pl->batch * pl->pa_slot * 8;
+  b_bytes = (size_t)pl->batch * pl->pb_slot * 8;
+  return true;
+}
+
+void set_slot_override(const SlotOverride *o) {
+  g_slot_ovr_set = o != nullptr;
+  g_slot_ovr = o ? *o : SlotOverride{};
+}
+
 }  // namespace stc
 
 // ======================================================================== ABI
@@ -1643,7 +1661,7 @@ int stc_workspace_size(const stc_problem *p, size_t *bytes) {
 // workspace region for this operand mode, already ordered before s (null: build it).
 static int contract_run(const stc_problem *p, const Plan &pl, const double *A, const double *B, double *C, char *ws,
                  cudaStream_t s, const int32_t *c_ready, cudaEvent_t ev_before, cudaEvent_t ev_after, bool direct,
-                 bool packed, int mode, int dev, const void *snap, stc_stats *stats) {
+                 bool packed, int mode, int dev, const void *snap, const SlotOverride *ovr, stc_stats *stats) {
   // The constant region is read where it lives: in the plan's snapshot once there is
   // one (nothing to restore), else in the workspace, where this call builds it.  Only
   // the tickets and work counters at its end are per call (zeroed in the workspace).
@@ -1667,7 +1685,10 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
   // per call: zero the tickets and counters (by the first k_presum launch when there is one)
   int32_t *const zero = restored ? tickets : nullptr;
   const int64_t zero_words = (int64_t)((pl.off_const - pl.off_tickets) / 4);
-  if (restored && !pl.presum) {
+  const bool shared_slots = ovr && pl.presum && pl.presum_sides == 3 && pl.nbatches == 1;
+  const bool skip_a = shared_slots && ovr->skip_a, skip_b = shared_slots && ovr->skip_b;
+  const bool presum_runs = pl.presum && !(skip_a && skip_b);
+  if (restored && !presum_runs) {
     CU(cudaMemsetAsync(ws + pl.off_tickets, 0, pl.off_const - pl.off_tickets, s), "zero tickets");
   } else if (!restored) {
     if (int rc = upload(pl.vecs.data(), pl.vecs.size() * sizeof(VecDesc), ws + pl.off_vecs, s, ws + pl.off_tickets,
@@ -1779,8 +1800,8 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
       // pre-summed operands: per batch of terms (exec order), one k_presum pass per side
       // writes the batch's operand sums into their slots, then one fused launch runs
       // the batch's items with one view per side (C updates ticket-ordered as ever)
-      double *PA = reinterpret_cast<double *>(ws + pl.off_pa);
-      double *PB = reinterpret_cast<double *>(ws + pl.off_pb);
+      double *PA = shared_slots && ovr->pa ? ovr->pa : reinterpret_cast<double *>(ws + pl.off_pa);
+      double *PB = shared_slots && ovr->pb ? ovr->pb : reinterpret_cast<double *>(ws + pl.off_pb);
       CoordJobs jobs{};
       if (!plan_fused(p, pl, naive_sides(pl), PA, PB, C, gf, maps, jobs))
         return fail(STC_EINVAL, "internal: pre-summed plan");
@@ -1795,12 +1816,15 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
       if (gf.cred) gf.mscratch = reinterpret_cast<double *>(ws + pl.off_mscr);
       for (int bi = 0; bi < pl.nbatches; ++bi) {
         const int t0 = bi * pl.batch, nb = std::min(T - t0, pl.batch);
-        PresumArgs pa = presum_args(pl, 0, A, PA, pool, t0, t0 + nb);
-        if (bi == 0 && zero) {
-          pa.zero = zero;
-          pa.zero_words = zero_words;
+        if (presum_runs) {
+          PresumArgs pa = presum_args(pl, 0, A, skip_a ? nullptr : PA, pool, t0, t0 + nb);
+          if (bi == 0 && zero) {
+            pa.zero = zero;
+            pa.zero_words = zero_words;
+          }
+          CU(launch_presum2(pa, presum_args(pl, 1, B, skip_b ? nullptr : PB, pool, t0, t0 + nb), s), "k_presum");
         }
-        CU(launch_presum2(pa, presum_args(pl, 1, B, PB, pool, t0, t0 + nb), s), "k_presum");
+        if (shared_slots && ovr->after_presum) CU(cudaEventRecord(ovr->after_presum, s), "cudaEventRecord");
         gf.terms = g.terms + t0;
         gf.nterms = nb;
         gf.total_items = (int)(P * nb);
@@ -1847,8 +1871,8 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
     // operands) or the operands' own / repacked views (AB); per batch of terms the slots,
     // one DMMA launch writing dense M, one ordered accumulate into C
     double *M = reinterpret_cast<double *>(ws + pl.off_M);
-    double *PA = reinterpret_cast<double *>(ws + pl.off_pa);
-    double *PB = reinterpret_cast<double *>(ws + pl.off_pb);
+    double *PA = shared_slots && ovr->pa ? ovr->pa : reinterpret_cast<double *>(ws + pl.off_pa);
+    double *PB = shared_slots && ovr->pb ? ovr->pb : reinterpret_cast<double *>(ws + pl.off_pb);
     const bool slot_a = slots && (pl.variant == STC_VARIANT_NAIVE || (pl.presum_sides & 1));
     const bool slot_b = slots && (pl.variant == STC_VARIANT_NAIVE || (pl.presum_sides & 2));
     struct Batch {
@@ -2006,13 +2030,17 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
       const int nb = b.t1 - b.t0;
       if (slots && pl.presum) {
         // one pass per side: every element position's 4^L quadrant values -> the batch's sums
-        PresumArgs pa = presum_args(pl, 0, A, slot_a ? PA : nullptr, pool, b.t0, b.t1);
-        if (bi == 0 && zero) {
-          pa.zero = zero;
-          pa.zero_words = zero_words;
+        if (presum_runs) {
+          PresumArgs pa = presum_args(pl, 0, A, slot_a && !skip_a ? PA : nullptr, pool, b.t0, b.t1);
+          if (bi == 0 && zero) {
+            pa.zero = zero;
+            pa.zero_words = zero_words;
+          }
+          CU(launch_presum2(pa, presum_args(pl, 1, B, slot_b && !skip_b ? PB : nullptr, pool, b.t0, b.t1), s),
+             "k_presum");
+          ++launches;
         }
-        CU(launch_presum2(pa, presum_args(pl, 1, B, slot_b ? PB : nullptr, pool, b.t0, b.t1), s), "k_presum");
-        ++launches;
+        if (shared_slots && ovr->after_presum) CU(cudaEventRecord(ovr->after_presum, s), "cudaEventRecord");
       } else if (slots) {
         UnpackArgs ua{};
         ua.pool = pool;
@@ -2138,6 +2166,10 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
   g_c_ready = nullptr;
   cudaEvent_t ev_before = g_ev_before, ev_after = g_ev_after;
   g_ev_before = g_ev_after = nullptr;
+  SlotOverride ovr_v = g_slot_ovr;
+  const SlotOverride *ovr = g_slot_ovr_set ? &ovr_v : nullptr;
+  g_slot_ovr_set = false;
+  g_slot_ovr = SlotOverride{};
   int dev = 0;
   CU(cudaGetDevice(&dev), "cudaGetDevice");
   Resident *res = pl.res.get();
@@ -2147,7 +2179,7 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
   const double flops = 2.0 * (double)pl.tm * (double)pl.tn * (double)pl.kq_pad *
                        (double)((pl.mq_pad / pl.tm) * (pl.nq_pad / pl.tn)) * (double)pl.terms.size();
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  const bool graphs = res && !ev_before && !ev_after && !c_ready && flops <= kGraphFlops && !getenv("STC_NO_GRAPH") &&
+  const bool graphs = res && !ev_before && !ev_after && !c_ready && !ovr && flops <= kGraphFlops && !getenv("STC_NO_GRAPH") &&
                       !getenv("STC_NO_SNAPSHOT") && cudaStreamIsCapturing(s, &cap) == cudaSuccess &&
                       cap == cudaStreamCaptureStatusNone;
   const GraphKey key{A, B, C, ws, dev, 0};
@@ -2183,7 +2215,8 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
   cudaStream_t cs = capture_stream(dev);
   if (graphs && snap && cs && cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
     stc_stats st{};
-    const int rc = contract_run(p, pl, A, B, C, ws, cs, nullptr, nullptr, nullptr, direct, packed, mode, dev, snap, &st);
+    const int rc =
+        contract_run(p, pl, A, B, C, ws, cs, nullptr, nullptr, nullptr, direct, packed, mode, dev, snap, nullptr, &st);
     cudaGraph_t graph = nullptr;
     const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
     cudaGraphExec_t exec = nullptr;
@@ -2204,7 +2237,8 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
     cudaGetLastError();  // nothing ran: fall through to direct launches
     if (rc != STC_OK && ec == cudaSuccess) return rc;
   }
-  return contract_run(p, pl, A, B, C, ws, s, c_ready, ev_before, ev_after, direct, packed, mode, dev, snap, stats);
+  return contract_run(p, pl, A, B, C, ws, s, c_ready, ev_before, ev_after, direct, packed, mode, dev, snap, ovr,
+                      stats);
 }
 
 int stc_bundle_scatter(const stc_bundle *bundle, int64_t base, int64_t out_len, int64_t *out, void *stream) {

@@ -61,7 +61,7 @@ int herr(int code, const char *fmt, ...) {
 
 constexpr int64_t kMinRunBytes = 4096;          // shortest copy run worth splitting for
 constexpr int64_t kMinSplitBytes = 32ll << 20;  // smaller problems: one piece
-constexpr int kMaxPieces = 32;
+constexpr int kMaxPieces = 64;
 constexpr size_t kFlagBytes = 256;  // per-piece "C piece arrived" flags, after the piece workspaces
 
 // Page-locked constants the flags are copied from: kMaxPieces zeros, then kMaxPieces ones.
@@ -204,7 +204,9 @@ Split choose_split(const stc_problem &p) {
   if (!C.compact()) return best;
   // I x J grid (STC_HOST_GRID=SAxSB forces it, "1" disables): for problems of 16 GB and
   // more a 1-D cut must upload a whole operand before the first piece can start (cfg5:
-  // 8.6 GB, 0.17 s); a 4 x 4 grid starts after a quarter of each (0.08 s)
+  // 8.6 GB, 0.17 s); a 4 x 8 grid starts after a quarter of A and an eighth of B (0.06 s).
+  // With the pieces sharing their operand slots (Share) the finer grid costs no extra
+  // pre-summing: cfg5 e2e 4 x 4 1637 ms, 4 x 8 1609 ms (8 x 8: 1877 ms, pieces too thin)
   const char *genv = getenv("STC_HOST_GRID");
   int ga = 0, gb = 0;
   if (genv && sscanf(genv, "%dx%d", &ga, &gb) != 2) ga = gb = 0;
@@ -213,7 +215,7 @@ Split choose_split(const stc_problem &p) {
     const bool forced = ga > 0;
     int la = 0, lb = 0, sa = 0, sb = 0;
     int64_t ra = 0, rb = 0;
-    if (best_cut(p, 0, forced ? ga : 4, forced, la, sa, ra) && best_cut(p, 1, forced ? gb : 4, forced, lb, sb, rb) &&
+    if (best_cut(p, 0, forced ? ga : 4, forced, la, sa, ra) && best_cut(p, 1, forced ? gb : 8, forced, lb, sb, rb) &&
         sa * sb <= kMaxPieces && (forced || (sa >= 2 && sb >= 2))) {
       best.la = la;
       best.sa = sa;
@@ -370,6 +372,42 @@ int piece_workspace(const stc_problem &p, const Split &sp, size_t &per_slot) {
   return STC_OK;
 }
 
+// Operand slots shared between the pieces of a grid (SlotOverride): the pre-summed A
+// slots of I range r are formed once, by piece (r, 0), into one of two alternating
+// buffers, and read by the pieces (r, 1..); the B slots of J range c once, by piece
+// (0, c), into buffer c.  Without it every piece re-forms both (cfg5, 4 x 4 grid: 43 ms
+// of pre-summing instead of 11).  Needs a uniform grid whose pieces pre-sum both sides
+// in one batch; STC_HOST_SHARE=0 disables.
+struct Share {
+  bool on = false;
+  size_t a_bytes = 0, b_bytes = 0;  // one A / one B slot buffer (256-aligned)
+  size_t bytes(const Split &sp) const { return on ? 2 * a_bytes + (size_t)sp.sb * b_bytes : 0; }
+};
+
+Share plan_share(const stc_problem &p, const Split &sp) {
+  Share sh;
+  if (sp.sa < 2 || sp.sb < 2) return sh;
+  if (const char *e = getenv("STC_HOST_SHARE"))
+    if (atoi(e) == 0) return sh;
+  size_t a0 = 0, b0 = 0;
+  for (int s = 0; s < sp.pieces; ++s) {
+    const PieceRange pr = piece_range(p, sp, s);
+    const stc_problem q = piece_problem(p, sp, pr.i0, pr.ni, pr.j0, pr.nj);
+    size_t a = 0, b = 0;
+    if (!plan_slot_bytes(&q, a, b)) return sh;
+    if (s == 0) {
+      a0 = a;
+      b0 = b;
+    } else if (a != a0 || b != b0) {
+      return sh;  // pieces of different shapes: their slots differ
+    }
+  }
+  sh.on = a0 > 0 && b0 > 0;
+  sh.a_bytes = align256(a0);
+  sh.b_bytes = align256(b0);
+  return sh;
+}
+
 // RAII set of events, destroyed after enqueue (the runtime releases them when
 // the work they mark completes).
 struct Events {
@@ -414,7 +452,7 @@ int stc_host_workspace_size(const stc_problem *p, size_t *bytes) {
   const Split sp = choose_split(*p);
   size_t per = 0;
   if (int rc = piece_workspace(*p, sp, per)) return rc;
-  size_t need = per * (sp.pieces > 1 ? 2 : 1) + kFlagBytes;
+  size_t need = per * (sp.pieces > 1 ? 2 : 1) + kFlagBytes + plan_share(*p, sp).bytes(sp);
   if (bytes) *bytes = need;
   return STC_OK;
 }
@@ -427,9 +465,10 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
   size_t per = 0;
   if (int rc = piece_workspace(*p, sp, per)) return rc;
   const int slots = sp.pieces > 1 ? 2 : 1;
-  if (!workspace || workspace_bytes < per * slots + kFlagBytes)
-    return herr(STC_EWORKSPACE, "workspace too small: need %zu bytes, got %zu", per * slots + kFlagBytes,
-                workspace_bytes);
+  const Share share = plan_share(*p, sp);
+  const size_t need = per * slots + kFlagBytes + share.bytes(sp);
+  if (!workspace || workspace_bytes < need)
+    return herr(STC_EWORKSPACE, "workspace too small: need %zu bytes, got %zu", need, workspace_bytes);
   if (reinterpret_cast<uintptr_t>(workspace) & 255) return herr(STC_EINVAL, "workspace must be 256-byte aligned");
   // the pieces: an I range x a J range each (the grid of choose_split)
   std::vector<stc_problem> parts;
@@ -542,14 +581,34 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
   const bool alternate = plan_ticketed(&parts[0]);
   stc_stats total{};
   char *ws = reinterpret_cast<char *>(workspace);
+  char *shared = ws + per * slots + kFlagBytes;  // A slot buffers [2], then B slot buffers [sb]
+  std::vector<cudaEvent_t> formed(sp.pieces, nullptr);  // piece (r, 0) / (0, c): its slots are formed
   for (int s = 0; s < sp.pieces; ++s) {
     cudaStream_t cs = hs->comp[alternate ? s % slots : 0];
     HCU(cudaStreamWaitEvent(cs, opin[s], 0), "cudaStreamWaitEvent");
     if (trace) HCU(cudaEventRecord(tr[2 + 4 * s], cs), "cudaEventRecord");
+    SlotOverride ovr;
+    const int r = s / sp.sb, c = s % sp.sb;
+    if (share.on) {
+      ovr.pa = reinterpret_cast<double *>(shared + (r % 2) * share.a_bytes);
+      ovr.pb = reinterpret_cast<double *>(shared + 2 * share.a_bytes + c * share.b_bytes);
+      ovr.skip_a = c > 0;
+      ovr.skip_b = r > 0;
+      if (c > 0) HCU(cudaStreamWaitEvent(cs, formed[r * sp.sb], 0), "cudaStreamWaitEvent");
+      if (r > 0) HCU(cudaStreamWaitEvent(cs, formed[c], 0), "cudaStreamWaitEvent");
+      if (c == 0 && r >= 2)  // A buffer r % 2: the pieces of I range r - 2 are done reading it
+        for (int k = 0; k < sp.sb; ++k) HCU(cudaStreamWaitEvent(cs, done[(r - 2) * sp.sb + k], 0), "cudaStreamWaitEvent");
+      if (c == 0 || r == 0) {
+        HCU(E.make(formed[s]), "cudaEventCreate");
+        ovr.after_presum = formed[s];
+      }
+    }
     stc_stats st{};
     stc_set_c_ready(flags + s);
+    if (share.on) set_slot_override(&ovr);
     if (int rc = stc_contract(&parts[s], dA, dB, dC, ws + (s % slots) * per, per, cs, &st)) {
       stc_set_c_ready(nullptr);
+      set_slot_override(nullptr);
       return rc;
     }
     HCU(E.make(done[s]), "cudaEventCreate");

@@ -218,6 +218,19 @@ cudaError_t launch_fused(const GemmArgs &a, int grid, cudaStream_t s, const void
 cudaError_t launch_pool_coords(const int64_t *pool, int4 *coords, const CoordJobs &jobs, cudaStream_t s);
 int gemm_max_grid(int max_ops);
 bool plan_ticketed(const stc_problem *p);  // stc_capi.cu
+// Operand-slot sharing between the pieces of stc_contract_host (stc_capi.cu): a piece
+// whose A (B) block another piece already pre-summed reads those slots instead of
+// forming them again.  slot_bytes: bytes of the A / B slots of the problem's plan
+// (0 unless it pre-sums both sides in one batch).  The override applies to the next
+// stc_contract on this thread: slots at pa / pb, presum of a side skipped when
+// skip_a / skip_b, `after_presum` (if set) recorded once the slots are formed.
+bool plan_slot_bytes(const stc_problem *p, size_t &a_bytes, size_t &b_bytes);
+struct SlotOverride {
+  double *pa = nullptr, *pb = nullptr;
+  bool skip_a = false, skip_b = false;
+  cudaEvent_t after_presum = nullptr;
+};
+void set_slot_override(const SlotOverride *o);
 cudaError_t launch_accumulate(const AccArgs &a, cudaStream_t s);
 cudaError_t launch_unpack(const UnpackArgs &a, cudaStream_t s);
 cudaError_t launch_presum2(const PresumArgs &pa, const PresumArgs &pb, cudaStream_t s);  // both sides, one launch

@@ -245,3 +245,26 @@ def test_host_grid_pieces_integer_exact(grid):
         sa, sb = (int(x) for x in grid.split("x"))
         assert st.pieces == sa * sb and st.leaf_multiplies == 7 ** level, st
         assert np.array_equal(c.data.numpy(), ref.data), (grid, level, variant)
+
+
+@pytest.mark.parametrize("grid", ["2x2", "4x2", "4x4"])
+def test_host_grid_shared_slots_match_unshared_bitwise(grid):
+    # pieces of a grid that pre-sum both sides share the slots of their A rows / B columns
+    # (formed once by the first piece of each); the C blocks must equal those of pieces
+    # that form their own slots, bit for bit, and the oracle's classical result
+    spec = stc.parse_benchmark_line("abij abef efij & a:32;b:16;i:32;j:16;e:32;f:16;")
+    a, b, c0 = (_tensor(spec, l, s, False) for l, s in ((spec.labels_a, 31), (spec.labels_b, 32), (spec.labels_c, 33)))
+    ref = c0.copy()
+    oracle.contract_reference(spec, a, b, ref, threads=oracle.max_threads())
+    for level, variant in ((2, "abc"), (1, "abc"), (2, "ab")):
+        outs = []
+        for share in ("1", "0"):
+            c = _pinned(c0.copy())
+            env = {"STC_HOST_GRID": grid, "STC_PRESUM_OPS": "1", "STC_HOST_SHARE": share}
+            st = _with_env(env, lambda: stc.contract(spec, _pinned(a), _pinned(b), c, level, variant))
+            sa, sb = (int(x) for x in grid.split("x"))
+            assert st.pieces == sa * sb and st.leaf_multiplies == 7 ** level, st
+            outs.append(c.data.numpy().copy())
+        assert np.array_equal(outs[0], outs[1]), (grid, level, variant)
+        got = stc.DenseTensor(c0.extents, c0.strides, outs[0])
+        assert oracle.relative_error(got, ref) <= TOL

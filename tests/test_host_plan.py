@@ -132,9 +132,9 @@ def _grid(line, env=None):
 
 
 def test_large_problems_get_an_i_by_j_grid():
-    # cfg5 (24 GiB of operands): 4 x 4 pieces, the outermost label of each bundle
+    # cfg5 (24 GiB of operands): 4 x 8 pieces, the outermost label of each bundle
     spec, (la, sa, lb, sb) = _grid("abcijk abcefg efgijk & a:32;b:32;c:32;i:32;j:32;k:32;e:32;f:32;g:32;")
-    assert (sa, sb) == (4, 4)
+    assert (sa, sb) == (4, 8)
     assert spec.bundle_i[la] == "a" and spec.bundle_j[lb] == "i"
     # STC_HOST_GRID=1 keeps the 1-D cut; a forced 2 x 8 grid
     assert _grid("abcijk abcefg efgijk & a:32;b:32;c:32;i:32;j:32;k:32;e:32;f:32;g:32;",

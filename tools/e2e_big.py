@@ -1,6 +1,7 @@
 """e2e (pinned host operands) of a large config at several host-pipeline piece counts, with the
 per-piece device timeline (STC_HOST_TRACE=1 prints it on stderr).
-Usage: python tools/e2e_big.py "<benchmark line>" level variant pieces...   (pieces: default | N)"""
+Usage: python tools/e2e_big.py "<benchmark line>" level variant setting...
+(setting: default | N pieces | K=V,K=V environment, e.g. STC_HOST_GRID=8x8,STC_HOST_SHARE=0)"""
 import os
 import pathlib
 import sys
@@ -33,8 +34,9 @@ a, b = pinned(spec.labels_a, 1), pinned(spec.labels_b, 2)
 ec = spec.tensor_extents(spec.labels_c)
 c = stc.DenseTensor(ec, row_major(ec), torch.zeros(int(np.prod(ec)), dtype=torch.float64, pin_memory=True))
 for p in sys.argv[4:]:
-    if p != "default":
-        os.environ["STC_HOST_PIECES"] = p
+    env = dict(kv.split("=") for kv in p.split(",")) if "=" in p else ({} if p == "default" else {"STC_HOST_PIECES": p})
+    saved = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     stc.contract(spec, a, b, c, level, variant)
     torch.cuda.synchronize()
     ts = []
@@ -45,4 +47,8 @@ for p in sys.argv[4:]:
     dt = min(ts)
     print(f"pieces={p} ({st.pieces}): e2e {dt * 1e3:.1f} ms  {flops / dt / 1e12:.2f} TF/s  "
           f"device {st.device_seconds * 1e3:.1f} ms", flush=True)
-    os.environ.pop("STC_HOST_PIECES", None)
+    for k, v in saved.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
