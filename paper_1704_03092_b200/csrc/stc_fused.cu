@@ -339,12 +339,15 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
   const int (&offA)[2][2] = oA;
   const int (&offB)[2][2] = oB;
   double fa[8], fb[4], xa[8], xb[4];
+  // stage (bits 0-15) and phase (bit 16) in one register through the loop: kept apart,
+  // ptxas spilled the phase (a local load + store per chunk next to the DMMAs)
+  uint32_t sp = (uint32_t)stage | (phase << 16);
   pipe_view<NA, NB, 0, 0, false, SGN, AV, BV, MT>(acc, fa, fb, fa, fb, stages + stage * sstride, true, offA, offB, negmask,
                                               bbase);
   for (int c = 0; c < kchunks; ++c) {
     // k-step 0 of chunk c (fa, fb) -> build k-step 1 of chunk c (xa, xb)
-    pipe_view<NA, NB, 0, 1, true, SGN, AV, BV, MT>(acc, fa, fb, xa, xb, stages + stage * sstride, true, offA, offB, negmask,
-                                               bbase);
+    pipe_view<NA, NB, 0, 1, true, SGN, AV, BV, MT>(acc, fa, fb, xa, xb, stages + (int)(sp & 0xffffu) * sstride, true,
+                                               offA, offB, negmask, bbase);
     // The stage's smem was read through the generic proxy and the producer refills it
     // with TMA (async proxy) once every consumer warp arrived: the proxy fence orders the
     // k-step 1 fragment loads just issued before the release.  Without it the refill
@@ -353,17 +356,17 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
     // those registers) is as safe but shortens the ring: 4-5% slower.
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);  // both k-steps of chunk c are in registers
-    if (++stage == S) {
-      stage = 0;
-      phase ^= 1;
-    }
+    if (lane == 0) mbar_arrive(&empty[sp & 0xffffu]);  // both k-steps of chunk c are in registers
+    ++sp;
+    if ((sp & 0xffffu) == (uint32_t)S) sp = (sp & 0x10000u) ^ 0x10000u;  // stage 0, phase flipped
     // k-step 1 of chunk c (xa, xb) -> build k-step 0 of chunk c + 1 (fa, fb)
     const bool more = c + 1 < kchunks;
-    if (more) mbar_wait(&full[stage], phase);
-    pipe_view<NA, NB, 0, 0, true, SGN, AV, BV, MT>(acc, xa, xb, fa, fb, stages + stage * sstride, more, offA, offB, negmask,
-                                               bbase);
+    if (more) mbar_wait(&full[sp & 0xffffu], sp >> 16);
+    pipe_view<NA, NB, 0, 0, true, SGN, AV, BV, MT>(acc, xa, xb, fa, fb, stages + (int)(sp & 0xffffu) * sstride, more,
+                                               offA, offB, negmask, bbase);
   }
+  stage = (int)(sp & 0xffffu);
+  phase = sp >> 16;
 }
 
 // TMA-reduce epilogue (ABC, C targets regular): for each C target in ticket
