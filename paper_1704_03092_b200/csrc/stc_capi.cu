@@ -366,11 +366,12 @@ struct Resident {
   std::vector<Graph> graphs;
   size_t graph_next = 0;
   ~Resident() {
-    for (Graph &g : graphs) cudaGraphExecDestroy(g.exec);
+    // cudaFree waits for the device's pending work (the graphs' replays read buf)
     for (int i = 0; i < 2; ++i) {
       if (buf[i]) cudaFree(buf[i]);
       if (ev[i]) cudaEventDestroy(ev[i]);
     }
+    for (Graph &g : graphs) cudaGraphExecDestroy(g.exec);
   }
   // Launch the graph of `key` on s; false if there is none (or the launch failed).
   bool replay(const GraphKey &key, cudaStream_t s, stc_stats &st) {
