@@ -1556,7 +1556,7 @@ struct PlanEntry {
 std::mutex g_plan_mu;
 std::vector<PlanEntry> g_plans;
 size_t g_plan_next = 0;
-constexpr size_t kPlanCache = 32;
+constexpr size_t kPlanCache = 128;  // (a 4 x 8 host grid alone plans 32-34 pieces)
 
 std::string plan_env() {
   static const char *knobs[] = {"STC_WORKSPACE_CAP_MB", "STC_EXEC_ORDER", "STC_PACK", "STC_TMA_PROMO",

@@ -303,13 +303,15 @@ cudaError_t copy_block(double *dst, const double *src, const TensorLabels &t, in
     std::swap(x0, y0);
     std::swap(xn, yn);
   }
-  // outer label x (stride xs), inner y: within one x index, rows of ye * ys elements
-  const int64_t pitch = ye * ys, rows = xs / pitch;
-  for (int64_t v = x0; v < x0 + xn; ++v) {
-    const int64_t off = t.base + v * xs + y0 * ys;
-    cudaError_t e = cudaMemcpy2DAsync(dst + off, pitch * 8, src + off, pitch * 8, yn * ys * 8, rows, kind, s);
-    if (e != cudaSuccess) return e;
-  }
+  // outer label x (stride xs), inner y: within one x index, rows of ye * ys elements;
+  // the labels outside x (strides >= xs * xe, compact) are `outer` blocks of xs * xe
+  const int64_t pitch = ye * ys, rows = xs / pitch, outer = t.elems() / (xs * xe);
+  for (int64_t o = 0; o < outer; ++o)
+    for (int64_t v = x0; v < x0 + xn; ++v) {
+      const int64_t off = t.base + o * xs * xe + v * xs + y0 * ys;
+      cudaError_t e = cudaMemcpy2DAsync(dst + off, pitch * 8, src + off, pitch * 8, yn * ys * 8, rows, kind, s);
+      if (e != cudaSuccess) return e;
+    }
   return cudaSuccess;
 }
 
@@ -356,10 +358,54 @@ struct DrainOnError {
   }
 };
 
+// The first cell of a grid split in two along one label of the P bundle: its two runs
+// (k halves, one after the other on one stream, adding into the same C block) start
+// after half of its A and B blocks arrived (cfg5, 4 x 8: 27 ms instead of 53 ms of PCIe
+// before the first DMMA).  The label: the P label with the largest stride in A of even
+// extent (long copy runs).  STC_HOST_KSPLIT=0 disables.
+struct KSplit {
+  bool on = false;
+  int lk = 0;                           // the P bundle label
+  int64_t k0[2] = {0, 0}, kn[2] = {0, 0};  // its halves
+};
+
+KSplit plan_ksplit(const stc_problem &p, const Split &sp) {
+  KSplit ks;
+  if (sp.sa < 2 || sp.sb < 2) return ks;
+  if (const char *e = getenv("STC_HOST_KSPLIT"))
+    if (atoi(e) == 0) return ks;
+  int best = -1;
+  for (int d = 0; d < p.a_col.nlab; ++d)
+    if (p.a_col.ext[d] >= 2 && p.a_col.ext[d] % 2 == 0 && (best < 0 || p.a_col.str[d] > p.a_col.str[best])) best = d;
+  if (best < 0) return ks;
+  // halves of at least two 16-deep chunks per quadrant
+  int64_t k = 1;
+  for (int d = 0; d < p.a_col.nlab; ++d) k *= p.a_col.ext[d];
+  if (k / 2 < ((int64_t)2 << p.level) * 16) return ks;
+  ks.on = true;
+  ks.lk = best;
+  const int64_t e = p.a_col.ext[best];
+  ks.k0[0] = 0;
+  ks.kn[0] = e / 2;
+  ks.k0[1] = e / 2;
+  ks.kn[1] = e - e / 2;
+  return ks;
+}
+
+// Half kh of a cell's problem: the split P label's extent in A and B halved, bases moved.
+stc_problem half_problem(const stc_problem &cell, const KSplit &ks, int kh) {
+  stc_problem q = cell;
+  q.a_col.ext[ks.lk] = ks.kn[kh];
+  q.b_row.ext[ks.lk] = ks.kn[kh];
+  q.a_base += ks.k0[kh] * cell.a_col.str[ks.lk];
+  q.b_base += ks.k0[kh] * cell.b_row.str[ks.lk];
+  return q;
+}
+
 // Workspace of one piece slot: the largest over the pieces (their plans differ in the
 // base offsets, which can change the path -- e.g. whether a view is a TMA box -- and
 // with it the workspace).
-int piece_workspace(const stc_problem &p, const Split &sp, size_t &per_slot) {
+int piece_workspace(const stc_problem &p, const Split &sp, const KSplit &ks, size_t &per_slot) {
   size_t most = 256;
   for (int s = 0; s < sp.pieces; ++s) {
     const PieceRange pr = piece_range(p, sp, s);
@@ -367,6 +413,12 @@ int piece_workspace(const stc_problem &p, const Split &sp, size_t &per_slot) {
     size_t b = 0;
     if (int rc = stc_workspace_size(&q, &b)) return rc;
     most = std::max(most, b);
+    if (s == 0 && ks.on)
+      for (int kh = 0; kh < 2; ++kh) {
+        const stc_problem h = half_problem(q, ks, kh);
+        if (int rc = stc_workspace_size(&h, &b)) return rc;
+        most = std::max(most, b);
+      }
   }
   per_slot = align256(most);
   return STC_OK;
@@ -451,7 +503,7 @@ int stc_host_workspace_size(const stc_problem *p, size_t *bytes) {
   if (!p) return herr(STC_EINVAL, "null problem");
   const Split sp = choose_split(*p);
   size_t per = 0;
-  if (int rc = piece_workspace(*p, sp, per)) return rc;
+  if (int rc = piece_workspace(*p, sp, plan_ksplit(*p, sp), per)) return rc;
   size_t need = per * (sp.pieces > 1 ? 2 : 1) + kFlagBytes + plan_share(*p, sp).bytes(sp);
   if (bytes) *bytes = need;
   return STC_OK;
@@ -462,22 +514,38 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
   if (!p) return herr(STC_EINVAL, "null problem");
   if (!hA || !hB || !hC || !dA || !dB || !dC) return herr(STC_EINVAL, "null operand pointer");
   const Split sp = choose_split(*p);
+  const KSplit ks = plan_ksplit(*p, sp);
   size_t per = 0;
-  if (int rc = piece_workspace(*p, sp, per)) return rc;
+  if (int rc = piece_workspace(*p, sp, ks, per)) return rc;
   const int slots = sp.pieces > 1 ? 2 : 1;
   const Share share = plan_share(*p, sp);
   const size_t need = per * slots + kFlagBytes + share.bytes(sp);
   if (!workspace || workspace_bytes < need)
     return herr(STC_EWORKSPACE, "workspace too small: need %zu bytes, got %zu", need, workspace_bytes);
   if (reinterpret_cast<uintptr_t>(workspace) & 255) return herr(STC_EINVAL, "workspace must be 256-byte aligned");
-  // the pieces: an I range x a J range each (the grid of choose_split)
-  std::vector<stc_problem> parts;
+  // the cells: an I range x a J range each (the grid of choose_split); the runs: one
+  // contraction per cell, or -- the first cell k-split (KSplit) -- two in k order
   std::vector<PieceRange> ranges;
+  std::vector<stc_problem> cells;
   for (int s = 0; s < sp.pieces; ++s) {
     const PieceRange pr = piece_range(*p, sp, s);
-    parts.push_back(sp.pieces > 1 ? piece_problem(*p, sp, pr.i0, pr.ni, pr.j0, pr.nj) : *p);
+    cells.push_back(sp.pieces > 1 ? piece_problem(*p, sp, pr.i0, pr.ni, pr.j0, pr.nj) : *p);
     ranges.push_back(pr);
   }
+  struct Run {
+    int cell, kh;  // kh: -1 the whole k range, 0 / 1 the halves of KSplit
+    stc_problem prob;
+  };
+  std::vector<Run> runs;
+  for (int s = 0; s < sp.pieces; ++s) {
+    if (s == 0 && ks.on) {
+      runs.push_back({0, 0, half_problem(cells[0], ks, 0)});
+      runs.push_back({0, 1, half_problem(cells[0], ks, 1)});
+    } else {
+      runs.push_back({s, -1, cells[s]});
+    }
+  }
+  const int nruns = (int)runs.size();
   HostStreams *hs = nullptr;
   if (int rc = host_streams(hs)) return rc;
   DrainOnError drain;
@@ -494,45 +562,57 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
   HCU(E.make(start), "cudaEventCreate");
   HCU(E.make(end), "cudaEventCreate");
   HCU(cudaEventRecord(start, us), "cudaEventRecord");
-  // STC_HOST_TRACE=1: timing events per piece (inputs in, compute start / end, C out), printed to stderr
+  // STC_HOST_TRACE=1: timing events per run (inputs in, compute start / end, C out), printed to stderr
   const bool trace = getenv("STC_HOST_TRACE") != nullptr;
-  std::vector<cudaEvent_t> tr(trace ? 1 + 4 * sp.pieces : 0);
+  std::vector<cudaEvent_t> tr(trace ? 1 + 4 * nruns : 0);
   for (auto &e : tr) HCU(cudaEventCreate(&e), "cudaEventCreate");
   if (trace) HCU(cudaEventRecord(tr[0], us), "cudaEventRecord");
   for (cudaStream_t s : {hs->h2d, hs->d2h, hs->comp[0], hs->comp[1]})
     HCU(cudaStreamWaitEvent(s, start, 0), "cudaStreamWaitEvent");
 
   // uploads: the operand all pieces share, then (operand piece, C piece, flag) per piece.
-  // A piece's kernels start once its operands are in (event opin) and wait on the
-  // device for its flag before their first access to C (stc_set_c_ready), so the
-  // C upload overlaps the piece's first MMAs.
+  // A run's kernels start once its operands are in (event opin) and wait on the
+  // device for its cell's flag before their first access to C (stc_set_c_ready), so
+  // the C upload overlaps the piece's first MMAs.
   const int32_t *pf = pinned_flag_values();
   if (!pf) return herr(STC_ECUDA, "cudaHostAlloc failed for the piece flags");
   int32_t *flags = reinterpret_cast<int32_t *>(reinterpret_cast<char *>(workspace) + per * slots);
   HCU(cudaMemcpyAsync(flags, pf, sp.pieces * sizeof(int32_t), cudaMemcpyHostToDevice, hs->h2d),
       "cudaMemcpyAsync(flags)");
-  std::vector<cudaEvent_t> opin(sp.pieces), done(sp.pieces);
-  auto c_arrived = [&](int s) -> int {
-    HCU(cudaMemcpyAsync(flags + s, pf + kMaxPieces, sizeof(int32_t), cudaMemcpyHostToDevice, hs->h2d),
+  std::vector<cudaEvent_t> opin(nruns), done(nruns);
+  std::vector<int> first_run(sp.pieces, -1), last_run(sp.pieces, -1);  // of each cell
+  for (int k = 0; k < nruns; ++k) {
+    if (first_run[runs[k].cell] < 0) first_run[runs[k].cell] = k;
+    last_run[runs[k].cell] = k;
+  }
+  auto c_arrived = [&](int cell) -> int {
+    HCU(cudaMemcpyAsync(flags + cell, pf + kMaxPieces, sizeof(int32_t), cudaMemcpyHostToDevice, hs->h2d),
         "cudaMemcpyAsync(flag)");
-    if (trace) HCU(cudaEventRecord(tr[1 + 4 * s], hs->h2d), "cudaEventRecord");
+    if (trace) HCU(cudaEventRecord(tr[1 + 4 * first_run[cell]], hs->h2d), "cudaEventRecord");
     return STC_OK;
   };
-  // A's I range r (all of A when the I bundle is not cut), B's J range c, C's block
-  auto copy_a = [&](int r) -> cudaError_t {
-    if (sp.sa == 1) return copy_span(dA, hA, A, cudaMemcpyHostToDevice, hs->h2d);
+  // A's I range r (all of A when the I bundle is not cut), B's J range c, C's block;
+  // kh >= 0: only the k half kh of them (the k-split first cell)
+  auto copy_a = [&](int r, int kh) -> cudaError_t {
     const PieceRange &pr = ranges[r * sp.sb];
+    if (kh >= 0)
+      return copy_block(dA, hA, A, p->a_row.str[sp.la], p->a_row.ext[sp.la], pr.i0, pr.ni, p->a_col.str[ks.lk],
+                        p->a_col.ext[ks.lk], ks.k0[kh], ks.kn[kh], cudaMemcpyHostToDevice, hs->h2d);
+    if (sp.sa == 1) return copy_span(dA, hA, A, cudaMemcpyHostToDevice, hs->h2d);
     return copy_piece(dA, hA, A, p->a_row.str[sp.la], p->a_row.ext[sp.la], pr.i0, pr.ni, cudaMemcpyHostToDevice,
                       hs->h2d);
   };
-  auto copy_b = [&](int c) -> cudaError_t {
-    if (sp.sb == 1) return copy_span(dB, hB, B, cudaMemcpyHostToDevice, hs->h2d);
+  auto copy_b = [&](int c, int kh) -> cudaError_t {
     const PieceRange &pr = ranges[c];
+    if (kh >= 0)
+      return copy_block(dB, hB, B, p->b_row.str[ks.lk], p->b_row.ext[ks.lk], ks.k0[kh], ks.kn[kh],
+                        p->b_col.str[sp.lb], p->b_col.ext[sp.lb], pr.j0, pr.nj, cudaMemcpyHostToDevice, hs->h2d);
+    if (sp.sb == 1) return copy_span(dB, hB, B, cudaMemcpyHostToDevice, hs->h2d);
     return copy_piece(dB, hB, B, p->b_col.str[sp.lb], p->b_col.ext[sp.lb], pr.j0, pr.nj, cudaMemcpyHostToDevice,
                       hs->h2d);
   };
-  auto copy_c = [&](double *dst, const double *src, int s, cudaMemcpyKind kind, cudaStream_t st) -> cudaError_t {
-    const PieceRange &pr = ranges[s];
+  auto copy_c = [&](double *dst, const double *src, int cell, cudaMemcpyKind kind, cudaStream_t st) -> cudaError_t {
+    const PieceRange &pr = ranges[cell];
     if (sp.sa > 1 && sp.sb > 1)
       return copy_block(dst, src, C, p->c_row.str[sp.la], p->c_row.ext[sp.la], pr.i0, pr.ni, p->c_col.str[sp.lb],
                         p->c_col.ext[sp.lb], pr.j0, pr.nj, kind, st);
@@ -540,33 +620,41 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
     if (sp.sb > 1) return copy_piece(dst, src, C, p->c_col.str[sp.lb], p->c_col.ext[sp.lb], pr.j0, pr.nj, kind, st);
     return copy_span(dst, src, C, kind, st);
   };
-  // uploads in piece order: A's range r, B's range c (first row of the grid only), then
-  // the piece's C block and its arrival flag
-  for (int r = 0; r < sp.sa; ++r) {
-    HCU(copy_a(r), "cudaMemcpyAsync(A piece)");
-    for (int c = 0; c < sp.sb; ++c) {
-      const int s = r * sp.sb + c;
-      if (r == 0) HCU(copy_b(c), "cudaMemcpyAsync(B piece)");
-      HCU(E.make(opin[s]), "cudaEventCreate");
-      HCU(cudaEventRecord(opin[s], hs->h2d), "cudaEventRecord");
-      HCU(copy_c(dC, hC, s, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(C piece)");
-      if (int rc = c_arrived(s)) return rc;
+  // uploads in run order: A's range r, B's range c (first row of the grid only), then the
+  // cell's C block and its arrival flag; the k-split first cell: its halves' A and B
+  // blocks one after the other (the first half's run starts after half the data)
+  for (int k = 0; k < nruns; ++k) {
+    const Run &ru = runs[k];
+    const int r = ru.cell / sp.sb, c = ru.cell % sp.sb;
+    if (ru.kh >= 0) {
+      HCU(copy_a(r, ru.kh), "cudaMemcpyAsync(A piece)");
+      HCU(copy_b(c, ru.kh), "cudaMemcpyAsync(B piece)");
+    } else {
+      if (c == 0) HCU(copy_a(r, -1), "cudaMemcpyAsync(A piece)");
+      if (r == 0) HCU(copy_b(c, -1), "cudaMemcpyAsync(B piece)");
+    }
+    HCU(E.make(opin[k]), "cudaEventCreate");
+    HCU(cudaEventRecord(opin[k], hs->h2d), "cudaEventRecord");
+    if (k == first_run[ru.cell]) {
+      HCU(copy_c(dC, hC, ru.cell, cudaMemcpyHostToDevice, hs->h2d), "cudaMemcpyAsync(C piece)");
+      if (int rc = c_arrived(ru.cell)) return rc;
     }
   }
-  // plan every piece before any of them is launched (the uploads above only fill
-  // the caller's device buffers; on an error they are drained before returning)
-  for (int s = 0; s < sp.pieces; ++s) {
-    size_t need = 0;
-    if (int rc = stc_workspace_size(&parts[s], &need)) {
+  // plan every run before any of them is launched (the uploads above only fill the
+  // caller's device buffers; on an error they are drained before returning)
+  for (int k = 0; k < nruns; ++k) {
+    size_t nb = 0;
+    if (int rc = stc_workspace_size(&runs[k].prob, &nb)) {
       cudaStreamSynchronize(hs->h2d);
       return rc;
     }
   }
-  // download of piece s's C once the piece finished
-  auto download = [&](int s) -> int {
-    HCU(cudaStreamWaitEvent(hs->d2h, done[s], 0), "cudaStreamWaitEvent");
-    HCU(copy_c(hC, dC, s, cudaMemcpyDeviceToHost, hs->d2h), "cudaMemcpyAsync(C piece)");
-    if (trace) HCU(cudaEventRecord(tr[4 + 4 * s], hs->d2h), "cudaEventRecord");
+  // download of a cell's C once its last run finished
+  auto download = [&](int k) -> int {
+    const int cell = runs[k].cell;
+    HCU(cudaStreamWaitEvent(hs->d2h, done[k], 0), "cudaStreamWaitEvent");
+    HCU(copy_c(hC, dC, cell, cudaMemcpyDeviceToHost, hs->d2h), "cudaMemcpyAsync(C piece)");
+    if (trace) HCU(cudaEventRecord(tr[4 + 4 * k], hs->d2h), "cudaEventRecord");
     return STC_OK;
   };
   // page-locked C: each download is enqueued right behind its piece (asynchronous);
@@ -577,43 +665,58 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
   // pieces on alternating compute streams (workspace slot = stream), so piece s+1's
   // CTAs fill the SMs of piece s's last wave -- unless the pieces run through dense M
   // slots (stc_contract's dense-M ABC mode, AB, Naive): their accumulate kernels would
-  // then wait behind the next piece's persistent kernel, and one stream is faster
-  const bool alternate = plan_ticketed(&parts[0]);
+  // then wait behind the next piece's persistent kernel, and one stream is faster.
+  // The runs of one cell (k halves) update the same C block: the later waits for the
+  // earlier.
+  const bool alternate = plan_ticketed(&cells[0]);
   stc_stats total{};
   char *ws = reinterpret_cast<char *>(workspace);
   char *shared = ws + per * slots + kFlagBytes;  // A slot buffers [2], then B slot buffers [sb]
-  std::vector<cudaEvent_t> formed(sp.pieces, nullptr);  // piece (r, 0) / (0, c): its slots are formed
-  for (int s = 0; s < sp.pieces; ++s) {
-    cudaStream_t cs = hs->comp[alternate ? s % slots : 0];
-    HCU(cudaStreamWaitEvent(cs, opin[s], 0), "cudaStreamWaitEvent");
-    if (trace) HCU(cudaEventRecord(tr[2 + 4 * s], cs), "cudaEventRecord");
+  // the run forming the shared slots of A range r / B range c: the first whole-k run of
+  // the row / column (KSplit's halves form their own)
+  std::vector<int> form_a(sp.sa, -1), form_b(sp.sb, -1);
+  for (int k = 0; k < nruns; ++k) {
+    if (runs[k].kh >= 0) continue;
+    const int r = runs[k].cell / sp.sb, c = runs[k].cell % sp.sb;
+    if (form_a[r] < 0) form_a[r] = k;
+    if (form_b[c] < 0) form_b[c] = k;
+  }
+  std::vector<cudaEvent_t> formed(nruns, nullptr);
+  for (int k = 0; k < nruns; ++k) {
+    const Run &ru = runs[k];
+    const int r = ru.cell / sp.sb, c = ru.cell % sp.sb;
+    cudaStream_t cs = hs->comp[alternate ? k % slots : 0];
+    HCU(cudaStreamWaitEvent(cs, opin[k], 0), "cudaStreamWaitEvent");
+    if (k > first_run[ru.cell]) HCU(cudaStreamWaitEvent(cs, done[k - 1], 0), "cudaStreamWaitEvent");
+    if (trace) HCU(cudaEventRecord(tr[2 + 4 * k], cs), "cudaEventRecord");
     SlotOverride ovr;
-    const int r = s / sp.sb, c = s % sp.sb;
-    if (share.on) {
+    const bool shares = share.on && ru.kh < 0 && form_a[r] >= 0 && form_b[c] >= 0;
+    if (shares) {
       ovr.pa = reinterpret_cast<double *>(shared + (r % 2) * share.a_bytes);
       ovr.pb = reinterpret_cast<double *>(shared + 2 * share.a_bytes + c * share.b_bytes);
-      ovr.skip_a = c > 0;
-      ovr.skip_b = r > 0;
-      if (c > 0) HCU(cudaStreamWaitEvent(cs, formed[r * sp.sb], 0), "cudaStreamWaitEvent");
-      if (r > 0) HCU(cudaStreamWaitEvent(cs, formed[c], 0), "cudaStreamWaitEvent");
-      if (c == 0 && r >= 2)  // A buffer r % 2: the pieces of I range r - 2 are done reading it
-        for (int k = 0; k < sp.sb; ++k) HCU(cudaStreamWaitEvent(cs, done[(r - 2) * sp.sb + k], 0), "cudaStreamWaitEvent");
-      if (c == 0 || r == 0) {
-        HCU(E.make(formed[s]), "cudaEventCreate");
-        ovr.after_presum = formed[s];
+      ovr.skip_a = k != form_a[r];
+      ovr.skip_b = k != form_b[c];
+      if (ovr.skip_a) HCU(cudaStreamWaitEvent(cs, formed[form_a[r]], 0), "cudaStreamWaitEvent");
+      if (ovr.skip_b) HCU(cudaStreamWaitEvent(cs, formed[form_b[c]], 0), "cudaStreamWaitEvent");
+      if (!ovr.skip_a && r >= 2)  // A buffer r % 2: the runs of I range r - 2 are done reading it
+        for (int j = 0; j < nruns; ++j)
+          if (runs[j].cell / sp.sb == r - 2) HCU(cudaStreamWaitEvent(cs, done[j], 0), "cudaStreamWaitEvent");
+      if (!ovr.skip_a || !ovr.skip_b) {
+        HCU(E.make(formed[k]), "cudaEventCreate");
+        ovr.after_presum = formed[k];
       }
     }
     stc_stats st{};
-    stc_set_c_ready(flags + s);
-    if (share.on) set_slot_override(&ovr);
-    if (int rc = stc_contract(&parts[s], dA, dB, dC, ws + (s % slots) * per, per, cs, &st)) {
+    stc_set_c_ready(flags + ru.cell);
+    if (shares) set_slot_override(&ovr);
+    if (int rc = stc_contract(&ru.prob, dA, dB, dC, ws + (k % slots) * per, per, cs, &st)) {
       stc_set_c_ready(nullptr);
       set_slot_override(nullptr);
       return rc;
     }
-    HCU(E.make(done[s]), "cudaEventCreate");
-    HCU(cudaEventRecord(done[s], cs), "cudaEventRecord");
-    if (trace) HCU(cudaEventRecord(tr[3 + 4 * s], cs), "cudaEventRecord");
+    HCU(E.make(done[k]), "cudaEventCreate");
+    HCU(cudaEventRecord(done[k], cs), "cudaEventRecord");
+    if (trace) HCU(cudaEventRecord(tr[3 + 4 * k], cs), "cudaEventRecord");
     total.total_flops += st.total_flops;
     total.fast_blocks += st.fast_blocks;
     total.slow_blocks += st.slow_blocks;
@@ -622,21 +725,24 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
     total.leaf_multiplies = std::max(total.leaf_multiplies, st.leaf_multiplies);
     total.work_items += st.work_items;
     total.kernel_launches += st.kernel_launches;
-    if (locked)
-      if (int rc = download(s)) return rc;
+    if (locked && k == last_run[ru.cell])
+      if (int rc = download(k)) return rc;
   }
   if (!locked)
-    for (int s = 0; s < sp.pieces; ++s)
-      if (int rc = download(s)) return rc;
+    for (int k = 0; k < nruns; ++k)
+      if (k == last_run[runs[k].cell])
+        if (int rc = download(k)) return rc;
   HCU(cudaEventRecord(end, hs->d2h), "cudaEventRecord");
   if (trace) {
     cudaEventSynchronize(end);
     float t = 0;
-    fprintf(stderr, "[stc host] pieces=%d (I label %d x %d, J label %d x %d):", sp.pieces, sp.la, sp.sa, sp.lb, sp.sb);
-    for (int s = 0; s < sp.pieces; ++s) {
-      fprintf(stderr, " |%d", s);
-      for (int k = 0; k < 4; ++k) {
-        cudaEventElapsedTime(&t, tr[0], tr[1 + 4 * s + k]);
+    fprintf(stderr, "[stc host] runs=%d (I label %d x %d, J label %d x %d, k-split first cell %d):", nruns, sp.la,
+            sp.sa, sp.lb, sp.sb, ks.on ? 1 : 0);
+    for (int k = 0; k < nruns; ++k) {
+      fprintf(stderr, " |%d", k);
+      for (int j = 0; j < 4; ++j) {
+        const int idx = j == 0 ? first_run[runs[k].cell] : j == 3 ? last_run[runs[k].cell] : k;
+        cudaEventElapsedTime(&t, tr[0], tr[1 + 4 * idx + j]);
         fprintf(stderr, " %.2f", t);
       }
     }
@@ -645,7 +751,7 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
   }
   HCU(cudaStreamWaitEvent(us, end, 0), "cudaStreamWaitEvent");
   drain.armed = false;
-  total.pieces = sp.pieces;
+  total.pieces = nruns;
   if (stats) *stats = total;
   return STC_OK;
 }
