@@ -38,6 +38,8 @@ CONFIGS = {
     # cfg5 host-pipeline pieces: 4 x 8 grid (8192 x 4096) and 8 x 8 (4096 x 4096), k = 32768
     "cfg5p48": ("abcijk abcefg efgijk & a:8;b:32;c:32;i:4;j:32;k:32;e:32;f:32;g:32;", [(2, "abc")]),
     "cfg5p88": ("abcijk abcefg efgijk & a:4;b:32;c:32;i:4;j:32;k:32;e:32;f:32;g:32;", [(2, "abc")]),
+    "cfg5v": ("abcijk abcefg efgijk & a:32;b:32;c:32;i:32;j:32;k:32;e:32;f:32;g:32;", [(2, "ab"), (2, "naive"),
+                                                                                      (1, "abc"), (0, "abc")]),
     "cfg5": ("abcijk abcefg efgijk & a:32;b:32;c:32;i:32;j:32;k:32;e:32;f:32;g:32;", [(2, "abc")]),
 }
 
