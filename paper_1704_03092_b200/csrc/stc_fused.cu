@@ -487,7 +487,7 @@ __device__ __forceinline__ void epilogue_warps(const GemmArgs &p, uint64_t *epi_
   const int lane = t & 31;
   bool c_seen = false;
   for (;;) {
-    mbar_wait(&epi_full[eb], ephase);
+    mbar_wait_parked(&epi_full[eb], ephase);
     const int item = epi_item[eb];
     if (item < 0) break;
     if (p.c_ready && !c_seen) {  // stc_set_c_ready
@@ -566,7 +566,7 @@ __device__ __forceinline__ void epilogue_warps_red(const GemmArgs &p, uint64_t *
   const int lane = t & 31;
   bool c_seen = false;
   for (;;) {
-    mbar_wait(&epi_full[eb], ephase);
+    mbar_wait_parked(&epi_full[eb], ephase);
     const int item = epi_item[eb];
     if (item < 0) break;
     if (p.c_ready && !c_seen) {  // stc_set_c_ready
