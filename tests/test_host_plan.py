@@ -144,3 +144,33 @@ def test_large_problems_get_an_i_by_j_grid():
     # small problems stay 1-D
     _, (la, sa, lb, sb) = _grid("aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;")
     assert sa * sb == 4 and min(sa, sb) == 1
+
+
+# ---- device-path planning (stc_plan_describe; host-only, grid of 148 SMs) ------------
+def _describe(line, level, variant="abc"):
+    import sys
+
+    sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1] / "tools"))
+    from describe import describe
+
+    return describe(line, level, variant)
+
+
+@pytest.mark.parametrize("line,level,tshape,sides", [
+    # cfg3 2^24, m = 256 / n = 256 at L2: 64-wide quadrants -> the narrow tiles, one-sided slots
+    ("abij abef efij & a:16;b:16;i:256;j:256;e:64;f:64;", 2, 1, 1),
+    ("abij abef efij & a:256;b:256;i:16;j:16;e:64;f:64;", 2, 2, 2),
+    # cfg1 (576^3): the items do not fill the SMs -> 64 x 128 tiles, both sides pre-summed
+    ("abij abef efij & a:24;b:24;i:24;j:24;e:24;f:24;", 1, 3, 3),
+    ("abij abef efij & a:24;b:24;i:24;j:24;e:24;f:24;", 2, 3, 3),
+    # cfg5 and cfg2: 128 x 128 tiles, both sides pre-summed, ticketed
+    ("abcijk abcefg efgijk & a:32;b:32;c:32;i:32;j:32;k:32;e:32;f:32;g:32;", 2, 0, 3),
+    ("aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;", 2, 0, 3),
+])
+def test_plan_shapes_and_slot_sides(line, level, tshape, sides):
+    info = _describe(line, level)
+    assert info["tshape"] == tshape, info
+    assert info["presum"] == 1 and info["presum_sides"] == sides, info
+    if tshape in (1, 2, 3):
+        assert info["ticketed"] == 0, info  # the narrow / small shapes write dense M
+    assert info["terms"] == 7 ** level
