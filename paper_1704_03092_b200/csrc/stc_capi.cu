@@ -460,7 +460,7 @@ struct Plan {
   int max_ops = 1;  // most views on one side of any term (2^L)
   size_t off_kbs = 0, off_coords = 0, off_mscr = 0, off_pka = 0, off_pkb = 0;
   bool need_pack = false;  // fused kernel on repacked operands (layout not box-regular)
-  int tshape = 0;          // fused kernel CTA tile shape (stc_fused.cu Shape): 0 128 x 128, 1 64 x 256, 2 256 x 64, 3 64 x 128
+  int tshape = 0;          // fused kernel CTA tile shape (stc_fused.cu Shape): 0 128 x 128, 1 64 x 256, 2 256 x 64, 3 64 x 128, 4 128 x 64
   int64_t tm = BM, tn = BN;  // its tile rows / columns (quadrants padded to them)
   // ABC with C updated straight from the kernel, ticket-ordered per C tile; false for AB,
   // Naive and the dense-M ABC mode (many terms in flight per tile: dense M slots, then one
@@ -613,6 +613,17 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   pl.mq = cdiv(pl.m, pl.Q);
   pl.nq = cdiv(pl.n, pl.Q);
   pl.kq = cdiv(pl.k, pl.Q);
+  // tile orders per bundle (see make_tiling)
+  const bool ref = (p->flags & STC_FLAG_REFERENCE_TILING) != 0;
+  const int a_min = min_stride_side(p->a_row, p->a_col);
+  const int b_min = min_stride_side(p->b_row, p->b_col);
+  const int c_min = min_stride_side(p->c_row, p->c_col);
+  const int64_t *key_i = a_min == 0 ? p->a_row.str : (c_min == 0 ? p->c_row.str : p->a_row.str);
+  const int64_t *key_j = b_min == 1 ? p->b_col.str : (c_min == 1 ? p->c_col.str : p->b_col.str);
+  const int64_t *key_p = a_min == 1 ? p->a_col.str : (b_min == 0 ? p->b_row.str : p->a_col.str);
+  const Tiling ti = make_tiling(p->a_row, pl.level, key_i, ref);
+  const Tiling tj = make_tiling(p->b_col, pl.level, key_j, ref);
+  const Tiling tp = make_tiling(p->a_col, pl.level, key_p, ref);
   // CTA tile shape: 64 x 256 (256 x 64) when the I (J) quadrants are at most 64 past a
   // multiple of 128 -- a 128-row tile would be half padding -- for the dense-M launches
   // with the summing warpgroup (AB, ABC with such C tiles, L >= 1); see shape_usable
@@ -631,38 +642,35 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     // quadrants) keeps 128 x 128 (87 % useful) over 256 x 64 (84 %)
     const int64_t a0 = rup(pl.mq, BM) * rup(pl.nq, BN), a1 = rup(pl.mq, 64) * rup(pl.nq, 256),
                   a2 = rup(pl.mq, 256) * rup(pl.nq, 64);
+    const int64_t a4 = rup(pl.mq, BM) * rup(pl.nq, 64);
+    // (shape 4, 128 x 64: dense-M plans only -- AB, Naive slots excluded above, ABC whose C
+    // tiles are not TMA-reduce boxes -- with at least 15 % less padded area: its 32 x 32
+    // warp tiles cost ~7 % per flop, cfg4 L2's 7 % less padding bought nothing; cfg1 L2
+    // (144-wide quadrants, 25 % less) 50.7 -> 48.7 us)
+    const bool dense_anyway = pl.variant != STC_VARIANT_ABC || !c_boxes_regular(p, ti, tj, pl.level);
     if (allowed && pl.mq % BM != 0 && pl.mq % BM <= 64 && pl.nq >= 256 && a1 < a0) pl.tshape = 1;
     else if (allowed && pl.nq % BN != 0 && pl.nq % BN <= 64 && pl.mq >= 256 && a2 < a0) pl.tshape = 2;
+    else if (allowed && dense_anyway && (double)a4 <= 0.85 * (double)a0) pl.tshape = 4;
     // shape 3 (64 x 128, 32 x 32 warp tiles): for problems of a few waves, when its
     // waves x tile area -- the per-SM work in sequence -- is clearly below the chosen
     // shape's (cfg1 L1: 105 items in one wave instead of 70; L2: 294 items in two waves
     // instead of 196 in two of twice the work).  Dense M output (grid >= 4 tiles per term).
     const int64_t T = (int64_t)std::pow(7.0, pl.level), grid = grid_hint > 0 ? grid_hint : 148;
-    const int64_t tm0 = pl.tshape == 1 ? 64 : pl.tshape == 2 ? 256 : BM, tn0 = pl.tshape == 1 ? 256 : pl.tshape == 2 ? 64 : BN;
+    const int64_t tm0 = pl.tshape == 1 ? 64 : pl.tshape == 2 ? 256 : BM,
+                  tn0 = pl.tshape == 1 ? 256 : pl.tshape == 2 || pl.tshape == 4 ? 64 : BN;
     const int64_t p_cur = cdiv(pl.mq, tm0) * cdiv(pl.nq, tn0), p3 = cdiv(pl.mq, 64) * cdiv(pl.nq, 128);
     const int64_t waves_cur = cdiv(T * p_cur, grid), waves3 = cdiv(T * p3, grid);
     if (allowed && T > 1 && grid >= 4 * p3 && waves_cur <= 4 &&
         (double)waves3 * 64 * 128 < 0.85 * (double)waves_cur * tm0 * tn0)
       pl.tshape = 3;
-    if (allowed && ts && atoi(ts) > 0 && atoi(ts) <= 3) pl.tshape = atoi(ts);  // forced (diagnostics)
+    if (allowed && ts && atoi(ts) > 0 && atoi(ts) <= 4) pl.tshape = atoi(ts);  // forced (diagnostics)
   }
   pl.tm = pl.tshape == 1 || pl.tshape == 3 ? 64 : pl.tshape == 2 ? 256 : BM;
-  pl.tn = pl.tshape == 1 ? 256 : pl.tshape == 2 ? 64 : pl.tshape == 3 ? 128 : BN;
+  pl.tn = pl.tshape == 1 ? 256 : pl.tshape == 2 || pl.tshape == 4 ? 64 : pl.tshape == 3 ? 128 : BN;
   pl.mq_pad = rup(pl.mq, pl.tm);
   pl.nq_pad = rup(pl.nq, pl.tn);
   pl.kq_pad = rup(pl.kq, BK);
 
-  // tile orders per bundle (see make_tiling)
-  const bool ref = (p->flags & STC_FLAG_REFERENCE_TILING) != 0;
-  const int a_min = min_stride_side(p->a_row, p->a_col);
-  const int b_min = min_stride_side(p->b_row, p->b_col);
-  const int c_min = min_stride_side(p->c_row, p->c_col);
-  const int64_t *key_i = a_min == 0 ? p->a_row.str : (c_min == 0 ? p->c_row.str : p->a_row.str);
-  const int64_t *key_j = b_min == 1 ? p->b_col.str : (c_min == 1 ? p->c_col.str : p->b_col.str);
-  const int64_t *key_p = a_min == 1 ? p->a_col.str : (b_min == 0 ? p->b_row.str : p->a_col.str);
-  const Tiling ti = make_tiling(p->a_row, pl.level, key_i, ref);
-  const Tiling tj = make_tiling(p->b_col, pl.level, key_j, ref);
-  const Tiling tp = make_tiling(p->a_col, pl.level, key_p, ref);
   pl.ti = ti;
   pl.tj = tj;
   pl.tp = tp;
@@ -725,8 +733,10 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     // Also when the C targets are not regular boxes: the kernel's C updates would then
     // be load/add/store scatters in the consumers (cfg4 L2: 5.2 ms ticketed, 3.2 dense).
     const char *de = getenv("STC_ABC_DENSE");
+    // (the shaped tiles 1-4 write dense M only)
     const bool dense = T > 1 && (de ? atoi(de) != 0
-                                    : (pl.grid >= 4 * P || !c_boxes_regular(p, pl.ti, pl.tj, pl.level)));
+                                    : (pl.grid >= 4 * P || pl.tshape != 0 ||
+                                       !c_boxes_regular(p, pl.ti, pl.tj, pl.level)));
     pl.ticketed = !dense;
   }
   {
@@ -2122,7 +2132,7 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
       st.slow_updates += b.nupd;
     }
   }
-  st.total_flops = 2.0 * BM * BN * (double)pl.kq_pad * (double)P * (double)T;
+  st.total_flops = 2.0 * (double)pl.tm * (double)pl.tn * (double)pl.kq_pad * (double)P * (double)T;
   // operand blocks (one view of one side x one k-chunk per tile): TMA-staged
   // boxes are the reference's fast (constant-stride) blocks
   (tma ? st.fast_blocks : st.slow_blocks) += 2 * (int64_t)(pl.kq_pad / BK) * P * T;

@@ -43,10 +43,12 @@ constexpr int VIEW_DOUBLES = BM * FK;        // one raw view of one chunk (BM ==
 // for problems whose items do not fill the 148 SMs (cfg1 L1: 105 items of half the
 // work instead of 70), dense M output.  Every element still accumulates the same
 // DMMA k-steps in the same order: bitwise the 128 x 128 result.
+// 4: 128 x 64 on the 8 consumer warps with 32 x 32 warp tiles -- for quadrants whose J
+// extent is far from a multiple of 128 (cfg4 L2: 788 columns pad to 832 instead of 896).
 template <int TS>
 struct Shape {
-  static constexpr int MT = TS == 3 ? 2 : 4;  // m16 blocks per warp tile (16 MT rows x 32 columns)
-  static constexpr int WM = TS == 1 ? 1 : TS == 2 ? 4 : 2;
+  static constexpr int MT = TS == 3 || TS == 4 ? 2 : 4;  // m16 blocks per warp tile (16 MT rows x 32 columns)
+  static constexpr int WM = TS == 1 ? 1 : TS == 2 || TS == 4 ? 4 : 2;
   static constexpr int WN = CONSUMER_WARPS / WM;
   static constexpr int ACTIVE = WM * WN;  // consumer warps with a warp tile
   static constexpr int BMT = 16 * MT * WM, BNT = 32 * WN;
@@ -143,8 +145,10 @@ size_t fused_stage_doubles(int max_ops, int ts) { return fused_stage_doubles2(ma
 
 // ... with va A views and vb B views per chunk (one-sided pre-summed slots)
 size_t fused_stage_doubles2(int va, int vb, int ts) {
-  const int av = ts == 1 ? Shape<1>::AV : ts == 2 ? Shape<2>::AV : ts == 3 ? Shape<3>::AV : Shape<0>::AV;
-  const int bv = ts == 1 ? Shape<1>::BV : ts == 2 ? Shape<2>::BV : ts == 3 ? Shape<3>::BV : Shape<0>::BV;
+  const int av = ts == 1 ? Shape<1>::AV : ts == 2 ? Shape<2>::AV : ts == 3 ? Shape<3>::AV : ts == 4 ? Shape<4>::AV
+                                                                                           : Shape<0>::AV;
+  const int bv = ts == 1 ? Shape<1>::BV : ts == 2 ? Shape<2>::BV : ts == 3 ? Shape<3>::BV : ts == 4 ? Shape<4>::BV
+                                                                                           : Shape<0>::BV;
   return (size_t)va * av + (size_t)vb * bv;
 }
 
@@ -872,8 +876,8 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
     // a tile is padding (skip_item) still cover all four sub-partitions
     // shapes 1 / 2: warp = wn (WM = 1) or wm + 4 wn (WM = 4): all sub-partitions busy either way
     // shape 3: wm = warp / 4, wn = warp % 4: both row halves on every sub-partition
-    const int wm = TS == 1 ? 0 : TS == 2 ? warp & 3 : TS == 3 || p.warp_map ? warp >> 2 : warp & 1;
-    const int wn = TS == 1 ? (warp & 7) : TS == 2 ? warp >> 2 : TS == 3 || p.warp_map ? warp & 3 : warp >> 1;
+    const int wm = TS == 1 ? 0 : TS == 2 || TS == 4 ? warp & 3 : TS == 3 || p.warp_map ? warp >> 2 : warp & 1;
+    const int wn = TS == 1 ? (warp & 7) : TS == 2 || TS == 4 ? warp >> 2 : TS == 3 || p.warp_map ? warp & 3 : warp >> 1;
     const bool idle_warp = warp >= SH::ACTIVE;
     // Fragment offsets inside a view: A (kk, h) + 128 * mt; B (kk, nt & 1) + 128 * (nt >> 1).
     // MMA row (column) g + 8 h of each 16-row block (16-column pair) reads tile row
@@ -1041,10 +1045,12 @@ static FusedKernel fused_for_ts(int akf, int bkf) {
 static FusedKernel fused_for(int akf, int bkf, bool ps, int ts, bool one) {
   if (ps)
     return ts == 1 ? fused_for_ts<true, 1>(akf, bkf) : ts == 2 ? fused_for_ts<true, 2>(akf, bkf)
-           : ts == 3 ? fused_for_ts<true, 3>(akf, bkf) : fused_for_ts<true, 0>(akf, bkf);
+           : ts == 3 ? fused_for_ts<true, 3>(akf, bkf) : ts == 4 ? fused_for_ts<true, 4>(akf, bkf)
+                                                     : fused_for_ts<true, 0>(akf, bkf);
   if (one)
     return ts == 1 ? fused_for_ts<false, 1, true>(akf, bkf) : ts == 2 ? fused_for_ts<false, 2, true>(akf, bkf)
-           : ts == 3 ? fused_for_ts<false, 3, true>(akf, bkf) : fused_for_ts<false, 0, true>(akf, bkf);
+           : ts == 3 ? fused_for_ts<false, 3, true>(akf, bkf) : ts == 4 ? fused_for_ts<false, 4, true>(akf, bkf)
+                                                     : fused_for_ts<false, 0, true>(akf, bkf);
   return fused_for_ts<false, 0>(akf, bkf);
 }
 

@@ -160,9 +160,9 @@ def _describe(line, level, variant="abc"):
     # cfg3 2^24, m = 256 / n = 256 at L2: 64-wide quadrants -> the narrow tiles, one-sided slots
     ("abij abef efij & a:16;b:16;i:256;j:256;e:64;f:64;", 2, 1, 1),
     ("abij abef efij & a:256;b:256;i:16;j:16;e:64;f:64;", 2, 2, 2),
-    # cfg1 (576^3): the items do not fill the SMs -> 64 x 128 tiles, both sides pre-summed
-    ("abij abef efij & a:24;b:24;i:24;j:24;e:24;f:24;", 1, 3, 3),
-    ("abij abef efij & a:24;b:24;i:24;j:24;e:24;f:24;", 2, 3, 3),
+    # cfg1 (576^3): 288- / 144-wide quadrants -> 128 x 64 tiles (least padding), both sides pre-summed
+    ("abij abef efij & a:24;b:24;i:24;j:24;e:24;f:24;", 1, 4, 3),
+    ("abij abef efij & a:24;b:24;i:24;j:24;e:24;f:24;", 2, 4, 3),
     # cfg5 and cfg2: 128 x 128 tiles, both sides pre-summed, ticketed
     ("abcijk abcefg efgijk & a:32;b:32;c:32;i:32;j:32;k:32;e:32;f:32;g:32;", 2, 0, 3),
     ("aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;", 2, 0, 3),
@@ -171,6 +171,6 @@ def test_plan_shapes_and_slot_sides(line, level, tshape, sides):
     info = _describe(line, level)
     assert info["tshape"] == tshape, info
     assert info["presum"] == 1 and info["presum_sides"] == sides, info
-    if tshape in (1, 2, 3):
+    if tshape in (1, 2, 3, 4):
         assert info["ticketed"] == 0, info  # the narrow / small shapes write dense M
     assert info["terms"] == 7 ** level
