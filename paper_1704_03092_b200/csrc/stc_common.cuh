@@ -93,7 +93,7 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs &p, const double (
         }
     return;
   }
-  if constexpr (MT != 4) return;  // 32-row warp tiles run with dense M output only
+  if constexpr (MT == 4) {  // (32-row warp tiles run with dense M output only)
   for (int j = 0; j < td.c_count; ++j) {
     const TgtDesc tg = p.tgts[td.c_first + j];
     int32_t *ticket = p.tickets + tg.ticket_base + pos;
@@ -137,6 +137,7 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs &p, const double (
       named_bar(2, 32 * CONSUMER_WARPS);
       if (tid == 0) st_release_gpu(ticket, tg.order + 1);
     }
+  }
   }
 }
 
