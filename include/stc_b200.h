@@ -217,6 +217,21 @@ int stc_sq_norms(int ndim, const int64_t *extents, const double *x, const int64_
 int stc_shard_problem(const stc_problem *p, int world, int rank, int label, stc_problem *out, int64_t *start,
                       int64_t *stop, int32_t *label_out);
 
+/* The n-split driven from one process over `ngpu` devices (SURVEY.md 8(b)'s
+ * stc_contract_sharded; the reference has no distributed path): shard g (the
+ * sub-problem of stc_shard_problem with rank g, world ngpu, the same `label`)
+ * runs on devices[g] with that device's copies A[g] (all of A), B[g] and C[g]
+ * (full storage, the problem's layout), workspace[g] of workspace_bytes[g]
+ * (>= stc_sharded_workspace_size) on streams[g].  gather != 0: every device's
+ * C then receives the other shards' blocks by peer copies over NVLink
+ * (cudaMemcpy2DAsync between devices, after the producing shard's event) --
+ * the all-gather of C without a collective library; needs a compact C.
+ * Asynchronous on the streams; stats summed over the shards. */
+int stc_sharded_workspace_size(const stc_problem *p, int ngpu, int label, size_t *bytes);
+int stc_contract_sharded(const stc_problem *p, int ngpu, const int *devices, int label, const double *const *A,
+                         const double *const *B, double *const *C, void *const *workspace,
+                         const size_t *workspace_bytes, void *const *streams, int gather, stc_stats *stats);
+
 /* ---- plan introspection (tests / tools; no reference counterpart) ----
  * Which execution path stc_contract takes for a problem on a `grid`-CTA launch
  * (0: 148).  Host-only: needs no device. */

@@ -67,7 +67,7 @@ _EXPORTS = (
     "stc_block_vector", "stc_fused_term_workspace_size", "stc_fused_term", "stc_accumulate_dense",
     "stc_unpack_sum", "stc_sq_norms", "stc_set_kernel_events", "stc_set_c_ready",
     "stc_host_workspace_size", "stc_contract_host", "stc_host_plan", "stc_fill_uniform", "stc_plan_describe",
-    "stc_shard_problem", "stc_host_grid",
+    "stc_shard_problem", "stc_host_grid", "stc_sharded_workspace_size", "stc_contract_sharded",
 )
 
 _lib = None
@@ -103,6 +103,9 @@ def _declare(l):
     l.stc_plan_describe.argtypes = [P(Problem), ctypes.c_int, P(PlanInfo)]
     l.stc_shard_problem.argtypes = [P(Problem), ctypes.c_int, ctypes.c_int, ctypes.c_int, P(Problem), P(i64), P(i64),
                                     P(i32)]
+    l.stc_sharded_workspace_size.argtypes = [P(Problem), ctypes.c_int, ctypes.c_int, P(sz)]
+    l.stc_contract_sharded.argtypes = [P(Problem), ctypes.c_int, P(ctypes.c_int), ctypes.c_int, pp, pp, pp, pp,
+                                       P(sz), pp, ctypes.c_int, P(Stats)]
     for name in _EXPORTS:
         if name not in ("stc_last_error",):
             getattr(l, name).restype = ctypes.c_int if name != "stc_last_error" else ctypes.c_char_p

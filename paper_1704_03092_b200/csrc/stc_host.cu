@@ -756,4 +756,89 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
   return STC_OK;
 }
 
+int stc_sharded_workspace_size(const stc_problem *p, int ngpu, int label, size_t *bytes) {
+  if (!p || ngpu < 1) return herr(STC_EINVAL, "null problem or no devices");
+  size_t most = 256;
+  int32_t lab = label;
+  for (int g = 0; g < ngpu; ++g) {
+    stc_problem q;
+    if (int rc = stc_shard_problem(p, ngpu, g, lab, &q, nullptr, nullptr, &lab)) return rc;
+    size_t b = 0;
+    if (int rc = stc_workspace_size(&q, &b)) return rc;
+    most = std::max(most, b);
+  }
+  if (bytes) *bytes = most;
+  return STC_OK;
+}
+
+int stc_contract_sharded(const stc_problem *p, int ngpu, const int *devices, int label, const double *const *A,
+                         const double *const *B, double *const *C, void *const *workspace,
+                         const size_t *workspace_bytes, void *const *streams, int gather, stc_stats *stats) {
+  if (!p || ngpu < 1 || !devices || !A || !B || !C || !workspace || !workspace_bytes || !streams)
+    return herr(STC_EINVAL, "null argument or no devices");
+  const TensorLabels Ct = labels_of(p->c_row, p->c_col, p->c_base);
+  if (gather && ngpu > 1 && !Ct.compact()) return herr(STC_EINVAL, "gather needs a compact C (dense storage)");
+  int cur = 0;
+  HCU(cudaGetDevice(&cur), "cudaGetDevice");
+  struct Restore {
+    int dev;
+    ~Restore() { cudaSetDevice(dev); }
+  } restore{cur};
+  // the shards (the label fixed by shard 0's choice)
+  std::vector<stc_problem> q(ngpu);
+  std::vector<int64_t> s0(ngpu), s1(ngpu);
+  int32_t lab = label;
+  for (int g = 0; g < ngpu; ++g)
+    if (int rc = stc_shard_problem(p, ngpu, g, lab, &q[g], &s0[g], &s1[g], &lab)) return rc;
+  stc_set_c_ready(nullptr);
+  stc_set_kernel_events(nullptr, nullptr);
+  Events E;
+  std::vector<cudaEvent_t> done(ngpu);
+  stc_stats total{};
+  for (int g = 0; g < ngpu; ++g) {
+    HCU(cudaSetDevice(devices[g]), "cudaSetDevice");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(streams[g]);
+    stc_stats st{};
+    if (int rc = stc_contract(&q[g], A[g], B[g], C[g], workspace[g], workspace_bytes[g], s, &st)) return rc;
+    HCU(E.make(done[g]), "cudaEventCreate");
+    HCU(cudaEventRecord(done[g], s), "cudaEventRecord");
+    total.total_flops += st.total_flops;
+    total.fast_blocks += st.fast_blocks;
+    total.slow_blocks += st.slow_blocks;
+    total.fast_updates += st.fast_updates;
+    total.slow_updates += st.slow_updates;
+    total.leaf_multiplies = std::max(total.leaf_multiplies, st.leaf_multiplies);
+    total.work_items += st.work_items;
+    total.kernel_launches += st.kernel_launches;
+  }
+  if (gather && ngpu > 1) {
+    // peer access where the devices differ (an already enabled pair is fine)
+    for (int d = 0; d < ngpu; ++d)
+      for (int g = 0; g < ngpu; ++g)
+        if (devices[d] != devices[g]) {
+          int ok = 0;
+          if (cudaDeviceCanAccessPeer(&ok, devices[d], devices[g]) == cudaSuccess && ok) {
+            cudaSetDevice(devices[d]);
+            cudaDeviceEnablePeerAccess(devices[g], 0);
+          }
+          cudaGetLastError();
+        }
+    // device d's C gets shard g's block of C[g]: rows of the label's range at its pitch
+    const int64_t lstr = p->c_col.str[lab], lext = p->c_col.ext[lab];
+    for (int d = 0; d < ngpu; ++d) {
+      HCU(cudaSetDevice(devices[d]), "cudaSetDevice");
+      cudaStream_t s = reinterpret_cast<cudaStream_t>(streams[d]);
+      for (int g = 0; g < ngpu; ++g) {
+        if (g == d) continue;
+        HCU(cudaStreamWaitEvent(s, done[g], 0), "cudaStreamWaitEvent");
+        HCU(copy_piece(C[d], C[g], Ct, lstr, lext, s0[g], s1[g] - s0[g], cudaMemcpyDefault, s),
+            "cudaMemcpy2DAsync(peer C block)");
+      }
+    }
+  }
+  total.pieces = ngpu;
+  if (stats) *stats = total;
+  return STC_OK;
+}
+
 }  // extern "C"

@@ -22,7 +22,7 @@ import numpy as np
 from .tensor import ContractionSpec, DenseTensor
 
 __all__ = ["Shard", "plan_shards", "shard_tensor", "shard_spec", "contract_sharded", "gather_shards", "Block",
-           "plan_grid", "block_spec", "block_tensor", "contract_grid", "gather_blocks"]
+           "plan_grid", "block_spec", "block_tensor", "contract_grid", "gather_blocks", "contract_devices"]
 
 
 @dataclass(frozen=True)
@@ -242,3 +242,54 @@ def gather_blocks(spec: ContractionSpec, c: DenseTensor, rank: int, gm: int, gn:
     for blk, buf in zip(blocks, bufs):
         d = dense(blk)
         d.copy_(buf[: d.numel()].reshape(d.shape))
+
+
+# ---------------------------------------------------------------- one process, several GPUs
+def contract_devices(spec: ContractionSpec, a: list, b: list, c: list, level: int, variant, devices: list,
+                     label: str | None = None, gather: bool = True):
+    """The n-split driven from one process (C ABI stc_contract_sharded).
+
+    a[g], b[g], c[g]: device g's copies (DenseTensors with CUDA storage on
+    devices[g], the full tensors' layouts); shard g of C (plan_shards order) is
+    contracted on devices[g], and with `gather` every device's C then gets the
+    other shards' blocks by peer copies over NVLink -- no collective library.
+    Synchronises the devices' current streams before returning; returns the
+    summed RunStats (pieces = number of devices).
+    """
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .stats import RunStats
+    from .strassen import _variant, problem_of
+
+    n = len(devices)
+    if not (len(a) == len(b) == len(c) == n) or n < 1:
+        raise ValueError("one A, B and C per device")
+    for t in (*a, *b, *c):
+        if not (isinstance(t.data, torch.Tensor) and t.data.is_cuda):
+            raise ValueError("contract_devices takes device (CUDA) storage")
+    lab = -1 if label is None else spec.bundle_j.index(label)
+    prob = problem_of(spec, a[0], b[0], c[0], level, _variant(variant))
+    L = _lib.lib()
+    need = ctypes.c_size_t()
+    _lib.check(L.stc_sharded_workspace_size(ctypes.byref(prob), n, lab, ctypes.byref(need)))
+    ws = [torch.empty(max(int(need.value), 256), dtype=torch.uint8, device=t.data.device) for t in c]
+    streams = [torch.cuda.current_stream(t.data.device) for t in c]
+
+    def ptrs(xs):
+        return (ctypes.c_void_p * n)(*[x.data_ptr() for x in xs])
+
+    st = _lib.Stats()
+    _lib.check(L.stc_contract_sharded(ctypes.byref(prob), n, (ctypes.c_int * n)(*devices), lab,
+                                      ptrs([t.data for t in a]), ptrs([t.data for t in b]),
+                                      ptrs([t.data for t in c]), ptrs(ws),
+                                      (ctypes.c_size_t * n)(*[w.numel() for w in ws]),
+                                      (ctypes.c_void_p * n)(*[s.cuda_stream for s in streams]), int(gather),
+                                      ctypes.byref(st)))
+    for s in streams:
+        s.synchronize()
+    out = RunStats()
+    out.absorb(st)
+    return out

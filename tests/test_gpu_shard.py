@@ -125,3 +125,46 @@ def test_two_rank_nccl_nsplit_against_oracle():
     for r in range(world):
         got = stc.DenseTensor(c0.extents, c0.strides, ret[r])
         assert oracle.relative_error(got, ref) <= TOL, r
+
+
+@pytest.mark.parametrize("gather", [True, False])
+def test_contract_devices_one_process(gather):
+    # stc_contract_sharded (one process driving several devices): here two "devices" that
+    # are the same GPU with separate copies of A, B, C -- the shards share no data; the
+    # gather is the device-to-device copy of each shard's block into the other copy of C.
+    # Integer data: every path is exact, so each C copy equals the oracle's classical result
+    # (gather) or holds exactly its own shard's block of it (no gather).
+    import torch
+
+    spec = stc.parse_benchmark_line("abij abef efij & a:8;b:16;i:12;j:16;e:8;f:16;")
+
+    def ints(labels, seed):
+        e = spec.tensor_extents(labels)
+        return stc.DenseTensor(e, _rm(e), np.random.default_rng(seed).integers(-16, 17, int(np.prod(e))).astype(
+            np.float64))
+
+    a, b, c0 = ints(spec.labels_a, 61), ints(spec.labels_b, 62), ints(spec.labels_c, 63)
+    ref = c0.copy()
+    oracle.contract_reference(spec, a, b, ref)
+    for level, variant in ((1, "abc"), (2, "abc"), (2, "ab")):
+        A = [a.to_device(), a.to_device()]
+        B = [b.to_device(), b.to_device()]
+        C = [c0.to_device(), c0.to_device()]
+        st = shard.contract_devices(spec, A, B, C, level, variant, [0, 0], gather=gather)
+        assert st.pieces == 2 and st.leaf_multiplies == 7 ** level
+        shards = shard.plan_shards(spec, c0, 2)
+        for g in range(2):
+            got = C[g].to_host()
+            if gather:
+                assert np.array_equal(got.data, ref.data), (level, variant, g)
+            else:  # its own block contracted, the other block untouched
+                for h, sh in enumerate(shards):
+                    v = shard.shard_tensor(got, spec.labels_c, sh)
+                    w = shard.shard_tensor(ref if h == g else c0, spec.labels_c, sh)
+                    vv = np.lib.stride_tricks.as_strided(got.data[v.base_offset:], v.extents,
+                                                         [s * 8 for s in v.strides])
+                    ww = np.lib.stride_tricks.as_strided((ref if h == g else c0).data[w.base_offset:], w.extents,
+                                                         [s * 8 for s in w.strides])
+                    assert np.array_equal(vv, ww), (level, variant, g, h)
+        del A, B, C
+        torch.cuda.empty_cache()

@@ -174,3 +174,25 @@ def test_plan_shapes_and_slot_sides(line, level, tshape, sides):
     if tshape in (1, 2, 3, 4):
         assert info["ticketed"] == 0, info  # the narrow / small shapes write dense M
     assert info["terms"] == 7 ** level
+
+
+def test_sharded_workspace_covers_every_shard():
+    # stc_sharded_workspace_size: at least each shard's own stc_workspace_size (host-only)
+    spec = stc.parse_benchmark_line("abij abef efij & a:8;b:16;i:12;j:16;e:8;f:16;")
+
+    def t(labels):
+        e = spec.tensor_extents(labels)
+        return stc.DenseTensor(e, _row_major(e), np.zeros(int(np.prod(e))))
+
+    p = problem_of(spec, t(spec.labels_a), t(spec.labels_b), t(spec.labels_c), 2, Variant.ABC)
+    L = _lib.lib()
+    need = ctypes.c_size_t()
+    _lib.check(L.stc_sharded_workspace_size(ctypes.byref(p), 3, -1, ctypes.byref(need)))
+    for rank in range(3):
+        q = _lib.Problem()
+        _lib.check(L.stc_shard_problem(ctypes.byref(p), 3, rank, -1, ctypes.byref(q), None, None, None))
+        each = ctypes.c_size_t()
+        _lib.check(L.stc_workspace_size(ctypes.byref(q), ctypes.byref(each)))
+        assert need.value >= each.value
+    with pytest.raises(ValueError):
+        _lib.check(L.stc_sharded_workspace_size(ctypes.byref(p), 0, -1, ctypes.byref(need)))
