@@ -430,15 +430,19 @@ int piece_workspace(const stc_problem &p, const Split &sp, const KSplit &ks, siz
 // (0, c), into buffer c.  Without it every piece re-forms both (cfg5, 4 x 4 grid: 43 ms
 // of pre-summing instead of 11).  Needs a uniform grid whose pieces pre-sum both sides
 // in one batch; STC_HOST_SHARE=0 disables.
+// A 1-D split shares the operand all its pieces use whole: B for a cut of the I bundle,
+// A for a cut of the J bundle.
 struct Share {
-  bool on = false;
-  size_t a_bytes = 0, b_bytes = 0;  // one A / one B slot buffer (256-aligned)
-  size_t bytes(const Split &sp) const { return on ? 2 * a_bytes + (size_t)sp.sb * b_bytes : 0; }
+  bool on = false, a = false, b = false;  // any / the A side / the B side shared
+  size_t a_bytes = 0, b_bytes = 0;        // one A / one B slot buffer (256-aligned)
+  size_t bytes(const Split &sp) const {
+    return (a ? 2 * a_bytes : 0) + (b ? (size_t)sp.sb * b_bytes : 0);
+  }
 };
 
 Share plan_share(const stc_problem &p, const Split &sp) {
   Share sh;
-  if (sp.sa < 2 || sp.sb < 2) return sh;
+  if (sp.pieces < 2) return sh;
   if (const char *e = getenv("STC_HOST_SHARE"))
     if (atoi(e) == 0) return sh;
   size_t a0 = 0, b0 = 0;
@@ -454,7 +458,10 @@ Share plan_share(const stc_problem &p, const Split &sp) {
       return sh;  // pieces of different shapes: their slots differ
     }
   }
-  sh.on = a0 > 0 && b0 > 0;
+  if (a0 == 0 || b0 == 0) return sh;
+  sh.a = sp.sb >= 2;  // A row blocks are reused along the J cut
+  sh.b = sp.sa >= 2;  // B column blocks along the I cut
+  sh.on = sh.a || sh.b;
   sh.a_bytes = align256(a0);
   sh.b_bytes = align256(b0);
   return sh;
@@ -692,16 +699,18 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
     SlotOverride ovr;
     const bool shares = share.on && ru.kh < 0 && form_a[r] >= 0 && form_b[c] >= 0;
     if (shares) {
-      ovr.pa = reinterpret_cast<double *>(shared + (r % 2) * share.a_bytes);
-      ovr.pb = reinterpret_cast<double *>(shared + 2 * share.a_bytes + c * share.b_bytes);
-      ovr.skip_a = k != form_a[r];
-      ovr.skip_b = k != form_b[c];
+      // a side not shared keeps its slots in the piece's own workspace (pa / pb null)
+      char *sb_base = shared + (share.a ? 2 * share.a_bytes : 0);
+      ovr.pa = share.a ? reinterpret_cast<double *>(shared + (r % 2) * share.a_bytes) : nullptr;
+      ovr.pb = share.b ? reinterpret_cast<double *>(sb_base + c * share.b_bytes) : nullptr;
+      ovr.skip_a = share.a && k != form_a[r];
+      ovr.skip_b = share.b && k != form_b[c];
       if (ovr.skip_a) HCU(cudaStreamWaitEvent(cs, formed[form_a[r]], 0), "cudaStreamWaitEvent");
       if (ovr.skip_b) HCU(cudaStreamWaitEvent(cs, formed[form_b[c]], 0), "cudaStreamWaitEvent");
-      if (!ovr.skip_a && r >= 2)  // A buffer r % 2: the runs of I range r - 2 are done reading it
+      if (share.a && !ovr.skip_a && r >= 2)  // A buffer r % 2: the runs of I range r - 2 are done reading it
         for (int j = 0; j < nruns; ++j)
           if (runs[j].cell / sp.sb == r - 2) HCU(cudaStreamWaitEvent(cs, done[j], 0), "cudaStreamWaitEvent");
-      if (!ovr.skip_a || !ovr.skip_b) {
+      if ((share.a && !ovr.skip_a) || (share.b && !ovr.skip_b)) {
         HCU(E.make(formed[k]), "cudaEventCreate");
         ovr.after_presum = formed[k];
       }

@@ -248,7 +248,7 @@ def test_host_grid_pieces_integer_exact(grid):
         assert np.array_equal(c.data.numpy(), ref.data), (grid, level, variant)
 
 
-@pytest.mark.parametrize("grid", ["2x2", "4x2", "4x4"])
+@pytest.mark.parametrize("grid", ["2x2", "4x2", "4x4", "pieces4"])
 def test_host_grid_shared_slots_match_unshared_bitwise(grid):
     # pieces of a grid that pre-sum both sides share the slots of their A rows / B columns
     # (formed once by the first piece of each); the C blocks must equal those of pieces
@@ -261,9 +261,11 @@ def test_host_grid_shared_slots_match_unshared_bitwise(grid):
         outs = []
         for share in ("1", "0"):
             c = _pinned(c0.copy())
-            env = {"STC_HOST_GRID": grid, "STC_PRESUM_OPS": "1", "STC_HOST_SHARE": share}
+            # (pieces4: a 1-D cut into 4 pieces, sharing the operand the pieces use whole)
+            split = {"STC_HOST_PIECES": "4"} if grid == "pieces4" else {"STC_HOST_GRID": grid}
+            env = {**split, "STC_PRESUM_OPS": "1", "STC_HOST_SHARE": share}
             st = _with_env(env, lambda: stc.contract(spec, _pinned(a), _pinned(b), c, level, variant))
-            sa, sb = (int(x) for x in grid.split("x"))
+            sa, sb = (4, 1) if grid == "pieces4" else (int(x) for x in grid.split("x"))
             assert st.pieces in (sa * sb, sa * sb + 1) and st.leaf_multiplies == 7 ** level, st
             outs.append(c.data.numpy().copy())
         assert np.array_equal(outs[0], outs[1]), (grid, level, variant)
