@@ -206,16 +206,19 @@ Split choose_split(const stc_problem &p) {
   // more a 1-D cut must upload a whole operand before the first piece can start (cfg5:
   // 8.6 GB, 0.17 s); a 4 x 8 grid starts after a quarter of A and an eighth of B (0.06 s).
   // With the pieces sharing their operand slots (Share) the finer grid costs no extra
-  // pre-summing: cfg5 e2e 4 x 4 1637 ms, 4 x 8 1609 ms (8 x 8: 1877 ms, pieces too thin)
+  // pre-summing: cfg5 e2e 4 x 4 1637 ms, 4 x 8 1609 ms (8 x 8: 1877 ms, pieces too thin).
+  // From 12 GB on, J cut in 8 when that leaves pieces at least 4096 wide, else in 4 (the
+  // cfg5 shard of 4 GPUs, 32768 x 8192: 4 x 4 435 ms, 4 x 8 452 ms, 1-D 482 ms)
   const char *genv = getenv("STC_HOST_GRID");
   int ga = 0, gb = 0;
   if (genv && sscanf(genv, "%dx%d", &ga, &gb) != 2) ga = gb = 0;
   const char *env = getenv("STC_HOST_PIECES");
-  if (!env && (ga > 0 || (!genv && bytes >= (16ll << 30))) && A.compact() && B.compact()) {
+  if (!env && (ga > 0 || (!genv && bytes >= (12ll << 30))) && A.compact() && B.compact()) {
     const bool forced = ga > 0;
     int la = 0, lb = 0, sa = 0, sb = 0;
     int64_t ra = 0, rb = 0;
-    if (best_cut(p, 0, forced ? ga : 4, forced, la, sa, ra) && best_cut(p, 1, forced ? gb : 8, forced, lb, sb, rb) &&
+    const int jb = bundle_elems(p.c_col) / 8 >= 4096 ? 8 : 4;
+    if (best_cut(p, 0, forced ? ga : 4, forced, la, sa, ra) && best_cut(p, 1, forced ? gb : jb, forced, lb, sb, rb) &&
         sa * sb <= kMaxPieces && (forced || (sa >= 2 && sb >= 2))) {
       best.la = la;
       best.sa = sa;
@@ -228,8 +231,10 @@ Split choose_split(const stc_problem &p) {
       return best;
     }
   }
-  // 1-D: 4 pieces; 8 for problems of 16 GB and more (a shorter tail: the last C piece's download)
-  const int want = env ? std::max(1, std::min(kMaxPieces, atoi(env))) : (bytes >= (16ll << 30) ? 8 : 4);
+  // 1-D: 4 pieces; 8 for problems of 4 GB and more (the first piece after an eighth of the
+  // cut operand; a shorter tail: the last C piece's download).  The cfg5 shard of 8 GPUs
+  // (32768 x 4096, 11 GB): 8 pieces 240 ms, 4 pieces 262 ms
+  const int want = env ? std::max(1, std::min(kMaxPieces, atoi(env))) : (bytes >= (4ll << 30) ? 8 : 4);
   if (want <= 1 || (!env && bytes < kMinSplitBytes)) return best;
   for (int side = 0; side < 2; ++side) {
     if (!(side == 0 ? A : B).compact()) continue;
