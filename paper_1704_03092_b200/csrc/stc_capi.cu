@@ -505,14 +505,19 @@ int64_t cap_bytes() {
   return std::max<int64_t>(floor_bytes, (int64_t)(tot / 10 * 4));
 }
 
-// Reorder terms so that terms running concurrently (within `window`
-// consecutive terms) update disjoint C quadrants: fewer ticket waits.
+// The terms' execution (and C-update) order: the reference's term order
+// (strassen.py:173-178), or -- STC_EXEC_ORDER=windowed -- reordered so that terms
+// running concurrently (within `window` consecutive terms) update disjoint C
+// quadrants.  The reordering was meant to shorten ticket waits but measured no
+// faster anywhere and 2 % slower at cfg2 L2 (3.44 vs 3.38 ms) and cfg3 N_a = 32 L2
+// (3.63 vs 3.56 ms); in the reference order the variants also add the M products
+// into C in the same order as the reference.
 std::vector<int> exec_order(const std::vector<Term> &terms, int window) {
   const int T = (int)terms.size();
   std::vector<int> seq;
   seq.reserve(T);
   const char *env = getenv("STC_EXEC_ORDER");
-  if (window <= 1 || (env && strcmp(env, "reference") == 0)) {
+  if (window <= 1 || !(env && strcmp(env, "windowed") == 0)) {
     for (int i = 0; i < T; ++i) seq.push_back(i);
     return seq;
   }
