@@ -506,18 +506,19 @@ int64_t cap_bytes() {
 }
 
 // The terms' execution (and C-update) order: the reference's term order
-// (strassen.py:173-178), or -- STC_EXEC_ORDER=windowed -- reordered so that terms
-// running concurrently (within `window` consecutive terms) update disjoint C
-// quadrants.  The reordering was meant to shorten ticket waits but measured no
-// faster anywhere and 2 % slower at cfg2 L2 (3.44 vs 3.38 ms) and cfg3 N_a = 32 L2
-// (3.63 vs 3.56 ms); in the reference order the variants also add the M products
-// into C in the same order as the reference.
-std::vector<int> exec_order(const std::vector<Term> &terms, int window) {
+// (strassen.py:173-178), or reordered so that terms running concurrently (within
+// `window` consecutive terms) update disjoint C quadrants (fewer ticket waits).
+// Measured: the reordering pays on quadrants taller than wide (cfg3 2^24 N_a = 128
+// L2, 4096 x 256: 3.63 vs 3.99 ms) and costs 2 % on square / wide ones (cfg2 L2 3.44
+// vs 3.38 ms, cfg3 N_a = 32 3.63 vs 3.56 ms), so `windowed` is the caller's choice
+// (tall ticketed plans); STC_EXEC_ORDER=reference|windowed forces either.  In the
+// reference order the variants add the M products into C as the reference does.
+std::vector<int> exec_order(const std::vector<Term> &terms, int window, bool windowed) {
   const int T = (int)terms.size();
   std::vector<int> seq;
   seq.reserve(T);
-  const char *env = getenv("STC_EXEC_ORDER");
-  if (window <= 1 || !(env && strcmp(env, "windowed") == 0)) {
+  if (const char *env = getenv("STC_EXEC_ORDER")) windowed = strcmp(env, "windowed") == 0;
+  if (window <= 1 || !windowed) {
     for (int i = 0; i < T; ++i) seq.push_back(i);
     return seq;
   }
@@ -730,7 +731,7 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     // problem gets the same C-update order, so their results stay bitwise equal)
     const int64_t P128 = cdiv(pl.mq, BM) * cdiv(pl.nq, BN);
     const int window = (int)std::min<int64_t>(T, cdiv(pl.grid, P128) + 1);
-    pl.seq = exec_order(pl.terms, window);
+    pl.seq = exec_order(pl.terms, window, cdiv(pl.mq, BM) > cdiv(pl.nq, BN));
     // dense-M mode when many terms per C tile would be in flight at once: the
     // ticket chains then serialise (cfg2 pieces of m = 1024: 9 terms in flight,
     // 1.56 ms ticketed vs 1.21 ms dense; 576^3 L2: 0.60 vs 0.15 ms).
