@@ -352,15 +352,7 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
     // k-step 0 of chunk c (fa, fb) -> build k-step 1 of chunk c (xa, xb)
     pipe_view<NA, NB, 0, 1, true, SGN, AV, BV, MT>(acc, fa, fb, xa, xb, stages + (int)(sp & 0xffffu) * sstride, true,
                                                offA, offB, negmask, bbase);
-    // The stage's smem was read through the generic proxy and the producer refills it
-    // with TMA (async proxy) once every consumer warp arrived: the proxy fence orders the
-    // k-step 1 fragment loads just issued before the release.  Without it the refill
-    // raced with loads still in flight (wrong 64-row blocks, cfg4 L0, about 1 run in 4;
-    // none with it in 120).  Releasing one k-step later instead (after MMAs that read
-    // those registers) is as safe but shortens the ring: 4-5% slower.
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[sp & 0xffffu]);  // both k-steps of chunk c are in registers
+    const uint32_t done_stage = sp & 0xffffu;
     ++sp;
     if ((sp & 0xffffu) == (uint32_t)S) sp = (sp & 0x10000u) ^ 0x10000u;  // stage 0, phase flipped
     // k-step 1 of chunk c (xa, xb) -> build k-step 0 of chunk c + 1 (fa, fb)
@@ -368,6 +360,14 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
     if (more) mbar_wait(&full[sp & 0xffffu], sp >> 16);
     pipe_view<NA, NB, 0, 0, true, SGN, AV, BV, MT>(acc, xa, xb, fa, fb, stages + (int)(sp & 0xffffu) * sstride, more,
                                                offA, offB, negmask, bbase);
+    // Stage c is released once the MMAs of its k-step 1 issued: they read the fragment
+    // registers, so every load from the stage has completed before the producer's TMA
+    // (async proxy) refills it.  (Round 1 released right after issuing those loads -- a
+    // refill raced with loads still in flight, wrong 64-row blocks on cfg4 L0 about one
+    // run in four -- and then needed a fence.proxy.async per chunk, 1-1.5 % slower:
+    // 16384^3 L2 195.1 vs 192.2 ms.)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[done_stage]);
   }
   stage = (int)(sp & 0xffffu);
   phase = sp >> 16;
