@@ -323,7 +323,7 @@ __device__ __forceinline__ void pipe_view(double (&acc)[4][4][4], const double (
 // k-step are built one view per group, so no DADD waits on a result it needs
 // right away behind the DMMAs queued on the shared FP64 pipe.  A chunk stage
 // is released as soon as both of its k-steps are in registers.
-template <int NA, int NB, bool SGN = true, int AV = VIEW_DOUBLES, int BV = VIEW_DOUBLES, int MT = 4>
+template <int NA, int NB, bool SGN = true, int AV = VIEW_DOUBLES, int BV = VIEW_DOUBLES, int MT = 4, bool LATE = false>
 __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const double *stages, int sstride, int S,
                                              uint64_t *full, uint64_t *empty, int &stage, uint32_t &phase, int kchunks,
                                              uint32_t negmask, const int (&offA_)[2][2], const int (&offB_)[2][2],
@@ -348,11 +348,25 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
   uint32_t sp = (uint32_t)stage | (phase << 16);
   pipe_view<NA, NB, 0, 0, false, SGN, AV, BV, MT>(acc, fa, fb, fa, fb, stages + stage * sstride, true, offA, offB, negmask,
                                               bbase);
+  // Stage release.  LATE (one view per side: 8 stages): once the MMAs of the stage's
+  // second k-step have issued -- they read the fragment registers, so every load from the
+  // stage has completed before the producer's TMA (async proxy) refills it.  Otherwise
+  // (3-4 stages of several views, where the later release shortens the ring too much:
+  // cfg3 2^24 N_a = 256 L2 4.14 -> 4.41 ms) right after the second k-step's loads issue,
+  // behind a fence.proxy.async (without the fence the refill raced with loads still in
+  // flight: wrong 64-row blocks on cfg4 L0 about one run in four, round 1).  The fence
+  // costs 1-1.5 % (16384^3 L2: 195.1 vs 192.2 ms).
+  constexpr bool late = LATE;
   for (int c = 0; c < kchunks; ++c) {
     // k-step 0 of chunk c (fa, fb) -> build k-step 1 of chunk c (xa, xb)
     pipe_view<NA, NB, 0, 1, true, SGN, AV, BV, MT>(acc, fa, fb, xa, xb, stages + (int)(sp & 0xffffu) * sstride, true,
                                                offA, offB, negmask, bbase);
     const uint32_t done_stage = sp & 0xffffu;
+    if constexpr (!late) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[done_stage]);
+    }
     ++sp;
     if ((sp & 0xffffu) == (uint32_t)S) sp = (sp & 0x10000u) ^ 0x10000u;  // stage 0, phase flipped
     // k-step 1 of chunk c (xa, xb) -> build k-step 0 of chunk c + 1 (fa, fb)
@@ -360,14 +374,10 @@ __device__ __forceinline__ void consume_item(double (&acc)[4][4][4], const doubl
     if (more) mbar_wait(&full[sp & 0xffffu], sp >> 16);
     pipe_view<NA, NB, 0, 0, true, SGN, AV, BV, MT>(acc, xa, xb, fa, fb, stages + (int)(sp & 0xffffu) * sstride, more,
                                                offA, offB, negmask, bbase);
-    // Stage c is released once the MMAs of its k-step 1 issued: they read the fragment
-    // registers, so every load from the stage has completed before the producer's TMA
-    // (async proxy) refills it.  (Round 1 released right after issuing those loads -- a
-    // refill raced with loads still in flight, wrong 64-row blocks on cfg4 L0 about one
-    // run in four -- and then needed a fence.proxy.async per chunk, 1-1.5 % slower:
-    // 16384^3 L2 195.1 vs 192.2 ms.)
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[done_stage]);
+    if constexpr (late) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[done_stage]);
+    }
   }
   stage = (int)(sp & 0xffffu);
   phase = sp >> 16;
@@ -943,8 +953,8 @@ __global__ void __launch_bounds__(PS ? FUSED_THREADS_PS : FUSED_THREADS, 1)
           }
         }
       } else if constexpr (ONE) {
-        consume_item<1, 1, false, SH::AV, SH::BV, SH::MT>(acc, stages, sstride, S, full, empty, stage, phase, kchunks, 0u,
-                                                  offA, offB, lane, SH::AV);
+        consume_item<1, 1, false, SH::AV, SH::BV, SH::MT, true>(acc, stages, sstride, S, full, empty, stage, phase,
+                                                                kchunks, 0u, offA, offB, lane, SH::AV);
       } else {
       // coefficient signs of the item's views: one load per lane, one ballot
       bool neg = false;
