@@ -198,3 +198,25 @@ def test_sharded_workspace_covers_every_shard():
         assert need.value >= each.value
     with pytest.raises(ValueError):
         _lib.check(L.stc_sharded_workspace_size(ctypes.byref(p), 0, -1, ctypes.byref(need)))
+
+
+@pytest.mark.parametrize("line,grid", [
+    # cfg5 (24 GiB, J 32768 wide): 4 x 8; its shards of 4 and 2 GPUs (14 / 20 GiB, J 8192 /
+    # 16384 wide): 4 x 4 (a J cut in 8 only while the pieces stay >= 4096 wide)
+    ("abcijk abcefg efgijk & a:32;b:32;c:32;i:32;j:32;k:32;e:32;f:32;g:32;", (4, 8)),
+    ("abcijk abcefg efgijk & a:32;b:32;c:32;i:8;j:32;k:32;e:32;f:32;g:32;", (4, 4)),
+    ("abcijk abcefg efgijk & a:32;b:32;c:32;i:16;j:32;k:32;e:32;f:32;g:32;", (4, 4)),
+])
+def test_host_grid_shapes(line, grid):
+    _, (la, sa, lb, sb) = _grid(line)
+    assert (sa, sb) == grid
+
+
+def test_host_one_d_cut_in_eight_from_4_gb():
+    # the cfg5 shard of 8 GPUs (11 GiB: below the grid threshold): 8 pieces along I
+    spec = stc.parse_benchmark_line("abcijk abcefg efgijk & a:32;b:32;c:32;i:4;j:32;k:32;e:32;f:32;g:32;")
+    t = lambda labels: _Stub(spec.tensor_extents(labels))  # noqa: E731
+    p = problem_of(spec, t(spec.labels_a), t(spec.labels_b), t(spec.labels_c), 2, Variant.ABC)
+    side, label, pieces = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _lib.check(_lib.lib().stc_host_plan(ctypes.byref(p), ctypes.byref(side), ctypes.byref(label), ctypes.byref(pieces)))
+    assert (side.value, pieces.value) == (0, 8)
