@@ -363,37 +363,45 @@ struct DrainOnError {
   }
 };
 
-// The first cell of a grid split in two along one label of the P bundle: its two runs
-// (k halves, one after the other on one stream, adding into the same C block) start
-// after half of its A and B blocks arrived (cfg5, 4 x 8: 27 ms instead of 53 ms of PCIe
-// before the first DMMA).  The label: the P label with the largest stride in A of even
-// extent (long copy runs).  STC_HOST_KSPLIT=0 disables.
+// The first cell of a grid split along one label of the P bundle: its runs (k parts, one
+// after the other on one stream, adding into the same C block) start after a part of
+// its A and B blocks arrived (cfg5, 4 x 8: 15 ms instead of 53 ms of PCIe before the first
+// DMMA).  The label: the P label with the largest stride in A that the parts divide
+// (long copy runs).  STC_HOST_KSPLIT=n forces n parts, 0 disables.
 struct KSplit {
   bool on = false;
-  int lk = 0;                           // the P bundle label
-  int64_t k0[2] = {0, 0}, kn[2] = {0, 0};  // its halves
+  int lk = 0;                  // the P bundle label
+  int parts = 0;               // its ranges (STC_HOST_KSPLIT=n: n parts, 0 disables; default 2)
+  int64_t k0[4] = {}, kn[4] = {};
 };
 
 KSplit plan_ksplit(const stc_problem &p, const Split &sp) {
   KSplit ks;
   if (sp.sa < 2 || sp.sb < 2) return ks;
-  if (const char *e = getenv("STC_HOST_KSPLIT"))
-    if (atoi(e) == 0) return ks;
-  int best = -1;
-  for (int d = 0; d < p.a_col.nlab; ++d)
-    if (p.a_col.ext[d] >= 2 && p.a_col.ext[d] % 2 == 0 && (best < 0 || p.a_col.str[d] > p.a_col.str[best])) best = d;
-  if (best < 0) return ks;
-  // halves of at least two 16-deep chunks per quadrant
+  // 4 parts (cfg5: the first DMMA after 15 ms; 2 parts 1568 ms, 4 parts 1564 ms per call), else 2
+  int n = 4;
+  const char *env = getenv("STC_HOST_KSPLIT");
+  if (env) n = std::max(0, std::min(4, atoi(env)));
   int64_t k = 1;
   for (int d = 0; d < p.a_col.nlab; ++d) k *= p.a_col.ext[d];
-  if (k / 2 < ((int64_t)2 << p.level) * 16) return ks;
+  int best = -1;
+  for (; n >= 2; n = env ? 0 : n / 2) {
+    best = -1;
+    for (int d = 0; d < p.a_col.nlab; ++d)
+      if (p.a_col.ext[d] >= n && p.a_col.ext[d] % n == 0 && (best < 0 || p.a_col.str[d] > p.a_col.str[best]))
+        best = d;
+    // parts of at least two 16-deep chunks per quadrant
+    if (best >= 0 && k / n >= ((int64_t)2 << p.level) * 16) break;
+  }
+  if (n < 2 || best < 0) return ks;
   ks.on = true;
   ks.lk = best;
+  ks.parts = n;
   const int64_t e = p.a_col.ext[best];
-  ks.k0[0] = 0;
-  ks.kn[0] = e / 2;
-  ks.k0[1] = e / 2;
-  ks.kn[1] = e - e / 2;
+  for (int i = 0; i < n; ++i) {
+    ks.k0[i] = e * i / n;
+    ks.kn[i] = e * (i + 1) / n - ks.k0[i];
+  }
   return ks;
 }
 
@@ -419,7 +427,7 @@ int piece_workspace(const stc_problem &p, const Split &sp, const KSplit &ks, siz
     if (int rc = stc_workspace_size(&q, &b)) return rc;
     most = std::max(most, b);
     if (s == 0 && ks.on)
-      for (int kh = 0; kh < 2; ++kh) {
+      for (int kh = 0; kh < ks.parts; ++kh) {
         const stc_problem h = half_problem(q, ks, kh);
         if (int rc = stc_workspace_size(&h, &b)) return rc;
         most = std::max(most, b);
@@ -545,14 +553,13 @@ int stc_contract_host(const stc_problem *p, const double *hA, const double *hB, 
     ranges.push_back(pr);
   }
   struct Run {
-    int cell, kh;  // kh: -1 the whole k range, 0 / 1 the halves of KSplit
+    int cell, kh;  // kh: -1 the whole k range, else the part of KSplit
     stc_problem prob;
   };
   std::vector<Run> runs;
   for (int s = 0; s < sp.pieces; ++s) {
     if (s == 0 && ks.on) {
-      runs.push_back({0, 0, half_problem(cells[0], ks, 0)});
-      runs.push_back({0, 1, half_problem(cells[0], ks, 1)});
+      for (int kh = 0; kh < ks.parts; ++kh) runs.push_back({0, kh, half_problem(cells[0], ks, kh)});
     } else {
       runs.push_back({s, -1, cells[s]});
     }

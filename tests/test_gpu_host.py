@@ -243,8 +243,8 @@ def test_host_grid_pieces_integer_exact(grid):
         c = _pinned(c0.copy())
         st = _with_env({"STC_HOST_GRID": grid}, lambda: stc.contract(spec, _pinned(a), _pinned(b), c, level, variant))
         sa, sb = (int(x) for x in grid.split("x"))
-        # (+1: the first cell may run as two k halves, STC_HOST_KSPLIT)
-        assert st.pieces in (sa * sb, sa * sb + 1) and st.leaf_multiplies == 7 ** level, st
+        # (up to +3: the first cell may run as 2 or 4 k parts, STC_HOST_KSPLIT)
+        assert sa * sb <= st.pieces <= sa * sb + 3 and st.leaf_multiplies == 7 ** level, st
         assert np.array_equal(c.data.numpy(), ref.data), (grid, level, variant)
 
 
@@ -266,7 +266,7 @@ def test_host_grid_shared_slots_match_unshared_bitwise(grid):
             env = {**split, "STC_PRESUM_OPS": "1", "STC_HOST_SHARE": share}
             st = _with_env(env, lambda: stc.contract(spec, _pinned(a), _pinned(b), c, level, variant))
             sa, sb = (4, 1) if grid == "pieces4" else (int(x) for x in grid.split("x"))
-            assert st.pieces in (sa * sb, sa * sb + 1) and st.leaf_multiplies == 7 ** level, st
+            assert sa * sb <= st.pieces <= sa * sb + 3 and st.leaf_multiplies == 7 ** level, st
             outs.append(c.data.numpy().copy())
         assert np.array_equal(outs[0], outs[1]), (grid, level, variant)
         got = stc.DenseTensor(c0.extents, c0.strides, outs[0])
