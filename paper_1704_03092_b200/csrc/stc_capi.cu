@@ -27,7 +27,35 @@
 
 using namespace stc;
 
+extern "C" char **environ;
+
 namespace {
+
+// getenv for the STC_* knobs, memoised per thread: the planner and the per-call path
+// consult ~20 of them per call, and a getenv scans the whole environment.  The memo is
+// dropped whenever the environment array changes (a putenv / setenv -- Python's
+// os.environ -- replaces an entry pointer; env_refresh compares the pointer array).
+struct EnvMemo {
+  std::vector<char *> snap;
+  std::vector<std::pair<const char *, const char *>> vals;  // (knob name literal, value)
+};
+thread_local EnvMemo g_env;
+
+void env_refresh() {
+  size_t n = 0;
+  while (environ && environ[n]) ++n;
+  if (n == g_env.snap.size() && std::equal(g_env.snap.begin(), g_env.snap.end(), environ)) return;
+  g_env.snap.assign(environ, environ + n);
+  g_env.vals.clear();
+}
+
+const char *stc_env(const char *name) {
+  for (const auto &kv : g_env.vals)
+    if (kv.first == name || strcmp(kv.first, name) == 0) return kv.second;
+  const char *v = getenv(name);
+  g_env.vals.emplace_back(name, v);
+  return v;
+}
 
 thread_local std::string g_err;
 thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;  // stc_set_kernel_events
@@ -378,7 +406,7 @@ struct Resident {
     std::lock_guard<std::mutex> lk(mu);
     for (const Graph &g : graphs)
       if (g.key == key) {
-        if (cudaStreamWaitEvent(s, ev[g.key.mode], 0) != cudaSuccess || cudaGraphLaunch(g.exec, s) != cudaSuccess) {
+        if (!order(g.key.mode, s) || cudaGraphLaunch(g.exec, s) != cudaSuccess) {
           cudaGetLastError();
           return false;
         }
@@ -399,18 +427,31 @@ struct Resident {
   }
   // The snapshot of `mode` on device d, ordered before the work next enqueued on s; null if none.
   const void *ready(int mode, int d, cudaStream_t s) {
-    if (getenv("STC_NO_SNAPSHOT")) return nullptr;
+    if (stc_env("STC_NO_SNAPSHOT")) return nullptr;
     std::lock_guard<std::mutex> lk(mu);
     if (!buf[mode] || dev[mode] != d) return nullptr;
-    if (cudaStreamWaitEvent(s, ev[mode], 0) != cudaSuccess) {
-      cudaGetLastError();
-      return nullptr;
-    }
+    if (!order(mode, s)) return nullptr;
     return buf[mode];
   }
+  // s ordered after the snapshot copy of `mode` (a stream wait until the copy is known
+  // complete; none after that).  Caller holds mu.
+  bool order(int mode, cudaStream_t s) {
+    if (settled[mode]) return true;
+    if (cudaEventQuery(ev[mode]) == cudaSuccess) {
+      settled[mode] = true;
+      return true;
+    }
+    cudaGetLastError();  // (cudaErrorNotReady)
+    if (cudaStreamWaitEvent(s, ev[mode], 0) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return true;
+  }
+  bool settled[2] = {false, false};
   // Copy [ws, ws + bytes) (complete in stream order on s) into a new snapshot of `mode`.
   cudaError_t save(int mode, int d, const void *ws, size_t bytes, cudaStream_t s) {
-    if (getenv("STC_NO_SNAPSHOT")) return cudaSuccess;
+    if (stc_env("STC_NO_SNAPSHOT")) return cudaSuccess;
     std::lock_guard<std::mutex> lk(mu);
     if (buf[mode] || bytes == 0) return cudaSuccess;
     void *p = nullptr;
@@ -495,7 +536,7 @@ struct Plan {
 // workspace size.  The batch count changes no result: each batch's C pass continues
 // the previous one's sums in the same order.
 int64_t cap_bytes() {
-  if (const char *e = getenv("STC_WORKSPACE_CAP_MB")) return atoll(e) * (int64_t)1024 * 1024;
+  if (const char *e = stc_env("STC_WORKSPACE_CAP_MB")) return atoll(e) * (int64_t)1024 * 1024;
   const int64_t floor_bytes = (int64_t)24 << 30;
   size_t fr = 0, tot = 0;
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
@@ -517,7 +558,7 @@ std::vector<int> exec_order(const std::vector<Term> &terms, int window, bool win
   const int T = (int)terms.size();
   std::vector<int> seq;
   seq.reserve(T);
-  if (const char *env = getenv("STC_EXEC_ORDER")) windowed = strcmp(env, "windowed") == 0;
+  if (const char *env = stc_env("STC_EXEC_ORDER")) windowed = strcmp(env, "windowed") == 0;
   if (window <= 1 || !windowed) {
     for (int i = 0; i < T; ++i) seq.push_back(i);
     return seq;
@@ -579,9 +620,9 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
 bool presum_wanted(const stc_problem *p, const Plan &pl) {
   if (pl.level < 1 || pl.level > 2 || pl.variant == STC_VARIANT_NAIVE) return false;
   if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
-  if (const char *e = getenv("STC_FUSED"))
+  if (const char *e = stc_env("STC_FUSED"))
     if (atoi(e) == 0) return false;
-  if (const char *e = getenv("STC_PRESUM_OPS")) return atoi(e) != 0;
+  if (const char *e = stc_env("STC_PRESUM_OPS")) return atoi(e) != 0;
   const double qa = (double)pl.mq_pad * pl.kq_pad, qb = (double)pl.kq_pad * pl.nq_pad;
   const double quads = (double)pl.nquads, T = pl.level == 1 ? 7.0 : 49.0;
   const double t_presum = 8.0 * (quads + T) * (qa + qb) / 5e12;
@@ -635,15 +676,15 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   // with the summing warpgroup (AB, ABC with such C tiles, L >= 1); see shape_usable
   pl.tshape = 0;
   {
-    const char *ts = getenv("STC_TSHAPE");
+    const char *ts = stc_env("STC_TSHAPE");
     // (A / B base offsets even: TMA needs 16-byte aligned views of the 256-byte aligned
     // allocations; the shaped plan has no gather-kernel fallback)
     const bool allowed = (!ts || atoi(ts) != 0) && pl.level >= 1 && pl.variant != STC_VARIANT_NAIVE &&
                          p->a_base % 2 == 0 && p->b_base % 2 == 0 &&
                          !(p->flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) &&
-                         !(getenv("STC_FUSED") && atoi(getenv("STC_FUSED")) == 0) &&
-                         !(getenv("STC_PRESUM") && atoi(getenv("STC_PRESUM")) != 1) &&
-                         !(pl.variant == STC_VARIANT_ABC && getenv("STC_ABC_DENSE") && atoi(getenv("STC_ABC_DENSE")) == 0);
+                         !(stc_env("STC_FUSED") && atoi(stc_env("STC_FUSED")) == 0) &&
+                         !(stc_env("STC_PRESUM") && atoi(stc_env("STC_PRESUM")) != 1) &&
+                         !(pl.variant == STC_VARIANT_ABC && stc_env("STC_ABC_DENSE") && atoi(stc_env("STC_ABC_DENSE")) == 0);
     // the shape with the least padded area (128 x 128 on ties): cfg4 L2 (1138 x 788
     // quadrants) keeps 128 x 128 (87 % useful) over 256 x 64 (84 %)
     const int64_t a0 = rup(pl.mq, BM) * rup(pl.nq, BN), a1 = rup(pl.mq, 64) * rup(pl.nq, 256),
@@ -682,7 +723,7 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   pl.tp = tp;
   pl.a_kfast = a_min == 1;
   pl.b_kfast = b_min == 0;
-  if (!getenv("STC_NO_USTEP")) {
+  if (!stc_env("STC_NO_USTEP")) {
     pl.a_ustep = pl.a_kfast ? unit_step(p->a_col, tp, rup(pl.kq, BK), pl.a_ugroup)
                             : unit_step(p->a_row, ti, rup(pl.mq, pl.tm), pl.a_ugroup);
     pl.b_ustep = pl.b_kfast ? unit_step(p->b_row, tp, rup(pl.kq, BK), pl.b_ugroup)
@@ -738,7 +779,7 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     // STC_ABC_DENSE = 0 / 1 forces either.
     // Also when the C targets are not regular boxes: the kernel's C updates would then
     // be load/add/store scatters in the consumers (cfg4 L2: 5.2 ms ticketed, 3.2 dense).
-    const char *de = getenv("STC_ABC_DENSE");
+    const char *de = stc_env("STC_ABC_DENSE");
     // (the shaped tiles 1-4 write dense M only)
     const bool dense = T > 1 && (de ? atoi(de) != 0
                                     : (pl.grid >= 4 * P || pl.tshape != 0 ||
@@ -746,7 +787,7 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     pl.ticketed = !dense;
   }
   {
-    const char *ti_env = getenv("STC_TERM_INNER");
+    const char *ti_env = stc_env("STC_TERM_INNER");
     const bool skinny = pl.mq_pad / pl.tm == 1 || pl.nq_pad / pl.tn == 1;
     pl.term_inner = !pl.ticketed && T > 1 && (ti_env ? atoi(ti_env) != 0 : skinny);
   }
@@ -758,8 +799,8 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   if (pl.variant != STC_VARIANT_NAIVE && !pl.ticketed && pl.level >= 1 && pl.level <= 2 &&
       !(pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) &&
       bundle_len(p->a_col) == pl.Q * pl.kq_pad) {  // (the direct side's k quadrants need no padding)
-    const char *e = getenv("STC_PRESUM_SIDES");  // 1 / 2 / 3 force (diagnostics), 0 disables one-sided
-    const int want = e ? (atoi(e) & 3) : getenv("STC_PRESUM_OPS") ? 0 : pl.tshape == 1 ? 1 : pl.tshape == 2 ? 2 : 0;
+    const char *e = stc_env("STC_PRESUM_SIDES");  // 1 / 2 / 3 force (diagnostics), 0 disables one-sided
+    const int want = e ? (atoi(e) & 3) : stc_env("STC_PRESUM_OPS") ? 0 : pl.tshape == 1 ? 1 : pl.tshape == 2 ? 2 : 0;
     if (want == 3) {
       pl.presum = true;
       pl.presum_sides = 3;
@@ -868,7 +909,7 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     CoordJobs jd{};
     const bool direct = plan_fused(p, pl, direct_sides(p, pl), nullptr, nullptr, nullptr, gd, md, jd);
     pl.need_pack = !direct && plan_fused(p, pl, packed_sides(pl), nullptr, nullptr, nullptr, gd, md, jd) &&
-                   !(getenv("STC_PACK") && atoi(getenv("STC_PACK")) == 0);
+                   !(stc_env("STC_PACK") && atoi(stc_env("STC_PACK")) == 0);
   }
   if (pl.ticketed) {
     pl.tab_bytes = pl.tdesc.size() * sizeof(TermDesc) + pl.ops.size() * sizeof(OpDesc) + pl.tgts.size() * sizeof(TgtDesc);
@@ -1075,7 +1116,7 @@ bool encode_side(const TmaSide &ts, const double *data, int64_t base, CUtensorMa
   if (!fn) return false;
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-  if (const char *e = getenv("STC_TMA_PROMO"))
+  if (const char *e = stc_env("STC_TMA_PROMO"))
     promo = atoi(e) == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
             : atoi(e) == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
             : atoi(e) == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
@@ -1089,7 +1130,7 @@ bool encode_side(const TmaSide &ts, const double *data, int64_t base, CUtensorMa
 // Both sides of the operand views of `p` (A: I x P, B: P x J) as tensor maps;
 // false (gather path) unless both qualify.  STC_TMA=0 disables.
 bool plan_tma(const stc_problem *p, const Plan &pl, const double *A, const double *B, GemmArgs &g, CUtensorMap maps[2]) {
-  if (const char *e = getenv("STC_TMA"))
+  if (const char *e = stc_env("STC_TMA"))
     if (atoi(e) == 0) return false;
   if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
   TmaSide sa, sb;
@@ -1115,7 +1156,7 @@ bool plan_tma(const stc_problem *p, const Plan &pl, const double *A, const doubl
   g.tma = 1;
   // prefetch distance: what the k-coordinate window keeps ready (KWIN/2 chunks minus the issue lookahead)
   int pf = std::min(16, (kwin / 2 - 2) * 2);
-  if (const char *e = getenv("STC_TMA_PF")) pf = atoi(e);
+  if (const char *e = stc_env("STC_TMA_PF")) pf = atoi(e);
   g.tma_prefetch = std::max(0, pf);
   g.nraw = nraw;
   g.kwin = kwin;
@@ -1444,7 +1485,7 @@ void packed_vecs(const Plan &pl, const FusedSides &f, VecDesc out[4]) {
 // STC_FUSED=0 disables.  A / B null: layout check only (no maps).
 bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, const double *A, const double *B,
                 const double *C, GemmArgs &g, CUtensorMap maps[3], CoordJobs &jobs) {
-  if (const char *e = getenv("STC_FUSED"))
+  if (const char *e = stc_env("STC_FUSED"))
     if (atoi(e) == 0) return false;
   if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
   // Naive and pre-summed sides: one packed view per side
@@ -1485,7 +1526,7 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
   // ABC: C updates by TMA reduce-add when the C targets are regular boxes (STC_CRED=0 disables)
   g.cred = 0;
   TmaSide sc;
-  if (pl.variant == STC_VARIANT_ABC && C && !(getenv("STC_CRED") && atoi(getenv("STC_CRED")) == 0) &&
+  if (pl.variant == STC_VARIANT_ABC && C && !(stc_env("STC_CRED") && atoi(stc_env("STC_CRED")) == 0) &&
       fused_stages_red(sd) >= 2 &&
       plan_cred_side(p->c_row, pl.ti, p->c_col, pl.tj, pl.level, C, p->c_base, sc) &&
       encode_side(sc, C, p->c_base, maps[2])) {
@@ -1521,7 +1562,7 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
   // cfg3 2^24 N_a = 16 L2 4.35 vs 4.01 ms)
   g.psum = 0;
   if (umax > 2) {
-    const char *e = getenv("STC_PRESUM");
+    const char *e = stc_env("STC_PRESUM");
     g.psum = e ? atoi(e) & 3 : 1;
     if (g.psum == 2) g.psum = 3;
   }
@@ -1581,7 +1622,7 @@ std::string plan_env() {
                                 "STC_PRESUM_SIDES"};
   std::string key;
   for (const char *k : knobs) {
-    const char *v = getenv(k);
+    const char *v = stc_env(k);
     key += v ? v : "\x01";
     key += '\0';
   }
@@ -1590,6 +1631,7 @@ std::string plan_env() {
 
 int cached_plan(const stc_problem *p, std::shared_ptr<const Plan> &out, int grid_hint) {
   if (!p) return fail(STC_EINVAL, "null problem");
+  env_refresh();
   const std::string env = plan_env();
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -1866,7 +1908,7 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
         // consumers' own load/add/store epilogue (the spare warps' DADDs starve behind the
         // DMMAs); STC_EPI_OFFLOAD overrides, 8-wide C boxes always go to the spare warps
         tma = !packed;
-        const char *eo = getenv("STC_EPI_OFFLOAD");
+        const char *eo = stc_env("STC_EPI_OFFLOAD");
         const int offload = (eo ? atoi(eo) : (gf.cred ? 1 : 0)) || (gf.cred && gf.cred8);
         if (offload) gf.mscratch = reinterpret_cast<double *>(ws + pl.off_mscr);
         if (ev_before) CU(cudaEventRecord(ev_before, s), "cudaEventRecord");
@@ -2168,6 +2210,7 @@ static cudaStream_t capture_stream(int dev) {
 
 int stc_contract(const stc_problem *p, const double *A, const double *B, double *C, void *workspace,
                  size_t workspace_bytes, void *stream, stc_stats *stats) {
+  env_refresh();
   std::shared_ptr<const Plan> plan;
   const int grid_hint = gemm_max_grid(MAX_OPS);
   if (grid_hint <= 0) return fail(STC_ECUDA, "could not size the DMMA grid");
@@ -2196,8 +2239,8 @@ int stc_contract(const stc_problem *p, const double *A, const double *B, double 
   const double flops = 2.0 * (double)pl.tm * (double)pl.tn * (double)pl.kq_pad *
                        (double)((pl.mq_pad / pl.tm) * (pl.nq_pad / pl.tn)) * (double)pl.terms.size();
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  const bool graphs = res && !ev_before && !ev_after && !c_ready && !ovr && flops <= kGraphFlops && !getenv("STC_NO_GRAPH") &&
-                      !getenv("STC_NO_SNAPSHOT") && cudaStreamIsCapturing(s, &cap) == cudaSuccess &&
+  const bool graphs = res && !ev_before && !ev_after && !c_ready && !ovr && flops <= kGraphFlops && !stc_env("STC_NO_GRAPH") &&
+                      !stc_env("STC_NO_SNAPSHOT") && cudaStreamIsCapturing(s, &cap) == cudaSuccess &&
                       cap == cudaStreamCaptureStatusNone;
   const GraphKey key{A, B, C, ws, dev, 0};
   if (graphs) {
@@ -2286,6 +2329,7 @@ int stc_block_vector(const int64_t *scat, int64_t len, int64_t blk, int64_t unit
 }
 
 int stc_fused_term_workspace_size(int64_t m, int64_t n, int64_t k, int n_a, int n_b, int n_c, size_t *bytes) {
+  env_refresh();
   if (m < 1 || n < 1 || k < 1) return fail(STC_EINVAL, "empty fused term %lldx%lldx%lld", (long long)m, (long long)n, (long long)k);
   if (n_a < 1 || n_b < 1 || n_c < 1 || n_a > MAX_OPS || n_b > MAX_OPS || n_c > MAX_OPS)
     return fail(STC_EINVAL, "need 1..%d views per side", MAX_OPS);
@@ -2301,6 +2345,7 @@ int stc_fused_term(int64_t m, int64_t n, int64_t k, const double *A, int n_a, co
                    const int64_t *const *b_rows, const int64_t *const *b_cols, const double *b_coeffs, double *C,
                    int n_c, const int64_t *const *c_rows, const int64_t *const *c_cols, const double *c_coeffs,
                    uint32_t flags, void *workspace, size_t workspace_bytes, void *stream, stc_stats *stats) {
+  env_refresh();
   size_t need = 0;
   if (int rc = stc_fused_term_workspace_size(m, n, k, n_a, n_b, n_c, &need)) return rc;
   if (!workspace || workspace_bytes < need)

@@ -758,8 +758,14 @@ static GemmKernel kernel_for(int nraw, int kwin, bool tma) {
 int gemm_max_grid(int max_ops) {
   (void)max_ops;
   int dev = 0, sms = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  static int cached[64] = {};  // SM count per device (queried once; a benign race at worst re-queries)
+  if (dev >= 0 && dev < 64 && cached[dev] > 0) return cached[dev];
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  if (dev >= 0 && dev < 64) cached[dev] = sms;
   return sms;
 }
 
