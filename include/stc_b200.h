@@ -72,8 +72,19 @@ typedef struct {
   int32_t level;   /* Strassen levels L >= 0 (7^L leaf products)          */
   int32_t variant; /* STC_VARIANT_*                                        */
   uint32_t flags;  /* STC_FLAG_*                                           */
-  int32_t _pad;
+  int32_t tiling;  /* STC_TILING(shape, stages); 0: the planner's choice     */
 } stc_problem;
+
+/* GPU tile config requested through stc_problem.tiling -- the B200 counterpart of
+ * the reference's cache / register blocking (BlockingParams, kernels.py:34-56,
+ * which only tunes its CPU loops and never changes which products are formed).
+ * shape: 1 + the fused kernel's CTA tile (0: 128 x 128, 1: 64 x 256, 2: 256 x 64,
+ * 3: 64 x 128, 4: 128 x 64), 0 = planner; stages: cap on the fused kernel's TMA
+ * ring depth (2..8), 0 = planner.  A shape the problem cannot use (the shaped
+ * tiles need L >= 1, a non-Naive variant and dense M output)
+ * fails with STC_EINVAL before any device work.  Every shape and depth gives
+ * bitwise the same C. */
+#define STC_TILING(shape, stages) ((int32_t)(((shape) & 0xf) | (((stages) & 0xf) << 4)))
 
 /* Mirrors RunStats counters (oracle.py:22-43); GPU tiles replace mr x nr
  * register blocks, so block/update counts are per GPU tile.  fast / slow

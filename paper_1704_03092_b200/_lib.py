@@ -43,7 +43,7 @@ class Problem(ctypes.Structure):
                 ("c_row", Bundle), ("c_col", Bundle),
                 ("a_base", ctypes.c_int64), ("b_base", ctypes.c_int64), ("c_base", ctypes.c_int64),
                 ("level", ctypes.c_int32), ("variant", ctypes.c_int32), ("flags", ctypes.c_uint32),
-                ("_pad", ctypes.c_int32)]
+                ("tiling", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):

@@ -501,6 +501,7 @@ struct Plan {
   int max_ops = 1;  // most views on one side of any term (2^L)
   size_t off_kbs = 0, off_coords = 0, off_mscr = 0, off_pka = 0, off_pkb = 0;
   bool need_pack = false;  // fused kernel on repacked operands (layout not box-regular)
+  int stage_cap = 0;       // stc_problem.tiling: cap on the fused ring depth (0: none)
   int tshape = 0;          // fused kernel CTA tile shape (stc_fused.cu Shape): 0 128 x 128, 1 64 x 256, 2 256 x 64, 3 64 x 128, 4 128 x 64
   int64_t tm = BM, tn = BN;  // its tile rows / columns (quadrants padded to them)
   // ABC with C updated straight from the kernel, ticket-ordered per C tile; false for AB,
@@ -675,6 +676,10 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   // multiple of 128 -- a 128-row tile would be half padding -- for the dense-M launches
   // with the summing warpgroup (AB, ABC with such C tiles, L >= 1); see shape_usable
   pl.tshape = 0;
+  const int req_shape = p->tiling & 0xf, req_stages = (p->tiling >> 4) & 0xf;
+  if ((p->tiling & ~0xff) != 0 || req_shape > 5 || req_stages == 1)
+    return fail(STC_EINVAL, "tiling 0x%x: shape must be 0..5 (1 + CTA tile shape), stages 0 or 2..15", p->tiling);
+  pl.stage_cap = req_stages;
   {
     const char *ts = stc_env("STC_TSHAPE");
     // (A / B base offsets even: TMA needs 16-byte aligned views of the 256-byte aligned
@@ -711,6 +716,12 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
         (double)waves3 * 64 * 128 < 0.85 * (double)waves_cur * tm0 * tn0)
       pl.tshape = 3;
     if (allowed && ts && atoi(ts) > 0 && atoi(ts) <= 4) pl.tshape = atoi(ts);  // forced (diagnostics)
+    if (req_shape > 0) {  // the caller's tile config (stc_problem.tiling)
+      if (req_shape - 1 != 0 && !allowed)
+        return fail(STC_EINVAL, "tile shape %d needs L >= 1, a non-Naive variant, even A / B base offsets and "
+                    "no force_slow / reference tiling", req_shape - 1);
+      pl.tshape = req_shape - 1;
+    }
   }
   pl.tm = pl.tshape == 1 || pl.tshape == 3 ? 64 : pl.tshape == 2 ? 256 : BM;
   pl.tn = pl.tshape == 1 ? 256 : pl.tshape == 2 || pl.tshape == 4 ? 64 : pl.tshape == 3 ? 128 : BN;
@@ -734,6 +745,8 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     CUtensorMap md[3];
     CoordJobs jd{};
     if (!plan_fused(p, pl, direct_sides(p, pl), nullptr, nullptr, nullptr, gd, md, jd) && !presum_wanted(p, pl)) {
+      if (req_shape > 0)
+        return fail(STC_EINVAL, "tile shape %d: the operand views cannot be cut into its TMA boxes", req_shape - 1);
       pl.tshape = 0;
       pl.tm = BM;
       pl.tn = BN;  // (the dense / ticketed choice below sees the 128 x 128 tiles)
@@ -1554,6 +1567,7 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
   g.umax = umax;
   g.one_view = umax == 2;  // L0, Naive slots, pre-summed slots: one view per side, sign +1
   g.stages = g.cred ? fused_stages_red(sd) : S;
+  if (pl.stage_cap >= 2) g.stages = std::min(g.stages, pl.stage_cap);  // stc_problem.tiling
   g.stage_dbl = (int32_t)sd;
   g.tshape = pl.tshape;
   // summing warpgroup when some side has more than one view per chunk (L >= 1):

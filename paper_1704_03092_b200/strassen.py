@@ -16,9 +16,10 @@ Operands may be reference-style ``DenseTensor`` objects with host (numpy)
 storage -- staged through HBM, C copied back -- or HBM-resident: strided
 float64 CUDA ``torch.Tensor`` or ``DenseTensor`` with CUDA storage.  The work
 itself always runs in ``libstc_b200.so`` (C ABI, include/stc_b200.h); there is
-no CPU path.  ``params`` (the reference's CPU cache blocking, validated on
-construction like the reference's) is accepted and has no GPU counterpart --
-the GPU tiling is fixed, described by views.TILE -- and ``threads`` is ignored.
+no CPU path.  ``params`` is the GPU tile config (``views.TileConfig``: CTA tile
+shape, ring depth -- bitwise the same C whatever it is) or the reference's CPU
+cache blocking (``BlockingParams``, validated on construction like the
+reference's; the planner then chooses); ``threads`` is ignored.
 """
 
 from __future__ import annotations
@@ -34,7 +35,7 @@ import numpy as np
 from . import _lib
 from .stats import RunStats, effective_gflops
 from .tensor import ContractionSpec, DenseTensor
-from .views import DEFAULT_BLOCKING, BlockingParams, check_c_targets, make_view, quadrant_views
+from .views import DEFAULT_BLOCKING, BlockingParams, check_c_targets, make_view, quadrant_views, tiling_code
 
 __all__ = ["MAX_LEVEL", "DEVICE_MAX_LEVEL", "StrassenTerm", "Variant", "contract", "strassen_terms",
            "problem_of", "quadrant_rc", "describe_plan"]
@@ -134,8 +135,9 @@ def _check_operands(spec: ContractionSpec, a: DenseTensor, b: DenseTensor, c: De
 
 
 def problem_of(spec: ContractionSpec, a: DenseTensor, b: DenseTensor, c: DenseTensor, level: int,
-               variant: Variant, flags: int = 0) -> _lib.Problem:
-    """The C-ABI problem descriptor: the six bundles of the three views."""
+               variant: Variant, flags: int = 0, tiling: int = 0) -> _lib.Problem:
+    """The C-ABI problem descriptor: the six bundles of the three views
+    (``tiling``: views.TileConfig.code, 0 for the planner's choice)."""
 
     def bundle(labels: str, tensor_labels: str, t: DenseTensor) -> _lib.Bundle:
         axes = [tensor_labels.index(l) for l in labels]
@@ -149,6 +151,7 @@ def problem_of(spec: ContractionSpec, a: DenseTensor, b: DenseTensor, c: DenseTe
     p.level = int(level)
     p.variant = _lib.VARIANT_CODES[variant.value]
     p.flags = int(flags)
+    p.tiling = int(tiling)
     return p
 
 
@@ -164,14 +167,14 @@ def _geometry(t: DenseTensor) -> tuple:
 
 
 def _checked_problem(spec: ContractionSpec, a: DenseTensor, b: DenseTensor, c: DenseTensor, level: int,
-                     variant: Variant, flags: int) -> _lib.Problem:
+                     variant: Variant, flags: int, tiling: int = 0) -> _lib.Problem:
     """_check_operands + problem_of, memoised (the descriptor is shared: read-only)."""
-    key = (id(spec), _geometry(a), _geometry(b), _geometry(c), int(level), variant, int(flags))
+    key = (id(spec), _geometry(a), _geometry(b), _geometry(c), int(level), variant, int(flags), int(tiling))
     hit = _PROBLEMS.get(key)
     if hit is not None and hit[0] is spec:
         return hit[1]
     _check_operands(spec, a, b, c)
-    prob = problem_of(spec, a, b, c, level, variant, flags)
+    prob = problem_of(spec, a, b, c, level, variant, flags, tiling)
     if len(_PROBLEMS) >= 256:
         _PROBLEMS.clear()
     _PROBLEMS[key] = (spec, prob)
@@ -179,13 +182,14 @@ def _checked_problem(spec: ContractionSpec, a: DenseTensor, b: DenseTensor, c: D
 
 
 def describe_plan(spec: ContractionSpec, a, b, c, level: int, variant, grid: int = 148,
-                  force_slow: bool = False, reference_tiling: bool = False) -> dict:
+                  force_slow: bool = False, reference_tiling: bool = False,
+                  params: BlockingParams = DEFAULT_BLOCKING) -> dict:
     """The execution path the library plans for this contraction (no device
     needed): ticketed / pre-summed / repacked / tile shape / batches / workspace."""
     a, b, c = _as_dense(a, "A"), _as_dense(b, "B"), _as_dense(c, "C")
     _check_operands(spec, a, b, c)
     flags = (_lib.FLAG_FORCE_SLOW if force_slow else 0) | (_lib.FLAG_REFERENCE_TILING if reference_tiling else 0)
-    prob = problem_of(spec, a, b, c, level, _variant(variant), flags)
+    prob = problem_of(spec, a, b, c, level, _variant(variant), flags, tiling_code(params))
     info = _lib.PlanInfo()
     _lib.check(_lib.lib().stc_plan_describe(ctypes.byref(prob), int(grid), ctypes.byref(info)))
     return info.as_dict()
@@ -215,7 +219,7 @@ def _flat_host(t: DenseTensor):
 
 
 def _contract_host(spec, a, b, c, level, variant, force_slow, reference_tiling, validate, terms, dev,
-                   t_start) -> RunStats:
+                   t_start, tiling=0) -> RunStats:
     """Host operands: stc_contract_host pipelines the uploads, the piecewise
     contraction and the download of C (stc_host.cu)."""
     import torch
@@ -226,7 +230,7 @@ def _contract_host(spec, a, b, c, level, variant, force_slow, reference_tiling, 
         _validate_targets(spec, DenseTensor(c.extents, c.strides, stand_in, c.base_offset), level, terms)
         del stand_in
     flags = (_lib.FLAG_FORCE_SLOW if force_slow else 0) | (_lib.FLAG_REFERENCE_TILING if reference_tiling else 0)
-    prob = problem_of(spec, a, b, c, level, variant, flags)
+    prob = problem_of(spec, a, b, c, level, variant, flags, tiling)
     L = _lib.lib()
     stats = RunStats()
     with torch.cuda.device(dev):
@@ -302,14 +306,14 @@ def contract(spec: ContractionSpec, a, b, c, level: int, variant, params: Blocki
     result up to floating-point reordering and execute exactly 7^level leaf
     products.  ``RunStats.seconds`` is the wall clock of the whole call (the
     reference's timer, strassen.py:154,205); ``device_seconds`` the CUDA-event
-    time of the work it enqueued on the current stream.  ``params`` (the
-    reference's CPU cache blocking) has no GPU counterpart: it is validated like
-    the reference does and otherwise ignored -- the GPU tiles are fixed
-    (views.TILE describes them).  ``threads`` is ignored.
+    time of the work it enqueued on the current stream.  ``params``: a
+    ``views.TileConfig`` (the GPU tile config that replaces the reference's
+    blocking: CTA tile shape, ring depth; bitwise the same C) or the reference's
+    ``BlockingParams`` (CPU cache blocking, validated like the reference does;
+    the planner chooses the tiles).  ``threads`` is ignored.
     """
     t_start = time.perf_counter()
-    if not all(hasattr(params, f) for f in ("mc", "nc", "kc", "mr", "nr", "kr")):
-        raise TypeError("params must be a BlockingParams (the reference's blocking; the GPU tiling is views.TILE)")
+    tiling = tiling_code(params)
     a, b, c = _as_dense(a, "A"), _as_dense(b, "B"), _as_dense(c, "C")
     flags = (_lib.FLAG_FORCE_SLOW if force_slow else 0) | (_lib.FLAG_REFERENCE_TILING if reference_tiling else 0)
     try:
@@ -317,7 +321,7 @@ def contract(spec: ContractionSpec, a, b, c, level: int, variant, params: Blocki
     except ValueError:
         known = None
     # the operand check (memoised with the descriptor), then the level, then the variant
-    prob = _checked_problem(spec, a, b, c, level, known, flags) if known is not None else None
+    prob = _checked_problem(spec, a, b, c, level, known, flags, tiling) if known is not None else None
     if prob is None:
         _check_operands(spec, a, b, c)
     terms = strassen_terms(level, allow_deep)
@@ -338,7 +342,7 @@ def contract(spec: ContractionSpec, a, b, c, level: int, variant, params: Blocki
     if not (a.on_device or b.on_device or c.on_device) and kernel_events is None \
             and os.environ.get("STC_HOST_PIPELINE", "1") != "0" and all(_flat_host(t) is not None for t in (a, b, c)):
         return _contract_host(spec, a, b, c, level, variant, force_slow, reference_tiling, validate, terms, dev,
-                              t_start)
+                              t_start, tiling)
     c_ready = None
     A = a if a.on_device else a.to_device(dev)
     B = b if b.on_device else b.to_device(dev)

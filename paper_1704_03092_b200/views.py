@@ -36,6 +36,8 @@ __all__ = [
     "PAD",
     "TILE",
     "BlockingParams",
+    "CTA_TILES",
+    "TileConfig",
     "DEFAULT_BLOCKING",
     "BlockScatterView",
     "FusedPrimitive",
@@ -55,7 +57,8 @@ __all__ = [
 PAD = _lib.PAD
 
 # GPU tiling of the fused DMMA kernel (csrc/stc_fused.cu), the counterpart of the
-# reference's BlockingParams: fixed, not configurable per call.
+# reference's BlockingParams: chosen per problem by the planner; TileConfig (below)
+# requests a CTA tile shape and caps the ring depth per call.
 TILE = {
     "cta_tile": (128, 128),              # 64 x 256 / 256 x 64 for 64-wide quadrants, 64 x 128 for small problems
     "warp_tile": (64, 32),               # 8 consumer warps (32 x 32 on the 64 x 128 tiles), m16n8k4.f64 (DMMA)
@@ -94,6 +97,52 @@ class BlockingParams:
 
 
 DEFAULT_BLOCKING = BlockingParams()
+
+# CTA tile shapes of the fused kernel, (rows of I, columns of J) -> stc_fused.cu Shape<ts>
+CTA_TILES = {(128, 128): 0, (64, 256): 1, (256, 64): 2, (64, 128): 3, (128, 64): 4}
+
+
+@dataclass(frozen=True)
+class TileConfig:
+    """The GPU tile config that replaces the reference's ``BlockingParams``
+    (kernels.py:34-56) as ``contract(..., params=...)``.
+
+    ``cta_tile``: the fused DMMA kernel's CTA tile (a key of ``CTA_TILES``), None
+    for the planner's choice; ``stages``: a cap on its TMA ring depth (2..8), None
+    for the most that fit in shared memory.  Like the reference's blocking it
+    only changes how the work is scheduled: every tile and depth gives bitwise the
+    same C (the DMMA k-steps of an element run in the same order).  A shape the
+    problem cannot use raises ValueError before any device work (the shaped tiles
+    need L >= 1 and a non-Naive variant).  ``BlockingParams`` (the reference's
+    CPU blocking) is still accepted and leaves every choice to the planner.
+    """
+
+    cta_tile: tuple | None = None
+    stages: int | None = None
+
+    def __post_init__(self):
+        if self.cta_tile is not None:
+            object.__setattr__(self, "cta_tile", tuple(int(v) for v in self.cta_tile))
+            if self.cta_tile not in CTA_TILES:
+                raise ValueError(f"cta_tile must be one of {sorted(CTA_TILES)}, got {self.cta_tile}")
+        if self.stages is not None and not 2 <= int(self.stages) <= 8:
+            raise ValueError(f"stages must be in 2..8, got {self.stages}")
+
+    @property
+    def code(self) -> int:
+        """stc_problem.tiling: STC_TILING(1 + shape, stages) (include/stc_b200.h)."""
+        shape = 0 if self.cta_tile is None else 1 + CTA_TILES[self.cta_tile]
+        return shape | ((self.stages or 0) << 4)
+
+
+def tiling_code(params) -> int:
+    """stc_problem.tiling for contract()'s ``params``: a TileConfig's request, 0
+    (the planner) for the reference's BlockingParams."""
+    if isinstance(params, TileConfig):
+        return params.code
+    if not all(hasattr(params, f) for f in ("mc", "nc", "kc", "mr", "nr", "kr")):
+        raise TypeError("params must be a TileConfig (GPU tiling) or a BlockingParams (the reference's blocking)")
+    return 0
 
 
 def _torch():

@@ -418,3 +418,31 @@ def test_eight_wide_c_boxes_match_dense_m_bitwise():
                 {"STC_ABC_DENSE": "0", "STC_PRESUM_OPS": "0", "STC_CRED": "0"}):
         ct, _ = _run_env(spec, a, b, c0, 2, "abc", env)
         assert np.array_equal(ct.data, cd.data), env
+
+
+@pytest.mark.parametrize("line", [
+    "abij abef efij & a:24;b:24;i:24;j:24;e:24;f:24;",   # cfg1 geometry (576^3)
+    "aibj eafb jfie & a:16;b:32;i:16;j:32;e:32;f:16;",   # cfg2's permuted layouts, 512^3
+])
+def test_tile_config_params_bitwise(line):
+    # contract(params=TileConfig(...)): every CTA tile shape and ring depth gives the C of
+    # the planner's choice bitwise (the tile config only reschedules the same DMMA k-steps)
+    spec = stc.parse_benchmark_line(line)
+    a, b, c0 = _operands(spec, 97)
+    classical = c0.copy()
+    oracle.contract_reference(spec, a.to_host(), b.to_host(), classical)
+    for level, variant in ((1, "abc"), (2, "ab"), (2, "abc")):
+        base = c0.to_device()
+        stc.contract(spec, a, b, base, level, variant)
+        base = base.to_host()
+        assert stc.relative_error(base, classical) <= TOL
+        configs = [stc.TileConfig(cta_tile=t) for t in sorted(stc.CTA_TILES)]
+        configs += [stc.TileConfig(stages=s) for s in (2, 3, 5)]
+        configs += [stc.TileConfig(cta_tile=(64, 128), stages=2)]
+        for cfg in configs:
+            c = c0.to_device()
+            stc.contract(spec, a, b, c, level, variant, params=cfg)
+            if cfg.cta_tile is not None:
+                assert stc.describe_plan(spec, a, b, c0, level, variant, params=cfg)["tshape"] == \
+                    stc.CTA_TILES[cfg.cta_tile]
+            assert np.array_equal(c.to_host().data, base.data), (line, level, variant, cfg)
