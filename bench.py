@@ -382,14 +382,19 @@ def main():
         h.copy_(t.data)
         return stc.DenseTensor(t.extents, t.strides, h, t.base_offset)
 
-    e2e = None
+    # Every rank must take the same branch (the timed region holds barriers): the pinned
+    # allocations are tried first and the outcome agreed on (min over ranks).
+    e2e, err = None, ""
     try:
         a_p, b_p = pinned_copy(A), pinned_copy(B)
-        del A, B
-        torch.cuda.empty_cache()
         esc = sp.tensor_extents(sp.labels_c)
         c_p = stc.DenseTensor(esc, row_major(esc), torch.zeros(int(np.prod(esc)), dtype=torch.float64,
                                                                pin_memory=True))
+    except (RuntimeError, MemoryError) as exc:  # host memory for pinned operands
+        err = str(exc)[:200]
+    del A, B
+    torch.cuda.empty_cache()
+    if -max_over_ranks(-float(not err)) > 0:
         stc.contract(sp, a_p, b_p, c_p, LEVEL, VARIANT)  # warm the host pipeline's plans and buffers
         barrier()
         w0 = time.perf_counter()
@@ -403,10 +408,10 @@ def main():
                "steps": args.e2e_steps,
                "timing": "wall clock around contract() on pinned host DenseTensors (per rank: A, B shard, "
                          "C shard), max over ranks"}
-        del a_p, b_p, c_p
-    except (RuntimeError, MemoryError) as exc:  # host memory for pinned operands
+    else:
         e2e = {"value": None, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-               "error": str(exc)[:200]}
+               "error": err or "pinned host allocation failed on another rank"}
+    a_p = b_p = c_p = None
 
     if rank != 0:
         if dist is not None:
