@@ -371,7 +371,7 @@ def main():
         allgather = {"ms": ag * 1e3, "bytes_per_rank_received": int(np.prod(ec)) * 8 * (world - 1) // world,
                      "value_with_allgather": flops_job / (elapsed / args.steps + ag) / 1e9,
                      "how": "shard.gather_shards: all_gather_into_tensor into a shard-major buffer + one "
-                            "strided copy per shard (NCCL)"}
+                            f"strided copy per shard ({dist.get_backend()})"}
     del c_full
     C = None
     torch.cuda.empty_cache()
