@@ -1785,6 +1785,12 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
 
   // Fused kernel set-up on the operands' own views or their repacked blocks: the
   // repacking runs every call (it reads A and B), the rest is constant.
+  // (errors are returned negated: 0 = the gather kernel, 1 = fused kernel prepared)
+#define CUN(expr, what)                                  \
+  do {                                                   \
+    cudaError_t _e = (expr);                             \
+    if (_e != cudaSuccess) return -cuda_fail(_e, what);  \
+  } while (0)
   auto prepare_fused = [&](GemmArgs &gf, CUtensorMap *maps, const double *Cp) -> int {
     CoordJobs jobs{};
     if (packed) {
@@ -1792,8 +1798,8 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
       double *PB = reinterpret_cast<double *>(ws + pl.off_pkb);
       PackArgs pa{pl.ar, pl.ac, pl.mq_pad, pl.kq_pad, (int32_t)pl.Q, 1, pl.a_kfast, 0, pl.a_ustep, pl.a_ugroup, 0};
       PackArgs pb{pl.bc, pl.br, pl.nq_pad, pl.kq_pad, (int32_t)pl.Q, 0, pl.b_kfast, 0, pl.b_ustep, pl.b_ugroup, 0};
-      CU(launch_pack_views(A, pool2, pa, PA, s), "k_pack_views(A)");
-      CU(launch_pack_views(B, pool2, pb, PB, s), "k_pack_views(B)");
+      CUN(launch_pack_views(A, pool2, pa, PA, s), "k_pack_views(A)");
+      CUN(launch_pack_views(B, pool2, pb, PB, s), "k_pack_views(B)");
       launches += 2;
       const FusedSides fs = packed_sides(pl);
       if (!restored) {
@@ -1801,7 +1807,7 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
         packed_vecs(pl, fs, pv);
         VecDesc *d_pv = reinterpret_cast<VecDesc *>(ws + pl.off_vecs) + pl.vecs.size();
         if (int rc = upload(pv, sizeof(pv), d_pv, s)) return -rc;
-        CU(launch_build_pool(d_pv, 4, pl.pool_len, pool, s), "k_build_pool(packed)");
+        CUN(launch_build_pool(d_pv, 4, pl.pool_len, pool, s), "k_build_pool(packed)");
         ++launches;
       }
       if (!plan_fused(p, pl, fs, PA, PB, Cp, gf, maps, jobs)) return -fail(STC_EINVAL, "internal: packed plan");
@@ -1817,11 +1823,12 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
     }
     gf.coords = coords;
     if (!restored) {
-      CU(launch_pool_coords(pool, coords, jobs, s), "k_pool_coords");
+      CUN(launch_pool_coords(pool, coords, jobs, s), "k_pool_coords");
       ++launches;
     }
     return 1;
   };
+#undef CUN
 
   GemmArgs g{};
   g.pool = pool;

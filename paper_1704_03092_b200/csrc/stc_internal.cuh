@@ -143,6 +143,7 @@ struct PackArgs {
   int32_t kfast, _pad; // packed block layout: 0 [k][x], 1 [x][k]
   int64_t ustep;       // > 0: fast-index step of the source's unit-stride label (unit_step)
   int32_t ugroup, _pad2;
+  int64_t fast_blocks; // set by launch_pack_views: blocks along the contiguous dimension (grid.x = these x row blocks)
 };
 
 // AB / Naive accumulate: C_q += sum over the quadrant's terms of sign * M_slot.

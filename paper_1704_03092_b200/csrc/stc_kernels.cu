@@ -280,18 +280,21 @@ constexpr int UNPACK_ROWS = 4;  // k_pack_views: rows of the slow dimension per 
 __global__ void __launch_bounds__(256) k_pack_views(const double *__restrict__ D, const int64_t *__restrict__ pool,
                                                     PackArgs a, double *__restrict__ out) {
   // block: 256 positions along the packed block's contiguous dimension x
-  // UNPACK_ROWS of the other (as k_unpack); blockIdx.z = quadrant pair
-  const int qa = blockIdx.z / a.Q, qb = blockIdx.z - qa * a.Q;
+  // UNPACK_ROWS of the other (as k_unpack); blockIdx.y = quadrant pair
+  const int qa = blockIdx.y / a.Q, qb = blockIdx.y - qa * a.Q;
   const int xq = a.xfirst ? qa : qb, kq = a.xfirst ? qb : qa;
   const int64_t *xv = pool + a.xv + (int64_t)xq * a.xlen;
   const int64_t *kv = pool + a.kv + (int64_t)kq * a.klen;
-  double *o = out + (int64_t)blockIdx.z * a.xlen * a.klen;
+  double *o = out + (int64_t)blockIdx.y * a.xlen * a.klen;
   const int64_t fast_len = a.kfast ? a.klen : a.xlen, slow_len = a.kfast ? a.xlen : a.klen;
   const int64_t *fv = a.kfast ? kv : xv, *sv = a.kfast ? xv : kv;
-  const int64_t f = FastMap(a.ustep, a.ugroup, blockDim.x).pos(blockIdx.x, threadIdx.x, blockDim.x, fast_len);
+  // blockIdx.x = row block * fast blocks + fast block (a long k of a tall-skinny problem
+  // exceeds the 65535 blocks of grid.y)
+  const int64_t bx = blockIdx.x % a.fast_blocks, by = blockIdx.x / a.fast_blocks;
+  const int64_t f = FastMap(a.ustep, a.ugroup, blockDim.x).pos(bx, threadIdx.x, blockDim.x, fast_len);
   if (f < 0) return;
   const int64_t fo = __ldg(fv + f);
-  const int64_t s0 = (int64_t)blockIdx.y * UNPACK_ROWS;
+  const int64_t s0 = by * UNPACK_ROWS;
 #pragma unroll 4
   for (int r = 0; r < UNPACK_ROWS; ++r) {
     const int64_t sl = s0 + r;
@@ -301,12 +304,14 @@ __global__ void __launch_bounds__(256) k_pack_views(const double *__restrict__ D
   }
 }
 
-cudaError_t launch_pack_views(const double *D, const int64_t *pool, const PackArgs &a, double *out, cudaStream_t s) {
+cudaError_t launch_pack_views(const double *D, const int64_t *pool, const PackArgs &a0, double *out, cudaStream_t s) {
+  PackArgs a = a0;
   const int64_t fast_len = a.kfast ? a.klen : a.xlen, slow_len = a.kfast ? a.xlen : a.klen;
   if (fast_len <= 0 || slow_len <= 0) return cudaSuccess;
   const int64_t gy = (slow_len + UNPACK_ROWS - 1) / UNPACK_ROWS;
-  if (gy > 65535 || a.Q * a.Q > 65535) return cudaErrorInvalidConfiguration;
-  dim3 grid((unsigned)FastMap(a.ustep, a.ugroup, 256).blocks(fast_len, 256), (unsigned)gy, (unsigned)(a.Q * a.Q));
+  a.fast_blocks = FastMap(a.ustep, a.ugroup, 256).blocks(fast_len, 256);
+  if (a.fast_blocks * gy > INT32_MAX || a.Q * a.Q > 65535) return cudaErrorInvalidConfiguration;
+  dim3 grid((unsigned)(a.fast_blocks * gy), (unsigned)(a.Q * a.Q));
   k_pack_views<<<grid, 256, 0, s>>>(D, pool, a, out);
   return cudaGetLastError();
 }

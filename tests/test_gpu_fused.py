@@ -446,3 +446,37 @@ def test_tile_config_params_bitwise(line):
                 assert stc.describe_plan(spec, a, b, c0, level, variant, params=cfg)["tshape"] == \
                     stc.CTA_TILES[cfg.cta_tile]
             assert np.array_equal(c.to_host().data, base.data), (line, level, variant, cfg)
+
+
+@pytest.mark.parametrize("line", [
+    # a short I / J with a very long P: the repacked operands' [k][x] blocks have 262144
+    # rows (k_pack_views' row blocks once overflowed grid.y and the error was dropped)
+    "ij ie ej & i:16;j:64;e:262144;",
+    "di edbc ecbi & d:16;i:64;e:128;b:32;c:64;",
+])
+def test_long_k_repacked_operands(line):
+    import torch
+
+    spec = stc.parse_benchmark_line(line)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+
+    def dev(labels):
+        e = spec.tensor_extents(labels)
+        return (torch.rand(e, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1).contiguous()
+
+    a, b, c0 = dev(spec.labels_a), dev(spec.labels_b), dev(spec.labels_c)
+    ref = c0 + torch.einsum(f"{spec.labels_a},{spec.labels_b}->{spec.labels_c}", a, b)
+    out = {}
+    for fused in ("1", "0"):
+        os.environ["STC_FUSED"] = fused
+        try:
+            for level in (0, 1):
+                c = c0.clone()
+                st = stc.contract(spec, a, b, c, level, "abc")
+                assert st.leaf_multiplies == 7 ** level
+                err = (torch.linalg.vector_norm(c - ref) / torch.linalg.vector_norm(ref)).item()
+                assert err <= TOL, (line, fused, level, err)
+                out[fused, level] = c
+        finally:
+            os.environ.pop("STC_FUSED", None)
+    assert torch.equal(out["1", 0], out["0", 0])  # repacked fused kernel == gather kernel, bitwise

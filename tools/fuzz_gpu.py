@@ -19,6 +19,9 @@ sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
 import paper_1704_03092_b200 as stc  # noqa: E402
 
 
+VERBOSE = bool(os.environ.get("STC_FUZZ_VERBOSE"))
+
+
 def rand_case(rng):
     ni, nj, np_ = rng.randint(1, 3), rng.randint(1, 3), rng.randint(1, 3)
     labels = list("abcdefghijkl")
@@ -73,7 +76,11 @@ def main(cases, seed):
                 os.environ.pop("STC_PRESUM_OPS", None)
                 os.environ.update(env)
                 cc = c.clone()
+                if VERBOSE:  # the case about to run (a crash is then attributable)
+                    print("RUN", case, stc.to_benchmark_line(spec), "offset", off, "L", level, variant, env, flush=True)
                 st = stc.contract(spec, a, b, cc, level, variant)
+                if VERBOSE:
+                    torch.cuda.synchronize()
                 paths["fast" if st.fast_blocks else "slow"] += 1
                 err = torch.linalg.vector_norm(cc - ref).item() / max(nref, 1e-300)
                 worst = max(worst, err)
