@@ -286,3 +286,40 @@ def test_graph_replay_follows_inputs_and_pointers():
         finally:
             del os.environ["STC_NO_GRAPH"]
         assert np.array_equal(cs[0].to_host().data, ref.data), (level, variant)
+
+
+# ---- degenerate specs the reference accepts (empty bundles, rank-0 C, extent-1 labels) -------
+DEGENERATE = [
+    ("ij", "i", "j", {"i": 4, "j": 5}),                      # empty P bundle: outer product (k = 1)
+    ("i", "ie", "e", {"i": 4, "e": 5}),                      # empty J bundle: matrix-vector (n = 1)
+    ("j", "e", "ej", {"j": 4, "e": 5}),                      # empty I bundle (m = 1)
+    ("", "e", "e", {"e": 37}),                               # rank-0 C: dot product
+    ("ij", "ie", "ej", {"i": 1, "j": 1, "e": 1}),            # all extents 1 (quadrants are PAD)
+    ("abij", "aeb", "ije", {"a": 1, "b": 300, "i": 1, "j": 3, "e": 130}),  # extent-1 labels inside bundles
+    ("ij", "i", "j", {"i": 300, "j": 200}),                  # outer product over several tiles
+]
+
+
+@pytest.mark.parametrize("case", DEGENERATE, ids=lambda c: f"{c[0] or '0'}-{c[1]}-{c[2]}")
+@pytest.mark.parametrize("where", ["device", "host"])
+def test_degenerate_specs_match_oracle_exactly(case, where):
+    """Integer data, so every level and variant must equal the classical oracle exactly;
+    the reference runs all of these (7^L leaves on PAD-only quadrants included)."""
+    lc, la, lb, ext = case
+    spec = stc.ContractionSpec(lc, la, lb, ext)
+    a, b, c0 = _tensors(spec, 3, fill="int")
+    c0.data[:] = np.random.default_rng(9).integers(-50, 51, c0.data.size).astype(np.float64)
+    gold = c0.copy()
+    oracle.contract_reference(spec, a, b, gold)
+    for level in (0, 1, 2):
+        for variant in ("abc", "ab", "naive"):
+            if where == "device":
+                ad, bd, c = a.to_device(), b.to_device(), c0.to_device()
+                st = stc.contract(spec, ad, bd, c, level, variant)
+                got = c.to_host().data
+            else:
+                c = c0.copy()
+                st = stc.contract(spec, a, b, c, level, variant)
+                got = c.data
+            assert st.leaf_multiplies == 7 ** level
+            assert np.array_equal(got, gold.data), (case, where, level, variant)
