@@ -1841,6 +1841,7 @@ static int contract_run(const stc_problem *p, const Plan &pl, const double *A, c
   g.warp_map = (pl.mq % BM != 0 && pl.mq % BM <= 64) && !(pl.nq % BN != 0 && pl.nq % BN <= 96);
   g.kchunks = (int)(pl.kq_pad / BK);
   g.group_m = 8;
+  if (const char *e = stc_env("STC_GROUP_M")) g.group_m = std::max(1, atoi(e));
   g.term_inner = pl.term_inner ? 1 : 0;
   g.max_ops = pl.max_ops;
   g.nraw = gemm_nraw(pl.max_ops);
