@@ -192,6 +192,38 @@ int stc_fused_term(int64_t m, int64_t n, int64_t k, const double *A, int n_a, co
                    int n_c, const int64_t *const *c_rows, const int64_t *const *c_cols, const double *c_coeffs,
                    uint32_t flags, void *workspace, size_t workspace_bytes, void *stream, stc_stats *stats);
 
+/* ---- subsystems (2) and (3) as the reference's component calls ----
+ * pack_a / pack_b (kernels.py:166-201, _jit.pack_a_block / pack_b_block, _jit.py:27-131):
+ * the Strassen packing pass on its own -- out[s, p, i] = sum_t coeffs[t] * view_t
+ * element, sliver-major (PackedBuffer, kernels.py:67-99: sliver s holds `width`
+ * consecutive rows (side 0, A: views m x k, element (x0 + s*width + i, k0 + p)) or
+ * columns (side 1, B: views k x n, element (k0 + p, x0 + s*width + i)); element
+ * offset (s*out_depth + p)*width + i).  Views are added in order starting from 0.0
+ * (the reference's roundings: bitwise equal), PAD and fringe positions give 0,
+ * p >= kcount is left untouched.  rows / cols / rbs / cbs / coeffs: HOST arrays of
+ * nviews device pointers / values (rbs, cbs: the views' block vectors at
+ * (width, kblock) geometry, stc_block_vector; may be NULL with stats NULL).
+ * stats (synchronises the stream): fast / slow blocks per (width x kblock)
+ * sub-block as the reference counts them. */
+int stc_pack_panel(int side, const double *data, int nviews, const int64_t *const *rows, const int64_t *const *cols,
+                   const int64_t *const *rbs, const int64_t *const *cbs, const double *coeffs, int64_t x0,
+                   int64_t xcount, int64_t k0, int64_t kcount, int64_t width, int64_t kblock, uint32_t flags,
+                   double *out, int64_t out_depth, void *stream, stc_stats *stats);
+
+/* microkernel (kernels.py:204-233; _jit.microtile_mats + store_tile, _jit.py:145-186):
+ * the mr x nr tile acc[i, j] = sum_{p<k} a_sliver[i*lda + p] * b_sliver[p*ldb + j],
+ * accumulated in p order with a multiply and an add per step (no FMA: the
+ * reference's roundings, bitwise equal), then C[rows_t[i0_t + i] + cols_t[j0_t + j]]
+ * += coeffs[t] * acc[i, j] for every target t in order, clipped to the target's
+ * m_t x n_t, PAD positions dropped.  Device slivers, HOST arrays of per-target
+ * device pointers / values; k == 0 leaves the targets untouched.  stats
+ * (synchronises): fast / slow updates per target as store_tile reports them. */
+int stc_microtile(const double *a_sliver, int64_t lda, const double *b_sliver, int64_t ldb, int64_t k, int mr, int nr,
+                  double *C, int n_targets, const int64_t *const *rows, const int64_t *const *cols,
+                  const int64_t *const *rbs, const int64_t *const *cbs, const double *coeffs, const int64_t *i0,
+                  const int64_t *j0, const int64_t *m, const int64_t *n, uint32_t flags, void *stream,
+                  stc_stats *stats);
+
 /* ---- subsystem (4): AB / Naive helpers ---- */
 
 /* accumulate_dense_to_view (kernels.py:236-247, _jit.py:223-256):

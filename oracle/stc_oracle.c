@@ -678,6 +678,58 @@ int ora_contract_reference(const ora_problem *pr, const double *A, const double 
 }
 
 /* oracle.py:102-107 */
+/* Component calls on raw scatter vectors (tests of the device pack_a / pack_b / microkernel):
+ * kernels.py:166-201 through pack_a_block / pack_b_block above.  Views are given by
+ * their scatter vectors (rows[t] of length m, cols[t] of length n) and unit strides;
+ * the block vectors are rebuilt at (rb, cb) as BlockScatterView.from_scatter does. */
+int ora_pack_panel(int which, const double *data, int nviews, const int64_t *const *rows, int64_t m,
+                   const int64_t *const *cols, int64_t n, int64_t rb, int64_t cb, int64_t row_unit,
+                   int64_t col_unit, const double *coeffs, int64_t x0, int64_t xcount, int64_t k0, int64_t kcount,
+                   int force_slow, double *out, int64_t depth, int64_t *fast, int64_t *slow) {
+  side_t sd;
+  sd.n = nviews;
+  sd.v = (view_t **)malloc(sizeof(view_t *) * (size_t)nviews);
+  sd.coeff = (double *)malloc(sizeof(double) * (size_t)nviews);
+  for (int t = 0; t < nviews; ++t) {
+    sd.v[t] = view_new(data, NULL, rows[t], m, cols[t], n, rb, cb, row_unit, col_unit);
+    sd.coeff[t] = coeffs[t];
+  }
+  *fast = *slow = 0;
+  if (which == 0)
+    pack_a_block(out, depth, &sd, x0, xcount, k0, kcount, rb, cb, force_slow, fast, slow);
+  else
+    pack_b_block(out, depth, &sd, k0, kcount, x0, xcount, rb, cb, force_slow, fast, slow);
+  for (int t = 0; t < nviews; ++t) view_free(sd.v[t]);
+  free(sd.v); free(sd.coeff);
+  return 0;
+}
+
+/* kernels.py:204-233: microtile_mats (_jit.py:145-155) on (mr, >= k) x (>= k, nr) row-major
+ * slivers, then store_tile into every target (view t: rows[t] of length tm[t], cols[t] of
+ * length tn[t], block vectors at (mr, nr)), clipped to the view. */
+int ora_microtile(const double *a, int64_t lda, const double *b, int64_t ldb, int64_t k, int64_t mr, int64_t nr,
+                  double *cdata, int ntargets, const int64_t *const *rows, const int64_t *tm,
+                  const int64_t *const *cols, const int64_t *tn, const int64_t *row_unit, const int64_t *col_unit,
+                  const double *coeffs, const int64_t *i0, const int64_t *j0, int force_slow, int64_t *fast,
+                  int64_t *slow) {
+  *fast = *slow = 0;
+  if (k == 0) return 0;
+  double *acc = (double *)calloc((size_t)(mr * nr), sizeof(double));
+  for (int64_t p = 0; p < k; ++p)
+    for (int64_t i = 0; i < mr; ++i) {
+      double av = a[i * lda + p];
+      for (int64_t j = 0; j < nr; ++j) acc[i * nr + j] += av * b[p * ldb + j];
+    }
+  for (int t = 0; t < ntargets; ++t) {
+    view_t *v = view_new(cdata, cdata, rows[t], tm[t], cols[t], tn[t], mr, nr, row_unit[t], col_unit[t]);
+    int64_t ilim = v->m - i0[t] < mr ? v->m - i0[t] : mr, jlim = v->n - j0[t] < nr ? v->n - j0[t] : nr;
+    if (store_tile(acc, v, coeffs[t], i0[t], ilim, j0[t], jlim, mr, nr, force_slow)) ++*fast; else ++*slow;
+    view_free(v);
+  }
+  free(acc);
+  return 0;
+}
+
 double ora_seq_sum_sq(const double *x, int64_t n) {
   double acc = 0.0;
   for (int64_t i = 0; i < n; ++i) acc += x[i] * x[i];

@@ -65,7 +65,7 @@ class PlanInfo(ctypes.Structure):
 _EXPORTS = (
     "stc_last_error", "stc_abi_version", "stc_workspace_size", "stc_contract", "stc_bundle_scatter",
     "stc_block_vector", "stc_fused_term_workspace_size", "stc_fused_term", "stc_accumulate_dense",
-    "stc_unpack_sum", "stc_sq_norms", "stc_set_kernel_events", "stc_set_c_ready",
+    "stc_unpack_sum", "stc_pack_panel", "stc_microtile", "stc_sq_norms", "stc_set_kernel_events", "stc_set_c_ready",
     "stc_host_workspace_size", "stc_contract_host", "stc_host_plan", "stc_fill_uniform", "stc_plan_describe",
     "stc_shard_problem", "stc_host_grid", "stc_sharded_workspace_size", "stc_contract_sharded",
 )
@@ -92,6 +92,10 @@ def _declare(l):
                                  u32, vp, sz, vp, P(Stats)]
     l.stc_accumulate_dense.argtypes = [vp, i64, i64, i64, vp, vp, vp, ctypes.c_double, vp, P(Stats)]
     l.stc_unpack_sum.argtypes = [vp, i64, i64, i64, vp, ctypes.c_int, pp, pp, dp, vp, P(Stats)]
+    l.stc_pack_panel.argtypes = [ctypes.c_int, vp, ctypes.c_int, pp, pp, pp, pp, dp, i64, i64, i64, i64, i64, i64, u32,
+                                 vp, i64, vp, P(Stats)]
+    l.stc_microtile.argtypes = [vp, i64, vp, i64, i64, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, pp, pp, pp, pp,
+                                dp, P(i64), P(i64), P(i64), P(i64), u32, vp, P(Stats)]
     l.stc_sq_norms.argtypes = [ctypes.c_int, P(i64), vp, P(i64), i64, vp, P(i64), i64, dp, vp]
     l.stc_set_kernel_events.argtypes = [vp, vp]
     l.stc_set_c_ready.argtypes = [vp]

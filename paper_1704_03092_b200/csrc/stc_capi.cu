@@ -2511,6 +2511,107 @@ int stc_unpack_sum(double *out, int64_t ldo, int64_t m, int64_t n, const double 
   return STC_OK;
 }
 
+namespace {
+// fast / slow counts of the component passes: written by the kernel into page-locked
+// host memory (one 16-byte block per thread, kept), read after a stream synchronise
+int64_t *host_counts() {
+  thread_local int64_t *p = nullptr;
+  if (!p && cudaHostAlloc(reinterpret_cast<void **>(&p), 2 * sizeof(int64_t), cudaHostAllocMapped) != cudaSuccess) {
+    cudaGetLastError();
+    p = nullptr;
+  }
+  return p;
+}
+}  // namespace
+
+int stc_pack_panel(int side, const double *data, int nviews, const int64_t *const *rows, const int64_t *const *cols,
+                   const int64_t *const *rbs, const int64_t *const *cbs, const double *coeffs, int64_t x0,
+                   int64_t xcount, int64_t k0, int64_t kcount, int64_t width, int64_t kblock, uint32_t flags,
+                   double *out, int64_t out_depth, void *stream, stc_stats *stats) {
+  if (side != 0 && side != 1) return fail(STC_EINVAL, "side must be 0 (A) or 1 (B)");
+  if (nviews < 1 || nviews > MAX_OPS) return fail(STC_EINVAL, "need 1..%d views", MAX_OPS);
+  if (!data || !rows || !cols || !coeffs || !out) return fail(STC_EINVAL, "null argument");
+  if (x0 < 0 || xcount < 0 || k0 < 0 || kcount < 0 || width < 1 || kblock < 1 || out_depth < kcount)
+    return fail(STC_EINVAL, "block [%lld,+%lld) x [%lld,+%lld), width %lld, k block %lld, depth %lld invalid",
+                (long long)x0, (long long)xcount, (long long)k0, (long long)kcount, (long long)width,
+                (long long)kblock, (long long)out_depth);
+  if (x0 % width || k0 % kblock) return fail(STC_EINVAL, "block origin must be a multiple of the register block");
+  const bool count = stats && rbs && cbs;
+  PanelArgs a{};
+  a.vs.n = nviews;
+  for (int t = 0; t < nviews; ++t) {
+    if (coeffs[t] != 1.0 && coeffs[t] != -1.0) return fail(STC_EINVAL, "coefficients must be +/-1");
+    a.vs.rows[t] = rows[t];
+    a.vs.cols[t] = cols[t];
+    a.vs.coeff[t] = coeffs[t];
+    if (count) {
+      a.xbs[t] = side == 0 ? rbs[t] : cbs[t];
+      a.kbs[t] = side == 0 ? cbs[t] : rbs[t];
+    }
+  }
+  a.side = side;
+  a.x0 = x0, a.xcount = xcount, a.k0 = k0, a.kcount = kcount, a.width = width, a.kblock = kblock, a.depth = out_depth;
+  a.force_slow = (flags & STC_FLAG_FORCE_SLOW) ? 1 : 0;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int64_t *cnt = count ? host_counts() : nullptr;
+  if (count && !cnt) return fail(STC_ECUDA, "cudaHostAlloc(counters) failed");
+  CU(launch_pack_panel(a, data, out, cnt, s), "k_pack_panel");
+  if (stats) {
+    stc_stats st{};
+    st.kernel_launches = count ? 2 : 1;
+    if (count) {
+      CU(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+      st.fast_blocks = cnt[0];
+      st.slow_blocks = cnt[1];
+    }
+    *stats = st;
+  }
+  return STC_OK;
+}
+
+int stc_microtile(const double *a_sliver, int64_t lda, const double *b_sliver, int64_t ldb, int64_t k, int mr, int nr,
+                  double *C, int n_targets, const int64_t *const *rows, const int64_t *const *cols,
+                  const int64_t *const *rbs, const int64_t *const *cbs, const double *coeffs, const int64_t *i0,
+                  const int64_t *j0, const int64_t *m, const int64_t *n, uint32_t flags, void *stream,
+                  stc_stats *stats) {
+  if (stats) *stats = stc_stats{};
+  if (k == 0) return STC_OK;  // the reference returns before touching the targets (kernels.py:211-212)
+  if (k < 0 || mr < 1 || nr < 1 || (int64_t)mr * nr > 4096 || lda < k || ldb < nr)
+    return fail(STC_EINVAL, "tile %d x %d, depth %lld, lda %lld, ldb %lld invalid", mr, nr, (long long)k,
+                (long long)lda, (long long)ldb);
+  if (n_targets < 0 || n_targets > MAX_OPS) return fail(STC_EINVAL, "at most %d targets", MAX_OPS);
+  if (!a_sliver || !b_sliver || (n_targets && (!C || !rows || !cols || !coeffs || !i0 || !j0 || !m || !n)))
+    return fail(STC_EINVAL, "null argument");
+  const bool count = stats && rbs && cbs;
+  TileTargets t{};
+  t.n_targets = n_targets;
+  for (int g = 0; g < n_targets; ++g) {
+    if (i0[g] % mr || j0[g] % nr) return fail(STC_EINVAL, "tile origin must be block-aligned");
+    if (i0[g] < 0 || j0[g] < 0 || i0[g] >= m[g] || j0[g] >= n[g])
+      return fail(STC_EINVAL, "tile origin (%lld, %lld) outside the %lld x %lld target", (long long)i0[g],
+                  (long long)j0[g], (long long)m[g], (long long)n[g]);
+    t.rows[g] = rows[g], t.cols[g] = cols[g];
+    t.rbs[g] = count ? rbs[g] : nullptr, t.cbs[g] = count ? cbs[g] : nullptr;
+    t.coeff[g] = coeffs[g];
+    t.i0[g] = i0[g], t.j0[g] = j0[g], t.m[g] = m[g], t.n[g] = n[g];
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int64_t *cnt = count ? host_counts() : nullptr;
+  if (count && !cnt) return fail(STC_ECUDA, "cudaHostAlloc(counters) failed");
+  CU(launch_microtile(a_sliver, lda, b_sliver, ldb, k, mr, nr, C, t, (flags & STC_FLAG_FORCE_SLOW) ? 1 : 0, cnt, s),
+     "k_microtile");
+  if (stats) {
+    stats->kernel_launches = 1;
+    stats->total_flops = 2.0 * mr * nr * (double)k;
+    if (count) {
+      CU(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+      stats->fast_updates = cnt[0];
+      stats->slow_updates = cnt[1];
+    }
+  }
+  return STC_OK;
+}
+
 int stc_sq_norms(int ndim, const int64_t *extents, const double *x, const int64_t *x_strides, int64_t x_base,
                  const double *ref, const int64_t *ref_strides, int64_t ref_base, double *out, void *stream) {
   if (ndim < 0 || ndim > STC_MAX_LABELS) return fail(STC_EINVAL, "bad rank %d", ndim);

@@ -247,6 +247,29 @@ struct ViewSet {
 };
 cudaError_t launch_unpack_views(double *out, int64_t ldo, int64_t m, int64_t n, const double *data,
                                 const ViewSet &vs, cudaStream_t s);
+// stc_pack_panel / stc_microtile: the reference's component kernels (pack_a / pack_b,
+// microkernel) as standalone device passes.  `counts` (device-visible, 2 int64) gets the
+// fast / slow block or update counts.
+struct PanelArgs {
+  ViewSet vs;
+  const int64_t *xbs[MAX_OPS];  // block vectors of the sliver dimension (rbs for A, cbs for B)
+  const int64_t *kbs[MAX_OPS];  // block vectors of the k dimension
+  int side;                     // 0: A (views m x k, mr-row slivers), 1: B (views k x n, nr-column slivers)
+  int64_t x0, xcount, k0, kcount, width, kblock, depth;
+  int force_slow;
+};
+cudaError_t launch_pack_panel(const PanelArgs &a, const double *data, double *out, int64_t *counts, cudaStream_t s);
+struct TileTargets {
+  const int64_t *rows[MAX_OPS];
+  const int64_t *cols[MAX_OPS];
+  const int64_t *rbs[MAX_OPS];
+  const int64_t *cbs[MAX_OPS];
+  double coeff[MAX_OPS];
+  int64_t i0[MAX_OPS], j0[MAX_OPS], m[MAX_OPS], n[MAX_OPS];
+  int n_targets;
+};
+cudaError_t launch_microtile(const double *a, int64_t lda, const double *b, int64_t ldb, int64_t k, int mr, int nr,
+                             double *C, const TileTargets &t, int force_slow, int64_t *counts, cudaStream_t s);
 cudaError_t launch_fill_uniform(double *out, int ndim, const int64_t *ext, const int64_t *str, int64_t base,
                                 uint64_t seed, cudaStream_t s);
 cudaError_t launch_sq_norms(int ndim, const int64_t *ext, const double *x, const int64_t *xs, int64_t xb,

@@ -516,6 +516,95 @@ cudaError_t launch_unpack_views(double *out, int64_t ldo, int64_t m, int64_t n, 
   return cudaGetLastError();
 }
 
+// ---- the reference's component kernels as standalone passes ------------------
+// pack_a_block / pack_b_block (_jit.py:27-131): out[s, p, i] = sum_t coeff_t * view_t
+// element, views added in order from 0.0 (the reference's roundings), PAD and fringe
+// positions 0; sliver s = `width` consecutive rows (A) or columns (B), p < kcount.
+__global__ void k_pack_panel(const PanelArgs a, const double *__restrict__ data, double *__restrict__ out) {
+  const int64_t slivers = (a.xcount + a.width - 1) / a.width;
+  const int64_t total = slivers * a.kcount * a.width;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % a.width, p = (e / a.width) % a.kcount, s = e / (a.width * a.kcount);
+    const int64_t x = s * a.width + i;
+    double acc = 0.0;
+    if (x < a.xcount) {
+      const int64_t ri = a.side == 0 ? a.x0 + x : a.k0 + p, ci = a.side == 0 ? a.k0 + p : a.x0 + x;
+      for (int t = 0; t < a.vs.n; ++t) {
+        const int64_t ro = a.vs.rows[t][ri], co = a.vs.cols[t][ci];
+        if (ro == kPad || co == kPad) continue;
+        acc = __dadd_rn(acc, __dmul_rn(a.vs.coeff[t], data[ro + co]));
+      }
+    }
+    out[(s * a.depth + p) * a.width + i] = acc;
+  }
+}
+
+// fast / slow sub-blocks as the reference counts them (per sliver x kblock-chunk: fast when
+// every view's block vectors are nonzero there): #regular slivers x #regular chunks.
+__global__ void k_pack_count(const PanelArgs a, int64_t *__restrict__ counts) {
+  __shared__ unsigned long long reg[2];
+  if (threadIdx.x < 2) reg[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t slivers = (a.xcount + a.width - 1) / a.width, chunks = (a.kcount + a.kblock - 1) / a.kblock;
+  for (int64_t e = threadIdx.x; e < slivers + chunks; e += blockDim.x) {
+    const bool is_x = e < slivers;
+    const int64_t blk = is_x ? (a.x0 + e * a.width) / a.width : (a.k0 + (e - slivers) * a.kblock) / a.kblock;
+    bool ok = !a.force_slow;
+    for (int t = 0; ok && t < a.vs.n; ++t) ok = (is_x ? a.xbs[t][blk] : a.kbs[t][blk]) != 0;
+    if (ok) atomicAdd(&reg[is_x ? 0 : 1], 1ULL);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int64_t fast = (int64_t)(reg[0] * reg[1]);
+    counts[0] = fast;
+    counts[1] = slivers * chunks - fast;
+  }
+}
+
+cudaError_t launch_pack_panel(const PanelArgs &a, const double *data, double *out, int64_t *counts, cudaStream_t s) {
+  const int64_t slivers = (a.xcount + a.width - 1) / a.width, total = slivers * a.kcount * a.width;
+  if (total > 0) {
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    k_pack_panel<<<blocks, 256, 0, s>>>(a, data, out);
+  }
+  if (counts) k_pack_count<<<1, 256, 0, s>>>(a, counts);
+  return cudaGetLastError();
+}
+
+// microtile_mats + store_tile (_jit.py:145-186): element (i, j) of the mr x nr tile
+// accumulates a[i, p] * b[p, j] over p in order (a multiply and an add per step, no
+// FMA: the reference's roundings), then adds coeff * acc into every target in target
+// order (one thread owns an element of all targets: identical targets stay ordered).
+__global__ void k_microtile(const double *__restrict__ a, int64_t lda, const double *__restrict__ b, int64_t ldb,
+                            int64_t k, int mr, int nr, double *__restrict__ C, const TileTargets t, int force_slow,
+                            int64_t *__restrict__ counts) {
+  for (int e = threadIdx.x; e < mr * nr; e += blockDim.x) {
+    const int i = e / nr, j = e - i * nr;
+    double acc = 0.0;
+    for (int64_t p = 0; p < k; ++p) acc = __dadd_rn(acc, __dmul_rn(a[i * lda + p], b[p * ldb + j]));
+    for (int g = 0; g < t.n_targets; ++g) {
+      if (i >= t.m[g] - t.i0[g] || j >= t.n[g] - t.j0[g]) continue;  // fringe tiles are clipped to the view
+      const int64_t ro = t.rows[g][t.i0[g] + i], co = t.cols[g][t.j0[g] + j];
+      if (ro == kPad || co == kPad) continue;
+      C[ro + co] = __dadd_rn(C[ro + co], __dmul_rn(t.coeff[g], acc));
+    }
+  }
+  if (counts && threadIdx.x == 0) {
+    int64_t fast = 0;
+    for (int g = 0; g < t.n_targets; ++g)
+      fast += !force_slow && t.rbs[g][t.i0[g] / mr] != 0 && t.cbs[g][t.j0[g] / nr] != 0;
+    counts[0] = fast;
+    counts[1] = t.n_targets - fast;
+  }
+}
+
+cudaError_t launch_microtile(const double *a, int64_t lda, const double *b, int64_t ldb, int64_t k, int mr, int nr,
+                             double *C, const TileTargets &t, int force_slow, int64_t *counts, cudaStream_t s) {
+  const int threads = std::min(1024, std::max(32, (mr * nr + 31) / 32 * 32));
+  k_microtile<<<1, threads, 0, s>>>(a, lda, b, ldb, k, mr, nr, C, t, force_slow, counts);
+  return cudaGetLastError();
+}
+
 // ---- deterministic squared norms over strided tensors ----------------------
 struct NormShape {
   int ndim;

@@ -403,3 +403,16 @@ def contract(spec: ContractionSpec, a, b, c, level: int, variant, params: Blocki
     stats.seconds = max(time.perf_counter() - t_start, 1e-12)
     stats.effective_gflops = effective_gflops(spec.n_i, spec.n_j, spec.n_p, stats.seconds)
     return stats
+
+
+def contract_reference(spec: ContractionSpec, a, b, c) -> None:
+    """C += the classical contraction (the reference's ``contract_reference``, oracle.py:82-94).
+
+    The reference loops every (I, J, P) multi-index on the CPU; here it is the
+    level-0 contraction on the DMMA kernel in the reference's tile order -- the
+    same products, summed over P in the kernel's k order (differences at
+    rounding level, exact on integer data).  Not the test oracle: the tests
+    check against ``oracle/`` on the CPU.
+    """
+    contract(spec, a, b, c, 0, Variant.ABC, reference_tiling=True)
+

@@ -11,6 +11,10 @@ Reference counterparts (``/root/reference/pkg/src/strassen_tc``):
 * ``OperandTermSide`` / ``FusedPrimitive`` / ``run_fused`` /
   ``run_gemm_dense`` -- kernels.py:102-154, driver.py:26-152: one fused
   Strassen term on the DMMA kernel (subsystems (2)+(3)).
+* ``PackedBuffer`` / ``pack_a`` / ``pack_b`` / ``microkernel`` -- kernels.py:67-233: the
+  packing pass and the micro-tile as standalone device calls (``stc_pack_panel``,
+  ``stc_microtile``), bitwise the reference's panels and tiles.  ``contract`` does this
+  work inside the fused kernel; these exist for callers of the component API.
 * ``accumulate_dense_to_view`` / ``unpack_to_dense`` -- kernels.py:236-264
   (subsystem (4)).
 * ``relative_error`` -- oracle.py:110-124, reduced on the device.
@@ -42,9 +46,13 @@ __all__ = [
     "BlockScatterView",
     "FusedPrimitive",
     "OperandTermSide",
+    "PackedBuffer",
     "accumulate_dense_to_view",
     "make_view",
     "matrix_view",
+    "microkernel",
+    "pack_a",
+    "pack_b",
     "pad_view",
     "quadrant_views",
     "relative_error",
@@ -440,6 +448,151 @@ def run_fused(prim: FusedPrimitive, params: BlockingParams = DEFAULT_BLOCKING, s
                                     flags, _ptr(ws), ws.numel(), _stream(), ctypes.byref(st)))
     stats.absorb(st)
     return stats
+
+
+# ---------------------------------------------------------------- component calls
+@dataclass(eq=False)
+class PackedBuffer:
+    """Sliver-major packed panel in HBM (kernels.py:67-99).
+
+    ``data[s, p, i]``: A side, row ``i`` of sliver ``s`` (width = mr) at depth
+    ``p``; B side, column ``i`` (width = nr).  A contiguous float64 CUDA tensor
+    (256-byte aligned by the allocator; the reference aligns to a cache line).
+    """
+
+    data: object
+    width: int
+    depth: int
+
+    @property
+    def n_slivers(self) -> int:
+        return self.data.shape[0]
+
+    def element(self, s: int, p: int, i: int) -> float:
+        return float(self.data[s, p, i])
+
+    @classmethod
+    def _panel(cls, extent: int, depth: int, width: int, device) -> "PackedBuffer":
+        torch = _torch()
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        return cls(torch.zeros((-(-extent // width), depth, width), dtype=torch.float64, device=dev), width, depth)
+
+    @classmethod
+    def a_panel(cls, params: BlockingParams, m: int | None = None, k: int | None = None, device=None):
+        return cls._panel(params.mc if m is None else min(params.mc, m),
+                          params.kc if k is None else min(params.kc, k), params.mr, device)
+
+    @classmethod
+    def b_panel(cls, params: BlockingParams, n: int | None = None, k: int | None = None, device=None):
+        return cls._panel(params.nc if n is None else min(params.nc, n),
+                          params.kc if k is None else min(params.kc, k), params.nr, device)
+
+
+def _interval(name: str, rng, limit: int, cap: int, align: int):
+    lo, hi = rng
+    if not 0 <= lo < hi <= limit:
+        raise ValueError(f"{name} interval [{lo},{hi}) out of bounds for size {limit}")
+    if hi - lo > cap:
+        raise ValueError(f"{name} interval [{lo},{hi}) exceeds cache block {cap}")
+    if lo % align:
+        raise ValueError(f"{name} interval must start at a multiple of {align}")
+    return lo, hi
+
+
+def _pack(which: int, side: OperandTermSide, x_rng, k_rng, width: int, kblock: int, out: PackedBuffer,
+          stats: RunStats | None, force_slow: bool) -> None:
+    torch = _torch()
+    (x0, x1), (k0, k1) = x_rng, k_rng
+    if out.width != width or out.depth < k1 - k0 or out.n_slivers < -(-(x1 - x0) // width):
+        raise ValueError("packed buffer too small for the requested block")
+    if not (isinstance(out.data, torch.Tensor) and out.data.is_cuda and out.data.is_contiguous()
+            and out.data.dtype == torch.float64):
+        raise ValueError("packed buffer must be a contiguous float64 CUDA tensor (PackedBuffer.a_panel / b_panel)")
+    tabs = [_ptr_array([f(v) for v in side.views])
+            for f in (lambda v: v.rscat, lambda v: v.cscat, lambda v: v.rbs, lambda v: v.cbs)]
+    co = _coeff_array(side.coeffs)
+    st = _lib.Stats()
+    with torch.cuda.device(side.data.device):
+        _lib.check(_lib.lib().stc_pack_panel(which, _ptr(side.data), len(side.views), tabs[0][0], tabs[1][0],
+                                             tabs[2][0], tabs[3][0], co, x0, x1 - x0, k0, k1 - k0, width, kblock,
+                                             _lib.FLAG_FORCE_SLOW if force_slow else 0, _ptr(out.data), out.depth,
+                                             _stream(), ctypes.byref(st)))
+    if stats is not None:
+        stats.fast_blocks += st.fast_blocks
+        stats.slow_blocks += st.slow_blocks
+
+
+def pack_a(side: OperandTermSide, row_block, k_block, params: BlockingParams, out: PackedBuffer,
+           stats: RunStats | None, force_slow: bool = False) -> None:
+    """The A-side term sum over row_block x k_block into mr-row slivers (kernels.py:166-182):
+    the Strassen packing pass on its own (``stc_pack_panel``), bitwise the reference's panel."""
+    if (side.rb, side.cb) != (params.mr, params.kr):
+        raise ValueError(f"A-side views need block geometry ({params.mr},{params.kr}), got ({side.rb},{side.cb})")
+    rows = _interval("row", row_block, side.m, params.mc, params.mr)
+    ks = _interval("k", k_block, side.n, params.kc, params.kr)
+    _pack(0, side, rows, ks, params.mr, params.kr, out, stats, force_slow)
+
+
+def pack_b(side: OperandTermSide, k_block, col_block, params: BlockingParams, out: PackedBuffer,
+           stats: RunStats | None, force_slow: bool = False) -> None:
+    """The B-side term sum over k_block x col_block into nr-column slivers (kernels.py:185-201)."""
+    if (side.rb, side.cb) != (params.kr, params.nr):
+        raise ValueError(f"B-side views need block geometry ({params.kr},{params.nr}), got ({side.rb},{side.cb})")
+    ks = _interval("k", k_block, side.m, params.kc, params.kr)
+    cols = _interval("col", col_block, side.n, params.nc, params.nr)
+    _pack(1, side, cols, ks, params.nr, params.kr, out, stats, force_slow)
+
+
+def microkernel(a_sliver, b_sliver, k: int, targets, stats: RunStats | None, force_slow: bool = False) -> None:
+    """One mr x nr tile product, then coeff * tile added into every target (kernels.py:204-233).
+
+    ``a_sliver`` (mr, >= k) and ``b_sliver`` (>= k, nr): numpy arrays or torch tensors;
+    ``targets``: ``(view, i0, j0, coeff)`` tuples over device views.  The tile is
+    accumulated in the reference's order and roundings (``stc_microtile``: bitwise equal).
+    """
+    if k == 0:
+        return
+    torch = _torch()
+    targets = list(targets)
+    dev = (targets[0][0].base.data.device if targets
+           else a_sliver.device if isinstance(a_sliver, torch.Tensor) and a_sliver.is_cuda
+           else torch.device("cuda", torch.cuda.current_device()))
+
+    def sliver(x):
+        x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)) if isinstance(x, np.ndarray) else x
+        if x.dim() != 2:
+            raise ValueError("slivers must be 2-D")
+        return x.to(device=dev, dtype=torch.float64).contiguous()
+
+    a, b = sliver(a_sliver), sliver(b_sliver)
+    mr, nr = a.shape[0], b.shape[1]
+    if a.shape[1] < k or b.shape[0] < k:
+        raise ValueError("slivers shorter than the requested accumulation depth")
+    for view, i0, j0, _ in targets:
+        if view.rb != mr or view.cb != nr:
+            raise ValueError(f"target blocks ({view.rb},{view.cb}) do not match tile ({mr},{nr})")
+        if i0 % mr or j0 % nr:
+            raise ValueError("tile origin must be block-aligned")
+        if view.base.data is not targets[0][0].base.data:
+            raise ValueError("targets of one tile must share one parent tensor")
+    if not targets:
+        return
+    views = [t[0] for t in targets]
+    tabs = [_ptr_array([f(v) for v in views])
+            for f in (lambda v: v.rscat, lambda v: v.cscat, lambda v: v.rbs, lambda v: v.cbs)]
+    co = _coeff_array([t[3] for t in targets])
+    i64s = lambda xs: (ctypes.c_int64 * len(xs))(*[int(x) for x in xs])
+    st = _lib.Stats()
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().stc_microtile(_ptr(a), a.stride(0), _ptr(b), b.stride(0), int(k), mr, nr,
+                                            _ptr(views[0].base.data), len(targets), tabs[0][0], tabs[1][0],
+                                            tabs[2][0], tabs[3][0], co, i64s([t[1] for t in targets]),
+                                            i64s([t[2] for t in targets]), i64s([v.m for v in views]),
+                                            i64s([v.n for v in views]), _lib.FLAG_FORCE_SLOW if force_slow else 0,
+                                            _stream(), ctypes.byref(st)))
+    if stats is not None:
+        stats.fast_updates += st.fast_updates
+        stats.slow_updates += st.slow_updates
 
 
 def _col_major_tensor(mat, name: str) -> DenseTensor:
