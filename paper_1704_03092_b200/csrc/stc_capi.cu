@@ -2516,7 +2516,7 @@ namespace {
 // host memory (one 16-byte block per thread, kept), read after a stream synchronise
 int64_t *host_counts() {
   thread_local int64_t *p = nullptr;
-  if (!p && cudaHostAlloc(reinterpret_cast<void **>(&p), 2 * sizeof(int64_t), cudaHostAllocMapped) != cudaSuccess) {
+  if (!p && cudaHostAlloc(reinterpret_cast<void **>(&p), 2 * sizeof(int64_t), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
     cudaGetLastError();
     p = nullptr;
   }
