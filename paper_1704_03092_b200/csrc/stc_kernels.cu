@@ -275,7 +275,10 @@ cudaError_t launch_unpack(const UnpackArgs &a, cudaStream_t s) {
 // view of x-quadrant (xfirst ? qa : qb) and k-quadrant (the other) copied into a
 // dense [k][x] (kfast = 0) or [x][k] (kfast = 1) block, PAD -> 0.  A pure copy:
 // the Strassen sums stay in the fused kernel, in the reference's view order.
-constexpr int UNPACK_ROWS = 4;  // k_pack_views: rows of the slow dimension per block
+#ifndef STC_PACK_ROWS
+#define STC_PACK_ROWS 8
+#endif
+constexpr int UNPACK_ROWS = STC_PACK_ROWS;  // k_pack_views: rows of the slow dimension per block
 
 __global__ void __launch_bounds__(256) k_pack_views(const double *__restrict__ D, const int64_t *__restrict__ pool,
                                                     PackArgs a, double *__restrict__ out) {
@@ -295,13 +298,16 @@ __global__ void __launch_bounds__(256) k_pack_views(const double *__restrict__ D
   if (f < 0) return;
   const int64_t fo = __ldg(fv + f);
   const int64_t s0 = by * UNPACK_ROWS;
-#pragma unroll 4
-  for (int r = 0; r < UNPACK_ROWS; ++r) {
-    const int64_t sl = s0 + r;
-    if (sl >= slow_len) break;
-    const int64_t so = __ldg(sv + sl);
-    o[sl * fast_len + f] = (fo == kPad || so == kPad) ? 0.0 : __ldg(D + fo + so);
-  }
+  // all of the thread's gathers in flight before the first store
+  int64_t so[UNPACK_ROWS];
+  double v[UNPACK_ROWS];
+#pragma unroll
+  for (int r = 0; r < UNPACK_ROWS; ++r) so[r] = s0 + r < slow_len ? __ldg(sv + s0 + r) : kPad;
+#pragma unroll
+  for (int r = 0; r < UNPACK_ROWS; ++r) v[r] = (fo == kPad || so[r] == kPad) ? 0.0 : __ldg(D + fo + so[r]);
+#pragma unroll
+  for (int r = 0; r < UNPACK_ROWS; ++r)
+    if (s0 + r < slow_len) o[(s0 + r) * fast_len + f] = v[r];
 }
 
 cudaError_t launch_pack_views(const double *D, const int64_t *pool, const PackArgs &a0, double *out, cudaStream_t s) {
