@@ -611,7 +611,7 @@ FusedSides mixed_sides(const stc_problem *p, const Plan &pl);
 bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, const double *A, const double *B,
                 const double *C, GemmArgs &g, CUtensorMap maps[3], CoordJobs &jobs);
 
-// Pre-summed operands for ABC / AB at L = 1, 2 (STC_PRESUM_OPS = 0 / 1 forces it off /
+// Pre-summed operands for ABC / AB at L = 1, 2, 3 (STC_PRESUM_OPS = 0 / 1 forces it off /
 // on).  The sums cost one HBM pass per side (4^L quadrant reads + 7^L slot writes per
 // element position) and take every DADD off the FP64 pipe the DMMAs use: the fused
 // kernel's in-SM sums cost it 4-10 % (L1; 10 % with A k-contiguous) / 18 % (L2) of its DMMA time (cfg2, 16384^3,
@@ -619,11 +619,14 @@ bool plan_fused(const stc_problem *p, const Plan &pl, const FusedSides &fs, cons
 // anyway (one read + one write of every quadrant), which the presum pass replaces.
 // Cost model at 5 TB/s and 33 TF/s executed.
 bool presum_wanted(const stc_problem *p, const Plan &pl) {
-  if (pl.level < 1 || pl.level > 2 || pl.variant == STC_VARIANT_NAIVE) return false;
+  if (pl.level < 1 || pl.level > 3 || pl.variant == STC_VARIANT_NAIVE) return false;
   if (pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) return false;
   if (const char *e = stc_env("STC_FUSED"))
     if (atoi(e) == 0) return false;
   if (const char *e = stc_env("STC_PRESUM_OPS")) return atoi(e) != 0;
+  // L = 3: up to 8 views per side are beyond the fused kernel's stages -- without slots the
+  // gather kernel runs the problem (16384^3 L3 ABC 562 ms against 208 ms through slots)
+  if (pl.level == 3) return true;
   const double qa = (double)pl.mq_pad * pl.kq_pad, qb = (double)pl.kq_pad * pl.nq_pad;
   const double quads = (double)pl.nquads, T = pl.level == 1 ? 7.0 : 49.0;
   const double t_presum = 8.0 * (quads + T) * (qa + qb) / 5e12;
@@ -684,7 +687,9 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
     const char *ts = stc_env("STC_TSHAPE");
     // (A / B base offsets even: TMA needs 16-byte aligned views of the 256-byte aligned
     // allocations; the shaped plan has no gather-kernel fallback)
-    const bool allowed = (!ts || atoi(ts) != 0) && pl.level >= 1 && pl.variant != STC_VARIANT_NAIVE &&
+    // (L >= 3 runs on the fused kernel only through pre-summed slots: L = 3 unless switched off)
+    const bool deep_gather = pl.level > 3 || (pl.level == 3 && stc_env("STC_PRESUM_OPS") && atoi(stc_env("STC_PRESUM_OPS")) == 0);
+    const bool allowed = (!ts || atoi(ts) != 0) && pl.level >= 1 && !deep_gather && pl.variant != STC_VARIANT_NAIVE &&
                          p->a_base % 2 == 0 && p->b_base % 2 == 0 &&
                          !(p->flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) &&
                          !(stc_env("STC_FUSED") && atoi(stc_env("STC_FUSED")) == 0) &&
@@ -806,8 +811,8 @@ int build_plan(const stc_problem *p, Plan &pl, int grid_hint) {
   }
   // Operand sums pre-formed into per-term slots (k_presum): ABC and AB when worth it
   // (AB with pre-summed operands is the Naive schedule: the same M products), and
-  // always for Naive (its explicit submatrix copies) at L <= 2.
-  pl.presum = pl.variant == STC_VARIANT_NAIVE ? (pl.level >= 1 && pl.level <= 2) : presum_wanted(p, pl);
+  // always for Naive (its explicit submatrix copies) at L <= 3 (k_unpack beyond).
+  pl.presum = pl.variant == STC_VARIANT_NAIVE ? (pl.level >= 1 && pl.level <= 3) : presum_wanted(p, pl);
   pl.presum_sides = pl.presum ? 3 : 0;
   if (pl.variant != STC_VARIANT_NAIVE && !pl.ticketed && pl.level >= 1 && pl.level <= 2 &&
       !(pl.flags & (STC_FLAG_FORCE_SLOW | STC_FLAG_REFERENCE_TILING)) &&

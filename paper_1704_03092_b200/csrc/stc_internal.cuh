@@ -180,7 +180,7 @@ struct UnpackArgs {
 // the Naive variant unpacks (_jit.unpack_sum, _jit.py:259-309) and the ABC / AB
 // variants form while packing (_jit.pack_a_block / pack_b_block, _jit.py:27-131),
 // same view order and roundings as the fused kernel's in-SM sums.
-constexpr int kPresumMaxTerms = 49;  // 7^L, L <= 2
+constexpr int kPresumMaxTerms = 343;  // 7^L, L <= 3
 struct PresumArgs {
   const double *D;
   const int64_t *pool;

@@ -331,22 +331,32 @@ constexpr int kL1Q[2][7][2] = {{{0, 3}, {2, 3}, {0, 0}, {3, 0}, {0, 1}, {2, 0}, 
 constexpr int kL1S[2][7][2] = {{{1, 1}, {1, 1}, {1, 1}, {1, 1}, {1, 1}, {1, -1}, {1, -1}},
                                {{1, 1}, {1, 1}, {1, -1}, {1, -1}, {1, 1}, {1, 1}, {1, 1}}};
 
-// View O of term T at level L (strassen.py:70-94: outer level first, quadrant
-// q1 * 4 + q2, sign s1 * s2), as (x quadrant, k quadrant, sign) of the side.
+// View O of term T at level L <= 3 (strassen.py:70-94: outer level first -- term
+// t1 * 7^(L-1) + ..., view order outer-major, quadrant q1 * 4^(L-1) + ..., sign the
+// product), as (x quadrant, k quadrant, sign) of the side.
+constexpr int ps_pow7(int l) { return l <= 0 ? 1 : 7 * ps_pow7(l - 1); }
 template <int L, int SIDE, int T>
 struct PsTerm {
-  static constexpr int t1 = L == 2 ? T / 7 : T, t2 = L == 2 ? T % 7 : 0;
-  static constexpr int n2 = L == 2 ? kL1Cnt[SIDE][t2] : 1;
-  static constexpr int count = kL1Cnt[SIDE][t1] * n2;
+  // base-7 digits of T, outer level first (unused levels: term 2, a single + view of quadrant 0)
+  static constexpr int t1 = T / ps_pow7(L - 1);
+  static constexpr int t2 = L >= 2 ? (T / ps_pow7(L - 2)) % 7 : 2;
+  static constexpr int t3 = L >= 3 ? T % 7 : 2;
+  static constexpr int n2 = L >= 2 ? kL1Cnt[SIDE][t2] : 1;
+  static constexpr int n3 = L >= 3 ? kL1Cnt[SIDE][t3] : 1;
+  static constexpr int count = kL1Cnt[SIDE][t1] * n2 * n3;
 };
 template <int L, int SIDE, int T, int O>
 struct PsOp {
   using TT = PsTerm<L, SIDE, T>;
-  static constexpr int o1 = O / TT::n2, o2 = O % TT::n2;
-  static constexpr int q1 = kL1Q[SIDE][TT::t1][o1], q2 = L == 2 ? kL1Q[SIDE][TT::t2][o2] : 0;
-  static constexpr int sign = kL1S[SIDE][TT::t1][o1] * (L == 2 ? kL1S[SIDE][TT::t2][o2] : 1);
-  static constexpr int r = L == 2 ? 2 * (q1 >> 1) + (q2 >> 1) : q1 >> 1;  // quad_rc
-  static constexpr int c = L == 2 ? 2 * (q1 & 1) + (q2 & 1) : q1 & 1;
+  static constexpr int o1 = O / (TT::n2 * TT::n3), o2 = (O / TT::n3) % TT::n2, o3 = O % TT::n3;
+  static constexpr int q1 = kL1Q[SIDE][TT::t1][o1];
+  static constexpr int q2 = L >= 2 ? kL1Q[SIDE][TT::t2][o2] : 0;
+  static constexpr int q3 = L >= 3 ? kL1Q[SIDE][TT::t3][o3] : 0;
+  static constexpr int sign = kL1S[SIDE][TT::t1][o1] * (L >= 2 ? kL1S[SIDE][TT::t2][o2] : 1) *
+                              (L >= 3 ? kL1S[SIDE][TT::t3][o3] : 1);
+  // quad_rc: row / column bits of the quadrant path, outer level most significant
+  static constexpr int r = L == 3 ? 4 * (q1 >> 1) + 2 * (q2 >> 1) + (q3 >> 1) : L == 2 ? 2 * (q1 >> 1) + (q2 >> 1) : q1 >> 1;
+  static constexpr int c = L == 3 ? 4 * (q1 & 1) + 2 * (q2 & 1) + (q3 & 1) : L == 2 ? 2 * (q1 & 1) + (q2 & 1) : q1 & 1;
   static constexpr int xq = SIDE == 0 ? r : c, kq = SIDE == 0 ? c : r;
 };
 
@@ -362,9 +372,11 @@ __device__ __forceinline__ double ps_rest(const double (&v)[Q][Q], double s) {
   }
 }
 
-template <int L, int SIDE, int T, int Q>
+// terms [T0, T1) in order (split in halves: 7^3 terms exceed the compiler's linear recursion depth)
+template <int L, int SIDE, int T0, int T1, int Q>
 __device__ __forceinline__ void ps_terms(const PresumArgs &a, const double (&v)[Q][Q], int64_t pos) {
-  if constexpr (T < (L == 2 ? 49 : 7)) {
+  if constexpr (T1 - T0 == 1) {
+    constexpr int T = T0;
     const int slot = a.slot[T];
     if (slot >= 0) {
       using op0 = PsOp<L, SIDE, T, 0>;
@@ -375,7 +387,10 @@ __device__ __forceinline__ void ps_terms(const PresumArgs &a, const double (&v)[
       s = ps_rest<L, SIDE, T, 1, Q>(v, s);
       a.out[(int64_t)slot * a.slot_stride + pos] = s;
     }
-    ps_terms<L, SIDE, T + 1, Q>(a, v, pos);
+  } else {
+    constexpr int M = T0 + (T1 - T0) / 2;
+    ps_terms<L, SIDE, T0, M, Q>(a, v, pos);
+    ps_terms<L, SIDE, M, T1, Q>(a, v, pos);
   }
 }
 
@@ -409,7 +424,7 @@ __device__ __forceinline__ void presum_block(const PresumArgs &a, int64_t bx, in
         const int64_t xo = a.kfast ? so[xq] : fo[xq], ko = a.kfast ? fo[kq] : so[kq];
         v[xq][kq] = (xo == kPad || ko == kPad) ? 0.0 : __ldcs(a.D + xo + ko);
       }
-    ps_terms<L, SIDE, 0, Q>(a, v, sl * fast_len + f);
+    ps_terms<L, SIDE, 0, ps_pow7(L), Q>(a, v, sl * fast_len + f);
   }
 }
 
@@ -447,6 +462,7 @@ cudaError_t launch_presum2(const PresumArgs &pa, const PresumArgs &pb, cudaStrea
   const int64_t ax1 = std::max<int64_t>(ax, 1), bx1 = std::max<int64_t>(bx, 1);
   if (pa.level == 1) return launch_pdl(k_presum<1>, dim3((unsigned)total), dim3(256), 0, s, pa, pb, ax1, na, bx1);
   if (pa.level == 2) return launch_pdl(k_presum<2>, dim3((unsigned)total), dim3(256), 0, s, pa, pb, ax1, na, bx1);
+  if (pa.level == 3) return launch_pdl(k_presum<3>, dim3((unsigned)total), dim3(256), 0, s, pa, pb, ax1, na, bx1);
   return cudaErrorInvalidValue;
 }
 

@@ -195,3 +195,26 @@ def test_cfg5_variants_and_levels():
             assert torch.equal(c.data, ab.data), variant
         del c
         torch.cuda.empty_cache()
+
+
+def test_cfg5_level_three_allow_deep():
+    # three levels (allow_deep; beyond the BASELINE levels): 343 pre-summed slot pairs
+    # (k_presum<3>) in batches on the one-view fused kernel, dense M + ordered accumulate;
+    # the whole 32768^3 tensor against the device classical contraction, ABC and Naive
+    # bitwise equal (the same M products added in the same term order)
+    import torch
+
+    dev = torch.device("cuda", 0)
+    spec, a, b = _problem(_cases("cfg5")[0]["line"], dev)
+    m, n, k = spec.n_i, spec.n_j, spec.n_p
+    classical = (a.data.view(m, k) @ b.data.view(k, n)).reshape(-1)
+    first = None
+    for variant in (stc.Variant.ABC, stc.Variant.NAIVE):
+        c = _zeros(spec, dev)
+        st = stc.contract(spec, a, b, c, 3, variant, allow_deep=True)
+        assert st.leaf_multiplies == 343
+        assert _normwise(c.data, classical) <= TOL, variant
+        if first is None:
+            first = c
+        else:
+            assert torch.equal(c.data, first.data)

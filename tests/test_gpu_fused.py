@@ -377,6 +377,44 @@ def test_presummed_irregular_layouts_match_oracle(line):
             assert stc.relative_error(cp, classical) <= TOL, (line, level, variant)
 
 
+def _run_env_deep(spec, a, b, c0, variant, env):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        c = c0.to_device()
+        st = stc.contract(spec, a, b, c, 3, variant, allow_deep=True)
+        return c.to_host(), st
+    finally:
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("line", [
+    LAYOUTS["ax_bk"], LAYOUTS["ak_bx"],
+    "abcij eafbc ifje & a:10;b:7;c:13;i:14;j:9;e:18;f:11;",  # irregular, PAD quadrants at L3
+])
+def test_level_three_presummed_slots_match_gather_kernel_bitwise(line):
+    # L3 (allow_deep): the 343 terms' operand sums (up to 8 views a side) come from k_presum<3>
+    # slots and run on the fused one-view kernel; bitwise equal to the gather kernel forming
+    # the same sums in its producers (STC_PRESUM_OPS=0), every variant, and to the oracle
+    spec = stc.parse_benchmark_line(line)
+    a, b, c0 = _operands(spec, 83)
+    classical = c0.copy()
+    oracle.contract_reference(spec, a.to_host(), b.to_host(), classical)
+    for variant in ("abc", "ab", "naive"):
+        cp, st = _run_env_deep(spec, a, b, c0, variant, {})
+        assert st.leaf_multiplies == 343 and st.fast_blocks > 0, (line, variant, st)
+        assert stc.relative_error(cp, classical) <= TOL, (line, variant)
+        if variant != "naive":
+            ck, _ = _run_env_deep(spec, a, b, c0, variant, {"STC_PRESUM_OPS": "0"})
+            assert np.array_equal(cp.data, ck.data), (line, variant)
+    plan = stc.describe_plan(spec, a, b, c0, 3, "abc")
+    assert plan["presum"] == 1 and plan["terms"] == 343, plan
+
+
 @pytest.mark.parametrize("line,level", [
     ("abcij eafbc ifje & a:50;b:7;c:13;i:70;j:45;e:90;f:33;", 0),  # cfg4 L0: the consumers' scatter epilogue
     ("aibj eafb jfie & a:32;b:64;i:32;j:64;e:32;f:32;", 2),         # L2 ABC, TMA reduce-add epilogue

@@ -40,6 +40,10 @@ CONFIGS = {
     "cfg5p88": ("abcijk abcefg efgijk & a:4;b:32;c:32;i:4;j:32;k:32;e:32;f:32;g:32;", [(2, "abc")]),
     "cfg5v": ("abcijk abcefg efgijk & a:32;b:32;c:32;i:32;j:32;k:32;e:32;f:32;g:32;", [(2, "ab"), (2, "naive"),
                                                                                       (1, "abc"), (0, "abc")]),
+    # three levels (allow_deep): pre-summed slots of 343 terms (k_presum<3>)
+    "deep": ("abij abef efij & a:128;b:128;i:128;j:128;e:128;f:128;", [(3, "abc"), (3, "ab"), (3, "naive")]),
+    "cfg5deep": ("abcijk abcefg efgijk & a:32;b:32;c:32;i:32;j:32;k:32;e:32;f:32;g:32;", [(3, "abc"), (3, "naive")]),
+    "cfg2deep": ("aibj eafb jfie & a:64;b:64;i:64;j:64;e:64;f:64;", [(3, "abc"), (3, "naive")]),
     "cfg5": ("abcijk abcefg efgijk & a:32;b:32;c:32;i:32;j:32;k:32;e:32;f:32;g:32;", [(2, "abc")]),
 }
 
@@ -71,11 +75,12 @@ def main(names):
         b = dev_tensor(spec.tensor_extents(spec.labels_b), 2)
         c = dev_tensor(spec.tensor_extents(spec.labels_c), 3, zero=True)
         for level, variant in runs:
-            stc.contract(spec, a, b, c, level, variant)  # warm-up
+            kw = {"allow_deep": True} if level > 2 else {}
+            stc.contract(spec, a, b, c, level, variant, **kw)  # warm-up
             best = 1e30
             reps = 3
             for _ in range(reps):
-                st = stc.contract(spec, a, b, c, level, variant)
+                st = stc.contract(spec, a, b, c, level, variant, **kw)
                 best = min(best, st.device_seconds)
             eff = 2.0 * spec.n_i * spec.n_j * spec.n_p / best / 1e12
             print(f"{name:6s} L{level} {variant:5s} m,n,k={spec.n_i},{spec.n_j},{spec.n_p}  {best * 1e3:9.3f} ms"
