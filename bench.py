@@ -23,7 +23,8 @@ its shard of C -- no data-path collective (strong scaling of one problem).
             contracts and downloads the C shard (stc_contract_host pipeline).
   secondary (N = 1) -- the north star's bar point (m = n = k = 16384,
             abij-abef-efij, extents 128, L2 ABC) and cfg2 (4096^3 permuted
-            layouts, L2 ABC), device-resident.
+            layouts, L2 ABC), device-resident; the bar point again with three
+            levels (allow_deep), an extra beyond the BASELINE levels.
   roofline -- the fused DMMA kernel's own CUDA events over the timed steps.
 
 --impl reference times the reference's own CPU implementation (strassen_tc,
@@ -213,8 +214,8 @@ def _spec(line):
     return stc.parse_benchmark_line(line)
 
 
-def _time_config(line, steps, warmup, dev):
-    """Effective TFLOP/s of L2 ABC on a device-resident config (secondary keys)."""
+def _time_config(line, steps, warmup, dev, level=LEVEL):
+    """Effective TFLOP/s of ABC at `level` on a device-resident config (secondary keys)."""
     import torch
 
     import paper_1704_03092_b200 as stc
@@ -225,21 +226,22 @@ def _time_config(line, steps, warmup, dev):
     b = uniform_tensor(SEED_B, spec.tensor_extents(spec.labels_b), dev)
     ec = spec.tensor_extents(spec.labels_c)
     c = stc.DenseTensor(ec, row_major(ec), torch.zeros(int(np.prod(ec)), dtype=torch.float64, device=dev))
+    kw = {"allow_deep": True} if level > 2 else {}
     for _ in range(warmup):
-        stc.contract(spec, a, b, c, LEVEL, VARIANT, synchronize=False)
+        stc.contract(spec, a, b, c, level, VARIANT, synchronize=False, **kw)
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for _ in range(steps):
-        stc.contract(spec, a, b, c, LEVEL, VARIANT, synchronize=False)
+        stc.contract(spec, a, b, c, level, VARIANT, synchronize=False, **kw)
     t1.record(stream)
     torch.cuda.synchronize()
     s = t0.elapsed_time(t1) * 1e-3 / steps
     tf = 2.0 * spec.n_i * spec.n_j * spec.n_p / s / 1e12
     del a, b, c
     torch.cuda.empty_cache()
-    return {"line": line, "level": LEVEL, "variant": VARIANT.upper(), "ms_per_step": s * 1e3,
+    return {"line": line, "level": level, "variant": VARIANT.upper(), "ms_per_step": s * 1e3,
             "effective_tflops": tf, "frac_of_fp64_peak": tf / FP64_TC_PEAK_TFLOPS, "steps": steps}
 
 
@@ -451,7 +453,9 @@ def main():
 
     secondary = None
     if world == 1 and not args.no_secondary:
-        secondary = {"bar_16384": _time_config(BAR, 3, 1, dev), "cfg2": _time_config(CFG2, 10, 3, dev)}
+        secondary = {"bar_16384": _time_config(BAR, 3, 1, dev), "cfg2": _time_config(CFG2, 10, 3, dev),
+                     # three levels (allow_deep; beyond the BASELINE levels), the same bar point
+                     "bar_16384_level3": _time_config(BAR, 3, 1, dev, level=3)}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
