@@ -75,7 +75,7 @@ TILE = {
     "producer_warps": 4,                 # warp 0 issues the TMA loads, warps 1-3 run the C epilogue
     "summing_warps": 4,                  # in-kernel operand sums (L >= 1 without pre-summed slots)
     "mma": "mma.sync.m16n8k4.row.col.f64 (SASS DMMA.8x8x4)",
-    "gather_kernel": {"cta_tile": (128, 128), "k_chunk": 16, "stages": 3},  # k_strassen_gemm (force_slow, L >= 3)
+    "gather_kernel": {"cta_tile": (128, 128), "k_chunk": 16, "stages": 3},  # k_strassen_gemm (force_slow, reference tiling, L >= 4)
 }
 
 
