@@ -171,6 +171,41 @@ def test_c_abi_library_exports_every_header_symbol():
         _lib.check(lib.stc_workspace_size(ctypes.byref(p), ctypes.byref(need)))
 
 
+def test_component_entries_reject_bad_arguments_before_device_work():
+    """stc_pack_panel / stc_microtile validate on the host (no GPU needed to fail)."""
+    import ctypes
+
+    lib = _lib.lib()
+    P = ctypes.POINTER
+    one = (ctypes.c_void_p * 1)(8)
+    pp = ctypes.cast(one, P(ctypes.c_void_p))
+    co = (ctypes.c_double * 1)(1.0)
+    dummy = ctypes.c_void_p(256)
+
+    def pack(side=0, nviews=1, x0=0, k0=0, width=8, kblock=4, depth=8, coeff=1.0):
+        co[0] = coeff
+        return lib.stc_pack_panel(side, dummy, nviews, pp, pp, None, None, co, x0, 16, k0, 8, width, kblock, 0, dummy,
+                                  depth, None, None)
+
+    for kw, word in ((dict(side=2), "side"), (dict(nviews=0), "views"), (dict(nviews=17), "views"),
+                     (dict(x0=4), "multiple"), (dict(k0=2), "multiple"), (dict(depth=4), "invalid"),
+                     (dict(width=0), "invalid"), (dict(coeff=2.0), r"\+/-1")):
+        with pytest.raises(ValueError, match=word):
+            _lib.check(pack(**kw))
+    i64 = lambda v: (ctypes.c_int64 * 1)(v)
+
+    def micro(k=4, mr=8, nr=4, lda=4, ldb=4, ntg=1, i0=0, j0=0, m=16, n=8):
+        return lib.stc_microtile(dummy, lda, dummy, ldb, k, mr, nr, dummy, ntg, pp, pp, None, None, co, i64(i0), i64(j0),
+                                 i64(m), i64(n), 0, None, None)
+
+    assert micro(k=0) == 0  # k = 0: nothing to do (kernels.py:211-212)
+    for kw, word in ((dict(lda=3), "invalid"), (dict(ldb=3), "invalid"), (dict(mr=0), "invalid"),
+                     (dict(ntg=17), "targets"), (dict(i0=4), "block-aligned"), (dict(j0=2), "block-aligned"),
+                     (dict(i0=16), "outside")):
+        with pytest.raises(ValueError, match=word):
+            _lib.check(micro(**kw))
+
+
 def test_no_cpu_fallback_in_product():
     """The product package never imports the oracle (test infrastructure)."""
     for f in (ROOT / "paper_1704_03092_b200").glob("*.py"):
