@@ -508,6 +508,8 @@ def _pack(which: int, side: OperandTermSide, x_rng, k_rng, width: int, kblock: i
     if not (isinstance(out.data, torch.Tensor) and out.data.is_cuda and out.data.is_contiguous()
             and out.data.dtype == torch.float64):
         raise ValueError("packed buffer must be a contiguous float64 CUDA tensor (PackedBuffer.a_panel / b_panel)")
+    if out.data.device != side.data.device:
+        raise ValueError(f"packed buffer on {out.data.device} but the views' parent on {side.data.device}")
     tabs = [_ptr_array([f(v) for v in side.views])
             for f in (lambda v: v.rscat, lambda v: v.cscat, lambda v: v.rbs, lambda v: v.cbs)]
     co = _coeff_array(side.coeffs)
